@@ -1,0 +1,190 @@
+/* glm130b.h — C ABI of the B200-native GLM-130B quantized inference hot path.
+ *
+ * Drop-in boundary for the glmlab reference's quantization + model-forward operator
+ * API (paths relative to /root/reference/proj). Every entry point names the reference
+ * interface it replaces. Exceptions never cross this ABI: each call returns a
+ * glm_status (the reference's error classes, include/glmlab/common.hpp:28-56) and
+ * glm_last_error() returns the thread-local "[module] message" text.
+ *
+ * All compute runs on the current CUDA device (sm_100a). There is no CPU fallback:
+ * without a usable B200 every compute call returns GLM_CUDA.
+ *
+ * Conventions
+ *   - "host" buffers are ordinary CPU memory owned by the caller; "device" buffers are
+ *     CUDA device pointers; `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - A weight matrix is the reference's row-major [rows = in (K), cols = out (N)]
+ *     (include/glmlab/model.hpp:41-49), used as y = x . W.
+ *   - Quantized payloads are the reference's canonical bytes: INT8 codes in flat
+ *     row-major order, or INT4 codes packed two per byte, even flat index in the low
+ *     nibble (quant.cpp:223-240). Scales are doubles, one per group (quant.hpp:26-42).
+ */
+#ifndef GLM130B_H_
+#define GLM130B_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GLM_OK = 0,
+  GLM_CONTRACT = 1,  /* ContractError  (common.hpp:43) */
+  GLM_DIMENSION = 2, /* DimensionError (common.hpp:38) */
+  GLM_FORMAT = 3,    /* FormatError    (common.hpp:48) */
+  GLM_POLICY = 4,    /* PolicyError    (common.hpp:53) */
+  GLM_CUDA = 5,      /* CUDA runtime / device failure (no reference equivalent) */
+  GLM_NCCL = 6       /* collective failure (no reference equivalent) */
+} glm_status;
+
+typedef enum { GLM_AXIS_ROW = 0, GLM_AXIS_COLUMN = 1, GLM_AXIS_WHOLE = 2 } glm_axis; /* quant.hpp:14 */
+typedef enum { GLM_ABSMAX = 0, GLM_ZEROPOINT = 1 } glm_scheme;                       /* quant.hpp:13 */
+typedef enum { GLM_F64 = 0, GLM_F32 = 1, GLM_BF16 = 2, GLM_F16 = 3 } glm_dtype;
+
+const char* glm_last_error(void);
+const char* glm_version(void);
+
+/* ---------------------------------------------------------------------------------
+ * Quantization (quantlab, include/glmlab/quant.hpp:44-51)
+ * ------------------------------------------------------------------------------- */
+
+/* Number of scale groups: rows (kRow), cols (kColumn) or 1 (kWhole) (quant.cpp:38-48). */
+int64_t glm_group_count(int64_t rows, int64_t cols, glm_axis axis);
+/* Canonical payload size: rows*cols (INT8) or ceil(rows*cols/2) (INT4). */
+int64_t glm_payload_bytes(int64_t rows, int64_t cols, int bits);
+
+/* quantize_absmax / quantize_zeropoint (quant.hpp:44-45, quant.cpp:113-186), computed on
+ * the GPU in FP64, bit-exact with the reference. Host buffers. `w` is [rows, cols] of
+ * `dtype` (F64 or F32 or BF16). zero_points/constant_group are written for
+ * GLM_ZEROPOINT only (may be NULL for GLM_ABSMAX). */
+glm_status glm_quantize_weight(const void* w, glm_dtype dtype, int64_t rows, int64_t cols,
+                               int bits, glm_scheme scheme, glm_axis axis, int8_t* payload,
+                               double* scales, double* zero_points, uint8_t* constant_group);
+/* Same, all pointers device pointers, stream-ordered. */
+glm_status glm_quantize_weight_device(const void* w, glm_dtype dtype, int64_t rows, int64_t cols,
+                                      int bits, glm_scheme scheme, glm_axis axis, int8_t* payload,
+                                      double* scales, double* zero_points,
+                                      uint8_t* constant_group, void* stream);
+
+/* dequantize (quant.hpp:46, quant.cpp:188-221) on the GPU; host buffers; out [rows, cols]. */
+glm_status glm_dequantize(const int8_t* payload, int64_t payload_bytes, const double* scales,
+                          const double* zero_points, int64_t rows, int64_t cols, int bits,
+                          glm_scheme scheme, glm_axis axis, double* out);
+
+/* pack_int4 / unpack_int4 (quant.hpp:50-51, quant.cpp:223-255) on the GPU; host buffers.
+ * pack: codes outside [-7, 7] -> GLM_CONTRACT. unpack: packed_bytes != ceil(count/2) ->
+ * GLM_FORMAT. */
+glm_status glm_pack_int4(const int8_t* codes, int64_t count, int8_t* packed);
+glm_status glm_unpack_int4(const int8_t* packed, int64_t packed_bytes, int64_t count,
+                           int8_t* codes);
+
+/* ---------------------------------------------------------------------------------
+ * Quantized linear: replaces `matmul(x, dequantize(q))` (quant.cpp:188-221 +
+ * tensor.cpp:135-155). The handle holds the codes in the B200 device layout
+ * plus runtime scales; the canonical payload can be
+ * exported back bit-exactly.
+ * ------------------------------------------------------------------------------- */
+typedef struct glm_qweight glm_qweight;
+
+/* From the canonical reference payload + FP64 scales (host buffers). Absmax only. */
+glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64_t rows,
+                              int64_t cols, int bits, glm_axis axis, glm_qweight** out);
+/* Quantize a [rows, cols] weight (host, dtype F64/F32/BF16) straight into a handle. */
+glm_status glm_qweight_quantize(const void* w, glm_dtype dtype, int64_t rows, int64_t cols,
+                                int bits, glm_axis axis, glm_qweight** out);
+glm_status glm_qweight_destroy(glm_qweight* q);
+/* Canonical payload + FP64 scales back out of the device layout (host buffers). */
+glm_status glm_qweight_export(const glm_qweight* q, int8_t* payload, double* scales);
+/* Device layout bytes (for layout tests), size via glm_qweight_device_bytes. */
+int64_t glm_qweight_device_bytes(const glm_qweight* q);
+glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out);
+
+/* y[M, cols] = x[M, rows] . dequantize(q), fp32 in/out, device pointers. M >= 1. */
+glm_status glm_qlinear(const glm_qweight* q, const float* x, int64_t M, float* y, void* stream);
+/* Same with host buffers (H2D, kernel, D2H inside). */
+glm_status glm_qlinear_host(const glm_qweight* q, const float* x, int64_t M, float* y);
+/* Time `iters` back-to-back GEMV launches of the kernel glm_qlinear uses at this M on
+ * device-resident inputs (CUDA events on the launching stream). Returns mean us/launch.
+ * Inputs are larger than L2 when rows*cols*bits/8 > 126 MB; `flush` writes a 256 MB
+ * buffer between launches otherwise. */
+glm_status glm_qlinear_bench(const glm_qweight* q, int64_t M, int iters, int flush, double* us);
+
+/* ---------------------------------------------------------------------------------
+ * GLM model (glmmodel, include/glmlab/model.hpp:15-101)
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int num_layers, hidden, num_heads, ffn_hidden, vocab; /* GLMConfig (model.hpp:15-31) */
+  double init_method_std, layernorm_eps, deepnorm_alpha; /* 0 -> reference defaults */
+} glm_config;
+
+typedef struct {
+  int64_t element_count, quant_payload_bytes, scale_bytes, half_baseline_bytes,
+      wide_baseline_bytes; /* MemoryAccounting (quant.hpp:80-86) */
+  int64_t device_weight_bytes, device_head_bytes, device_kv_bytes; /* B200 layout */
+} glm_memory;
+
+typedef struct glm_model glm_model;
+
+/* Allocates a model for `max_batch` concurrent sequences of up to `max_ctx` positions.
+ * bits in {4, 8}; axis GLM_AXIS_ROW (reference default) or GLM_AXIS_COLUMN (per output
+ * channel). head_bf16 != 0 stores the tied embedding/head in bf16, else fp32.
+ * tp_rank/tp_size: Megatron tensor-parallel shard of this process (1 GPU per rank). */
+glm_status glm_model_create(const glm_config* cfg, int bits, glm_axis axis, int max_batch,
+                            int max_ctx, int head_bf16, int tp_rank, int tp_size,
+                            glm_model** out);
+glm_status glm_model_destroy(glm_model* m);
+/* Tensor parallelism (tp_size > 1): rank 0 calls glm_tp_unique_id, shares the 128 bytes
+ * with every rank (e.g. over torch.distributed), then each rank calls
+ * glm_model_init_comm before loading weights. No-op at tp_size == 1. */
+glm_status glm_tp_unique_id(void* out128);
+glm_status glm_model_init_comm(glm_model* m, const void* unique_id);
+/* Reference parameters (host doubles, model.hpp:41-65), quantized on the GPU with the
+ * model's policy (quantize_model, quant.cpp:284-311). which: 0 qkv [d,3d], 1 out_proj
+ * [d,d], 2 ffn_w1 [d,f], 3 ffn_v [d,f], 4 ffn_w2 [f,d], 5 ln1_gain, 6 ln1_bias,
+ * 7 ln2_gain, 8 ln2_bias; embedding [vocab, d] via glm_model_set_embedding. */
+glm_status glm_model_set_embedding(glm_model* m, const double* embedding);
+glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double* values);
+/* Synthetic random-init weights of the configured shape, generated and quantized on the
+ * GPU with the counter-based generator of DESIGN.md (same stds as model.cpp:69-104). */
+glm_status glm_model_init_synthetic(glm_model* m, uint64_t seed);
+/* Canonical payload/scales of one quantized linear of this rank's shard (host). */
+glm_status glm_model_export_linear(const glm_model* m, int layer, int which, int8_t* payload,
+                                   double* scales);
+glm_status glm_model_memory(const glm_model* m, glm_memory* out);
+
+/* Prefill: runs `n` tokens of sequence `seq` (tokens/positions host arrays) through the
+ * model, filling its KV cache from slot 0. Visibility is the GLM blank-infilling rule for
+ * a [gMASK] sample: key j visible to query i iff j < max(context_length, i + 1)
+ * (corruption.cpp:338-367; context_length = n gives a fully bidirectional prefix).
+ * logits (host, optional) receives [n, vocab] fp32. */
+glm_status glm_model_prefill(glm_model* m, int seq, const int* tokens, const int* positions,
+                             int n, int context_length, float* logits);
+/* One decode step for sequences 0..batch-1: token b at position positions[b] attends to
+ * its whole cache plus itself (decode rows are causal-suffix rows, corruption.cpp:349-362).
+ * next_tokens (host, optional) = greedy argmax; logits (host, optional) [batch, vocab]. */
+glm_status glm_model_decode_step(glm_model* m, int batch, const int* tokens,
+                                 const int* positions, int* next_tokens, float* logits);
+/* Sequence length currently cached for `seq`. */
+int glm_model_cached_length(const glm_model* m, int seq);
+glm_status glm_model_reset(glm_model* m);
+/* Sublayer taps: when enabled, the last prefill/decode call records per layer
+ * the attention output after out_proj and the GeGLU output after W2 (before the DeepNorm
+ * residual), [layers, rows, hidden] fp32, rows = n (prefill) or batch (decode). */
+glm_status glm_model_enable_taps(glm_model* m, int enable);
+glm_status glm_model_get_taps(const glm_model* m, float* attn, float* ffn);
+/* Test hook: force every sublayer output to zero (the "echo" chain of SURVEY §8c). */
+glm_status glm_model_zero_sublayers(glm_model* m, int enable);
+
+/* Decode benchmark: `steps` greedy decode steps for `batch` sequences, starting from the
+ * current caches, on device-resident state via the captured CUDA graph. Times the steps
+ * with CUDA events on the model stream. ms_per_step receives the mean; gemv_us (optional)
+ * the mean duration of the W4/W8 GEMV launches measured with events around each. */
+glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup,
+                                  double* ms_per_step, double* gemv_ms_per_step,
+                                  int* launches_per_step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLM130B_H_ */

@@ -1,0 +1,505 @@
+// block.cu — the GLM block around the quantized linears (glmmodel, model.cpp:125-226).
+//
+// All kernels keep the residual stream, the DeepNorm add and the LayerNorm statistics in
+// fp32 (at N = 70 a sublayer is ~1e-5 of the residual, below any 16-bit
+// epsilon). Their fp16 outputs are written straight into the fragment-ordered x_frag
+// layout (layout.cuh) of the NEXT quantized linear, with that linear's kRow scale fold,
+// so no separate activation-formatting pass exists on the decode path.
+#include <cfloat>
+
+#include "block.h"
+#include "common.cuh"
+
+namespace glm {
+
+namespace {
+
+constexpr float kInvSqrt2 = 0.70710678118654752440f;
+
+// Sum over ksplit partials of element n of row m, times the group scale.
+__device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t n) {
+  float acc = 0.f;
+  for (int s = 0; s < in.ksplit; ++s) acc += in.p[static_cast<int64_t>(s) * in.split_stride + m * in.ld + n];
+  return in.scale ? acc * in.scale[n] : acc;
+}
+
+__device__ __forceinline__ void store_xfrag_pair(const XOut& xo, int m, int64_t k, float v0, float v1) {
+  if (!xo.xf) return;
+  const float s0 = xo.row_scale ? xo.row_scale[k] : 1.f, s1 = xo.row_scale ? xo.row_scale[k + 1] : 1.f;
+  *reinterpret_cast<__half2*>(xo.xf + xfrag_index(xo.nch, m, k)) = __floats2half2_rn(v0 * s0, v1 * s1);
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.x < 32) {
+    s = (l < NT / 32) ? red[l] : 0.f;
+    s = warp_sum(s);
+    if (l == 0) red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// ---- embedding_rows (tensor.cpp:396-412) ---------------------------------------------
+template <typename ET>
+__global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restrict__ tokens, int M,
+                        float* __restrict__ h, XOut xo) {
+  const int m = blockIdx.x;
+  const int64_t row = tokens[m];
+  for (int64_t k = 2 * threadIdx.x; k < d; k += 2 * blockDim.x) {
+    float v0, v1;
+    if constexpr (sizeof(ET) == 4) {
+      v0 = E[row * d + k];
+      v1 = E[row * d + k + 1];
+    } else {
+      v0 = __bfloat162float(E[row * d + k]);
+      v1 = __bfloat162float(E[row * d + k + 1]);
+    }
+    h[m * d + k] = v0;
+    h[m * d + k + 1] = v1;
+    store_xfrag_pair(xo, m, k, v0, v1);
+  }
+}
+
+// ---- deepnorm_residual = LN(alpha * x + y) (model.cpp:125-131, tensor.cpp:256-274) -----
+// One CTA per row; the row lives in registers (<= kLnPer values per thread).
+constexpr int kLnThreads = 1024;
+constexpr int kLnPer = 16;  // supports d <= 16384
+
+__global__ void __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  float z[kLnPer];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnPer; ++i) {
+    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    z[i] = 0.f;
+    if (n < a.d) {
+      const float y = a.zero_sublayer ? 0.f : reduce_partial(a.in, m, n);
+      if (a.tap) a.tap[static_cast<int64_t>(m) * a.d + n] = y;
+      z[i] = a.alpha * a.h[static_cast<int64_t>(m) * a.d + n] + y;
+      sum += z[i];
+    }
+  }
+  const float mean = block_sum<kLnThreads>(sum, red) / static_cast<float>(a.d);
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnPer; ++i) {
+    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    if (n < a.d) sq += (z[i] - mean) * (z[i] - mean);
+  }
+  const float var = block_sum<kLnThreads>(sq, red) / static_cast<float>(a.d);  // biased (tensor.cpp:267)
+  const float rstd = rsqrtf(var + a.eps);
+  // Each thread owns elements n = tid + i*1024; write h, then the x_frag pairs below.
+#pragma unroll
+  for (int i = 0; i < kLnPer; ++i) {
+    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    if (n < a.d) a.h[static_cast<int64_t>(m) * a.d + n] = (z[i] - mean) * rstd * a.gain[n] + a.bias[n];
+  }
+  __syncthreads();
+  __threadfence_block();
+  // x_frag outputs need pairs (k, k+1): re-read the row just written (L1 hit).
+  for (int64_t k = 2 * threadIdx.x; k < a.d; k += 2 * kLnThreads) {
+    const float v0 = a.h[static_cast<int64_t>(m) * a.d + k], v1 = a.h[static_cast<int64_t>(m) * a.d + k + 1];
+    store_xfrag_pair(a.x0, m, k, v0, v1);
+    store_xfrag_pair(a.x1, m, k, v0, v1);
+  }
+}
+
+// ---- GeGLU activation: gelu(x W1) * (x V) (model.cpp:133-135, tensor.cpp:313-318) --------
+__global__ void k_geglu_act(ActArgs a) {
+  const int64_t pairs = static_cast<int64_t>(a.M) * (a.f / 2);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / (a.f / 2));
+    const int64_t n = (i % (a.f / 2)) * 2;
+    float o[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float u = reduce_partial(a.w1, m, n + e);
+      const float v = reduce_partial(a.v, m, n + e);
+      o[e] = 0.5f * u * (1.f + erff(u * kInvSqrt2)) * v;
+    }
+    store_xfrag_pair(a.xo, m, n, o[0], o[1]);
+  }
+}
+
+// ---- decode attention (model.cpp:137-152 for the rows of the generation part) ----------
+// grid (heads, batch, splits); each CTA owns keys [split*kSplitKeys, ...) of its sequence.
+// The CTA whose range holds the new slot also rotates/stores the new k, v. The last CTA to
+// finish a (head, batch) merges the splits in split order (deterministic).
+constexpr int kAttnThreads = 128;
+constexpr int kSplitKeys = 256;
+
+__global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
+  extern __shared__ float sm[];
+  const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
+  const int dh = a.dh, half = dh / 2;
+  const int len = a.cache_len[b];       // keys already cached; the new one goes to slot len
+  const int total = len + 1;
+  const int k0 = split * kSplitKeys, k1 = min(total, k0 + kSplitKeys);
+  float* q = sm;                        // [dh] rotated q, pre-scaled by 1/sqrt(dh)
+  float* p = sm + dh;                   // [kSplitKeys] scores / probabilities
+  float* red = p + kSplitKeys;          // [32]
+  float* onew = red + 32;               // [dh] (new k rotated) then v
+  const int pos = a.positions[b];
+  const float inv_sqrt = rsqrtf(static_cast<float>(dh));
+  __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * dh;
+  __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * dh;
+  const bool has_new = (len >= k0 && len < k0 + kSplitKeys);
+
+  if (k0 < total) {
+    // q (and, for the CTA holding the new slot, k and v): reduce GEMV partials, RoPE.
+    for (int j = threadIdx.x; j < half; j += blockDim.x) {
+      const float2 cs = a.rope[static_cast<int64_t>(pos) * half + j];  // (cos, sin) (tensor.cpp:357-363)
+      const int64_t fq = static_cast<int64_t>(head) * dh + 2 * j;
+      const float qa = reduce_partial(a.qkv, b, fq), qb = reduce_partial(a.qkv, b, fq + 1);
+      q[2 * j] = (cs.x * qa - cs.y * qb) * inv_sqrt;
+      q[2 * j + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
+      if (has_new) {
+        const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
+        const float ka = reduce_partial(a.qkv, b, fk), kb = reduce_partial(a.qkv, b, fk + 1);
+        const float r0 = cs.x * ka - cs.y * kb, r1 = cs.y * ka + cs.x * kb;
+        *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * dh + 2 * j) = __floats2half2_rn(r0, r1);
+        const float va = reduce_partial(a.qkv, b, fv), vb = reduce_partial(a.qkv, b, fv + 1);
+        *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * dh + 2 * j) = __floats2half2_rn(va, vb);
+      }
+    }
+    __syncthreads();
+    // scores: one warp per key, lanes over dh
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int s = k0 + warp; s < k1; s += kAttnThreads / 32) {
+      const __half* kr = kc + static_cast<int64_t>(s) * dh;
+      float acc = 0.f;
+      for (int c = 2 * lane; c < dh; c += 64) {
+        const float2 kv = __half22float2(*reinterpret_cast<const __half2*>(kr + c));
+        acc += q[c] * kv.x + q[c + 1] * kv.y;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) p[s - k0] = acc;
+    }
+    __syncthreads();
+    float mx = -FLT_MAX;
+    for (int s = threadIdx.x; s < k1 - k0; s += blockDim.x) mx = fmaxf(mx, p[s]);
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < kAttnThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int s = threadIdx.x; s < k1 - k0; s += blockDim.x) {
+      const float e = __expf(p[s] - mx);
+      p[s] = e;
+      sum += e;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    sum = 0.f;
+    for (int w = 0; w < kAttnThreads / 32; ++w) sum += red[w];
+    // o = P . V over this split (unnormalised), thread per feature
+    float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (dh + 2);
+    for (int c = threadIdx.x; c < dh; c += blockDim.x) {
+      float o = 0.f;
+      for (int s = k0; s < k1; ++s) o += p[s - k0] * __half2float(vc[static_cast<int64_t>(s) * dh + c]);
+      part[c] = o;
+    }
+    if (threadIdx.x == 0) {
+      part[dh] = mx;
+      part[dh + 1] = sum;
+    }
+  } else if (threadIdx.x == 0) {
+    float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (dh + 2);
+    part[dh] = -FLT_MAX;
+    part[dh + 1] = 0.f;
+  }
+  // last CTA of this (head, b) merges
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    int* ctr = a.counters + b * a.heads + head;
+    last = (atomicAdd(ctr, 1) == a.max_splits - 1);
+    if (last) *ctr = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (dh + 2);
+  float gm = -FLT_MAX;
+  for (int s = 0; s < a.max_splits; ++s) gm = fmaxf(gm, base[s * (dh + 2) + dh]);
+  float gl = 0.f;
+  for (int s = 0; s < a.max_splits; ++s) {
+    const float l = base[s * (dh + 2) + dh + 1];
+    if (l > 0.f) gl += l * __expf(base[s * (dh + 2) + dh] - gm);
+  }
+  for (int c2 = threadIdx.x; c2 < half; c2 += blockDim.x) {
+    float o[2] = {0.f, 0.f};
+    for (int s = 0; s < a.max_splits; ++s) {
+      const float l = base[s * (dh + 2) + dh + 1];
+      if (l > 0.f) {
+        const float w = __expf(base[s * (dh + 2) + dh] - gm);
+        o[0] += w * base[s * (dh + 2) + 2 * c2];
+        o[1] += w * base[s * (dh + 2) + 2 * c2 + 1];
+      }
+    }
+    const int64_t k = static_cast<int64_t>(head) * dh + 2 * c2;
+    store_xfrag_pair(a.xo, b, k, o[0] / gl, o[1] / gl);
+    if (a.out) {
+      a.out[static_cast<int64_t>(b) * a.heads * dh + k] = o[0] / gl;
+      a.out[static_cast<int64_t>(b) * a.heads * dh + k + 1] = o[1] / gl;
+    }
+  }
+}
+
+// Cache length bookkeeping after a decode step (kept on the device for CUDA graphs).
+__global__ void k_advance(int* __restrict__ cache_len, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) cache_len[b] += 1;
+}
+
+// ---- prefill attention (model.cpp:137-152 over a whole [gMASK] sample) -------------------
+// RoPE + KV-cache write for all rows, then one CTA per (head, query row block) computes
+// softmax(q k^T / sqrt(dh) + mask) v with the blank-infilling visibility
+// key j visible to query i  <=>  j < max(C, i + 1)   (corruption.cpp:338-367, gMASK).
+__global__ void k_rope_store(RopeStoreArgs a) {
+  // grid (n rows, heads); threads over pairs
+  const int i = blockIdx.x, head = blockIdx.y, half = a.dh / 2;
+  const int pos = a.positions[i];
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    const float2 cs = a.rope[static_cast<int64_t>(pos) * half + j];
+    const int64_t fq = static_cast<int64_t>(head) * a.dh + 2 * j;
+    const float* row = a.qkv + static_cast<int64_t>(i) * a.ldqkv;
+    const float qa = row[fq], qb = row[fq + 1];
+    const float ka = row[a.d_local + fq], kb = row[a.d_local + fq + 1];
+    const float va = row[2 * a.d_local + fq], vb = row[2 * a.d_local + fq + 1];
+    const int64_t q_off = (static_cast<int64_t>(head) * a.n + i) * a.dh + 2 * j;
+    a.q[q_off] = cs.x * qa - cs.y * qb;
+    a.q[q_off + 1] = cs.y * qa + cs.x * qb;
+    const int64_t c_off = ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx + a.slot0 + i) * a.dh + 2 * j;
+    *reinterpret_cast<__half2*>(a.kcache + c_off) = __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
+    *reinterpret_cast<__half2*>(a.vcache + c_off) = __floats2half2_rn(va, vb);
+  }
+}
+
+constexpr int kPfRows = 16;      // query rows per CTA
+constexpr int kPfThreads = 256;
+
+__global__ void __launch_bounds__(kPfThreads) k_attn_prefill(AttnPrefillArgs a) {
+  // Two-pass over keys in fp32 with online softmax per query row. One warp per query row.
+  extern __shared__ float sm[];
+  const int head = blockIdx.y, i0 = blockIdx.x * kPfRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dh = a.dh;
+  const float inv_sqrt = rsqrtf(static_cast<float>(dh));
+  const __half* kc = a.kcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * dh;
+  const __half* vc = a.vcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * dh;
+  float* qs = sm + warp * dh;  // this warp's q row
+  for (int r = warp; r < kPfRows; r += kPfThreads / 32) {
+    const int i = i0 + r;
+    if (i >= a.n) break;
+    for (int c = lane; c < dh; c += 32) qs[c] = a.q[(static_cast<int64_t>(head) * a.n + i) * dh + c] * inv_sqrt;
+    __syncwarp();
+    const int nkeys = max(a.context_len, i + 1) < a.n ? max(a.context_len, i + 1) : a.n;
+    // online softmax; lane owns features c = lane + 32*t
+    float mrun = -FLT_MAX, lrun = 0.f;
+    float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // dh <= 256
+    for (int s = 0; s < nkeys; ++s) {
+      const __half* kr = kc + static_cast<int64_t>(s) * dh;
+      float acc = 0.f;
+      for (int c = lane; c < dh; c += 32) acc += qs[c] * __half2float(kr[c]);
+      acc = warp_sum(acc);
+      const float mnew = fmaxf(mrun, acc);
+      const float corr = __expf(mrun - mnew), e = __expf(acc - mnew);
+      lrun = lrun * corr + e;
+      const __half* vr = vc + static_cast<int64_t>(s) * dh;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int c = lane + 32 * t;
+        if (c < dh) o[t] = o[t] * corr + e * __half2float(vr[c]);
+      }
+      mrun = mnew;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = lane + 32 * t;
+      if (c < dh) a.out[static_cast<int64_t>(i) * a.ldout + static_cast<int64_t>(head) * dh + c] = o[t] / lrun;
+    }
+    __syncwarp();
+  }
+}
+
+// x_frag from an fp32 [M][K] matrix (row stride ld) for the next linear.
+__global__ void k_rows_to_xfrag(const float* __restrict__ x, int64_t ld, int M, int64_t K, XOut xo) {
+  const int64_t pairs = static_cast<int64_t>(M) * (K / 2);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / (K / 2));
+    const int64_t k = (i % (K / 2)) * 2;
+    store_xfrag_pair(xo, m, k, x[m * ld + k], x[m * ld + k + 1]);
+  }
+}
+
+// ---- tied output head logits = h E^T + greedy argmax (model.cpp:225) -----------------------
+constexpr int kHeadThreads = 256;
+constexpr int kHeadRowsPerGroup = 4;
+
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u >> 31) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(idx));
+}
+
+template <typename ET>
+__global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
+  extern __shared__ float hs[];  // [kHeadRowsPerGroup][d]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ET* E = static_cast<const ET*>(a.E);
+  for (int m0 = 0; m0 < a.M; m0 += kHeadRowsPerGroup) {
+    const int mg = min(kHeadRowsPerGroup, a.M - m0);
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(mg) * a.d; i += blockDim.x)
+      hs[i] = a.h[static_cast<int64_t>(m0) * a.d + i];
+    __syncthreads();
+    unsigned long long best[kHeadRowsPerGroup];
+#pragma unroll
+    for (int r = 0; r < kHeadRowsPerGroup; ++r) best[r] = 0ull;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kHeadThreads / 32);
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * (kHeadThreads / 32) + warp; v < a.vocab_local; v += nwarps) {
+      float acc[kHeadRowsPerGroup] = {0.f, 0.f, 0.f, 0.f};
+      const ET* er = E + (a.vocab_offset + v) * a.d;
+      if constexpr (sizeof(ET) == 2) {
+        for (int64_t k = lane * 8; k < a.d; k += 256) {
+          const uint4 raw = ld_stream(reinterpret_cast<const uint4*>(er + k));
+          const uint32_t ws[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float lo = __uint_as_float(ws[e] << 16), hi = __uint_as_float(ws[e] & 0xFFFF0000u);
+#pragma unroll
+            for (int r = 0; r < kHeadRowsPerGroup; ++r)
+              if (r < mg) acc[r] += lo * hs[r * a.d + k + 2 * e] + hi * hs[r * a.d + k + 2 * e + 1];
+          }
+        }
+      } else {
+        for (int64_t k = lane * 4; k < a.d; k += 128) {
+          const uint4 raw = ld_stream(reinterpret_cast<const uint4*>(er + k));
+          const float w4[4] = {__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
+                               __uint_as_float(raw.w)};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int r = 0; r < kHeadRowsPerGroup; ++r)
+              if (r < mg) acc[r] += w4[e] * hs[r * a.d + k + e];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kHeadRowsPerGroup; ++r) {
+        if (r < mg) {
+          const float lv = warp_sum(acc[r]);
+          if (lane == 0) {
+            if (a.logits) a.logits[static_cast<int64_t>(m0 + r) * a.ld_logits + a.vocab_offset + v] = lv;
+            const unsigned long long key = argmax_key(lv, static_cast<int>(a.vocab_offset + v));
+            best[r] = key > best[r] ? key : best[r];
+          }
+        }
+      }
+    }
+    if (lane == 0)
+      for (int r = 0; r < mg; ++r)
+        if (best[r]) atomicMax(a.argmax + m0 + r, best[r]);
+  }
+}
+
+__global__ void k_argmax_finish(unsigned long long* __restrict__ keys, int* __restrict__ tokens, int M) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < M) {
+    tokens[m] = static_cast<int>(~static_cast<uint32_t>(keys[m] & 0xFFFFFFFFull));
+    keys[m] = 0ull;
+  }
+}
+
+int grid_for(int64_t n, int threads, int cap = 148 * 16) {
+  const int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+
+void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
+                  cudaStream_t st) {
+  if (bf16) k_embed<__nv_bfloat16><<<M, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
+  else k_embed<float><<<M, 256, 0, st>>>(static_cast<const float*>(E), d, tokens, M, h, xo);
+  LAUNCH_CHECK("k_embed");
+}
+
+void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
+  if (a.d > static_cast<int64_t>(kLnThreads) * kLnPer) fail(GLM_DIMENSION, "glmmodel", "hidden too large for LN kernel");
+  k_deepnorm_ln<<<M, kLnThreads, 0, st>>>(a);
+  LAUNCH_CHECK("k_deepnorm_ln");
+}
+
+void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
+  k_geglu_act<<<grid_for(static_cast<int64_t>(a.M) * (a.f / 2), 256), 256, 0, st>>>(a);
+  LAUNCH_CHECK("k_geglu_act");
+}
+
+int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplitKeys; }
+
+void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st) {
+  const size_t smem = (2 * a.dh + kSplitKeys + 32) * sizeof(float);
+  k_attn_decode<<<dim3(a.heads, B, a.max_splits), kAttnThreads, smem, st>>>(a);
+  LAUNCH_CHECK("k_attn_decode");
+}
+
+void launch_advance(int* cache_len, int B, cudaStream_t st) {
+  k_advance<<<1, 32, 0, st>>>(cache_len, B);
+  LAUNCH_CHECK("k_advance");
+}
+
+void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
+  k_rope_store<<<dim3(a.n, a.heads), 64, 0, st>>>(a);
+  LAUNCH_CHECK("k_rope_store");
+}
+
+void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st) {
+  if (a.dh > 256) fail(GLM_DIMENSION, "glmmodel", "head dim > 256 unsupported");
+  const size_t smem = (kPfThreads / 32) * a.dh * sizeof(float);
+  k_attn_prefill<<<dim3((a.n + kPfRows - 1) / kPfRows, a.heads), kPfThreads, smem, st>>>(a);
+  LAUNCH_CHECK("k_attn_prefill");
+}
+
+void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st) {
+  k_rows_to_xfrag<<<grid_for(static_cast<int64_t>(M) * (K / 2), 256), 256, 0, st>>>(x, ld, M, K, xo);
+  LAUNCH_CHECK("k_rows_to_xfrag");
+}
+
+void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(kHeadRowsPerGroup) * a.d * sizeof(float);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[bf16]) {
+    if (bf16) CUDA_CHECK(cudaFuncSetAttribute(k_head<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    else CUDA_CHECK(cudaFuncSetAttribute(k_head<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set[bf16] = true;
+  }
+  if (smem > 227 * 1024) fail(GLM_DIMENSION, "glmmodel", "hidden too large for head kernel");
+  if (a.d % 256 != 0) fail(GLM_DIMENSION, "glmmodel", "head kernel needs hidden % 256 == 0");
+  const int grid = kNumSMs * (smem > 110 * 1024 ? 1 : 2);
+  if (bf16) k_head<__nv_bfloat16><<<grid, kHeadThreads, smem, st>>>(a);
+  else k_head<float><<<grid, kHeadThreads, smem, st>>>(a);
+  LAUNCH_CHECK("k_head");
+}
+
+void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st) {
+  k_argmax_finish<<<grid_for(M, 32), 32, 0, st>>>(keys, tokens, M);
+  LAUNCH_CHECK("k_argmax_finish");
+}
+
+}  // namespace glm

@@ -1,0 +1,102 @@
+// block.h — argument blocks + launchers of the GLM block kernels (block.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "layout.cuh"
+
+namespace glm {
+
+// A sublayer output still in GEMV split-K partial form: value(m, n) =
+// scale[n] * sum_s p[s * split_stride + m * ld + n] (scale may be null = 1).
+struct SubIn {
+  const float* p = nullptr;
+  int ksplit = 1;
+  int64_t split_stride = 0, ld = 0;
+  const float* scale = nullptr;
+};
+
+// Destination x_frag (fp16, fragment order) of the next quantized linear, with its
+// kRow activation fold (row_scale may be null = 1). xf == null disables the output.
+struct XOut {
+  __half* xf = nullptr;
+  int64_t nch = 0;
+  const float* row_scale = nullptr;
+};
+
+struct LnArgs {
+  SubIn in;
+  float* h;                 // [M][d] residual in / LN output out
+  const float *gain, *bias;
+  float alpha, eps;
+  int64_t d;
+  XOut x0, x1;              // up to two consumers (ffn_w1 and ffn_v have distinct kRow scales)
+  float* tap;               // optional [M][d] copy of the sublayer output
+  int zero_sublayer;
+};
+
+struct ActArgs {
+  SubIn w1, v;
+  int M;
+  int64_t f;
+  XOut xo;
+};
+
+struct AttnDecodeArgs {
+  SubIn qkv;                // partials of the fused qkv GEMV, local columns [q | k | v]
+  int64_t d_local;          // heads_local * dh
+  int heads, dh, max_ctx, max_splits;
+  const int* positions;     // [B]
+  const int* cache_len;     // [B]
+  const float2* rope;       // [max_pos][dh/2] (cos, sin)
+  __half *kcache, *vcache;  // [B][heads][max_ctx][dh] for this layer
+  float* part;              // [B][heads][max_splits][dh + 2]
+  int* counters;            // [B][heads], zero-initialised
+  XOut xo;                  // x_frag of out_proj
+  float* out;               // optional fp32 [B][d_local]
+};
+
+struct RopeStoreArgs {
+  const float* qkv;         // [n][ldqkv] reduced fp32 (local columns [q | k | v])
+  int64_t ldqkv, d_local;
+  int n, heads, dh, seq, max_ctx, slot0;
+  const int* positions;
+  const float2* rope;
+  float* q;                 // [heads][n][dh] rotated q
+  __half *kcache, *vcache;
+};
+
+struct AttnPrefillArgs {
+  const float* q;           // [heads][n][dh]
+  const __half *kcache, *vcache;
+  int n, heads, dh, seq, max_ctx, context_len;
+  float* out;               // [n][ldout]
+  int64_t ldout;
+};
+
+struct HeadArgs {
+  const void* E;            // [vocab][d] fp32 or bf16 (full table; rows offset below)
+  const float* h;           // [M][d]
+  int M;
+  int64_t d, vocab_offset, vocab_local;
+  float* logits;            // optional [M][ld_logits], written at column vocab_offset + v
+  int64_t ld_logits;
+  unsigned long long* argmax;  // [M] packed (value, ~index), zero-initialised
+};
+
+void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
+                  cudaStream_t st);
+void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st);
+void launch_geglu_act(const ActArgs& a, cudaStream_t st);
+int attn_decode_splits(int max_ctx);
+void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st);
+void launch_advance(int* cache_len, int B, cudaStream_t st);
+void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st);
+void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st);
+void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st);
+void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st);
+void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st);
+
+}  // namespace glm

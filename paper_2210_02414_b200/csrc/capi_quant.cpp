@@ -1,0 +1,285 @@
+// capi_quant.cpp — C ABI for quantization and the quantized linear (include/glm130b.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "device_buffer.h"
+#include "kernels.h"
+
+namespace glm {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+int64_t group_count(int64_t rows, int64_t cols, int axis) {
+  return axis == GLM_AXIS_ROW ? rows : axis == GLM_AXIS_COLUMN ? cols : 1;
+}
+int64_t payload_bytes(int64_t rows, int64_t cols, int bits) {
+  return bits == 4 ? (rows * cols + 1) / 2 : rows * cols;
+}
+size_t dtype_size(glm_dtype d) {
+  switch (d) {
+    case GLM_F64: return 8;
+    case GLM_F32: return 4;
+    case GLM_BF16: case GLM_F16: return 2;
+  }
+  fail(GLM_CONTRACT, "quantlab", "unknown dtype");
+}
+
+}  // namespace glm
+
+struct glm_qweight {
+  glm::QWeightDev w;
+  glm::DeviceBuffer codes, col_scale, row_scale, scales64;
+  int bits = 8;
+};
+
+namespace glm {
+
+// Builds a handle from a canonical payload + FP64 scales already on the device.
+std::unique_ptr<glm_qweight> make_qweight(const int8_t* d_payload, const double* d_scales, int64_t rows,
+                                          int64_t cols, int bits, int axis, cudaStream_t st) {
+  auto q = std::make_unique<glm_qweight>();
+  q->bits = bits;
+  q->w.L = make_layout(rows, cols, bits);
+  q->w.axis = axis;
+  q->w.nscales = group_count(rows, cols, axis);
+  q->codes.alloc(q->w.L.bytes());
+  q->col_scale.alloc(q->w.L.Np * sizeof(float));
+  q->row_scale.alloc(q->w.L.Kp * sizeof(float));
+  q->scales64.alloc(q->w.nscales * sizeof(double));
+  q->w.codes = q->codes.ptr;
+  q->w.col_scale = q->col_scale.as<float>();
+  q->w.row_scale = q->row_scale.as<float>();
+  q->w.scales64 = q->scales64.as<double>();
+  CUDA_CHECK(cudaMemcpyAsync(q->w.scales64, d_scales, q->w.nscales * 8, cudaMemcpyDeviceToDevice, st));
+  repack_device(d_payload, q->w.L, q->w.codes, st);
+  runtime_scales_device(q->w.scales64, q->w.nscales, q->w.L, axis, q->w.col_scale, q->w.row_scale, st);
+  return q;
+}
+
+void check_policy(int bits, int axis) {
+  if (bits != 4 && bits != 8) fail(GLM_CONTRACT, "quantlab", "bit width must be 4 or 8, got " + std::to_string(bits));
+  if (axis < 0 || axis > 2) fail(GLM_CONTRACT, "quantlab", "unknown group axis");
+}
+
+// y = x . dequantize(q) for any M >= 1 (device pointers), GEMV path in 16-row slabs.
+void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, cudaStream_t st) {
+  const QWeightDev& w = q->w;
+  const int64_t slab = 16;
+  const GemvPlan p = plan_gemv(w.L, static_cast<int>(slab < M ? slab : M));
+  DeviceBuffer xf(slab * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * slab * w.L.Np * 4);
+  CUDA_CHECK(cudaMemsetAsync(xf.ptr, 0, xf.bytes, st));
+  for (int64_t m0 = 0; m0 < M; m0 += slab) {
+    const int mm = static_cast<int>(M - m0 < slab ? M - m0 : slab);
+    xfrag_from_f32(x + m0 * w.L.K, w.L.K, mm, w, xf.as<__half>(), st);
+    gemv_launch(w, xf.as<__half>(), mm, part.as<float>(), p, st);
+    gemv_reduce(part.as<float>(), p.ksplit, mm, w, y + m0 * w.L.N, w.L.N, st);
+  }
+  CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+}  // namespace glm
+
+using namespace glm;
+
+extern "C" {
+
+const char* glm_last_error(void) { return g_last_error.c_str(); }
+const char* glm_version(void) { return "glm130b-b200 0.1 (sm_100a)"; }
+
+int64_t glm_group_count(int64_t rows, int64_t cols, glm_axis axis) { return group_count(rows, cols, axis); }
+int64_t glm_payload_bytes(int64_t rows, int64_t cols, int bits) { return payload_bytes(rows, cols, bits); }
+
+glm_status glm_quantize_weight_device(const void* w, glm_dtype dtype, int64_t rows, int64_t cols, int bits,
+                                      glm_scheme scheme, glm_axis axis, int8_t* payload, double* scales,
+                                      double* zero_points, uint8_t* constant_group, void* stream) {
+  return guarded([&] {
+    if (scheme == GLM_ZEROPOINT && !zero_points) fail(GLM_CONTRACT, "quantlab", "zeropoint needs zero_points");
+    quantize_device(w, dtype, rows, cols, bits, scheme, axis, payload, scales, zero_points, constant_group,
+                    static_cast<cudaStream_t>(stream));
+  });
+}
+
+glm_status glm_quantize_weight(const void* w, glm_dtype dtype, int64_t rows, int64_t cols, int bits,
+                               glm_scheme scheme, glm_axis axis, int8_t* payload, double* scales,
+                               double* zero_points, uint8_t* constant_group) {
+  return guarded([&] {
+    check_policy(bits, axis);
+    if (rows < 0 || cols < 0) fail(GLM_DIMENSION, "quantlab", "negative shape");
+    const int64_t n = rows * cols, g = group_count(rows, cols, axis), pb = payload_bytes(rows, cols, bits);
+    if (n == 0) return;
+    cudaStream_t st = nullptr;
+    DeviceBuffer dw(n * dtype_size(dtype)), dp(pb), ds(g * 8), dz(g * 8), dc(g);
+    CUDA_CHECK(cudaMemcpy(dw.ptr, w, dw.bytes, cudaMemcpyHostToDevice));
+    quantize_device(dw.ptr, dtype, rows, cols, bits, scheme, axis, dp.as<int8_t>(), ds.as<double>(),
+                    dz.as<double>(), dc.as<uint8_t>(), st);
+    CUDA_CHECK(cudaMemcpy(payload, dp.ptr, pb, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(scales, ds.ptr, g * 8, cudaMemcpyDeviceToHost));
+    if (scheme == GLM_ZEROPOINT) {
+      if (zero_points) CUDA_CHECK(cudaMemcpy(zero_points, dz.ptr, g * 8, cudaMemcpyDeviceToHost));
+      if (constant_group) CUDA_CHECK(cudaMemcpy(constant_group, dc.ptr, g, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+glm_status glm_dequantize(const int8_t* payload, int64_t pbytes, const double* scales, const double* zero_points,
+                          int64_t rows, int64_t cols, int bits, glm_scheme scheme, glm_axis axis, double* out) {
+  return guarded([&] {
+    // header / payload validation (quant.cpp:189-197)
+    if (rows < 0 || cols < 0 || (bits != 4 && bits != 8))
+      fail(GLM_FORMAT, "quantlab", "corrupt quantized matrix header");
+    const int64_t expected = payload_bytes(rows, cols, bits);
+    if (pbytes != expected)
+      fail(GLM_FORMAT, "quantlab",
+           "payload length " + std::to_string(pbytes) + " does not match " + std::to_string(expected));
+    if (scheme == GLM_ZEROPOINT && !zero_points) fail(GLM_FORMAT, "quantlab", "zeropoint payload lacks zero points");
+    const int64_t n = rows * cols, g = group_count(rows, cols, axis);
+    if (n == 0) return;
+    DeviceBuffer dp(pbytes), ds(g * 8), dz(g * 8), dout(n * 8);
+    CUDA_CHECK(cudaMemcpy(dp.ptr, payload, pbytes, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(ds.ptr, scales, g * 8, cudaMemcpyHostToDevice));
+    if (scheme == GLM_ZEROPOINT) CUDA_CHECK(cudaMemcpy(dz.ptr, zero_points, g * 8, cudaMemcpyHostToDevice));
+    dequantize_device(dp.as<int8_t>(), ds.as<double>(), dz.as<double>(), rows, cols, bits, scheme, axis,
+                      dout.as<double>(), nullptr);
+    CUDA_CHECK(cudaMemcpy(out, dout.ptr, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_pack_int4(const int8_t* codes, int64_t count, int8_t* packed) {
+  return guarded([&] {
+    if (count < 0) fail(GLM_DIMENSION, "quantlab", "negative count");
+    if (count == 0) return;
+    const int64_t nb = (count + 1) / 2;
+    DeviceBuffer dc(count), dp(nb);
+    CUDA_CHECK(cudaMemcpy(dc.ptr, codes, count, cudaMemcpyHostToDevice));
+    pack_int4_device(dc.as<int8_t>(), count, dp.as<int8_t>(), nullptr);
+    CUDA_CHECK(cudaMemcpy(packed, dp.ptr, nb, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_unpack_int4(const int8_t* packed, int64_t packed_bytes, int64_t count, int8_t* codes) {
+  return guarded([&] {
+    if (count < 0 || packed_bytes != (count + 1) / 2)
+      fail(GLM_FORMAT, "quantlab", "packed INT4 length does not match the recorded count");
+    if (count == 0) return;
+    DeviceBuffer dp(packed_bytes), dc(count);
+    CUDA_CHECK(cudaMemcpy(dp.ptr, packed, packed_bytes, cudaMemcpyHostToDevice));
+    unpack_int4_device(dp.as<int8_t>(), count, dc.as<int8_t>(), nullptr);
+    CUDA_CHECK(cudaMemcpy(codes, dc.ptr, count, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64_t rows, int64_t cols, int bits,
+                              glm_axis axis, glm_qweight** out) {
+  return guarded([&] {
+    check_policy(bits, axis);
+    if (rows <= 0 || cols <= 0) fail(GLM_DIMENSION, "qlinear", "empty weight");
+    const int64_t pb = payload_bytes(rows, cols, bits), g = group_count(rows, cols, axis);
+    DeviceBuffer dp(pb), ds(g * 8);
+    CUDA_CHECK(cudaMemcpy(dp.ptr, payload, pb, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(ds.ptr, scales, g * 8, cudaMemcpyHostToDevice));
+    if (bits == 4) {  // validate nibbles: -8 is not a legal absmax code (quant.cpp:225)
+      std::vector<int8_t> codes(rows * cols);
+      DeviceBuffer dc(rows * cols);
+      unpack_int4_device(dp.as<int8_t>(), rows * cols, dc.as<int8_t>(), nullptr);
+      CUDA_CHECK(cudaMemcpy(codes.data(), dc.ptr, codes.size(), cudaMemcpyDeviceToHost));
+      for (int8_t c : codes)
+        if (c < -7) fail(GLM_CONTRACT, "quantlab", "INT4 code -8 outside [-7, 7]");
+    }
+    auto q = make_qweight(dp.as<int8_t>(), ds.as<double>(), rows, cols, bits, axis, nullptr);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    *out = q.release();
+  });
+}
+
+glm_status glm_qweight_quantize(const void* w, glm_dtype dtype, int64_t rows, int64_t cols, int bits,
+                                glm_axis axis, glm_qweight** out) {
+  return guarded([&] {
+    check_policy(bits, axis);
+    if (rows <= 0 || cols <= 0) fail(GLM_DIMENSION, "qlinear", "empty weight");
+    const int64_t n = rows * cols, pb = payload_bytes(rows, cols, bits), g = group_count(rows, cols, axis);
+    DeviceBuffer dw(n * dtype_size(dtype)), dp(pb), ds(g * 8);
+    CUDA_CHECK(cudaMemcpy(dw.ptr, w, dw.bytes, cudaMemcpyHostToDevice));
+    quantize_device(dw.ptr, dtype, rows, cols, bits, GLM_ABSMAX, axis, dp.as<int8_t>(), ds.as<double>(), nullptr,
+                    nullptr, nullptr);
+    auto q = make_qweight(dp.as<int8_t>(), ds.as<double>(), rows, cols, bits, axis, nullptr);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    *out = q.release();
+  });
+}
+
+glm_status glm_qweight_destroy(glm_qweight* q) {
+  return guarded([&] { delete q; });
+}
+
+glm_status glm_qweight_export(const glm_qweight* q, int8_t* payload, double* scales) {
+  return guarded([&] {
+    const int64_t pb = payload_bytes(q->w.L.K, q->w.L.N, q->bits);
+    DeviceBuffer dp(pb);
+    unrepack_device(q->w.codes, q->w.L, dp.as<int8_t>(), nullptr);
+    CUDA_CHECK(cudaMemcpy(payload, dp.ptr, pb, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(scales, q->w.scales64, q->w.nscales * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int64_t glm_qweight_device_bytes(const glm_qweight* q) { return q ? q->w.L.bytes() : 0; }
+
+glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out) {
+  return guarded([&] { CUDA_CHECK(cudaMemcpy(host_out, q->w.codes, q->w.L.bytes(), cudaMemcpyDeviceToHost)); });
+}
+
+glm_status glm_qlinear(const glm_qweight* q, const float* x, int64_t M, float* y, void* stream) {
+  return guarded([&] {
+    if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
+    qlinear_device(q, x, M, y, static_cast<cudaStream_t>(stream));
+  });
+}
+
+glm_status glm_qlinear_host(const glm_qweight* q, const float* x, int64_t M, float* y) {
+  return guarded([&] {
+    if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
+    DeviceBuffer dx(M * q->w.L.K * 4), dy(M * q->w.L.N * 4);
+    CUDA_CHECK(cudaMemcpy(dx.ptr, x, dx.bytes, cudaMemcpyHostToDevice));
+    qlinear_device(q, dx.as<float>(), M, dy.as<float>(), nullptr);
+    CUDA_CHECK(cudaMemcpy(y, dy.ptr, dy.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_qlinear_bench(const glm_qweight* q, int64_t M, int iters, int flush, double* us) {
+  return guarded([&] {
+    if (M < 1 || M > 16) fail(GLM_DIMENSION, "qlinear", "bench covers the GEMV path, M in 1..16");
+    const QWeightDev& w = q->w;
+    const GemvPlan p = plan_gemv(w.L, static_cast<int>(M));
+    DeviceBuffer xf(M * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
+    DeviceBuffer fl(flush ? (256ll << 20) : 0);
+    CUDA_CHECK(cudaMemset(xf.ptr, 0, xf.bytes));
+    cudaStream_t st;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) gemv_launch(w, xf.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+    cudaEvent_t e0, e1;
+    CUDA_CHECK(cudaEventCreate(&e0));
+    CUDA_CHECK(cudaEventCreate(&e1));
+    double total = 0.0;
+    for (int i = 0; i < iters; ++i) {
+      if (flush) CUDA_CHECK(cudaMemsetAsync(fl.ptr, i & 0xFF, fl.bytes, st));
+      CUDA_CHECK(cudaEventRecord(e0, st));
+      gemv_launch(w, xf.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+      CUDA_CHECK(cudaEventRecord(e1, st));
+      CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    *us = 1000.0 * total / iters;
+  });
+}
+
+}  // extern "C"

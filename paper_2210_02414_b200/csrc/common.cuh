@@ -1,0 +1,88 @@
+// common.cuh — error plumbing and small device helpers shared by every kernel.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "glm130b.h"
+
+namespace glm {
+
+// Error taxonomy of include/glmlab/common.hpp:28-56 carried as a status code; the
+// C ABI turns it into glm_status + glm_last_error() ("[module] message").
+struct Error : std::runtime_error {
+  glm_status code;
+  Error(glm_status c, const std::string& module, const std::string& msg)
+      : std::runtime_error("[" + module + "] " + msg), code(c) {}
+};
+
+[[noreturn]] inline void fail(glm_status c, const char* module, const std::string& msg) {
+  throw Error(c, module, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(GLM_CUDA, "cuda", std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_CHECK(x) ::glm::cuda_check((x), #x)
+#define LAUNCH_CHECK(what) ::glm::cuda_check(cudaGetLastError(), what)
+
+void set_last_error(const std::string& s);
+
+template <typename F>
+glm_status guarded(F&& f) {
+  try {
+    f();
+    return GLM_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("[runtime] host allocation failed");
+    return GLM_CUDA;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return GLM_CONTRACT;
+  }
+}
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Streaming 128-bit load that does not allocate in L1 (weights are read once).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+// Read-only 128-bit load that may stay in L1 (activations re-read by every warp).
+__device__ __forceinline__ uint4 ld_nc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace glm

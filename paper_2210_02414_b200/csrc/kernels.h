@@ -1,0 +1,79 @@
+// kernels.h — host-side launchers shared by the C ABI and the model runner.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "glm130b.h"
+#include "layout.cuh"
+
+namespace glm {
+
+// ---- quant.cu ----
+void quantize_device(const void* w, glm_dtype dtype, int64_t rows, int64_t cols, int bits, int scheme,
+                     int axis, int8_t* payload, double* scales, double* zps, uint8_t* constant_group,
+                     cudaStream_t st);
+void dequantize_device(const int8_t* payload, const double* scales, const double* zps, int64_t rows,
+                       int64_t cols, int bits, int scheme, int axis, double* out, cudaStream_t st);
+void pack_int4_device(const int8_t* codes, int64_t n, int8_t* packed, cudaStream_t st);
+void unpack_int4_device(const int8_t* packed, int64_t n, int8_t* codes, cudaStream_t st);
+void repack_device(const int8_t* payload, const QLayout& L, void* dev, cudaStream_t st);
+struct ShardSpec;
+// canonical FULL payload [Kfull, Nfull] -> device layout of the local shard L
+void repack_shard_device(const int8_t* payload, int64_t Nfull, const ShardSpec& shard, const QLayout& L,
+                         void* dev, cudaStream_t st);
+void unrepack_device(const void* dev, const QLayout& L, int8_t* payload, cudaStream_t st);
+void runtime_scales_device(const double* scales, int64_t nscales, const QLayout& L, int axis,
+                           float* col_scale, float* row_scale, cudaStream_t st);
+double host_unkey(unsigned long long k);
+
+// Megatron shard of a [K, N] linear: local column j maps to full column
+// (j / col_per_rank_block) * col_block + col_offset + (j % col_per_rank_block);
+// local row i maps to full row row_offset + i.
+struct ShardSpec {
+  int64_t col_block, col_per_rank_block, col_offset, row_offset;
+};
+void gen_quantize_device(uint64_t seed, uint32_t tensor_id, int64_t K, int64_t N, float s_lo,
+                         float s_hi, int64_t split, int bits, int axis, const ShardSpec& shard,
+                         const QLayout& L, void* dev, double* scales_full, cudaStream_t st);
+void gather_scales_device(const double* full, const ShardSpec& shard, int axis, int64_t n_local,
+                          double* local, cudaStream_t st);
+
+// ---- gemv.cu : W4A16 / W8A16 decode GEMV (M <= 16) ----
+struct QWeightDev {
+  QLayout L;
+  int axis = 0;
+  void* codes = nullptr;         // device layout
+  float* col_scale = nullptr;    // [Np] epilogue scale
+  float* row_scale = nullptr;    // [Kp] activation fold (kRow), 1 otherwise
+  double* scales64 = nullptr;    // canonical FP64 scales of this (local) matrix
+  int64_t nscales = 0;
+};
+
+struct GemvPlan {
+  int ksplit = 1;
+  int grid = 1;
+};
+GemvPlan plan_gemv(const QLayout& L, int M);
+GemvPlan plan_gemv(int64_t nrt, int64_t nch);
+// One GEMV launch over nrt row tiles of contiguous device-layout codes; row tiles
+// >= rt_split read x_frag xf2 (fused W1|V launch, distinct kRow folds).
+struct GemvOp {
+  const void* codes;
+  int bits;
+  int64_t nrt, nch;
+  const __half* xf;
+  const __half* xf2;
+  int64_t rt_split;
+};
+void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
+// partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over chunk slice s of x . W
+void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,
+                 cudaStream_t st);
+// x fp32 [M][K] (row stride ldx) -> x_frag fp16 with the kRow scale fold
+void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xfrag, cudaStream_t st);
+// y[m][n] (row stride ldy) = col_scale[n] * sum_s partial[s][m][n]
+void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, float* y, int64_t ldy,
+                 cudaStream_t st);
+
+}  // namespace glm

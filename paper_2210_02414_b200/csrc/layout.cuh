@@ -1,0 +1,83 @@
+// layout.cuh — the B200 device layout of a quantized linear and of its activations.
+//
+// A reference weight W[K][N] (row-major, y = x.W, model.hpp:41-49) is stored as
+// "row tiles" of 16 output features x "chunks" of 64 input features, each tile/chunk a
+// contiguous 512 B (INT4) or 1024 B (INT8) block, tiles outermost:
+//
+//     block(rt, c) at ((rt * nch) + c) * kChunkBytes
+//
+// Inside a block, lane l = 4g + t of a warp owns exactly the mma.sync.m16n8k16 A
+// fragments it needs for the 4 k-tiles of the chunk, so one coalesced 512 B warp load
+// (LDG.128 per lane) feeds 4 (INT4) or 2 (INT8) tensor-core MMAs with no shuffles.
+// A fragment register r in 0..3 holds rows {g, g+8}[r&1] and k columns
+// {2t, 2t+1} + 8*(r>>1) of the 16x16 k-tile (PTX ISA m16n8k16 .f16 A layout).
+//
+// INT4: word j (k-tile j) of the lane's uint4 holds 8 nibbles, offset-binary (code+8):
+//   nibble p = r + 4*hi  ->  register r, half hi (hi = odd k column)
+//   so (w & 0x000F000F) | 0x64006400 is register 0 as fp16 (1024+u), etc.
+// INT8: each k-tile takes two words (8 B); the uint4 at +0 holds k-tiles 0,1, the uint4
+//   at +512 B holds k-tiles 2,3. Word wd holds registers 2wd, 2wd+1 as bytes
+//   [r.lo, r.hi, r'.lo, r'.hi], offset-binary (code+128) for the 0x64 PRMT transcode.
+//
+// Activations for a GEMV are stored pre-permuted in "fragment order" x_frag (fp16):
+//   x_frag[m][c][t][16]: the 16 halves lane (g = m mod 8, t) needs as B fragments for
+//   the 4 k-tiles of chunk c, so a lane reads 32 contiguous bytes per chunk.
+#pragma once
+#include <stdint.h>
+
+namespace glm {
+
+constexpr int kTileN = 16;   // output features per row tile
+constexpr int kChunkK = 64;  // input features per chunk
+
+struct QLayout {
+  int64_t K, N;     // logical (reference) shape [K, N]
+  int64_t Kp, Np;   // padded to kChunkK / kTileN
+  int64_t nrt, nch; // row tiles, chunks
+  int bits;
+  __host__ __device__ int64_t chunk_bytes() const { return bits == 4 ? 512 : 1024; }
+  __host__ __device__ int64_t bytes() const { return nrt * nch * chunk_bytes(); }
+};
+
+inline QLayout make_layout(int64_t K, int64_t N, int bits) {
+  QLayout L;
+  L.K = K;
+  L.N = N;
+  L.Kp = (K + kChunkK - 1) / kChunkK * kChunkK;
+  L.Np = (N + kTileN - 1) / kTileN * kTileN;
+  L.nrt = L.Np / kTileN;
+  L.nch = L.Kp / kChunkK;
+  L.bits = bits;
+  return L;
+}
+
+// Byte offset (and nibble shift for INT4) of element (k, n) in the device layout.
+__host__ __device__ inline int64_t layout_offset(const QLayout& L, int64_t k, int64_t n,
+                                                 int* shift) {
+  const int64_t rt = n / kTileN, c = k / kChunkK;
+  const int row = static_cast<int>(n % kTileN), kk = static_cast<int>(k % kChunkK);
+  const int g = row & 7, rsel = row >> 3;
+  const int j = kk >> 4, kc = kk & 15;
+  const int hi = kc & 1, t = (kc & 7) >> 1, r = rsel | ((kc >> 3) << 1);
+  const int lane = g * 4 + t;
+  const int64_t base = (rt * L.nch + c) * L.chunk_bytes();
+  if (L.bits == 4) {
+    const int p = r + 4 * hi;
+    *shift = (p & 1) * 4;
+    return base + lane * 16 + j * 4 + (p >> 1);
+  }
+  *shift = 0;
+  const int half = j >> 1, jj = j & 1, wd = r >> 1, b = (r & 1) * 2 + hi;
+  return base + half * 512 + lane * 16 + jj * 8 + wd * 4 + b;
+}
+
+// Half index of activation (m, k) in x_frag for a layer with nch chunks.
+__host__ __device__ inline int64_t xfrag_index(int64_t nch, int64_t m, int64_t k) {
+  const int64_t c = k / kChunkK;
+  const int kk = static_cast<int>(k % kChunkK);
+  const int j = kk >> 4, kc = kk & 15;
+  const int t = (kc & 7) >> 1;
+  return ((m * nch + c) * 4 + t) * 16 + j * 4 + (kc >> 3) * 2 + (kc & 1);
+}
+
+}  // namespace glm

@@ -1,0 +1,862 @@
+// model.cu — the GLM model runner behind the glm_model_* C ABI.
+//
+// Follows forward() of model.cpp:166-226 (embedding -> N x {attention + DeepNorm,
+// GeGLU + DeepNorm} -> tied head) with the five linears of every layer quantized on the
+// GPU exactly as quantize_model does (quant.cpp:284-311), and adds what the reference
+// lacks for serving: a KV cache, prefill/decode split and a CUDA-graph decode step.
+//
+// Megatron tensor parallelism: rank r of t owns heads [r*H/t, (r+1)*H/t)
+// (q/k/v column blocks of qkv, rows of out_proj) and ffn columns [r*f/t, ...) (columns of
+// ffn_w1/ffn_v, rows of ffn_w2). Quantization runs on the FULL matrix before sharding so
+// scale groups that span ranks are identical on every rank. The row-parallel outputs are
+// summed across ranks (collective.cu) before the DeepNorm residual.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "block.h"
+#include "collective.h"
+#include "common.cuh"
+#include "device_buffer.h"
+#include "gen.cuh"
+#include "kernels.h"
+
+namespace glm {
+
+namespace {
+
+struct Linear {
+  QWeightDev w;
+  GemvPlan plan;
+  int64_t Kfull = 0, Nfull = 0;
+  ShardSpec shard{};
+  bool loaded = false;
+};
+
+struct Layer {
+  Linear lin[5];  // qkv, out_proj, ffn_w1, ffn_v, ffn_w2 (model.hpp:41-49)
+  float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+};
+
+enum { QKV = 0, OUT = 1, W1 = 2, VV = 3, W2 = 4 };
+
+__global__ void k_fill(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
+__global__ void k_f64_to_bf16(const double* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(static_cast<float>(in[i]));
+}
+
+__global__ void k_gen_table(uint64_t seed, uint32_t id, int64_t rows, int64_t cols, float sigma, void* out,
+                            int bf16) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint16_t b = gen_bf16(seed, id, static_cast<uint64_t>(i), sigma);
+    if (bf16) static_cast<uint16_t*>(out)[i] = b;
+    else static_cast<float*>(out)[i] = __uint_as_float(static_cast<uint32_t>(b) << 16);
+  }
+}
+
+// After a decode step: the greedy token becomes the next input, positions advance.
+__global__ void k_feed(const int* __restrict__ next, int* __restrict__ tokens, int* __restrict__ positions, int B) {
+  const int b = threadIdx.x;
+  if (b < B) {
+    tokens[b] = next[b];
+    positions[b] += 1;
+  }
+}
+
+int grid_of(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return static_cast<int>(b < 1 ? 1 : (b < 148 * 16 ? b : 148 * 16));
+}
+
+}  // namespace
+}  // namespace glm
+
+using namespace glm;
+
+struct glm_model {
+  // config (GLMConfig, model.hpp:15-31)
+  int L = 0, d = 0, H = 0, dh = 0, f = 0, V = 0;
+  double alpha = 0, eps = 1e-5, init_std = 0.0052;
+  int bits = 8, axis = 0, max_batch = 1, max_ctx = 1;
+  bool head_bf16 = false;
+  int tp_rank = 0, tp_size = 1;
+  int Hl = 0, dl = 0, fl = 0;
+  int64_t vocab_offset = 0, vocab_local = 0;
+
+  std::vector<Layer> layers;
+  std::vector<DeviceBuffer> pool;
+  void* E = nullptr;
+  float2* rope = nullptr;
+  __half* kv = nullptr;
+
+  // decode state
+  int *d_tokens = nullptr, *d_positions = nullptr, *d_len = nullptr, *d_next = nullptr;
+  int *h_tokens = nullptr, *h_positions = nullptr, *h_next = nullptr;  // pinned
+  unsigned long long* d_argmax = nullptr;
+  float* attn_part = nullptr;
+  int* attn_ctr = nullptr;
+  int attn_splits = 1;
+  std::vector<int> h_len;
+
+  // row buffers (grown for prefill)
+  int64_t rows_cap = 0;
+  DeviceBuffer h, xf_qkv, xf_out, xf_w1, xf_v, xf_w2, logits, taps_attn, taps_ffn;
+  DeviceBuffer y_qkv, q_rot, attn_out, y_out, y_a, y_b, y_ffn, ar_buf;
+  DeviceBuffer partial;
+  int64_t partial_cap = 0;
+  int64_t taps_rows = 0;
+
+  bool taps = false, zero_sub = false;
+  int64_t last_rows = 0;
+
+  cudaStream_t st = nullptr;
+  std::map<std::tuple<int, bool, bool>, cudaGraphExec_t> graphs;
+  std::unique_ptr<Collective> comm;
+
+  ~glm_model() {
+    for (auto& kv_ : graphs) cudaGraphExecDestroy(kv_.second);
+    if (h_tokens) cudaFreeHost(h_tokens);
+    if (h_positions) cudaFreeHost(h_positions);
+    if (h_next) cudaFreeHost(h_next);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  template <typename T>
+  T* alloc(int64_t count, bool zero = true) {
+    pool.emplace_back(count * static_cast<int64_t>(sizeof(T)));
+    if (zero && count) CUDA_CHECK(cudaMemsetAsync(pool.back().ptr, 0, pool.back().bytes, st));
+    return pool.back().as<T>();
+  }
+
+  int64_t nch_of(int64_t K) const { return (K + kChunkK - 1) / kChunkK; }
+  int64_t kp_of(int64_t K) const { return nch_of(K) * kChunkK; }
+
+  // ---------------------------------------------------------------------------------
+  void setup(const glm_config& c, int bits_, int axis_, int max_batch_, int max_ctx_, bool head_bf16_, int r, int t) {
+    if (c.num_layers < 1) fail(GLM_CONTRACT, "glmmodel", "num_layers must be >= 1");
+    if (c.hidden < 1 || c.num_heads < 1 || c.hidden % c.num_heads != 0)
+      fail(GLM_CONTRACT, "glmmodel", "hidden must be divisible by num_heads");
+    if ((c.hidden / c.num_heads) % 2 != 0) fail(GLM_CONTRACT, "glmmodel", "head dimension must be even for rotary pairs");
+    if (c.vocab <= 4) fail(GLM_CONTRACT, "glmmodel", "vocabulary must cover the reserved control ids");
+    if (bits_ != 4 && bits_ != 8) fail(GLM_CONTRACT, "quantlab", "bit width must be 4 or 8, got " + std::to_string(bits_));
+    if (axis_ != GLM_AXIS_ROW && axis_ != GLM_AXIS_COLUMN && axis_ != GLM_AXIS_WHOLE)
+      fail(GLM_CONTRACT, "quantlab", "unknown group axis");
+    if (max_batch_ < 1 || max_batch_ > 16) fail(GLM_CONTRACT, "glmmodel", "max_batch must be in 1..16");
+    if (max_ctx_ < 1) fail(GLM_CONTRACT, "glmmodel", "max_ctx must be >= 1");
+    if (t < 1 || r < 0 || r >= t) fail(GLM_CONTRACT, "glmmodel", "bad tensor-parallel rank");
+    L = c.num_layers;
+    d = c.hidden;
+    H = c.num_heads;
+    dh = d / H;
+    f = c.ffn_hidden > 0 ? c.ffn_hidden : default_ffn(d, H);
+    V = c.vocab;
+    alpha = c.deepnorm_alpha > 0 ? c.deepnorm_alpha : std::sqrt(2.0 * L);  // model.cpp:39, :65-67
+    eps = c.layernorm_eps > 0 ? c.layernorm_eps : 1e-5;
+    init_std = c.init_method_std > 0 ? c.init_method_std : 0.0052;
+    bits = bits_;
+    axis = axis_;
+    max_batch = max_batch_;
+    max_ctx = max_ctx_;
+    head_bf16 = head_bf16_;
+    tp_rank = r;
+    tp_size = t;
+    if (H % t != 0 || f % t != 0) fail(GLM_CONTRACT, "glmmodel", "heads and ffn_hidden must divide by tp_size");
+    if (d % 256 != 0) fail(GLM_CONTRACT, "glmmodel", "this build needs hidden % 256 == 0");
+    if (dh > 256) fail(GLM_CONTRACT, "glmmodel", "head dimension > 256 unsupported");
+    Hl = H / t;
+    dl = Hl * dh;
+    fl = f / t;
+    vocab_local = (V + t - 1) / t;
+    vocab_offset = static_cast<int64_t>(r) * vocab_local;
+    if (vocab_offset + vocab_local > V) vocab_local = V - vocab_offset;
+
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    layers.resize(L);
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      auto mk = [&](Linear& lin, int64_t K, int64_t N, int64_t Kl, int64_t Nl, ShardSpec sh) {
+        lin.Kfull = K;
+        lin.Nfull = N;
+        lin.shard = sh;
+        lin.w.L = make_layout(Kl, Nl, bits);
+        lin.w.axis = axis;
+        lin.w.nscales = axis == GLM_AXIS_ROW ? Kl : axis == GLM_AXIS_COLUMN ? Nl : 1;
+        lin.w.col_scale = alloc<float>(lin.w.L.Np);
+        lin.w.row_scale = alloc<float>(lin.w.L.Kp);
+        lin.w.scales64 = alloc<double>(lin.w.nscales);
+        lin.plan = plan_gemv(lin.w.L, 1);
+      };
+      mk(ly.lin[QKV], d, 3 * d, d, 3 * dl, ShardSpec{d, dl, static_cast<int64_t>(r) * dl, 0});
+      mk(ly.lin[OUT], d, d, dl, d, ShardSpec{d, d, 0, static_cast<int64_t>(r) * dl});
+      mk(ly.lin[W1], d, f, d, fl, ShardSpec{f, fl, static_cast<int64_t>(r) * fl, 0});
+      mk(ly.lin[VV], d, f, d, fl, ShardSpec{f, fl, static_cast<int64_t>(r) * fl, 0});
+      mk(ly.lin[W2], f, d, fl, d, ShardSpec{d, d, 0, static_cast<int64_t>(r) * fl});
+      // codes: qkv, out, [w1 | v] contiguous (one fused GEMV launch), w2
+      ly.lin[QKV].w.codes = alloc<uint8_t>(ly.lin[QKV].w.L.bytes(), false);
+      ly.lin[OUT].w.codes = alloc<uint8_t>(ly.lin[OUT].w.L.bytes(), false);
+      uint8_t* w1v = alloc<uint8_t>(ly.lin[W1].w.L.bytes() + ly.lin[VV].w.L.bytes(), false);
+      ly.lin[W1].w.codes = w1v;
+      ly.lin[VV].w.codes = w1v + ly.lin[W1].w.L.bytes();
+      ly.lin[W2].w.codes = alloc<uint8_t>(ly.lin[W2].w.L.bytes(), false);
+      ly.ln1g = alloc<float>(d);
+      ly.ln1b = alloc<float>(d);
+      ly.ln2g = alloc<float>(d);
+      ly.ln2b = alloc<float>(d);
+      k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln1g, d, 1.f);
+      k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln2g, d, 1.f);
+    }
+    fused_plan = plan_gemv(layers[0].lin[W1].w.L.nrt + layers[0].lin[VV].w.L.nrt, layers[0].lin[W1].w.L.nch);
+    E = head_bf16 ? static_cast<void*>(alloc<__nv_bfloat16>(static_cast<int64_t>(V) * d))
+                  : static_cast<void*>(alloc<float>(static_cast<int64_t>(V) * d));
+    // RoPE table in double -> float (tensor.cpp:335-341: theta_j = 10000^(-2j/dh))
+    const int half = dh / 2;
+    std::vector<float2> tab(static_cast<size_t>(max_ctx + 1) * half);
+    for (int p = 0; p <= max_ctx; ++p)
+      for (int j = 0; j < half; ++j) {
+        const double th = std::pow(10000.0, -2.0 * j / static_cast<double>(dh));
+        const double ang = static_cast<double>(p) * th;
+        tab[static_cast<size_t>(p) * half + j] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+      }
+    rope = alloc<float2>(static_cast<int64_t>(tab.size()), false);
+    CUDA_CHECK(cudaMemcpyAsync(rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+    kv = alloc<__half>(kv_elems(), true);
+    d_tokens = alloc<int>(max_batch);
+    d_positions = alloc<int>(max_batch);
+    d_len = alloc<int>(max_batch);
+    d_next = alloc<int>(max_batch);
+    attn_splits = attn_decode_splits(max_ctx);
+    attn_part = alloc<float>(static_cast<int64_t>(max_batch) * Hl * attn_splits * (dh + 2));
+    attn_ctr = alloc<int>(static_cast<int64_t>(max_batch) * Hl);
+    CUDA_CHECK(cudaMallocHost(&h_tokens, max_batch * sizeof(int)));
+    CUDA_CHECK(cudaMallocHost(&h_positions, max_batch * sizeof(int)));
+    CUDA_CHECK(cudaMallocHost(&h_next, max_batch * sizeof(int)));
+    h_len.assign(max_batch, 0);
+    ensure_rows(max_batch);
+    int64_t pmax = 0;
+    for (int i = 0; i < 5; ++i) {
+      const Linear& lin = layers[0].lin[i];
+      pmax = std::max<int64_t>(pmax, static_cast<int64_t>(lin.plan.ksplit) * 16 * lin.w.L.Np);
+    }
+    pmax = std::max<int64_t>(pmax, static_cast<int64_t>(fused_plan.ksplit) * 16 *
+                                       (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
+    partial.alloc(pmax * 4);
+    partial_cap = pmax;
+    if (tp_size > 1) comm = std::make_unique<Collective>();
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  GemvPlan fused_plan;
+
+  static int default_ffn(int hidden, int heads) {  // model.cpp:30-37
+    if ((8 * hidden) % 3 == 0) return (8 * hidden) / 3;
+    const double target = 8.0 * hidden / 3.0;
+    const int step = (heads % 2 == 0) ? heads : 2 * heads;
+    const int lo = static_cast<int>(std::floor(target / step)) * step;
+    const int hi = lo + step;
+    return (target - lo <= hi - target && lo > 0) ? lo : hi;
+  }
+
+  int64_t kv_layer_elems() const { return 2ll * max_batch * Hl * static_cast<int64_t>(max_ctx) * dh; }
+  int64_t kv_elems() const { return kv_layer_elems() * L; }
+  __half* kcache(int l) { return kv + kv_layer_elems() * l; }
+  __half* vcache(int l) { return kv + kv_layer_elems() * l + kv_layer_elems() / 2; }
+
+  void ensure_rows(int64_t rows) {
+    if (rows <= rows_cap) return;
+    drop_graphs();  // captured graphs hold the old buffer addresses
+    const Layer& ly = layers[0];
+    auto zero = [&](DeviceBuffer& b, int64_t bytes) {
+      b.alloc(bytes);
+      CUDA_CHECK(cudaMemsetAsync(b.ptr, 0, bytes, st));
+    };
+    zero(h, rows * d * 4);
+    zero(xf_qkv, rows * ly.lin[QKV].w.L.Kp * 2);
+    zero(xf_out, rows * ly.lin[OUT].w.L.Kp * 2);
+    zero(xf_w1, rows * ly.lin[W1].w.L.Kp * 2);
+    zero(xf_v, rows * ly.lin[VV].w.L.Kp * 2);
+    zero(xf_w2, rows * ly.lin[W2].w.L.Kp * 2);
+    zero(logits, rows * V * 4);
+    pool.emplace_back(rows * 8);
+    d_argmax_rows = pool.back().as<unsigned long long>();
+    CUDA_CHECK(cudaMemsetAsync(d_argmax_rows, 0, rows * 8, st));
+    d_argmax = d_argmax_rows;
+    pool.emplace_back(rows * 4);
+    d_next_rows = pool.back().as<int>();
+    rows_cap = rows;
+  }
+  unsigned long long* d_argmax_rows = nullptr;
+  int* d_next_rows = nullptr;
+
+  void ensure_prefill(int64_t n) {
+    ensure_rows(n);
+    if (y_qkv.bytes >= n * 3 * dl * 4) return;
+    y_qkv.alloc(n * 3 * dl * 4);
+    q_rot.alloc(n * dl * 4);
+    attn_out.alloc(n * dl * 4);
+    y_out.alloc(n * d * 4);
+    y_a.alloc(n * fl * 4);
+    y_b.alloc(n * fl * 4);
+    y_ffn.alloc(n * d * 4);
+  }
+
+  void ensure_taps(int64_t rows) {
+    if (taps_rows >= rows) return;
+    drop_graphs();
+    taps_attn.alloc(static_cast<int64_t>(L) * rows * d * 4);
+    taps_ffn.alloc(static_cast<int64_t>(L) * rows * d * 4);
+    taps_rows = rows;
+  }
+
+  XOut xout(__half* xf, const Linear& lin) const { return XOut{xf, lin.w.L.nch, lin.w.row_scale}; }
+
+  // ---- weights -------------------------------------------------------------------------
+  void finish_linear(Linear& lin, const double* full_scales) {
+    gather_scales_device(full_scales, lin.shard, axis, lin.w.nscales, lin.w.scales64, st);
+    runtime_scales_device(lin.w.scales64, lin.w.nscales, lin.w.L, axis, lin.w.col_scale, lin.w.row_scale, st);
+    lin.loaded = true;
+  }
+
+  void set_linear_from_host(int l, int which, const double* w) {
+    Linear& lin = layers[l].lin[which];
+    const int64_t K = lin.Kfull, N = lin.Nfull, n = K * N;
+    DeviceBuffer dw(n * 8), dp(bits == 4 ? (n + 1) / 2 : n), ds((axis == GLM_AXIS_ROW ? K : axis == GLM_AXIS_COLUMN ? N : 1) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(dw.ptr, w, n * 8, cudaMemcpyHostToDevice, st));
+    quantize_device(dw.ptr, GLM_F64, K, N, bits, GLM_ABSMAX, axis, dp.as<int8_t>(), ds.as<double>(), nullptr, nullptr, st);
+    repack_shard_device(dp.as<int8_t>(), N, lin.shard, lin.w.L, lin.w.codes, st);
+    finish_linear(lin, ds.as<double>());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  void set_embedding(const double* e) {
+    const int64_t n = static_cast<int64_t>(V) * d;
+    DeviceBuffer de(n * 8);
+    CUDA_CHECK(cudaMemcpyAsync(de.ptr, e, n * 8, cudaMemcpyHostToDevice, st));
+    if (head_bf16) k_f64_to_bf16<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<__nv_bfloat16*>(E), n);
+    else k_f64_to_f32<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<float*>(E), n);
+    LAUNCH_CHECK("embedding upload");
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  void set_vector(int l, int which, const double* v) {
+    float* dst = which == 5 ? layers[l].ln1g : which == 6 ? layers[l].ln1b : which == 7 ? layers[l].ln2g : layers[l].ln2b;
+    DeviceBuffer dv(static_cast<int64_t>(d) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(dv.ptr, v, d * 8, cudaMemcpyHostToDevice, st));
+    k_f64_to_f32<<<grid_of(d), 256, 0, st>>>(dv.as<double>(), dst, d);
+    LAUNCH_CHECK("ln upload");
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  void init_synthetic(uint64_t seed) {
+    // stds of init_parameters (model.cpp:69-104); values from the counter-based generator
+    const double factor = 1.0 / std::sqrt(2.0 * L);
+    auto xavier = [](double a, double b) { return std::sqrt(2.0 / (a + b)); };
+    const float s_init = static_cast<float>(init_std);
+    const float s_v = static_cast<float>(xavier(d, d) * factor);
+    const float s_out = static_cast<float>(xavier(d, d) * factor);
+    const float s_ffn = static_cast<float>(xavier(d, f) * factor);
+    const float s_w2 = static_cast<float>(xavier(f, d) * factor);
+    for (int l = 0; l < L; ++l) {
+      for (int which = 0; which < 5; ++which) {
+        Linear& lin = layers[l].lin[which];
+        const int64_t groups = axis == GLM_AXIS_ROW ? lin.Kfull : lin.Nfull;
+        if (axis == GLM_AXIS_WHOLE) fail(GLM_CONTRACT, "glmmodel", "synthetic init supports row/column axes");
+        DeviceBuffer full(groups * 8);
+        float lo, hi;
+        int64_t split;
+        switch (which) {
+          case QKV: lo = s_init; hi = s_v; split = 2ll * d; break;
+          case OUT: lo = hi = s_out; split = d; break;
+          case W1: case VV: lo = hi = s_ffn; split = f; break;
+          default: lo = hi = s_w2; split = d; break;
+        }
+        gen_quantize_device(seed, static_cast<uint32_t>(l) * 8u + which, lin.Kfull, lin.Nfull, lo, hi, split, bits, axis,
+                            lin.shard, lin.w.L, lin.w.codes, full.as<double>(), st);
+        finish_linear(lin, full.as<double>());
+        CUDA_CHECK(cudaStreamSynchronize(st));
+      }
+    }
+    const int64_t n = static_cast<int64_t>(V) * d;
+    k_gen_table<<<grid_of(n), 256, 0, st>>>(seed, kEmbedTensorId, V, d, s_init, E, head_bf16 ? 1 : 0);
+    LAUNCH_CHECK("k_gen_table");
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  void check_loaded() const {
+    for (const Layer& ly : layers)
+      for (const Linear& lin : ly.lin)
+        if (!lin.loaded) fail(GLM_CONTRACT, "glmmodel", "model weights are not loaded");
+  }
+
+  // ---- row-parallel output sum across ranks (identity at t = 1) -------------------------
+  // Decode: partials are reduced into ar_buf [M][d], allreduced, then consumed with scale 1.
+  SubIn row_parallel_out(const Linear& lin, const GemvPlan& p, int M) {
+    SubIn in{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale};
+    if (tp_size == 1) return in;
+    if (ar_buf.bytes < static_cast<int64_t>(M) * d * 4) ar_buf.alloc(static_cast<int64_t>(max_batch > M ? max_batch : M) * d * 4);
+    gemv_reduce(partial.as<float>(), p.ksplit, M, lin.w, ar_buf.as<float>(), d, st);
+    comm->allreduce_sum(ar_buf.as<float>(), static_cast<int64_t>(M) * d, st);
+    return SubIn{ar_buf.as<float>(), 1, 0, d, nullptr};
+  }
+
+  // ---- decode step (enqueued; captured into a CUDA graph) --------------------------------
+  int enqueue_decode(int B) {
+    int launches = 0;
+    const Layer& l0 = layers[0];
+    launch_embed(E, head_bf16, d, d_tokens, B, h.as<float>(), xout(xf_qkv.as<__half>(), l0.lin[QKV]), st);
+    ++launches;
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
+      gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan, st);
+      AttnDecodeArgs aa;
+      aa.qkv = SubIn{partial.as<float>(), qkv.plan.ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
+      aa.d_local = dl;
+      aa.heads = Hl;
+      aa.dh = dh;
+      aa.max_ctx = max_ctx;
+      aa.max_splits = attn_splits;
+      aa.positions = d_positions;
+      aa.cache_len = d_len;
+      aa.rope = rope;
+      aa.kcache = kcache(l);
+      aa.vcache = vcache(l);
+      aa.part = attn_part;
+      aa.counters = attn_ctr;
+      aa.xo = xout(xf_out.as<__half>(), out);
+      aa.out = nullptr;
+      launch_attn_decode(aa, B, st);
+      gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan, st);
+      LnArgs ln;
+      ln.in = row_parallel_out(out, out.plan, B);
+      ln.h = h.as<float>();
+      ln.gain = ly.ln1g;
+      ln.bias = ly.ln1b;
+      ln.alpha = static_cast<float>(alpha);
+      ln.eps = static_cast<float>(eps);
+      ln.d = d;
+      ln.x0 = xout(xf_w1.as<__half>(), w1);
+      ln.x1 = xout(xf_v.as<__half>(), v);
+      ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
+      ln.zero_sublayer = zero_sub;
+      launch_deepnorm_ln(ln, B, st);
+      GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(), xf_v.as<__half>(), w1.w.L.nrt};
+      gemv_launch(op, B, partial.as<float>(), fused_plan, st);
+      ActArgs act;
+      const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
+      act.w1 = SubIn{partial.as<float>(), fused_plan.ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
+      act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan.ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
+      act.M = B;
+      act.f = fl;
+      act.xo = xout(xf_w2.as<__half>(), w2);
+      launch_geglu_act(act, st);
+      gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan, st);
+      LnArgs ln2 = ln;
+      ln2.in = row_parallel_out(w2, w2.plan, B);
+      ln2.gain = ly.ln2g;
+      ln2.bias = ly.ln2b;
+      const bool last = l + 1 == L;
+      ln2.x0 = last ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]);
+      ln2.x1 = XOut{};
+      ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
+      launch_deepnorm_ln(ln2, B, st);
+      launches += 8 + (tp_size > 1 ? 4 : 0);
+    }
+    launches += enqueue_head(B, logits.as<float>());
+    launch_argmax_finish(d_argmax, d_next, B, st);
+    launch_advance(d_len, B, st);
+    k_feed<<<1, 32, 0, st>>>(d_next, d_tokens, d_positions, B);
+    LAUNCH_CHECK("k_feed");
+    return launches + 3;
+  }
+
+  int enqueue_head(int M, float* logit_out) {
+    HeadArgs ha;
+    ha.E = E;
+    ha.h = h.as<float>();
+    ha.M = M;
+    ha.d = d;
+    ha.vocab_offset = vocab_offset;
+    ha.vocab_local = vocab_local;
+    ha.logits = logit_out;
+    ha.ld_logits = V;
+    ha.argmax = d_argmax;
+    launch_head(ha, head_bf16, st);
+    if (tp_size > 1) {
+      comm->allreduce_max_u64(d_argmax, M, st);
+      if (logit_out) comm->allgather_logits(logit_out, M, V, vocab_offset, vocab_local, st);
+    }
+    return 1;
+  }
+
+  cudaGraphExec_t graph_for(int B) {
+    auto key = std::make_tuple(B, taps, zero_sub);
+    auto it = graphs.find(key);
+    if (it != graphs.end()) return it->second;
+    if (taps) ensure_taps(B);
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_decode(B);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t ge;
+    CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    graphs[key] = ge;
+    return ge;
+  }
+
+  void drop_graphs() {
+    for (auto& kv_ : graphs) cudaGraphExecDestroy(kv_.second);
+    graphs.clear();
+  }
+
+  void decode_step(int B, const int* tokens, const int* positions, int* next_tokens, float* logits_out) {
+    check_loaded();
+    if (B < 1 || B > max_batch) fail(GLM_CONTRACT, "glmmodel", "batch must be in 1..max_batch");
+    for (int b = 0; b < B; ++b) {
+      if (tokens[b] < 0 || tokens[b] >= V)  // model.cpp:170-175
+        fail(GLM_CONTRACT, "glmmodel", "token id " + std::to_string(tokens[b]) + " overflows vocabulary " + std::to_string(V));
+      if (positions[b] < 0 || positions[b] > max_ctx) fail(GLM_CONTRACT, "glmmodel", "position outside the RoPE table");
+      if (h_len[b] + 1 > max_ctx) fail(GLM_CONTRACT, "glmmodel", "KV cache of sequence " + std::to_string(b) + " is full");
+      h_tokens[b] = tokens[b];
+      h_positions[b] = positions[b];
+    }
+    CUDA_CHECK(cudaMemcpyAsync(d_tokens, h_tokens, B * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(d_positions, h_positions, B * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaGraphLaunch(graph_for(B), st));
+    if (logits_out) CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(B) * V * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(h_next, d_next, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+      if (next_tokens) next_tokens[b] = h_next[b];
+      h_len[b] += 1;
+    }
+    last_rows = B;
+  }
+
+  // ---- prefill ---------------------------------------------------------------------------
+  // y[M][N] = x_frag rows . W for M rows, GEMV path in 16-row slabs.
+  void linear_rows(const Linear& lin, const __half* xf, int64_t M, float* y) {
+    const int64_t slab_halves = lin.w.L.nch * kChunkK * 16;
+    for (int64_t m0 = 0; m0 < M; m0 += 16) {
+      const int mm = static_cast<int>(M - m0 < 16 ? M - m0 : 16);
+      gemv_launch(lin.w, xf + (m0 / 16) * slab_halves, mm, partial.as<float>(), lin.plan, st);
+      gemv_reduce(partial.as<float>(), lin.plan.ksplit, mm, lin.w, y + m0 * lin.w.L.N, lin.w.L.N, st);
+    }
+  }
+
+  void prefill(int seq, const int* tokens, const int* positions, int n, int context_len, float* logits_out) {
+    check_loaded();
+    if (seq < 0 || seq >= max_batch) fail(GLM_CONTRACT, "glmmodel", "sequence index outside max_batch");
+    if (n < 1 || n > max_ctx) fail(GLM_CONTRACT, "glmmodel", "prefill length must be in 1..max_ctx");
+    if (context_len < 0 || context_len > n) fail(GLM_CONTRACT, "glmmodel", "context_length must be in 0..n");
+    for (int i = 0; i < n; ++i) {
+      if (tokens[i] < 0 || tokens[i] >= V)
+        fail(GLM_CONTRACT, "glmmodel", "token id " + std::to_string(tokens[i]) + " overflows vocabulary " + std::to_string(V));
+      if (positions[i] < 0 || positions[i] > max_ctx) fail(GLM_CONTRACT, "glmmodel", "position outside the RoPE table");
+    }
+    ensure_prefill(n);
+    if (taps) ensure_taps(n);
+    DeviceBuffer dtok(n * 4), dpos(n * 4);
+    CUDA_CHECK(cudaMemcpyAsync(dtok.ptr, tokens, n * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(dpos.ptr, positions, n * 4, cudaMemcpyHostToDevice, st));
+    launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV]), st);
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
+      linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
+      RopeStoreArgs rs{y_qkv.as<float>(), 3ll * dl, dl, n, Hl, dh, seq, max_ctx, 0, dpos.as<int>(), rope,
+                       q_rot.as<float>(), kcache(l), vcache(l)};
+      launch_rope_store(rs, st);
+      AttnPrefillArgs ap{q_rot.as<float>(), kcache(l), vcache(l), n, Hl, dh, seq, max_ctx, context_len,
+                         attn_out.as<float>(), dl};
+      launch_attn_prefill(ap, st);
+      launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out), st);
+      linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
+      if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
+      LnArgs ln;
+      ln.in = SubIn{y_out.as<float>(), 1, 0, d, nullptr};
+      ln.h = h.as<float>();
+      ln.gain = ly.ln1g;
+      ln.bias = ly.ln1b;
+      ln.alpha = static_cast<float>(alpha);
+      ln.eps = static_cast<float>(eps);
+      ln.d = d;
+      ln.x0 = xout(xf_w1.as<__half>(), w1);
+      ln.x1 = xout(xf_v.as<__half>(), v);
+      ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
+      ln.zero_sublayer = zero_sub;
+      launch_deepnorm_ln(ln, n, st);
+      linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
+      linear_rows(v, xf_v.as<__half>(), n, y_b.as<float>());
+      ActArgs act;
+      act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
+      act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
+      act.M = n;
+      act.f = fl;
+      act.xo = xout(xf_w2.as<__half>(), w2);
+      launch_geglu_act(act, st);
+      linear_rows(w2, xf_w2.as<__half>(), n, y_ffn.as<float>());
+      if (tp_size > 1) comm->allreduce_sum(y_ffn.as<float>(), static_cast<int64_t>(n) * d, st);
+      LnArgs ln2 = ln;
+      ln2.in = SubIn{y_ffn.as<float>(), 1, 0, d, nullptr};
+      ln2.gain = ly.ln2g;
+      ln2.bias = ly.ln2b;
+      ln2.x0 = l + 1 == L ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]);
+      ln2.x1 = XOut{};
+      ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
+      launch_deepnorm_ln(ln2, n, st);
+    }
+    if (logits_out) {
+      enqueue_head(n, logits.as<float>());
+      launch_argmax_finish(d_argmax, d_next_rows, n, st);
+      CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(n) * V * 4, cudaMemcpyDeviceToHost, st));
+    }
+    const int len = n;
+    CUDA_CHECK(cudaMemcpyAsync(d_len + seq, &len, 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    h_len[seq] = n;
+    last_rows = n;
+  }
+};
+
+// ======================================================================================
+// C ABI (include/glm130b.h)
+// ======================================================================================
+namespace {
+
+glm_model* checked(glm_model* m) {
+  if (!m) fail(GLM_CONTRACT, "glmmodel", "null model handle");
+  return m;
+}
+const glm_model* checked(const glm_model* m) {
+  if (!m) fail(GLM_CONTRACT, "glmmodel", "null model handle");
+  return m;
+}
+
+int64_t pbytes(int64_t K, int64_t N, int bits) { return bits == 4 ? (K * N + 1) / 2 : K * N; }
+
+}  // namespace
+
+extern "C" {
+
+glm_status glm_tp_unique_id(void* out128) {
+  return guarded([&] { Collective::unique_id(out128); });
+}
+
+glm_status glm_model_create(const glm_config* cfg, int bits, glm_axis axis, int max_batch, int max_ctx, int head_bf16,
+                            int tp_rank, int tp_size, glm_model** out) {
+  return guarded([&] {
+    if (!cfg || !out) fail(GLM_CONTRACT, "glmmodel", "null argument");
+    auto m = std::make_unique<glm_model>();
+    m->setup(*cfg, bits, axis, max_batch, max_ctx, head_bf16 != 0, tp_rank, tp_size);
+    *out = m.release();
+  });
+}
+
+glm_status glm_model_init_comm(glm_model* m, const void* unique_id) {
+  return guarded([&] {
+    checked(m);
+    if (m->tp_size == 1) return;
+    m->comm->init(m->tp_rank, m->tp_size, unique_id);
+  });
+}
+
+glm_status glm_model_destroy(glm_model* m) {
+  return guarded([&] { delete m; });
+}
+
+glm_status glm_model_set_embedding(glm_model* m, const double* e) {
+  return guarded([&] { checked(m)->set_embedding(e); });
+}
+
+glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double* values) {
+  return guarded([&] {
+    checked(m);
+    if (layer < 0 || layer >= m->L) fail(GLM_CONTRACT, "glmmodel", "layer index out of range");
+    if (which >= 0 && which < 5) m->set_linear_from_host(layer, which, values);
+    else if (which >= 5 && which < 9) m->set_vector(layer, which, values);
+    else fail(GLM_CONTRACT, "glmmodel", "unknown tensor slot");
+  });
+}
+
+glm_status glm_model_init_synthetic(glm_model* m, uint64_t seed) {
+  return guarded([&] { checked(m)->init_synthetic(seed); });
+}
+
+glm_status glm_model_export_linear(const glm_model* m, int layer, int which, int8_t* payload, double* scales) {
+  return guarded([&] {
+    checked(m);
+    if (layer < 0 || layer >= m->L || which < 0 || which > 4) fail(GLM_CONTRACT, "glmmodel", "bad linear index");
+    const Linear& lin = m->layers[layer].lin[which];
+    const int64_t pb = pbytes(lin.w.L.K, lin.w.L.N, m->bits);
+    DeviceBuffer dp(pb);
+    unrepack_device(lin.w.codes, lin.w.L, dp.as<int8_t>(), m->st);
+    CUDA_CHECK(cudaMemcpyAsync(payload, dp.ptr, pb, cudaMemcpyDeviceToHost, m->st));
+    CUDA_CHECK(cudaMemcpyAsync(scales, lin.w.scales64, lin.w.nscales * 8, cudaMemcpyDeviceToHost, m->st));
+    CUDA_CHECK(cudaStreamSynchronize(m->st));
+  });
+}
+
+glm_status glm_model_memory(const glm_model* m, glm_memory* out) {
+  return guarded([&] {
+    checked(m);
+    // memory_accounting (quant.cpp:344-358) over the full (unsharded) model
+    glm_memory r{};
+    for (const Layer& ly : m->layers)
+      for (const Linear& lin : ly.lin) {
+        r.element_count += lin.Kfull * lin.Nfull;
+        r.quant_payload_bytes += pbytes(lin.Kfull, lin.Nfull, m->bits);
+        const int64_t groups = m->axis == GLM_AXIS_ROW ? lin.Kfull : m->axis == GLM_AXIS_COLUMN ? lin.Nfull : 1;
+        r.scale_bytes += groups * 8;
+        r.device_weight_bytes += lin.w.L.bytes();
+      }
+    r.half_baseline_bytes = 2 * r.element_count;
+    r.wide_baseline_bytes = 8 * r.element_count;
+    r.device_head_bytes = static_cast<int64_t>(m->V) * m->d * (m->head_bf16 ? 2 : 4);
+    r.device_kv_bytes = m->kv_elems() * 2;
+    *out = r;
+  });
+}
+
+glm_status glm_model_prefill(glm_model* m, int seq, const int* tokens, const int* positions, int n, int context_length,
+                             float* logits) {
+  return guarded([&] { checked(m)->prefill(seq, tokens, positions, n, context_length, logits); });
+}
+
+glm_status glm_model_decode_step(glm_model* m, int batch, const int* tokens, const int* positions, int* next_tokens,
+                                 float* logits) {
+  return guarded([&] { checked(m)->decode_step(batch, tokens, positions, next_tokens, logits); });
+}
+
+int glm_model_cached_length(const glm_model* m, int seq) {
+  if (!m || seq < 0 || seq >= m->max_batch) return -1;
+  return m->h_len[seq];
+}
+
+glm_status glm_model_reset(glm_model* m) {
+  return guarded([&] {
+    checked(m);
+    std::fill(m->h_len.begin(), m->h_len.end(), 0);
+    CUDA_CHECK(cudaMemsetAsync(m->d_len, 0, m->max_batch * sizeof(int), m->st));
+    CUDA_CHECK(cudaStreamSynchronize(m->st));
+  });
+}
+
+glm_status glm_model_enable_taps(glm_model* m, int enable) {
+  return guarded([&] { checked(m)->taps = enable != 0; });
+}
+
+glm_status glm_model_get_taps(const glm_model* m, float* attn, float* ffn) {
+  return guarded([&] {
+    checked(m);
+    if (!m->taps || m->taps_rows < m->last_rows || m->last_rows == 0)
+      fail(GLM_CONTRACT, "glmmodel", "taps were not recorded by the last call");
+    const int64_t bytes = static_cast<int64_t>(m->L) * m->last_rows * m->d * 4;
+    CUDA_CHECK(cudaMemcpy(attn, m->taps_attn.ptr, bytes, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(ffn, m->taps_ffn.ptr, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_model_zero_sublayers(glm_model* m, int enable) {
+  return guarded([&] { checked(m)->zero_sub = enable != 0; });
+}
+
+glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup, double* ms_per_step,
+                                  double* gemv_ms_per_step, int* launches_per_step) {
+  return guarded([&] {
+    checked(m);
+    m->check_loaded();
+    if (batch < 1 || batch > m->max_batch) fail(GLM_CONTRACT, "glmmodel", "batch must be in 1..max_batch");
+    for (int b = 0; b < batch; ++b)
+      if (m->h_len[b] + warmup + steps > m->max_ctx) fail(GLM_CONTRACT, "glmmodel", "bench would overflow the KV cache");
+    // counts our kernel launches of one step (capture-free dry count happens in graph_for)
+    cudaGraphExec_t ge = m->graph_for(batch);
+    for (int i = 0; i < warmup; ++i) CUDA_CHECK(cudaGraphLaunch(ge, m->st));
+    cudaEvent_t e0, e1;
+    CUDA_CHECK(cudaEventCreate(&e0));
+    CUDA_CHECK(cudaEventCreate(&e1));
+    CUDA_CHECK(cudaStreamSynchronize(m->st));
+    CUDA_CHECK(cudaEventRecord(e0, m->st));
+    for (int i = 0; i < steps; ++i) CUDA_CHECK(cudaGraphLaunch(ge, m->st));
+    CUDA_CHECK(cudaEventRecord(e1, m->st));
+    CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_step = ms / steps;
+    for (int b = 0; b < batch; ++b) m->h_len[b] += warmup + steps;
+    if (launches_per_step) {
+      // count kernel nodes of the step graph
+      cudaGraph_t g;
+      CUDA_CHECK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      m->enqueue_decode(batch);
+      CUDA_CHECK(cudaStreamEndCapture(m->st, &g));
+      size_t nn = 0;
+      CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
+      int kernels = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel) ++kernels;
+      }
+      cudaGraphDestroy(g);
+      *launches_per_step = kernels;
+    }
+    if (gemv_ms_per_step) {
+      // the GEMV launches of one step alone (same buffers), timed as a graph
+      cudaGraph_t g;
+      CUDA_CHECK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      for (int l = 0; l < m->L; ++l) {
+        Layer& ly = m->layers[l];
+        gemv_launch(ly.lin[QKV].w, m->xf_qkv.as<__half>(), batch, m->partial.as<float>(), ly.lin[QKV].plan, m->st);
+        gemv_launch(ly.lin[OUT].w, m->xf_out.as<__half>(), batch, m->partial.as<float>(), ly.lin[OUT].plan, m->st);
+        GemvOp op{ly.lin[W1].w.codes, m->bits, ly.lin[W1].w.L.nrt + ly.lin[VV].w.L.nrt, ly.lin[W1].w.L.nch,
+                  m->xf_w1.as<__half>(), m->xf_v.as<__half>(), ly.lin[W1].w.L.nrt};
+        gemv_launch(op, batch, m->partial.as<float>(), m->fused_plan, m->st);
+        gemv_launch(ly.lin[W2].w, m->xf_w2.as<__half>(), batch, m->partial.as<float>(), ly.lin[W2].plan, m->st);
+      }
+      CUDA_CHECK(cudaStreamEndCapture(m->st, &g));
+      cudaGraphExec_t gx;
+      CUDA_CHECK(cudaGraphInstantiate(&gx, g, 0));
+      cudaGraphDestroy(g);
+      CUDA_CHECK(cudaGraphLaunch(gx, m->st));
+      const int reps = steps < 5 ? 5 : steps;
+      CUDA_CHECK(cudaEventRecord(e0, m->st));
+      for (int i = 0; i < reps; ++i) CUDA_CHECK(cudaGraphLaunch(gx, m->st));
+      CUDA_CHECK(cudaEventRecord(e1, m->st));
+      CUDA_CHECK(cudaEventSynchronize(e1));
+      CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      *gemv_ms_per_step = ms / reps;
+      cudaGraphExecDestroy(gx);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+}  // extern "C"

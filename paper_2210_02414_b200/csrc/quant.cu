@@ -1,0 +1,548 @@
+// quant.cu — bit-exact FP64 weight quantization on the GPU and the device-layout
+// repack (quantlab: /root/reference/proj/src/quant.cpp:19-255).
+//
+// Per group the reference computes (quant.cpp:113-143):
+//     absmax = max |w|  (start 0.0)        s = absmax / cap   (cap = 127 or 7)
+//     code   = (int8) clamp(nearbyint(w / s), -cap, cap)     s == 0 -> codes 0
+// and for the zeropoint scheme (quant.cpp:145-186) s = (hi - lo)/(2^b - 2),
+// z = nearbyint(lo / s) + cap, code = round_code(nearbyint(w/s) - z).
+// max/min are order independent and IEEE division + rint (round-half-even) are
+// correctly rounded on the GPU, so codes and scales match the CPU bit for bit.
+#include "common.cuh"
+#include "gen.cuh"
+#include "kernels.h"
+#include "layout.cuh"
+
+namespace glm {
+
+namespace {
+
+// Monotone map of doubles onto unsigned 64-bit keys (for atomicMin/Max reductions).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dunkey(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(static_cast<long long>(b));
+#else
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+
+template <typename T>
+__device__ __forceinline__ double load_as_double(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ double load_as_double<double>(const double* p, int64_t i) { return p[i]; }
+template <>
+__device__ __forceinline__ double load_as_double<float>(const float* p, int64_t i) {
+  return static_cast<double>(p[i]);
+}
+template <>
+__device__ __forceinline__ double load_as_double<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return static_cast<double>(__bfloat162float(p[i]));
+}
+
+__device__ __forceinline__ int64_t group_of(int axis, int64_t r, int64_t c) {
+  return axis == GLM_AXIS_ROW ? r : axis == GLM_AXIS_COLUMN ? c : 0;
+}
+
+// Pass 1: per-group min/max keys + non-finite flag. Grid-stride over elements.
+template <typename T>
+__global__ void k_group_minmax(const T* __restrict__ w, int64_t rows, int64_t cols, int axis,
+                               unsigned long long* __restrict__ lo, unsigned long long* __restrict__ hi,
+                               int* __restrict__ nonfinite) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = load_as_double(w, i);
+    if (!isfinite(x)) {
+      atomicOr(nonfinite, 1);
+      continue;
+    }
+    const int64_t g = group_of(axis, i / cols, i % cols);
+    // Warp-aggregate when the whole warp hits one group (kRow/kWhole): fewer atomics.
+    const unsigned long long kx = dkey(x);
+    atomicMin(lo + g, kx);
+    atomicMax(hi + g, kx);
+  }
+}
+
+// Pass 2: scales (and zero points) per group.
+__global__ void k_group_params(const unsigned long long* __restrict__ lo,
+                               const unsigned long long* __restrict__ hi, int64_t groups, int bits,
+                               int scheme, double* __restrict__ scales, double* __restrict__ zps,
+                               uint8_t* __restrict__ constant_group) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= groups) return;
+  const double vlo = dunkey(lo[g]), vhi = dunkey(hi[g]);
+  const double cap = static_cast<double>((1 << (bits - 1)) - 1);
+  if (scheme == GLM_ABSMAX) {
+    // max(0.0, |w|...) == max(|lo|, |hi|) (quant.cpp:127-130)
+    const double absmax = fmax(0.0, fmax(fabs(vlo), fabs(vhi)));
+    scales[g] = absmax / cap;
+  } else {
+    if (vhi == vlo) {  // constant group (quant.cpp:166-171)
+      scales[g] = 0.0;
+      zps[g] = vlo;
+      if (constant_group) constant_group[g] = 1;
+    } else {
+      const double s = (vhi - vlo) / static_cast<double>((1 << bits) - 2);
+      scales[g] = s;
+      zps[g] = rint(vlo / s) + cap;
+      if (constant_group) constant_group[g] = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ int8_t round_code(double x, double cap) {  // quant.cpp:27-31
+  const double r = rint(x);
+  return static_cast<int8_t>(fmin(fmax(r, -cap), cap));
+}
+
+template <typename T>
+__device__ __forceinline__ int8_t code_at(const T* w, int64_t i, int64_t cols, int axis, int bits,
+                                          int scheme, const double* scales, const double* zps) {
+  const double cap = static_cast<double>((1 << (bits - 1)) - 1);
+  const int64_t g = group_of(axis, i / cols, i % cols);
+  const double s = scales[g];
+  if (s == 0.0) return 0;
+  const double x = load_as_double(w, i);
+  if (scheme == GLM_ABSMAX) return round_code(x / s, cap);
+  return round_code(rint(x / s) - zps[g], cap);
+}
+
+// Pass 3: canonical payload (INT8 flat, or INT4 two-per-byte, even index low nibble).
+template <typename T>
+__global__ void k_codes(const T* __restrict__ w, int64_t rows, int64_t cols, int axis, int bits,
+                        int scheme, const double* __restrict__ scales, const double* __restrict__ zps,
+                        int8_t* __restrict__ payload) {
+  const int64_t n = rows * cols;
+  const int64_t nbytes = bits == 4 ? (n + 1) / 2 : n;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nbytes;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (bits == 8) {
+      payload[b] = code_at(w, b, cols, axis, bits, scheme, scales, zps);
+    } else {
+      const uint8_t c0 = static_cast<uint8_t>(code_at(w, 2 * b, cols, axis, bits, scheme, scales, zps)) & 0xF;
+      const uint8_t c1 = (2 * b + 1 < n)
+                             ? static_cast<uint8_t>(code_at(w, 2 * b + 1, cols, axis, bits, scheme, scales, zps)) & 0xF
+                             : 0;
+      payload[b] = static_cast<int8_t>(c0 | (c1 << 4));
+    }
+  }
+}
+
+__device__ __forceinline__ int canonical_code(const int8_t* payload, int64_t flat, int bits) {
+  if (bits == 8) return payload[flat];
+  const uint8_t b = static_cast<uint8_t>(payload[flat >> 1]);
+  int v = (flat & 1) ? (b >> 4) : (b & 0xF);
+  return v >= 8 ? v - 16 : v;
+}
+
+// Canonical payload -> device layout. One thread per 32-bit word of the layout. The
+// payload is the FULL [Kfull, Nfull] matrix; (rmap, cmap) place the local shard in it
+// (quantize first, then shard: SURVEY §8e).
+struct RepackMap {
+  int64_t Nfull, col_block, cpr, col_offset, row_offset;
+  __device__ __forceinline__ int64_t col(int64_t j) const { return (j / cpr) * col_block + col_offset + (j % cpr); }
+};
+
+__global__ void k_repack(const int8_t* __restrict__ payload, QLayout L, RepackMap mp, uint32_t* __restrict__ out) {
+  const int64_t words = L.bytes() / 4;
+  for (int64_t wi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; wi < words;
+       wi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t byte0 = wi * 4;
+    const int64_t blk = byte0 / L.chunk_bytes();
+    const int64_t rt = blk / L.nch, c = blk % L.nch;
+    int inblk = static_cast<int>(byte0 % L.chunk_bytes());
+    uint32_t word = 0;
+    if (L.bits == 4) {
+      const int lane = inblk / 16, j = (inblk % 16) / 4;
+      const int g = lane >> 2, t = lane & 3;
+      for (int p = 0; p < 8; ++p) {
+        const int r = p & 3, hi = p >> 2;
+        const int64_t n = rt * kTileN + g + 8 * (r & 1);
+        const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
+        const int code =
+            (k < L.K && n < L.N) ? canonical_code(payload, (mp.row_offset + k) * mp.Nfull + mp.col(n), 4) : 0;
+        word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * p);
+      }
+    } else {
+      const int half = inblk / 512;
+      inblk %= 512;
+      const int lane = inblk / 16, jj = (inblk % 16) / 8, wd = (inblk % 8) / 4;
+      const int g = lane >> 2, t = lane & 3, j = half * 2 + jj;
+      for (int b = 0; b < 4; ++b) {
+        const int r = wd * 2 + (b >> 1), hi = b & 1;
+        const int64_t n = rt * kTileN + g + 8 * (r & 1);
+        const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
+        const int code =
+            (k < L.K && n < L.N) ? canonical_code(payload, (mp.row_offset + k) * mp.Nfull + mp.col(n), 8) : 0;
+        word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * b);
+      }
+    }
+    out[wi] = word;
+  }
+}
+
+__device__ __forceinline__ int layout_code(const uint8_t* dev, const QLayout& L, int64_t k, int64_t n) {
+  int shift;
+  const int64_t off = layout_offset(L, k, n, &shift);
+  if (L.bits == 4) return static_cast<int>((dev[off] >> shift) & 0xF) - 8;
+  return static_cast<int>(dev[off]) - 128;
+}
+
+// Device layout -> canonical payload (export / bit-exact round trip).
+__global__ void k_unrepack(const uint8_t* __restrict__ dev, QLayout L, int8_t* __restrict__ payload) {
+  const int64_t n = L.K * L.N;
+  const int64_t nbytes = L.bits == 4 ? (n + 1) / 2 : n;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nbytes;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (L.bits == 8) {
+      payload[b] = static_cast<int8_t>(layout_code(dev, L, b / L.N, b % L.N));
+    } else {
+      const int64_t f0 = 2 * b, f1 = 2 * b + 1;
+      const int c0 = layout_code(dev, L, f0 / L.N, f0 % L.N);
+      const int c1 = f1 < n ? layout_code(dev, L, f1 / L.N, f1 % L.N) : 0;
+      payload[b] = static_cast<int8_t>((c0 & 0xF) | ((c1 & 0xF) << 4));
+    }
+  }
+}
+
+__global__ void k_dequantize(const int8_t* __restrict__ payload, const double* __restrict__ scales,
+                             const double* __restrict__ zps, int64_t rows, int64_t cols, int bits,
+                             int scheme, int axis, double* __restrict__ out) {
+  // quant.cpp:188-221
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = group_of(axis, i / cols, i % cols);
+    const double s = scales[g];
+    const double code = static_cast<double>(canonical_code(payload, i, bits));
+    double v;
+    if (scheme == GLM_ABSMAX) v = s * code;
+    else if (s == 0.0) v = zps[g];
+    else v = s * (code + zps[g]);
+    out[i] = v;
+  }
+}
+
+__global__ void k_pack4(const int8_t* __restrict__ codes, int64_t n, int8_t* __restrict__ packed,
+                        int* __restrict__ bad) {
+  const int64_t nb = (n + 1) / 2;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c0 = codes[2 * b];
+    const int c1 = 2 * b + 1 < n ? codes[2 * b + 1] : 0;
+    if (c0 < -7 || c0 > 7 || c1 < -7 || c1 > 7) atomicOr(bad, 1);
+    packed[b] = static_cast<int8_t>((c0 & 0xF) | ((c1 & 0xF) << 4));
+  }
+}
+
+__global__ void k_unpack4(const int8_t* __restrict__ packed, int64_t n, int8_t* __restrict__ codes) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    codes[i] = static_cast<int8_t>(canonical_code(packed, i, 4));
+}
+
+// Runtime scales used by the GEMV: kColumn/kWhole -> per-output fp32 scale (epilogue);
+// kRow -> per-input fp32 scale normalised by the largest row scale S (folded into the
+// fp16 activation so it stays in the normal range), with S applied in the epilogue.
+__global__ void k_runtime_scales(const double* __restrict__ scales, QLayout L, int axis,
+                                 float* __restrict__ col_scale, float* __restrict__ row_scale,
+                                 const unsigned long long* __restrict__ smax_key) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (axis == GLM_AXIS_ROW) {
+    const double S = dunkey(*smax_key);
+    if (i < L.Kp) row_scale[i] = (i < L.K && S > 0.0) ? static_cast<float>(scales[i] / S) : 0.f;
+    if (i < L.Np) col_scale[i] = (i < L.N) ? static_cast<float>(S) : 0.f;
+  } else {
+    if (i < L.Np) col_scale[i] = i < L.N ? static_cast<float>(scales[axis == GLM_AXIS_COLUMN ? i : 0]) : 0.f;
+    if (i < L.Kp) row_scale[i] = 1.f;
+  }
+}
+
+__global__ void k_max_key(const double* __restrict__ v, int64_t n, unsigned long long* __restrict__ key) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicMax(key, dkey(v[i]));
+}
+
+// ---- fused synthetic generation + quantization straight into the device layout ----
+// Weight tensors of the counter-based model: value(k, n) = gen(seed, id, k*N + n,
+// sigma(n)), sigma(n) = n < split ? s_lo : s_hi (the qkv v-block std, model.cpp:83-92).
+struct GenSpec {
+  uint64_t seed;
+  uint32_t tensor_id;
+  int64_t K, N;       // full (unsharded) reference shape
+  float s_lo, s_hi;
+  int64_t split;
+};
+
+__device__ __forceinline__ double gen_value(const GenSpec& g, int64_t k, int64_t n) {
+  return bf16_bits_to_double(gen_bf16(g.seed, g.tensor_id, static_cast<uint64_t>(k * g.N + n),
+                                      n < g.split ? g.s_lo : g.s_hi));
+}
+
+// Column map of a shard: local column j -> full column (Megatron column split of the
+// q/k/v blocks or of f), row map: local row i -> full row.
+struct ShardMap {
+  int64_t col_block, col_per_rank_block, col_offset;  // qkv: 3 blocks of d, each split
+  int64_t row_offset;
+  __device__ __forceinline__ int64_t col(int64_t j) const {
+    const int64_t b = j / col_per_rank_block, r = j % col_per_rank_block;
+    return b * col_block + col_offset + r;
+  }
+  __device__ __forceinline__ int64_t row(int64_t i) const { return row_offset + i; }
+};
+
+// absmax per group over the FULL matrix (groups spanning a split dimension must see
+// every rank's values: quantize-then-shard).
+__global__ void k_gen_absmax_rows(GenSpec g, unsigned long long* __restrict__ key) {
+  // one block per full row k
+  const int64_t k = blockIdx.x;
+  double m = 0.0;
+  for (int64_t n = threadIdx.x; n < g.N; n += blockDim.x) m = fmax(m, fabs(gen_value(g, k, n)));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w) m = fmax(m, red[w]);
+    key[k] = dkey(m);
+  }
+}
+
+__global__ void k_gen_absmax_cols(GenSpec g, int64_t rows_per_block, unsigned long long* __restrict__ key) {
+  // thread per full column, block-y splits the rows; atomicMax merges.
+  const int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (n >= g.N) return;
+  const int64_t k0 = blockIdx.y * rows_per_block, k1 = min(g.K, k0 + rows_per_block);
+  double m = 0.0;
+  for (int64_t k = k0; k < k1; ++k) m = fmax(m, fabs(gen_value(g, k, n)));
+  atomicMax(key + n, dkey(m));
+}
+
+__global__ void k_keys_to_scales(const unsigned long long* __restrict__ key, int64_t n, double cap,
+                                 double* __restrict__ scales) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) scales[i] = dunkey(key[i]) / cap;
+}
+
+// Pass 2: codes into the device layout of the local shard [Kl, Nl].
+__global__ void k_gen_codes(GenSpec g, ShardMap sm, QLayout L, int axis, const double* __restrict__ scales,
+                            uint32_t* __restrict__ out) {
+  const int64_t words = L.bytes() / 4;
+  const double cap = static_cast<double>((1 << (L.bits - 1)) - 1);
+  for (int64_t wi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; wi < words;
+       wi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t byte0 = wi * 4;
+    const int64_t blk = byte0 / L.chunk_bytes();
+    const int64_t rt = blk / L.nch, c = blk % L.nch;
+    int inblk = static_cast<int>(byte0 % L.chunk_bytes());
+    uint32_t word = 0;
+    const int nvals = L.bits == 4 ? 8 : 4;
+    int half = 0, lane, j, wd = 0;
+    if (L.bits == 4) {
+      lane = inblk / 16;
+      j = (inblk % 16) / 4;
+    } else {
+      half = inblk / 512;
+      inblk %= 512;
+      lane = inblk / 16;
+      j = half * 2 + (inblk % 16) / 8;
+      wd = (inblk % 8) / 4;
+    }
+    const int gg = lane >> 2, t = lane & 3;
+    for (int p = 0; p < nvals; ++p) {
+      int r, hi;
+      if (L.bits == 4) {
+        r = p & 3;
+        hi = p >> 2;
+      } else {
+        r = wd * 2 + (p >> 1);
+        hi = p & 1;
+      }
+      const int64_t n = rt * kTileN + gg + 8 * (r & 1);
+      const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
+      int code = 0;
+      if (k < L.K && n < L.N) {
+        const int64_t fk = sm.row(k), fn = sm.col(n);
+        const double s = scales[axis == GLM_AXIS_ROW ? fk : fn];
+        if (s != 0.0) code = round_code(gen_value(g, fk, fn) / s, cap);
+      }
+      if (L.bits == 4) word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * p);
+      else word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * p);
+    }
+    out[wi] = word;
+  }
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  const int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32);
+}
+
+}  // namespace
+
+double host_unkey(unsigned long long k) { return dunkey(k); }
+
+void quantize_device(const void* w, glm_dtype dtype, int64_t rows, int64_t cols, int bits, int scheme,
+                     int axis, int8_t* payload, double* scales, double* zps, uint8_t* constant_group,
+                     cudaStream_t st) {
+  if (bits != 4 && bits != 8) fail(GLM_CONTRACT, "quantlab", "bit width must be 4 or 8, got " + std::to_string(bits));
+  if (axis < 0 || axis > 2) fail(GLM_CONTRACT, "quantlab", "unknown group axis");
+  if (scheme != GLM_ABSMAX && scheme != GLM_ZEROPOINT) fail(GLM_CONTRACT, "quantlab", "unknown quantization scheme");
+  if (rows < 0 || cols < 0) fail(GLM_DIMENSION, "quantlab", "negative shape");
+  const int64_t n = rows * cols;
+  const int64_t groups = axis == GLM_AXIS_ROW ? rows : axis == GLM_AXIS_COLUMN ? cols : 1;
+  if (n == 0) return;
+  unsigned long long *lo, *hi;
+  int* flag;
+  CUDA_CHECK(cudaMallocAsync(&lo, groups * 8, st));
+  CUDA_CHECK(cudaMallocAsync(&hi, groups * 8, st));
+  CUDA_CHECK(cudaMallocAsync(&flag, 4, st));
+  CUDA_CHECK(cudaMemsetAsync(lo, 0xFF, groups * 8, st));
+  CUDA_CHECK(cudaMemsetAsync(hi, 0x00, groups * 8, st));
+  CUDA_CHECK(cudaMemsetAsync(flag, 0, 4, st));
+  const int g = grid_for(n);
+  switch (dtype) {
+    case GLM_F64: k_group_minmax<<<g, 256, 0, st>>>(static_cast<const double*>(w), rows, cols, axis, lo, hi, flag); break;
+    case GLM_F32: k_group_minmax<<<g, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, axis, lo, hi, flag); break;
+    case GLM_BF16: k_group_minmax<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), rows, cols, axis, lo, hi, flag); break;
+    default: fail(GLM_CONTRACT, "quantlab", "unsupported weight dtype");
+  }
+  LAUNCH_CHECK("k_group_minmax");
+  int hflag = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  if (hflag) {
+    cudaFreeAsync(lo, st);
+    cudaFreeAsync(hi, st);
+    cudaFreeAsync(flag, st);
+    fail(GLM_CONTRACT, "quantlab", "quantization requires finite inputs");
+  }
+  k_group_params<<<grid_for(groups), 256, 0, st>>>(lo, hi, groups, bits, scheme, scales, zps, constant_group);
+  LAUNCH_CHECK("k_group_params");
+  switch (dtype) {
+    case GLM_F64: k_codes<<<g, 256, 0, st>>>(static_cast<const double*>(w), rows, cols, axis, bits, scheme, scales, zps, payload); break;
+    case GLM_F32: k_codes<<<g, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, axis, bits, scheme, scales, zps, payload); break;
+    default: k_codes<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), rows, cols, axis, bits, scheme, scales, zps, payload); break;
+  }
+  LAUNCH_CHECK("k_codes");
+  CUDA_CHECK(cudaFreeAsync(lo, st));
+  CUDA_CHECK(cudaFreeAsync(hi, st));
+  CUDA_CHECK(cudaFreeAsync(flag, st));
+}
+
+void dequantize_device(const int8_t* payload, const double* scales, const double* zps, int64_t rows,
+                       int64_t cols, int bits, int scheme, int axis, double* out, cudaStream_t st) {
+  if (rows * cols == 0) return;
+  k_dequantize<<<grid_for(rows * cols), 256, 0, st>>>(payload, scales, zps, rows, cols, bits, scheme, axis, out);
+  LAUNCH_CHECK("k_dequantize");
+}
+
+void pack_int4_device(const int8_t* codes, int64_t n, int8_t* packed, cudaStream_t st) {
+  if (n == 0) return;
+  int* bad;
+  CUDA_CHECK(cudaMallocAsync(&bad, 4, st));
+  CUDA_CHECK(cudaMemsetAsync(bad, 0, 4, st));
+  k_pack4<<<grid_for((n + 1) / 2), 256, 0, st>>>(codes, n, packed, bad);
+  LAUNCH_CHECK("k_pack4");
+  int h = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFreeAsync(bad, st);
+  if (h) fail(GLM_CONTRACT, "quantlab", "INT4 code outside [-7, 7]");
+}
+
+void unpack_int4_device(const int8_t* packed, int64_t n, int8_t* codes, cudaStream_t st) {
+  if (n == 0) return;
+  k_unpack4<<<grid_for(n), 256, 0, st>>>(packed, n, codes);
+  LAUNCH_CHECK("k_unpack4");
+}
+
+void repack_device(const int8_t* payload, const QLayout& L, void* dev, cudaStream_t st) {
+  RepackMap mp{L.N, L.N, L.N, 0, 0};
+  k_repack<<<grid_for(L.bytes() / 4), 256, 0, st>>>(payload, L, mp, static_cast<uint32_t*>(dev));
+  LAUNCH_CHECK("k_repack");
+}
+
+void repack_shard_device(const int8_t* payload, int64_t Nfull, const ShardSpec& s, const QLayout& L, void* dev,
+                         cudaStream_t st) {
+  RepackMap mp{Nfull, s.col_block, s.col_per_rank_block, s.col_offset, s.row_offset};
+  k_repack<<<grid_for(L.bytes() / 4), 256, 0, st>>>(payload, L, mp, static_cast<uint32_t*>(dev));
+  LAUNCH_CHECK("k_repack");
+}
+
+void unrepack_device(const void* dev, const QLayout& L, int8_t* payload, cudaStream_t st) {
+  const int64_t n = L.K * L.N;
+  if (n == 0) return;
+  k_unrepack<<<grid_for(L.bits == 4 ? (n + 1) / 2 : n), 256, 0, st>>>(static_cast<const uint8_t*>(dev), L, payload);
+  LAUNCH_CHECK("k_unrepack");
+}
+
+void runtime_scales_device(const double* scales, int64_t nscales, const QLayout& L, int axis,
+                           float* col_scale, float* row_scale, cudaStream_t st) {
+  unsigned long long* key;
+  CUDA_CHECK(cudaMallocAsync(&key, 8, st));
+  CUDA_CHECK(cudaMemsetAsync(key, 0, 8, st));
+  if (axis == GLM_AXIS_ROW) {
+    k_max_key<<<grid_for(nscales), 256, 0, st>>>(scales, nscales, key);
+    LAUNCH_CHECK("k_max_key");
+  }
+  const int64_t n = L.Kp > L.Np ? L.Kp : L.Np;
+  k_runtime_scales<<<grid_for(n), 256, 0, st>>>(scales, L, axis, col_scale, row_scale, key);
+  LAUNCH_CHECK("k_runtime_scales");
+  CUDA_CHECK(cudaFreeAsync(key, st));
+}
+
+__global__ void k_gather_scales(const double* __restrict__ full, ShardSpec sh, int axis, int64_t n,
+                                double* __restrict__ local) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  int64_t f;
+  if (axis == GLM_AXIS_ROW) f = sh.row_offset + i;
+  else f = (i / sh.col_per_rank_block) * sh.col_block + sh.col_offset + (i % sh.col_per_rank_block);
+  local[i] = full[f];
+}
+
+void gather_scales_device(const double* full, const ShardSpec& shard, int axis, int64_t n_local,
+                          double* local, cudaStream_t st) {
+  if (n_local == 0) return;
+  k_gather_scales<<<grid_for(n_local), 256, 0, st>>>(full, shard, axis, n_local, local);
+  LAUNCH_CHECK("k_gather_scales");
+}
+
+// Synthetic generate + quantize of one linear into the local shard's device layout.
+// scales_full receives the FP64 scales of the full matrix's groups.
+void gen_quantize_device(uint64_t seed, uint32_t tensor_id, int64_t K, int64_t N, float s_lo,
+                         float s_hi, int64_t split, int bits, int axis, const ShardSpec& shard,
+                         const QLayout& L, void* dev, double* scales_full, cudaStream_t st) {
+  GenSpec g{seed, tensor_id, K, N, s_lo, s_hi, split};
+  const int64_t groups = axis == GLM_AXIS_ROW ? K : N;
+  unsigned long long* key;
+  CUDA_CHECK(cudaMallocAsync(&key, groups * 8, st));
+  CUDA_CHECK(cudaMemsetAsync(key, 0, groups * 8, st));
+  if (axis == GLM_AXIS_ROW) {
+    k_gen_absmax_rows<<<static_cast<unsigned>(K), 256, 0, st>>>(g, key);
+  } else {
+    const int64_t rpb = 512;
+    dim3 grid(static_cast<unsigned>((N + 255) / 256), static_cast<unsigned>((K + rpb - 1) / rpb));
+    k_gen_absmax_cols<<<grid, 256, 0, st>>>(g, rpb, key);
+  }
+  LAUNCH_CHECK("k_gen_absmax");
+  const double cap = static_cast<double>((1 << (bits - 1)) - 1);
+  k_keys_to_scales<<<grid_for(groups), 256, 0, st>>>(key, groups, cap, scales_full);
+  LAUNCH_CHECK("k_keys_to_scales");
+  ShardMap sm{shard.col_block, shard.col_per_rank_block, shard.col_offset, shard.row_offset};
+  k_gen_codes<<<grid_for(L.bytes() / 4), 256, 0, st>>>(g, sm, L, axis, scales_full, static_cast<uint32_t*>(dev));
+  LAUNCH_CHECK("k_gen_codes");
+  CUDA_CHECK(cudaFreeAsync(key, st));
+}
+
+}  // namespace glm

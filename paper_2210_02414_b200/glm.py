@@ -1,0 +1,380 @@
+"""ctypes binding of include/glm130b.h with the reference's names and error classes.
+
+Mirrors the glmlab operator API (quantize_absmax / quantize_zeropoint / dequantize /
+pack_int4 / unpack_int4, quant.hpp:44-51; GLMConfig + forward, model.hpp:15-91) so the
+parity tests read like the reference's own tests. All compute happens in
+libglm130b.so on the GPU; there is no CPU path here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglm130b.so")
+_LIB = None
+
+AXIS = {"row": 0, "column": 1, "whole": 2}
+SCHEME = {"absmax": 0, "zeropoint": 1}
+DTYPE = {np.dtype(np.float64): 0, np.dtype(np.float32): 1}
+GLM_BF16 = 2
+
+
+class GLMError(RuntimeError):
+    """glmlab::Error (common.hpp:28-36): message carries the "[module] ..." tag."""
+    code = -1
+
+
+class ContractError(GLMError):
+    code = 1
+
+
+class DimensionError(GLMError):
+    code = 2
+
+
+class FormatError(GLMError):
+    code = 3
+
+
+class PolicyError(GLMError):
+    code = 4
+
+
+class CudaError(GLMError):
+    code = 5
+
+
+class NcclError(GLMError):
+    code = 6
+
+
+_ERRORS = {c.code: c for c in (ContractError, DimensionError, FormatError, PolicyError, CudaError, NcclError)}
+
+
+class _Config(C.Structure):
+    _fields_ = [("num_layers", C.c_int), ("hidden", C.c_int), ("num_heads", C.c_int),
+                ("ffn_hidden", C.c_int), ("vocab", C.c_int), ("init_method_std", C.c_double),
+                ("layernorm_eps", C.c_double), ("deepnorm_alpha", C.c_double)]
+
+
+class _Memory(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("element_count", "quant_payload_bytes", "scale_bytes",
+                                         "half_baseline_bytes", "wide_baseline_bytes",
+                                         "device_weight_bytes", "device_head_bytes", "device_kv_bytes")]
+
+
+# name -> (restype, argtypes); every symbol declared in include/glm130b.h
+P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+SIGNATURES = {
+    "glm_last_error": (C.c_char_p, []),
+    "glm_version": (C.c_char_p, []),
+    "glm_group_count": (I64, [I64, I64, I32]),
+    "glm_payload_bytes": (I64, [I64, I64, I32]),
+    "glm_quantize_weight": (I32, [P, I32, I64, I64, I32, I32, I32, P, P, P, P]),
+    "glm_quantize_weight_device": (I32, [P, I32, I64, I64, I32, I32, I32, P, P, P, P, P]),
+    "glm_dequantize": (I32, [P, I64, P, P, I64, I64, I32, I32, I32, P]),
+    "glm_pack_int4": (I32, [P, I64, P]),
+    "glm_unpack_int4": (I32, [P, I64, I64, P]),
+    "glm_qweight_create": (I32, [P, P, I64, I64, I32, I32, C.POINTER(P)]),
+    "glm_qweight_quantize": (I32, [P, I32, I64, I64, I32, I32, C.POINTER(P)]),
+    "glm_qweight_destroy": (I32, [P]),
+    "glm_qweight_export": (I32, [P, P, P]),
+    "glm_qweight_device_bytes": (I64, [P]),
+    "glm_qweight_device_copy": (I32, [P, P]),
+    "glm_qlinear": (I32, [P, P, I64, P, P]),
+    "glm_qlinear_host": (I32, [P, P, I64, P]),
+    "glm_qlinear_bench": (I32, [P, I64, I32, I32, C.POINTER(D)]),
+    "glm_model_create": (I32, [C.POINTER(_Config), I32, I32, I32, I32, I32, I32, I32, C.POINTER(P)]),
+    "glm_model_destroy": (I32, [P]),
+    "glm_tp_unique_id": (I32, [P]),
+    "glm_model_init_comm": (I32, [P, P]),
+    "glm_model_set_embedding": (I32, [P, P]),
+    "glm_model_set_tensor": (I32, [P, I32, I32, P]),
+    "glm_model_init_synthetic": (I32, [P, C.c_uint64]),
+    "glm_model_export_linear": (I32, [P, I32, I32, P, P]),
+    "glm_model_memory": (I32, [P, C.POINTER(_Memory)]),
+    "glm_model_prefill": (I32, [P, I32, P, P, I32, I32, P]),
+    "glm_model_decode_step": (I32, [P, I32, P, P, P, P]),
+    "glm_model_cached_length": (I32, [P, I32]),
+    "glm_model_reset": (I32, [P]),
+    "glm_model_enable_taps": (I32, [P, I32]),
+    "glm_model_get_taps": (I32, [P, P, P]),
+    "glm_model_zero_sublayers": (I32, [P, I32]),
+    "glm_model_bench_decode": (I32, [P, I32, I32, I32, C.POINTER(D), C.POINTER(D), C.POINTER(I32)]),
+}
+
+
+def lib():
+    """Loads libglm130b.so (raises if it was not built: there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()) first; "
+                              "this package has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().glm_last_error().decode()
+        raise _ERRORS.get(rc, GLMError)(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def group_count(rows, cols, axis="row"):
+    return lib().glm_group_count(rows, cols, AXIS[axis])
+
+
+def payload_bytes(rows, cols, bits):
+    return lib().glm_payload_bytes(rows, cols, bits)
+
+
+def _weights(w):
+    w = np.asarray(w)
+    if w.dtype == np.uint16:  # raw bf16 bits
+        return np.ascontiguousarray(w), GLM_BF16
+    if w.dtype not in (np.float64, np.float32):
+        w = w.astype(np.float64)
+    return np.ascontiguousarray(w), DTYPE[w.dtype]
+
+
+def quantize_weight(w, bits, axis="row", scheme="absmax"):
+    """QuantizedMatrix as a dict (quant.hpp:26-42), computed on the GPU."""
+    w, dt = _weights(w)
+    if w.ndim != 2:
+        raise DimensionError("[quantlab] expected a matrix")
+    rows, cols = w.shape
+    g = group_count(rows, cols, axis)
+    pb = payload_bytes(rows, cols, bits) if bits in (4, 8) else 0
+    payload = np.zeros(max(pb, 1), np.int8)
+    scales = np.zeros(max(g, 1), np.float64)
+    zp = np.zeros(max(g, 1), np.float64)
+    cg = np.zeros(max(g, 1), np.uint8)
+    _check(lib().glm_quantize_weight(_p(w), dt, rows, cols, bits, SCHEME[scheme], AXIS[axis], _p(payload),
+                                     _p(scales), _p(zp), _p(cg)))
+    q = dict(bits=bits, scheme=scheme, axis=axis, rows=rows, cols=cols, payload=payload[:pb], scales=scales[:g])
+    if scheme == "zeropoint":
+        q.update(zero_points=zp[:g], constant_group=cg[:g])
+    return q
+
+
+def quantize_absmax(w, bits, axis="row"):
+    return quantize_weight(w, bits, axis, "absmax")
+
+
+def quantize_zeropoint(w, bits, axis="row"):
+    return quantize_weight(w, bits, axis, "zeropoint")
+
+
+def dequantize(q):
+    out = np.empty((q["rows"], q["cols"]), np.float64)
+    payload = np.ascontiguousarray(q["payload"], np.int8)
+    scales = np.ascontiguousarray(q["scales"], np.float64)
+    zp = q.get("zero_points")
+    zp = None if zp is None else np.ascontiguousarray(zp, np.float64)
+    _check(lib().glm_dequantize(_p(payload), len(payload), _p(scales), _p(zp), q["rows"], q["cols"], q["bits"],
+                                SCHEME[q["scheme"]], AXIS[q["axis"]], _p(out)))
+    return out
+
+
+def pack_int4(codes):
+    codes = np.ascontiguousarray(codes, np.int8)
+    out = np.zeros((len(codes) + 1) // 2, np.int8)
+    _check(lib().glm_pack_int4(_p(codes), len(codes), _p(out)))
+    return out
+
+
+def unpack_int4(packed, count):
+    packed = np.ascontiguousarray(packed, np.int8)
+    out = np.zeros(max(count, 0), np.int8)
+    _check(lib().glm_unpack_int4(_p(packed), len(packed), count, _p(out)))
+    return out
+
+
+class QLinear:
+    """Quantized linear y = x . dequantize(q) on the B200 (device layout handle)."""
+
+    def __init__(self, handle, rows, cols, bits, axis):
+        self.h, self.rows, self.cols, self.bits, self.axis = handle, rows, cols, bits, axis
+
+    @classmethod
+    def from_payload(cls, q):
+        h = C.c_void_p()
+        payload = np.ascontiguousarray(q["payload"], np.int8)
+        scales = np.ascontiguousarray(q["scales"], np.float64)
+        _check(lib().glm_qweight_create(_p(payload), _p(scales), q["rows"], q["cols"], q["bits"], AXIS[q["axis"]],
+                                        C.byref(h)))
+        return cls(h, q["rows"], q["cols"], q["bits"], q["axis"])
+
+    @classmethod
+    def quantize(cls, w, bits, axis="row"):
+        w, dt = _weights(w)
+        h = C.c_void_p()
+        _check(lib().glm_qweight_quantize(_p(w), dt, w.shape[0], w.shape[1], bits, AXIS[axis], C.byref(h)))
+        return cls(h, w.shape[0], w.shape[1], bits, axis)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _LIB is not None:
+            _LIB.glm_qweight_destroy(self.h)
+            self.h = None
+
+    def export(self):
+        pb = payload_bytes(self.rows, self.cols, self.bits)
+        payload = np.zeros(pb, np.int8)
+        scales = np.zeros(group_count(self.rows, self.cols, self.axis), np.float64)
+        _check(lib().glm_qweight_export(self.h, _p(payload), _p(scales)))
+        return dict(bits=self.bits, scheme="absmax", axis=self.axis, rows=self.rows, cols=self.cols,
+                    payload=payload, scales=scales)
+
+    def device_bytes(self):
+        n = lib().glm_qweight_device_bytes(self.h)
+        out = np.zeros(n, np.uint8)
+        _check(lib().glm_qweight_device_copy(self.h, _p(out)))
+        return out
+
+    def __call__(self, x):
+        x = np.ascontiguousarray(np.atleast_2d(x), np.float32)
+        y = np.empty((x.shape[0], self.cols), np.float32)
+        _check(lib().glm_qlinear_host(self.h, _p(x), x.shape[0], _p(y)))
+        return y
+
+    def bench(self, M, iters=20, flush=True):
+        us = C.c_double()
+        _check(lib().glm_qlinear_bench(self.h, M, iters, int(flush), C.byref(us)))
+        return us.value
+
+
+@dataclass
+class GLMConfig:
+    """GLMConfig (model.hpp:15-31)."""
+    num_layers: int = 2
+    hidden: int = 64
+    num_heads: int = 4
+    ffn_hidden: int = 0
+    vocab: int = 262
+    init_method_std: float = 0.0052
+    layernorm_eps: float = 1e-5
+    deepnorm_alpha: float = 0.0
+
+    def c(self):
+        return _Config(self.num_layers, self.hidden, self.num_heads, self.ffn_hidden, self.vocab,
+                       self.init_method_std, self.layernorm_eps, self.deepnorm_alpha)
+
+
+def gmask_layout(prefix_len, n_gen):
+    """Positions of a [gMASK] sample (corruption.cpp:266-290): prefix 0..P-1, [gMASK] at P,
+    generation input j at P + max(0, j-1). Returns (positions, context_length)."""
+    P = prefix_len
+    pos = list(range(P)) + [P] + [P + max(0, j - 1) for j in range(n_gen)]
+    return pos, P + 1
+
+
+class Model:
+    """GLM model on the B200: quantized linears, fp32 residual stream, KV cache."""
+
+    QKV, OUT, W1, V, W2, LN1G, LN1B, LN2G, LN2B = range(9)
+
+    def __init__(self, cfg: GLMConfig, bits=8, axis="row", max_batch=1, max_ctx=256, head_bf16=False,
+                 tp_rank=0, tp_size=1):
+        self.cfg = cfg
+        self.bits, self.axis = bits, axis
+        self._c = cfg.c()
+        h = C.c_void_p()
+        _check(lib().glm_model_create(C.byref(self._c), bits, AXIS[axis], max_batch, max_ctx, int(head_bf16),
+                                      tp_rank, tp_size, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _LIB is not None:
+            _LIB.glm_model_destroy(self.h)
+            self.h = None
+
+    # -- weights --
+    def set_embedding(self, e):
+        e = np.ascontiguousarray(e, np.float64)
+        _check(lib().glm_model_set_embedding(self.h, _p(e)))
+
+    def set_tensor(self, layer, which, values):
+        v = np.ascontiguousarray(values, np.float64)
+        _check(lib().glm_model_set_tensor(self.h, layer, which, _p(v)))
+
+    def load_reference_params(self, tensor_fn):
+        """tensor_fn(layer, slot) -> float64 array; slot in QKV..W2 and 'embed'."""
+        self.set_embedding(tensor_fn(0, "embed"))
+        d = self.cfg.hidden
+        for layer in range(self.cfg.num_layers):
+            for which in (self.QKV, self.OUT, self.W1, self.V, self.W2):
+                self.set_tensor(layer, which, tensor_fn(layer, which))
+            for which in (self.LN1G, self.LN2G):
+                self.set_tensor(layer, which, np.ones(d))
+            for which in (self.LN1B, self.LN2B):
+                self.set_tensor(layer, which, np.zeros(d))
+
+    def init_synthetic(self, seed):
+        _check(lib().glm_model_init_synthetic(self.h, seed))
+
+    def export_linear(self, layer, which, rows, cols):
+        payload = np.zeros(payload_bytes(rows, cols, self.bits), np.int8)
+        scales = np.zeros(group_count(rows, cols, self.axis), np.float64)
+        _check(lib().glm_model_export_linear(self.h, layer, which, _p(payload), _p(scales)))
+        return payload, scales
+
+    def memory(self):
+        m = _Memory()
+        _check(lib().glm_model_memory(self.h, C.byref(m)))
+        return {n: getattr(m, n) for n, _ in _Memory._fields_}
+
+    # -- inference --
+    def prefill(self, tokens, positions, context_length=None, seq=0, logits=True):
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        positions = np.ascontiguousarray(positions, np.int32)
+        n = len(tokens)
+        out = np.empty((n, self.cfg.vocab), np.float32) if logits else None
+        _check(lib().glm_model_prefill(self.h, seq, _p(tokens), _p(positions), n,
+                                       n if context_length is None else context_length, _p(out)))
+        return out
+
+    def decode_step(self, tokens, positions, logits=True):
+        tokens = np.ascontiguousarray(np.atleast_1d(tokens), np.int32)
+        positions = np.ascontiguousarray(np.atleast_1d(positions), np.int32)
+        b = len(tokens)
+        nxt = np.empty(b, np.int32)
+        out = np.empty((b, self.cfg.vocab), np.float32) if logits else None
+        _check(lib().glm_model_decode_step(self.h, b, _p(tokens), _p(positions), _p(nxt), _p(out)))
+        return nxt, out
+
+    def cached_length(self, seq=0):
+        return lib().glm_model_cached_length(self.h, seq)
+
+    def reset(self):
+        _check(lib().glm_model_reset(self.h))
+
+    def enable_taps(self, on=True):
+        _check(lib().glm_model_enable_taps(self.h, int(on)))
+
+    def taps(self, rows):
+        a = np.empty((self.cfg.num_layers, rows, self.cfg.hidden), np.float32)
+        f = np.empty_like(a)
+        _check(lib().glm_model_get_taps(self.h, _p(a), _p(f)))
+        return a, f
+
+    def zero_sublayers(self, on=True):
+        _check(lib().glm_model_zero_sublayers(self.h, int(on)))
+
+    def bench_decode(self, batch, steps, warmup=3):
+        ms, gemv, launches = C.c_double(), C.c_double(), C.c_int()
+        _check(lib().glm_model_bench_decode(self.h, batch, steps, warmup, C.byref(ms), C.byref(gemv),
+                                            C.byref(launches)))
+        return ms.value, gemv.value, launches.value

@@ -1,0 +1,74 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every symbol
+include/glm130b.h declares, the ctypes binding covers them, and the header is valid C.
+No compute call runs here (there is no GPU in the build container)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2210_02414_b200 import glm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "glm130b.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:glm_status|int64_t|int|const char\s*\*)\s+(glm_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    assert len(names) >= 30
+    for must in ("glm_quantize_weight", "glm_dequantize", "glm_pack_int4", "glm_unpack_int4", "glm_qlinear",
+                 "glm_model_prefill", "glm_model_decode_step", "glm_model_memory"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(glm.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_covers_every_symbol():
+    assert sorted(glm.SIGNATURES) == declared_functions()
+
+
+def test_header_is_valid_c_and_cpp():
+    for lang, std in (("c", "-std=c99"), ("c++", "-std=c++17")):
+        subprocess.run(["/usr/bin/gcc", "-x", lang, std, "-fsyntax-only", "-Wall", "-Werror", HEADER], check=True)
+
+
+def test_pure_host_entry_points_work_without_gpu():
+    lib = glm.lib()
+    assert lib.glm_group_count(3, 5, 0) == 3 and lib.glm_group_count(3, 5, 1) == 5 and lib.glm_group_count(3, 5, 2) == 1
+    assert lib.glm_payload_bytes(3, 5, 4) == 8 and lib.glm_payload_bytes(3, 5, 8) == 15
+    assert b"sm_100a" in lib.glm_version()
+
+
+def _has_gpu():
+    try:
+        return subprocess.run(["nvidia-smi"], capture_output=True).returncode == 0
+    except FileNotFoundError:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="a GPU is present; the no-GPU failure mode is not observable")
+def test_compute_fails_loudly_without_gpu():
+    with pytest.raises(glm.CudaError):
+        glm.quantize_absmax([[1.0, -2.0, 0.5]], 8)
+    with pytest.raises(glm.CudaError):
+        glm.Model(glm.GLMConfig(num_layers=1, hidden=256, num_heads=4), bits=8)
+
+
+def test_policy_errors_are_raised_before_device_work():
+    with pytest.raises(glm.ContractError):
+        glm.quantize_absmax([[1.0, 2.0]], 5)
+    with pytest.raises(glm.ContractError):
+        glm.Model(glm.GLMConfig(num_layers=0, hidden=256, num_heads=4))
+    with pytest.raises(glm.ContractError):
+        glm.Model(glm.GLMConfig(num_layers=1, hidden=256, num_heads=3))

@@ -1,0 +1,74 @@
+"""Quantized-linear parity: the W4A16/W8A16 GEMV (M <= 16) and its 16-row slabs against
+y = x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155).
+
+Two bars: (1) exact-arithmetic check against a float64 evaluation of the kernel's own
+contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only fp32
+accumulation error remains, <= 2e-6 relative; (2) the reference check against the oracle's
+float64 x . dequantize(q), max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2210_02414_b200 import glm
+
+pytestmark = pytest.mark.gpu
+
+
+def kernel_contract(x, q):
+    """float64 evaluation of what the kernel computes."""
+    K, N = q["rows"], q["cols"]
+    codes = O.codes_of(q).reshape(K, N).astype(np.float64)
+    s = q["scales"]
+    x32 = x.astype(np.float32)
+    if q["axis"] == "row":
+        S = s.max()
+        fold = (s / S).astype(np.float32) if S > 0 else np.zeros(K, np.float32)
+        xh = (x32 * fold[None, :]).astype(np.float16).astype(np.float64)
+        return (xh @ codes) * np.float64(np.float32(S))
+    xh = x32.astype(np.float16).astype(np.float64)
+    cs = (s if q["axis"] == "column" else np.full(N, s[0])).astype(np.float32).astype(np.float64)
+    return (xh @ codes) * cs[None, :]
+
+
+SHAPES = [(64, 16), (512, 1536), (1368, 512), (512, 1368), (200, 90), (4096, 1024)]
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("axis", ["row", "column", "whole"])
+@pytest.mark.parametrize("K,N", SHAPES)
+def test_qlinear_matches_contract_and_oracle(bits, axis, K, N):
+    rng = np.random.default_rng(K * 7 + N + bits)
+    w = rng.normal(0, 0.02, size=(K, N))
+    q = glm.quantize_absmax(w, bits, axis)
+    lin = glm.QLinear.from_payload(q)
+    for M in (1, 3, 8, 9, 16, 37):
+        x = rng.normal(0, 1, size=(M, K))
+        y = lin(x).astype(np.float64)
+        c = kernel_contract(x, q)
+        assert np.abs(y - c).max() <= 2e-6 * np.abs(c).max() + 1e-30, (M, np.abs(y - c).max())
+        ref = x @ O.dequantize(q)
+        assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
+
+
+def test_qlinear_glm130b_k_dimension_with_split_k():
+    # K = 12288 (GLM-130B hidden) exercises ksplit > 1 and long per-warp chunk streams
+    rng = np.random.default_rng(1)
+    K, N = 12288, 512
+    w = rng.normal(0, 5.6e-4, size=(K, N))
+    for bits, axis in ((4, "column"), (8, "row")):
+        q = glm.quantize_absmax(w, bits, axis)
+        lin = glm.QLinear.from_payload(q)
+        x = rng.normal(0, 1, size=(2, K))
+        y = lin(x).astype(np.float64)
+        c = kernel_contract(x, q)
+        assert np.abs(y - c).max() <= 2e-6 * np.abs(c).max()
+
+
+def test_qlinear_quantize_handle_equals_payload_handle():
+    rng = np.random.default_rng(2)
+    w = rng.normal(0, 0.01, size=(256, 128))
+    a = glm.QLinear.quantize(w, 4, "row")
+    b = glm.QLinear.from_payload(glm.quantize_absmax(w, 4, "row"))
+    x = rng.normal(size=(4, 256))
+    assert np.array_equal(a(x), b(x))
+    assert np.array_equal(a.device_bytes(), b.device_bytes())
