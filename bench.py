@@ -1,0 +1,296 @@
+"""Headline benchmark: GLM-130B-shaped INT4 (W4A16) autoregressive decode, batch 1.
+
+A "step" is one greedy decode step of one token through all 70 layers + the tied head
+(BASELINE.json configs[3] at t = N, the only configuration its metric is quoted on).
+Weights are random-init of the GLM-130B shape, generated and quantized on the GPU with the
+counter-based generator, per-output-channel absmax INT4 (north_star).
+
+Timed regions (CUDA events on the model's stream, max over ranks):
+  value  : K graph replays of the decode step, state resident in HBM (63.4 GB/t of INT4
+           weights per step >> 126 MB L2, so no flush is needed)
+  e2e    : K calls of glm_model_decode_step (the public C ABI): pinned H2D of the token +
+           position, graph replay, D2H of the greedy token, host-synchronised
+  roofline: the W4A16 GEMV launches of one step replayed alone, algorithmic bytes
+           (codes + fp32 scales + fp16 activations + fp32 partials) / their event time
+
+`--impl reference` times the reference's CPU path (oracle port of x . dequantize(q), the
+reference's forward() arithmetic, quant.cpp:188-221 + tensor.cpp:135-155) on one GLM-130B
+layer per step with all host threads and extrapolates to 70 layers + head.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+G = dict(num_layers=70, hidden=12288, num_heads=96, ffn_hidden=32768, vocab=150528)
+METRIC = "GLM-130B INT4 decode tokens/s (batch 1)"
+PROMPT = 127  # P = 127 + [gMASK] + [sop]
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.samples, self.reasons, self.maxc = [], set(), None
+        self.index = index
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip().split(", ")
+                self.samples.append(float(out[0]))
+                self.maxc = float(out[1])
+                for n, v in zip(names, out[2:]):
+                    if v.strip() == "Active":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.maxc,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference path) — checker infrastructure, not product
+# ---------------------------------------------------------------------------------------
+def cpu_layer_setup(bits=4, axis="column", seed=1):
+    from oracle import pyoracle as O
+    d, f = G["hidden"], G["ffn_hidden"]
+    L = G["num_layers"]
+    fac = (2.0 * L) ** -0.5
+    xs = lambda a, b: (2.0 / (a + b)) ** 0.5
+    mats = [
+        O.gen_quantize(seed, 0, d, 3 * d, bits, axis, 0.0052, xs(d, d) * fac, 2 * d),
+        O.gen_quantize(seed, 1, d, d, bits, axis, xs(d, d) * fac),
+        O.gen_quantize(seed, 2, d, f, bits, axis, xs(d, f) * fac),
+        O.gen_quantize(seed, 3, d, f, bits, axis, xs(d, f) * fac),
+        O.gen_quantize(seed, 4, f, d, bits, axis, xs(f, d) * fac),
+    ]
+    return mats
+
+
+def cpu_layer_step(mats, x):
+    """One GLM-130B layer for one token: the 5 quantized linears (x . dequantize(q)) in f64."""
+    import numpy as np
+    from oracle import pyoracle as O
+    qkv = O.qlinear_full(x, mats[0])
+    a = O.qlinear_full(qkv[:, :G["hidden"]], mats[1])
+    u = O.qlinear_full(a, mats[2])
+    v = O.qlinear_full(a, mats[3])
+    g = O.gelu(u) * v
+    return O.qlinear_full(g, mats[4]), np.abs(qkv).max()
+
+
+def cpu_baseline(steps, warmup):
+    import numpy as np
+    t0 = time.time()
+    mats = cpu_layer_setup()
+    setup_s = time.time() - t0
+    x = np.random.default_rng(0).normal(size=(1, G["hidden"]))
+    for _ in range(warmup):
+        cpu_layer_step(mats, x)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        cpu_layer_step(mats, x)
+        times.append(time.perf_counter() - t)
+    layer_s = statistics.median(times)
+    d, f, V = G["hidden"], G["ffn_hidden"], G["vocab"]
+    layer_macs = d * 3 * d + d * d + 2 * d * f + f * d
+    head_s = layer_s * (V * d) / layer_macs  # bf16 head GEMV, same per-MAC cost (labelled)
+    token_s = G["num_layers"] * layer_s + head_s
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {
+        "value": 1.0 / token_s, "unit": "tokens/s", "cores": threads, "kind": "port",
+        "sample": (f"one GLM-130B layer decode (5 INT4 per-output-channel linears, x . dequantize(q) in f64, "
+                   f"oracle port of quant.cpp:188-221 + tensor.cpp:135-155) per step, median of {steps} after "
+                   f"{warmup} warm-up; extrapolated x70 layers + head by MACs; {layer_s:.2f} s/layer; "
+                   f"setup {setup_s:.0f} s (gen+quantize one layer)"),
+        "seconds_per_token": token_s,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_token"] * 1000.0,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "GLM-130B INT4 decode, batch 1 (CPU reference path, extrapolated from one layer)",
+                       "model": "GLM-130B-shaped (70L, d 12288, 96 heads, ffn 32768, vocab 150528)",
+                       "global_batch": 1, "seq_len": PROMPT + 2, "parallelism": "cpu"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------------------
+def gemv_bytes_per_step(m_rows, t):
+    """Algorithmic bytes of the W4A16 GEMV launches of one decode step on one rank."""
+    d, f, L = G["hidden"], G["ffn_hidden"], G["num_layers"]
+    shapes = [(d, 3 * d // t), (d // t, d), (d, 2 * f // t), (f // t, d)]  # qkv, out, w1|v fused, w2
+    total = 0
+    for K, N in shapes:
+        total += K * N // 2 + N * 4 + m_rows * K * 2 + m_rows * N * 4
+    return total * L
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_02414_b200 import glm
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch
+    cfg = glm.GLMConfig(**G)
+    max_ctx = PROMPT + 2 + args.warmup + args.steps + args.e2e_steps + 8
+    t0 = time.time()
+    m = glm.Model(cfg, bits=4, axis="column", max_batch=B, max_ctx=max_ctx, head_bf16=True, tp_rank=rank,
+                  tp_size=world)
+    if world > 1:
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            glm._check(glm.lib().glm_tp_unique_id(glm._p(uid)))
+        t = torch.from_numpy(uid).cuda()
+        dist.broadcast(t, 0)
+        uid = t.cpu().numpy()
+        glm._check(glm.lib().glm_model_init_comm(m.h, glm._p(uid)))
+    m.init_synthetic(args.seed)
+    init_s = time.time() - t0
+    rng = np.random.default_rng(1234)
+    prompt = [int(v) for v in rng.integers(6, 150000, size=PROMPT)]
+    positions, C = glm.gmask_layout(PROMPT, 0)
+    for b in range(B):
+        m.prefill(prompt + [2], positions[:C], C, seq=b, logits=False)
+    # e2e through the public API: host buffers, H2D + D2H inside the timed region
+    tok = [3] * B
+    pos = [PROMPT] * B
+    for _ in range(3):
+        nxt, _ = m.decode_step(tok, pos)
+        tok, pos = [int(v) for v in nxt], [p + 1 for p in pos]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        nxt, _ = m.decode_step(tok, pos, logits=False)
+        tok, pos = [int(v) for v in nxt], [p + 1 for p in pos]
+    e2e_s = time.perf_counter() - t
+    if world > 1:
+        e2e_t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_t.item())
+    e2e_tps = B * args.e2e_steps / e2e_s
+    # device-timed K steps (graph replays), clocks sampled during the region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms, gemv_ms, launches = m.bench_decode(B, args.steps, args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        mt = torch.tensor([ms, gemv_ms], device="cuda")
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms, gemv_ms = (float(v) for v in mt.tolist())
+    mem = m.memory()
+    if rank != 0:
+        return
+    pk = peaks()
+    hbm = pk["hbm_gbs"]
+    gb = gemv_bytes_per_step(B, world)
+    achieved = gb / (gemv_ms * 1e-3) / 1e9
+    value = B * 1000.0 / ms
+    weights_per_rank = mem["quant_payload_bytes"] / world
+    roofline_step_ms = weights_per_rank / (hbm * 1e9) * 1e3
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "w4a16 (int4 weights, fp16 activations, fp32 accumulate/residual)", "data": "synthetic",
+        "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode (BASELINE configs[3])",
+                   "model": "GLM-130B shape: 70 layers, hidden 12288, 96 heads, ffn 32768 (GeGLU), vocab 150528, "
+                            "random-init (counter-based, model.cpp:69-104 stds)",
+                   "quantization": "absmax INT4 per output channel (kColumn), bit-exact codes",
+                   "global_batch": B, "seq_len": PROMPT + 2, "context_at_timing": PROMPT + 2 + 3 + args.e2e_steps,
+                   "parallelism": f"tp{world}", "l2": "inputs larger than L2 (63.4 GB weights / rank count)",
+                   "frac_of_weight_roofline": roofline_step_ms / ms},
+        "e2e": {"value": e2e_tps, "unit": "tokens/s", "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": 4 * B,
+                "steps": args.e2e_steps},
+        "gpu_launches": launches * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "kernel": "k_gemv<4,1> (W4A16 GEMV, 280 launches/step)",
+                     "algorithmic_bytes_per_step": gb, "gemv_ms_per_step": gemv_ms,
+                     "gemv_share_of_step": gemv_ms / ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650"},
+        "clocks": clk.summary(),
+        "init_seconds": init_s,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(max(1, min(3, args.steps)), 1)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--seed", type=int, default=2210)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

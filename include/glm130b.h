@@ -93,6 +93,10 @@ glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64
 /* Quantize a [rows, cols] weight (host, dtype F64/F32/BF16) straight into a handle. */
 glm_status glm_qweight_quantize(const void* w, glm_dtype dtype, int64_t rows, int64_t cols,
                                 int bits, glm_axis axis, glm_qweight** out);
+/* A [rows, cols] weight of counter-based synthetic values (DESIGN.md "Synthetic weights":
+ * seed, tensor_id, std sigma) generated and quantized on the GPU (config-5 sweeps). */
+glm_status glm_qweight_synthetic(uint64_t seed, uint32_t tensor_id, int64_t rows, int64_t cols,
+                                 float sigma, int bits, glm_axis axis, glm_qweight** out);
 glm_status glm_qweight_destroy(glm_qweight* q);
 /* Canonical payload + FP64 scales back out of the device layout (host buffers). */
 glm_status glm_qweight_export(const glm_qweight* q, int8_t* payload, double* scales);

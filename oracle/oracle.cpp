@@ -788,6 +788,88 @@ int or_qlinear_cols(const double* x, int64_t M, int64_t K, int64_t N, const int8
   });
 }
 
+int or_gen_quantize(uint64_t seed, uint32_t tensor_id, int64_t K, int64_t N, float sigma_lo, float sigma_hi,
+                    int64_t split_col, int bits, int axis, int8_t* payload, double* scales) {
+  // quantize_absmax (quant.cpp:113-143) over generated values, two passes.
+  return guarded([&] {
+    check_bits(bits);
+    if (axis == OR_AXIS_WHOLE) fail(OR_CONTRACT, "oracle", "streaming quantizer covers row/column");
+    const double cap = static_cast<double>(max_code(bits));
+    auto val = [&](int64_t k, int64_t n) {
+      return bf16_to_double(gen_bf16(seed, tensor_id, static_cast<uint64_t>(k * N + n), n < split_col ? sigma_lo : sigma_hi));
+    };
+    const int64_t groups = axis == OR_AXIS_ROW ? K : N;
+    std::vector<double> amax(static_cast<size_t>(groups), 0.0);
+    if (axis == OR_AXIS_ROW) {
+#pragma omp parallel for schedule(static)
+      for (int64_t k = 0; k < K; ++k) {
+        double m = 0.0;
+        for (int64_t n = 0; n < N; ++n) m = std::max(m, std::fabs(val(k, n)));
+        amax[static_cast<size_t>(k)] = m;
+      }
+    } else {
+#pragma omp parallel
+      {
+        std::vector<double> loc(static_cast<size_t>(N), 0.0);
+#pragma omp for schedule(static)
+        for (int64_t k = 0; k < K; ++k)
+          for (int64_t n = 0; n < N; ++n) loc[static_cast<size_t>(n)] = std::max(loc[static_cast<size_t>(n)], std::fabs(val(k, n)));
+#pragma omp critical
+        for (int64_t n = 0; n < N; ++n) amax[static_cast<size_t>(n)] = std::max(amax[static_cast<size_t>(n)], loc[static_cast<size_t>(n)]);
+      }
+    }
+    for (int64_t g = 0; g < groups; ++g) scales[g] = amax[static_cast<size_t>(g)] / cap;
+    const int64_t nb = bits == 4 ? (K * N + 1) / 2 : K * N;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < nb; ++b) {
+      auto code = [&](int64_t flat) -> int {
+        const int64_t k = flat / N, n = flat % N;
+        const double s = scales[axis == OR_AXIS_ROW ? k : n];
+        return s == 0.0 ? 0 : round_code(val(k, n) / s, bits);
+      };
+      if (bits == 8) {
+        payload[b] = static_cast<int8_t>(code(b));
+      } else {
+        const int c0 = code(2 * b), c1 = (2 * b + 1 < K * N) ? code(2 * b + 1) : 0;
+        payload[b] = static_cast<int8_t>((c0 & 0xF) | ((c1 & 0xF) << 4));
+      }
+    }
+  });
+}
+
+int or_qlinear_full(const double* x, int64_t M, int64_t K, int64_t N, const int8_t* payload,
+                    const double* scales, int bits, int axis, double* y) {
+  // x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155), W[k][n] = s_g * code formed
+  // per element as dequantize does, accumulated k-outer like a row-major GEMM.
+  return guarded([&] {
+    check_bits(bits);
+    const int64_t NB = 2048;
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t nb = 0; nb < N; nb += NB) {
+      const int64_t n1 = std::min(N, nb + NB);
+      std::vector<double> acc(static_cast<size_t>((n1 - nb) * M), 0.0);
+      for (int64_t k = 0; k < K; ++k) {
+        for (int64_t n = nb; n < n1; ++n) {
+          const int64_t flat = k * N + n;
+          int code;
+          if (bits == 8) {
+            code = payload[flat];
+          } else {
+            const uint8_t byte = static_cast<uint8_t>(payload[flat >> 1]);
+            code = (flat & 1) ? (byte >> 4) : (byte & 0x0f);
+            if (code >= 8) code -= 16;
+          }
+          const double s = axis == OR_AXIS_ROW ? scales[k] : axis == OR_AXIS_COLUMN ? scales[n] : scales[0];
+          const double w = s * static_cast<double>(code);
+          for (int64_t m = 0; m < M; ++m) acc[static_cast<size_t>((n - nb) * M + m)] += x[m * K + k] * w;
+        }
+      }
+      for (int64_t n = nb; n < n1; ++n)
+        for (int64_t m = 0; m < M; ++m) y[m * N + n] = acc[static_cast<size_t>((n - nb) * M + m)];
+    }
+  });
+}
+
 uint64_t or_fnv1a64(const uint8_t* data, int64_t n, uint64_t h) {
   for (int64_t i = 0; i < n; ++i) h = (h ^ data[i]) * 1099511628211ull;
   return h;

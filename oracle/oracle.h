@@ -103,6 +103,14 @@ int or_qlinear_cols(const double* x, int64_t M, int64_t K, int64_t N, const int8
                     const double* scales, int bits, int axis, const int64_t* cols, int64_t ncols,
                     double* y);
 
+/* Streaming generate + quantize_absmax of a counter-based [K, N] matrix (never
+ * materialises the doubles): codes/scales identical to or_quantize(or_gen_matrix(...)). */
+int or_gen_quantize(uint64_t seed, uint32_t tensor_id, int64_t K, int64_t N, float sigma_lo, float sigma_hi,
+                    int64_t split_col, int bits, int axis, int8_t* payload, double* scales);
+/* y[M, N] = x[M, K] . dequantize(q) over all columns, k-outer (row-major streaming). */
+int or_qlinear_full(const double* x, int64_t M, int64_t K, int64_t N, const int8_t* payload,
+                    const double* scales, int bits, int axis, double* y);
+
 /* FNV-1a-64 running hash (SURVEY §8c golden hashes) */
 uint64_t or_fnv1a64(const uint8_t* data, int64_t n, uint64_t h);
 

@@ -80,6 +80,8 @@ def lib():
         L.or_philox_bf16.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_float]
         L.or_philox_bf16.restype = C.c_uint16
         L.or_gen_matrix.argtypes = [C.c_uint64, C.c_uint32, i64, i64, C.c_float, C.c_float, i64, p]
+        L.or_gen_quantize.argtypes = [C.c_uint64, C.c_uint32, i64, i64, C.c_float, C.c_float, i64, i32, i32, p, p]
+        L.or_qlinear_full.argtypes = [p, i64, i64, i64, p, p, i32, i32, p]
         L.or_fnv1a64.argtypes = [p, i64, C.c_uint64]
         L.or_fnv1a64.restype = C.c_uint64
         L.or_qlinear_cols.argtypes = [p, i64, i64, i64, p, p, i32, i32, p, i64, p]
@@ -324,3 +326,23 @@ def fnv1a64(data, h=1469598103934665603):
     a = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8) if isinstance(data, (bytes, bytearray))
                              else np.asarray(data).view(np.uint8).ravel())
     return lib().or_fnv1a64(_ptr(a), a.size, h)
+
+
+def gen_quantize(seed, tensor_id, K, N, bits, axis, sigma_lo, sigma_hi=None, split_col=None):
+    """Counter-based weights quantized with quantize_absmax, streamed (no double matrix)."""
+    sigma_hi = sigma_lo if sigma_hi is None else sigma_hi
+    split_col = N if split_col is None else split_col
+    nb = (K * N + 1) // 2 if bits == 4 else K * N
+    payload = np.empty(nb, np.int8)
+    scales = np.empty(K if axis == "row" else N, np.float64)
+    _check(lib().or_gen_quantize(seed, tensor_id, K, N, sigma_lo, sigma_hi, split_col, bits, AXIS[axis],
+                                 _ptr(payload), _ptr(scales)))
+    return dict(bits=bits, scheme="absmax", axis=axis, rows=K, cols=N, payload=payload, scales=scales)
+
+
+def qlinear_full(x, q):
+    x = np.ascontiguousarray(np.atleast_2d(x), np.float64)
+    y = np.empty((x.shape[0], q["cols"]), np.float64)
+    _check(lib().or_qlinear_full(_ptr(x), x.shape[0], q["rows"], q["cols"], _ptr(np.ascontiguousarray(q["payload"])),
+                                 _ptr(np.ascontiguousarray(q["scales"])), q["bits"], AXIS[q["axis"]], _ptr(y)))
+    return y

@@ -213,6 +213,34 @@ glm_status glm_qweight_quantize(const void* w, glm_dtype dtype, int64_t rows, in
   });
 }
 
+glm_status glm_qweight_synthetic(uint64_t seed, uint32_t tensor_id, int64_t rows, int64_t cols, float sigma, int bits,
+                                 glm_axis axis, glm_qweight** out) {
+  return guarded([&] {
+    check_policy(bits, axis);
+    if (axis == GLM_AXIS_WHOLE) fail(GLM_CONTRACT, "qlinear", "synthetic weights use row or column groups");
+    if (rows <= 0 || cols <= 0) fail(GLM_DIMENSION, "qlinear", "empty weight");
+    auto q = std::make_unique<glm_qweight>();
+    q->bits = bits;
+    q->w.L = make_layout(rows, cols, bits);
+    q->w.axis = axis;
+    q->w.nscales = group_count(rows, cols, axis);
+    q->codes.alloc(q->w.L.bytes());
+    q->col_scale.alloc(q->w.L.Np * sizeof(float));
+    q->row_scale.alloc(q->w.L.Kp * sizeof(float));
+    q->scales64.alloc(q->w.nscales * sizeof(double));
+    q->w.codes = q->codes.ptr;
+    q->w.col_scale = q->col_scale.as<float>();
+    q->w.row_scale = q->row_scale.as<float>();
+    q->w.scales64 = q->scales64.as<double>();
+    ShardSpec identity{cols, cols, 0, 0};
+    gen_quantize_device(seed, tensor_id, rows, cols, sigma, sigma, cols, bits, axis, identity, q->w.L, q->w.codes,
+                        q->w.scales64, nullptr);
+    runtime_scales_device(q->w.scales64, q->w.nscales, q->w.L, axis, q->w.col_scale, q->w.row_scale, nullptr);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    *out = q.release();
+  });
+}
+
 glm_status glm_qweight_destroy(glm_qweight* q) {
   return guarded([&] { delete q; });
 }

@@ -25,7 +25,6 @@ namespace {
 
 constexpr int kWarps = 8;       // warps per CTA
 constexpr int kCtasPerSM = 2;   // resident CTAs per SM (128 regs/thread budget)
-constexpr int kUnroll = 4;      // chunks per pipeline stage
 
 __device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
   uint32_t d;
@@ -110,6 +109,7 @@ template <int BITS, int NT>
 __global__ void __launch_bounds__(kWarps * 32, kCtasPerSM) k_gemv(GemvArgs a) {
   constexpr int WV = BITS == 4 ? 1 : 2;              // uint4 weight loads per chunk per lane
   constexpr int CHUNK_U4 = BITS == 4 ? 32 : 64;      // uint4 per chunk block
+  constexpr int kUnroll = BITS == 4 ? 8 : 4;         // chunks per stage: 4 KB per warp in flight
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t nitems = a.nrt * a.ksplit;

@@ -80,6 +80,7 @@ SIGNATURES = {
     "glm_unpack_int4": (I32, [P, I64, I64, P]),
     "glm_qweight_create": (I32, [P, P, I64, I64, I32, I32, C.POINTER(P)]),
     "glm_qweight_quantize": (I32, [P, I32, I64, I64, I32, I32, C.POINTER(P)]),
+    "glm_qweight_synthetic": (I32, [C.c_uint64, C.c_uint32, I64, I64, C.c_float, I32, I32, C.POINTER(P)]),
     "glm_qweight_destroy": (I32, [P]),
     "glm_qweight_export": (I32, [P, P, P]),
     "glm_qweight_device_bytes": (I64, [P]),
@@ -224,6 +225,12 @@ class QLinear:
         h = C.c_void_p()
         _check(lib().glm_qweight_quantize(_p(w), dt, w.shape[0], w.shape[1], bits, AXIS[axis], C.byref(h)))
         return cls(h, w.shape[0], w.shape[1], bits, axis)
+
+    @classmethod
+    def synthetic(cls, seed, tensor_id, rows, cols, sigma, bits, axis="column"):
+        h = C.c_void_p()
+        _check(lib().glm_qweight_synthetic(seed, tensor_id, rows, cols, sigma, bits, AXIS[axis], C.byref(h)))
+        return cls(h, rows, cols, bits, axis)
 
     def __del__(self):
         if getattr(self, "h", None) and _LIB is not None:

@@ -137,7 +137,7 @@ def test_qweight_export_round_trip_and_layout(bits, axis):
         if bits == 4:
             p = r + 4 * hi
             byte = dev[base + lane * 16 + j * 4 + p // 2]
-            got = ((byte >> (4 * (p & 1))) & 0xF) - 8
+            got = ((int(byte) >> (4 * (p & 1))) & 0xF) - 8
         else:
             half, jj, wd, b = j >> 1, j & 1, r >> 1, (r & 1) * 2 + hi
             got = int(dev[base + half * 512 + lane * 16 + jj * 8 + wd * 4 + b]) - 128

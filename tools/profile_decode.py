@@ -1,0 +1,37 @@
+"""Profiling window for ncu: builds the GLM-130B INT4 model, prefills, warms up, then runs
+`--steps` decode steps between cudaProfilerStart/Stop (use ncu --profile-from-start off)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2210_02414_b200 import glm
+import bench
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--layers", type=int, default=70)
+ap.add_argument("--bits", type=int, default=4)
+a = ap.parse_args()
+torch.cuda.set_device(0)
+cfg = dict(bench.G)
+cfg["num_layers"] = a.layers
+m = glm.Model(glm.GLMConfig(**cfg), bits=a.bits, axis="column", max_ctx=256, head_bf16=True)
+m.init_synthetic(2210)
+pos, C = glm.gmask_layout(127, 0)
+m.prefill([7] * 127 + [2], pos[:C], C, logits=False)
+tok, p = [3], [127]
+for _ in range(3):
+    nxt, _ = m.decode_step(tok, p, logits=False)
+    tok, p = [int(nxt[0])], [p[0] + 1]
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+for _ in range(a.steps):
+    nxt, _ = m.decode_step(tok, p, logits=False)
+    tok, p = [int(nxt[0])], [p[0] + 1]
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print("profiled", a.steps, "decode steps")
