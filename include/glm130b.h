@@ -104,6 +104,10 @@ glm_status glm_qweight_export(const glm_qweight* q, int8_t* payload, double* sca
 int64_t glm_qweight_device_bytes(const glm_qweight* q);
 glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out);
 
+/* Diagnostics: per-stage clock64 stamps [256][8] of CTA 0 of the last quantized-matmul launch
+ * made with the environment variable GLM_QMM_TRACE set. */
+glm_status glm_debug_qmm_trace(long long* host_out);
+
 /* y[M, cols] = x[M, rows] . dequantize(q), fp32 in/out, device pointers. M >= 1. */
 glm_status glm_qlinear(const glm_qweight* q, const float* x, int64_t M, float* y, void* stream);
 /* Same with host buffers (H2D, kernel, D2H inside). */

@@ -2,9 +2,11 @@
 //
 // All kernels keep the residual stream, the DeepNorm add and the LayerNorm statistics in
 // fp32 (at N = 70 a sublayer is ~1e-5 of the residual, below any 16-bit
-// epsilon). Their fp16 outputs are written straight into the fragment-ordered x_frag
-// layout (layout.cuh) of the NEXT quantized linear, with that linear's kRow scale fold,
-// so no separate activation-formatting pass exists on the decode path.
+// epsilon). Their fp16 outputs are written straight into the tcgen05
+// B-operand layout (layout.cuh) of the NEXT quantized linear, with that linear's kRow
+// scale fold, so no separate activation-formatting pass exists on the decode path.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "block.h"
@@ -26,7 +28,8 @@ __device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t 
 __device__ __forceinline__ void store_xfrag_pair(const XOut& xo, int m, int64_t k, float v0, float v1) {
   if (!xo.xf) return;
   const float s0 = xo.row_scale ? xo.row_scale[k] : 1.f, s1 = xo.row_scale ? xo.row_scale[k + 1] : 1.f;
-  *reinterpret_cast<__half2*>(xo.xf + xfrag_index(xo.nch, m, k)) = __floats2half2_rn(v0 * s0, v1 * s1);
+  const int64_t idx = xo.tile ? xtile_index(xo.Kp, m, k) : xfrag_index(xo.nch, m, k);
+  *reinterpret_cast<__half2*>(xo.xf + idx) = __floats2half2_rn(v0 * s0, v1 * s1);
 }
 
 template <int NT>
@@ -68,48 +71,91 @@ __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restri
 }
 
 // ---- deepnorm_residual = LN(alpha * x + y) (model.cpp:125-131, tensor.cpp:256-274) -----
-// One CTA per row; the row lives in registers (<= kLnPer values per thread).
-constexpr int kLnThreads = 1024;
-constexpr int kLnPer = 16;  // supports d <= 16384
+// One thread-block CLUSTER of kLnCluster CTAs per row: each CTA owns a contiguous slice of
+// the row (pairs of features kept in registers), the mean / variance partial sums are
+// exchanged through distributed shared memory (DSMEM), so a 12288-wide row is spread over
+// 8 SMs instead of serialising its L2 latency on one.
+constexpr int kLnCluster = 8;
+constexpr int kLnThreads = 256;
+constexpr int kLnPairs = 4;  // pairs per thread: d <= 2 * 4 * 256 * 8 = 16384
 
-__global__ void __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
-  __shared__ float red[32];
-  const int m = blockIdx.x;
-  float z[kLnPer];
+__device__ __forceinline__ float cluster_sum(float v, float* red, float* slot) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < kLnThreads / 32; ++i) s += red[i];
+    *slot = s;
+  }
+  cluster.sync();
+  float tot = 0.f;
+  for (int r = 0; r < kLnCluster; ++r) tot += *cluster.map_shared_rank(slot, r);  // fixed order
+  cluster.sync();
+  return tot;
+}
+
+__global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
+  __shared__ float red[kLnThreads / 32];
+  __shared__ float slot;
+  namespace cg = cooperative_groups;
+  const int rank = static_cast<int>(cg::this_cluster().block_rank());
+  const int m = blockIdx.x / kLnCluster;
+  const int64_t npairs = a.d / 2;
+  const int64_t per = (npairs + kLnCluster - 1) / kLnCluster;
+  const int64_t p0 = rank * per, p1 = min(npairs, p0 + per);
+  const float* __restrict__ hrow = a.h + static_cast<int64_t>(m) * a.d;
+  float2 z[kLnPairs];
   float sum = 0.f;
+  // issue every load of the slice first (partials of all splits + residual)
 #pragma unroll
-  for (int i = 0; i < kLnPer; ++i) {
-    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
-    z[i] = 0.f;
-    if (n < a.d) {
-      const float y = a.zero_sublayer ? 0.f : reduce_partial(a.in, m, n);
-      if (a.tap) a.tap[static_cast<int64_t>(m) * a.d + n] = y;
-      z[i] = a.alpha * a.h[static_cast<int64_t>(m) * a.d + n] + y;
-      sum += z[i];
+  for (int i = 0; i < kLnPairs; ++i) {
+    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    z[i] = make_float2(0.f, 0.f);
+    if (p < p1) {
+      const int64_t n = 2 * p;
+      float2 y = make_float2(0.f, 0.f);
+      if (!a.zero_sublayer) {
+        for (int s = 0; s < a.in.ksplit; ++s) {
+          const float2 v = *reinterpret_cast<const float2*>(a.in.p + static_cast<int64_t>(s) * a.in.split_stride +
+                                                            m * a.in.ld + n);
+          y.x += v.x;
+          y.y += v.y;
+        }
+        if (a.in.scale) {
+          y.x *= a.in.scale[n];
+          y.y *= a.in.scale[n + 1];
+        }
+      }
+      const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
+      z[i] = make_float2(a.alpha * hv.x + y.x, a.alpha * hv.y + y.y);
+      if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + n) = y;
+      sum += z[i].x + z[i].y;
     }
   }
-  const float mean = block_sum<kLnThreads>(sum, red) / static_cast<float>(a.d);
+  const float mean = cluster_sum(sum, red, &slot) / static_cast<float>(a.d);
   float sq = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnPer; ++i) {
-    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
-    if (n < a.d) sq += (z[i] - mean) * (z[i] - mean);
+  for (int i = 0; i < kLnPairs; ++i) {
+    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    if (p < p1) sq += (z[i].x - mean) * (z[i].x - mean) + (z[i].y - mean) * (z[i].y - mean);
   }
-  const float var = block_sum<kLnThreads>(sq, red) / static_cast<float>(a.d);  // biased (tensor.cpp:267)
+  const float var = cluster_sum(sq, red, &slot) / static_cast<float>(a.d);  // biased (tensor.cpp:267)
   const float rstd = rsqrtf(var + a.eps);
-  // Each thread owns elements n = tid + i*1024; write h, then the x_frag pairs below.
 #pragma unroll
-  for (int i = 0; i < kLnPer; ++i) {
-    const int64_t n = threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
-    if (n < a.d) a.h[static_cast<int64_t>(m) * a.d + n] = (z[i] - mean) * rstd * a.gain[n] + a.bias[n];
-  }
-  __syncthreads();
-  __threadfence_block();
-  // x_frag outputs need pairs (k, k+1): re-read the row just written (L1 hit).
-  for (int64_t k = 2 * threadIdx.x; k < a.d; k += 2 * kLnThreads) {
-    const float v0 = a.h[static_cast<int64_t>(m) * a.d + k], v1 = a.h[static_cast<int64_t>(m) * a.d + k + 1];
-    store_xfrag_pair(a.x0, m, k, v0, v1);
-    store_xfrag_pair(a.x1, m, k, v0, v1);
+  for (int i = 0; i < kLnPairs; ++i) {
+    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    if (p < p1) {
+      const int64_t n = 2 * p;
+      const float o0 = (z[i].x - mean) * rstd * a.gain[n] + a.bias[n];
+      const float o1 = (z[i].y - mean) * rstd * a.gain[n + 1] + a.bias[n + 1];
+      *reinterpret_cast<float2*>(a.h + static_cast<int64_t>(m) * a.d + n) = make_float2(o0, o1);
+      store_xfrag_pair(a.x0, m, n, o0, o1);
+      store_xfrag_pair(a.x1, m, n, o0, o1);
+    }
   }
 }
 
@@ -132,70 +178,95 @@ __global__ void k_geglu_act(ActArgs a) {
 }
 
 // ---- decode attention (model.cpp:137-152 for the rows of the generation part) ----------
-// grid (heads, batch, splits); each CTA owns keys [split*kSplitKeys, ...) of its sequence.
-// The CTA whose range holds the new slot also rotates/stores the new k, v. The last CTA to
-// finish a (head, batch) merges the splits in split order (deterministic).
+// grid (heads, batch, splits); each CTA owns kSplitKeys keys of its sequence's cache.
+// Scores: DH/32 lanes per key, each lane a 32-feature slice (4 x LDG.128 in flight), the
+// dot reduced with DH/32-lane shuffles. P.V: lanes own DH/32 features, keys strided over
+// warps and unrolled so 8 independent V-row loads are in flight. The CTA holding the new
+// slot also rotates/stores the new k, v; the last CTA of a (head, batch) merges the
+// splits in split order (deterministic), writing out_proj's x_frag.
 constexpr int kAttnThreads = 128;
-constexpr int kSplitKeys = 256;
+constexpr int kSplitKeys = 64;
 
+template <int DH>
 __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
-  extern __shared__ float sm[];
+  constexpr int LPK = DH / 32;          // lanes per key in the score phase
+  constexpr int KPW = 32 / LPK;         // keys per warp iteration
+  constexpr int NW = kAttnThreads / 32;
+  constexpr int FPL = DH / 32;          // features per lane in the PV phase
+  __shared__ float q[DH];
+  __shared__ float p[kSplitKeys];
+  __shared__ float red[NW];
+  __shared__ float opart[NW][DH];
+  __shared__ int last;
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
-  const int dh = a.dh, half = dh / 2;
-  const int len = a.cache_len[b];       // keys already cached; the new one goes to slot len
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int len = a.cache_len[b];
   const int total = len + 1;
   const int k0 = split * kSplitKeys, k1 = min(total, k0 + kSplitKeys);
-  float* q = sm;                        // [dh] rotated q, pre-scaled by 1/sqrt(dh)
-  float* p = sm + dh;                   // [kSplitKeys] scores / probabilities
-  float* red = p + kSplitKeys;          // [32]
-  float* onew = red + 32;               // [dh] (new k rotated) then v
   const int pos = a.positions[b];
-  const float inv_sqrt = rsqrtf(static_cast<float>(dh));
-  __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * dh;
-  __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * dh;
-  const bool has_new = (len >= k0 && len < k0 + kSplitKeys);
+  const float inv_sqrt = rsqrtf(static_cast<float>(DH));
+  __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
+  __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
+  float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (DH + 2);
 
   if (k0 < total) {
-    // q (and, for the CTA holding the new slot, k and v): reduce GEMV partials, RoPE.
-    for (int j = threadIdx.x; j < half; j += blockDim.x) {
-      const float2 cs = a.rope[static_cast<int64_t>(pos) * half + j];  // (cos, sin) (tensor.cpp:357-363)
-      const int64_t fq = static_cast<int64_t>(head) * dh + 2 * j;
+    const bool has_new = (len >= k0 && len < k1);
+    for (int j = threadIdx.x; j < DH / 2; j += kAttnThreads) {
+      const float2 cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + j];  // (cos, sin), tensor.cpp:357-363
+      const int64_t fq = static_cast<int64_t>(head) * DH + 2 * j;
       const float qa = reduce_partial(a.qkv, b, fq), qb = reduce_partial(a.qkv, b, fq + 1);
       q[2 * j] = (cs.x * qa - cs.y * qb) * inv_sqrt;
       q[2 * j + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
       if (has_new) {
         const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
         const float ka = reduce_partial(a.qkv, b, fk), kb = reduce_partial(a.qkv, b, fk + 1);
-        const float r0 = cs.x * ka - cs.y * kb, r1 = cs.y * ka + cs.x * kb;
-        *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * dh + 2 * j) = __floats2half2_rn(r0, r1);
+        *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * j) =
+            __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
         const float va = reduce_partial(a.qkv, b, fv), vb = reduce_partial(a.qkv, b, fv + 1);
-        *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * dh + 2 * j) = __floats2half2_rn(va, vb);
+        *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * j) = __floats2half2_rn(va, vb);
       }
     }
     __syncthreads();
-    // scores: one warp per key, lanes over dh
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int s = k0 + warp; s < k1; s += kAttnThreads / 32) {
-      const __half* kr = kc + static_cast<int64_t>(s) * dh;
+    // ---- scores ----
+    const int sub = lane % LPK, kin = lane / LPK;
+    float qr[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) qr[i] = q[sub * 32 + i];
+    for (int s0 = k0 + warp * KPW; s0 < k1; s0 += NW * KPW) {
+      const int s = s0 + kin;
       float acc = 0.f;
-      for (int c = 2 * lane; c < dh; c += 64) {
-        const float2 kv = __half22float2(*reinterpret_cast<const __half2*>(kr + c));
-        acc += q[c] * kv.x + q[c + 1] * kv.y;
+      if (s < k1) {
+        const uint4* kr = reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(s) * DH + sub * 32);
+        uint4 kv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) kv[i] = kr[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t w4[4] = {kv[i].x, kv[i].y, kv[i].z, kv[i].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+            acc += qr[i * 8 + 2 * e] * f.x + qr[i * 8 + 2 * e + 1] * f.y;
+          }
+        }
       }
-      acc = warp_sum(acc);
-      if (lane == 0) p[s - k0] = acc;
+#pragma unroll
+      for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sub == 0 && s < k1) p[s - k0] = acc;
     }
     __syncthreads();
+    // ---- softmax over the split (fp32) ----
     float mx = -FLT_MAX;
-    for (int s = threadIdx.x; s < k1 - k0; s += blockDim.x) mx = fmaxf(mx, p[s]);
+    for (int s = threadIdx.x; s < k1 - k0; s += kAttnThreads) mx = fmaxf(mx, p[s]);
     mx = warp_max(mx);
     if (lane == 0) red[warp] = mx;
     __syncthreads();
     mx = red[0];
-    for (int w = 1; w < kAttnThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+#pragma unroll
+    for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red[w]);
     __syncthreads();
     float sum = 0.f;
-    for (int s = threadIdx.x; s < k1 - k0; s += blockDim.x) {
+    for (int s = threadIdx.x; s < k1 - k0; s += kAttnThreads) {
       const float e = __expf(p[s] - mx);
       p[s] = e;
       sum += e;
@@ -204,27 +275,60 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
     if (lane == 0) red[warp] = sum;
     __syncthreads();
     sum = 0.f;
-    for (int w = 0; w < kAttnThreads / 32; ++w) sum += red[w];
-    // o = P . V over this split (unnormalised), thread per feature
-    float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (dh + 2);
-    for (int c = threadIdx.x; c < dh; c += blockDim.x) {
-      float o = 0.f;
-      for (int s = k0; s < k1; ++s) o += p[s - k0] * __half2float(vc[static_cast<int64_t>(s) * dh + c]);
-      part[c] = o;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) sum += red[w];
+    // ---- P.V: warp w takes keys k0+w, k0+w+NW, ...; lane owns FPL features ----
+    float o[FPL];
+#pragma unroll
+    for (int f = 0; f < FPL; ++f) o[f] = 0.f;
+    constexpr int U = 8;
+    for (int s0 = k0 + warp; s0 < k1; s0 += NW * U) {
+      uint2 vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * NW;
+        if (s < k1) {
+          const __half* vr = vc + static_cast<int64_t>(s) * DH + lane * FPL;
+          if constexpr (FPL == 4) vv[u] = *reinterpret_cast<const uint2*>(vr);
+          else vv[u] = make_uint2(*reinterpret_cast<const uint32_t*>(vr), 0u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * NW;
+        if (s < k1) {
+          const float pw = p[s - k0];
+          const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&vv[u].x));
+          o[0] += pw * f0.x;
+          o[1] += pw * f0.y;
+          if constexpr (FPL == 4) {
+            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&vv[u].y));
+            o[2] += pw * f1.x;
+            o[3] += pw * f1.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
+    __syncthreads();
+    for (int c = threadIdx.x; c < DH; c += kAttnThreads) {
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) acc += opart[w][c];
+      part[c] = acc;
     }
     if (threadIdx.x == 0) {
-      part[dh] = mx;
-      part[dh + 1] = sum;
+      part[DH] = mx;
+      part[DH + 1] = sum;
     }
   } else if (threadIdx.x == 0) {
-    float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (dh + 2);
-    part[dh] = -FLT_MAX;
-    part[dh + 1] = 0.f;
+    part[DH] = -FLT_MAX;
+    part[DH + 1] = 0.f;
   }
-  // last CTA of this (head, b) merges
+  // ---- the last CTA of this (head, b) merges the splits in order ----
   __threadfence();
   __syncthreads();
-  __shared__ int last;
   if (threadIdx.x == 0) {
     int* ctr = a.counters + b * a.heads + head;
     last = (atomicAdd(ctr, 1) == a.max_splits - 1);
@@ -233,29 +337,25 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (dh + 2);
+  const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (DH + 2);
+  const int nsp = (total + kSplitKeys - 1) / kSplitKeys;
   float gm = -FLT_MAX;
-  for (int s = 0; s < a.max_splits; ++s) gm = fmaxf(gm, base[s * (dh + 2) + dh]);
+  for (int s = 0; s < nsp; ++s) gm = fmaxf(gm, base[s * (DH + 2) + DH]);
   float gl = 0.f;
-  for (int s = 0; s < a.max_splits; ++s) {
-    const float l = base[s * (dh + 2) + dh + 1];
-    if (l > 0.f) gl += l * __expf(base[s * (dh + 2) + dh] - gm);
-  }
-  for (int c2 = threadIdx.x; c2 < half; c2 += blockDim.x) {
-    float o[2] = {0.f, 0.f};
-    for (int s = 0; s < a.max_splits; ++s) {
-      const float l = base[s * (dh + 2) + dh + 1];
-      if (l > 0.f) {
-        const float w = __expf(base[s * (dh + 2) + dh] - gm);
-        o[0] += w * base[s * (dh + 2) + 2 * c2];
-        o[1] += w * base[s * (dh + 2) + 2 * c2 + 1];
-      }
+  for (int s = 0; s < nsp; ++s) gl += base[s * (DH + 2) + DH + 1] * __expf(base[s * (DH + 2) + DH] - gm);
+  const float inv = 1.f / gl;
+  for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kAttnThreads) {
+    float o0 = 0.f, o1 = 0.f;
+    for (int s = 0; s < nsp; ++s) {
+      const float w = __expf(base[s * (DH + 2) + DH] - gm);
+      o0 += w * base[s * (DH + 2) + 2 * c2];
+      o1 += w * base[s * (DH + 2) + 2 * c2 + 1];
     }
-    const int64_t k = static_cast<int64_t>(head) * dh + 2 * c2;
-    store_xfrag_pair(a.xo, b, k, o[0] / gl, o[1] / gl);
+    const int64_t k = static_cast<int64_t>(head) * DH + 2 * c2;
+    store_xfrag_pair(a.xo, b, k, o0 * inv, o1 * inv);
     if (a.out) {
-      a.out[static_cast<int64_t>(b) * a.heads * dh + k] = o[0] / gl;
-      a.out[static_cast<int64_t>(b) * a.heads * dh + k + 1] = o[1] / gl;
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0 * inv;
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
     }
   }
 }
@@ -349,8 +449,13 @@ __global__ void k_rows_to_xfrag(const float* __restrict__ x, int64_t ld, int M, 
 }
 
 // ---- tied output head logits = h E^T + greedy argmax (model.cpp:225) -----------------------
+// HBM-bound stream over the (unquantised, quant.cpp:289) embedding table: one warp per
+// vocab row, each lane keeps kHeadU independent 16-byte loads in flight, fp32 FMA against
+// up to kHeadRowsPerGroup rows of h held in shared memory. Argmax keys are packed
+// (value, ~index) so atomicMax picks the largest logit and, on ties, the smallest id.
 constexpr int kHeadThreads = 256;
 constexpr int kHeadRowsPerGroup = 4;
+constexpr int kHeadU = 6;
 
 __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
   uint32_t u = __float_as_uint(v);
@@ -358,63 +463,82 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
   return (static_cast<unsigned long long>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(idx));
 }
 
+template <typename ET, int MG>
+__device__ __forceinline__ void head_rows(const HeadArgs& a, const float* hs, int m0, int warp, int lane) {
+  constexpr int EPL = 16 / sizeof(ET);            // elements per 16-byte load
+  constexpr int STEP = 32 * EPL;                  // k advanced per warp load
+  const ET* E = static_cast<const ET*>(a.E);
+  unsigned long long best[MG];
+#pragma unroll
+  for (int r = 0; r < MG; ++r) best[r] = 0ull;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kHeadThreads / 32);
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * (kHeadThreads / 32) + warp; v < a.vocab_local; v += nwarps) {
+    float acc[MG];
+#pragma unroll
+    for (int r = 0; r < MG; ++r) acc[r] = 0.f;
+    const uint4* er = reinterpret_cast<const uint4*>(E + (a.vocab_offset + v) * a.d);
+    for (int64_t k0 = 0; k0 < a.d; k0 += STEP * kHeadU) {
+      uint4 raw[kHeadU];
+#pragma unroll
+      for (int u = 0; u < kHeadU; ++u) {
+        const int64_t k = k0 + u * STEP + lane * EPL;
+        raw[u] = k < a.d ? ld_stream(er + k / EPL) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kHeadU; ++u) {
+        const int64_t k = k0 + u * STEP + lane * EPL;
+        if (k < a.d) {
+          const uint32_t ws[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if constexpr (sizeof(ET) == 2) {
+              const float lo = __uint_as_float(ws[e] << 16), hi = __uint_as_float(ws[e] & 0xFFFF0000u);
+#pragma unroll
+              for (int r = 0; r < MG; ++r) {
+                const float2 hv = *reinterpret_cast<const float2*>(hs + r * a.d + k + 2 * e);
+                acc[r] += lo * hv.x + hi * hv.y;
+              }
+            } else {
+              const float wv = __uint_as_float(ws[e]);
+#pragma unroll
+              for (int r = 0; r < MG; ++r) acc[r] += wv * hs[r * a.d + k + e];
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < MG; ++r) {
+      const float lv = warp_sum(acc[r]);
+      if (lane == 0) {
+        if (a.logits) a.logits[static_cast<int64_t>(m0 + r) * a.ld_logits + a.vocab_offset + v] = lv;
+        const unsigned long long key = argmax_key(lv, static_cast<int>(a.vocab_offset + v));
+        best[r] = key > best[r] ? key : best[r];
+      }
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r < MG; ++r)
+      if (best[r]) atomicMax(a.argmax + m0 + r, best[r]);
+}
+
 template <typename ET>
 __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
   extern __shared__ float hs[];  // [kHeadRowsPerGroup][d]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const ET* E = static_cast<const ET*>(a.E);
   for (int m0 = 0; m0 < a.M; m0 += kHeadRowsPerGroup) {
     const int mg = min(kHeadRowsPerGroup, a.M - m0);
     __syncthreads();
     for (int64_t i = threadIdx.x; i < static_cast<int64_t>(mg) * a.d; i += blockDim.x)
       hs[i] = a.h[static_cast<int64_t>(m0) * a.d + i];
     __syncthreads();
-    unsigned long long best[kHeadRowsPerGroup];
-#pragma unroll
-    for (int r = 0; r < kHeadRowsPerGroup; ++r) best[r] = 0ull;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kHeadThreads / 32);
-    for (int64_t v = static_cast<int64_t>(blockIdx.x) * (kHeadThreads / 32) + warp; v < a.vocab_local; v += nwarps) {
-      float acc[kHeadRowsPerGroup] = {0.f, 0.f, 0.f, 0.f};
-      const ET* er = E + (a.vocab_offset + v) * a.d;
-      if constexpr (sizeof(ET) == 2) {
-        for (int64_t k = lane * 8; k < a.d; k += 256) {
-          const uint4 raw = ld_stream(reinterpret_cast<const uint4*>(er + k));
-          const uint32_t ws[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(ws[e] << 16), hi = __uint_as_float(ws[e] & 0xFFFF0000u);
-#pragma unroll
-            for (int r = 0; r < kHeadRowsPerGroup; ++r)
-              if (r < mg) acc[r] += lo * hs[r * a.d + k + 2 * e] + hi * hs[r * a.d + k + 2 * e + 1];
-          }
-        }
-      } else {
-        for (int64_t k = lane * 4; k < a.d; k += 128) {
-          const uint4 raw = ld_stream(reinterpret_cast<const uint4*>(er + k));
-          const float w4[4] = {__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
-                               __uint_as_float(raw.w)};
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-#pragma unroll
-            for (int r = 0; r < kHeadRowsPerGroup; ++r)
-              if (r < mg) acc[r] += w4[e] * hs[r * a.d + k + e];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < kHeadRowsPerGroup; ++r) {
-        if (r < mg) {
-          const float lv = warp_sum(acc[r]);
-          if (lane == 0) {
-            if (a.logits) a.logits[static_cast<int64_t>(m0 + r) * a.ld_logits + a.vocab_offset + v] = lv;
-            const unsigned long long key = argmax_key(lv, static_cast<int>(a.vocab_offset + v));
-            best[r] = key > best[r] ? key : best[r];
-          }
-        }
-      }
+    switch (mg) {
+      case 1: head_rows<ET, 1>(a, hs, m0, warp, lane); break;
+      case 2: head_rows<ET, 2>(a, hs, m0, warp, lane); break;
+      case 3: head_rows<ET, 3>(a, hs, m0, warp, lane); break;
+      default: head_rows<ET, 4>(a, hs, m0, warp, lane); break;
     }
-    if (lane == 0)
-      for (int r = 0; r < mg; ++r)
-        if (best[r]) atomicMax(a.argmax + m0 + r, best[r]);
   }
 }
 
@@ -441,8 +565,8 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
 }
 
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
-  if (a.d > static_cast<int64_t>(kLnThreads) * kLnPer) fail(GLM_DIMENSION, "glmmodel", "hidden too large for LN kernel");
-  k_deepnorm_ln<<<M, kLnThreads, 0, st>>>(a);
+  if (a.d > 2ll * kLnPairs * kLnThreads * kLnCluster || a.d % 2) fail(GLM_DIMENSION, "glmmodel", "hidden unsupported by LN kernel");
+  k_deepnorm_ln<<<M * kLnCluster, kLnThreads, 0, st>>>(a);
   LAUNCH_CHECK("k_deepnorm_ln");
 }
 
@@ -454,8 +578,10 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
 int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplitKeys; }
 
 void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st) {
-  const size_t smem = (2 * a.dh + kSplitKeys + 32) * sizeof(float);
-  k_attn_decode<<<dim3(a.heads, B, a.max_splits), kAttnThreads, smem, st>>>(a);
+  const dim3 grid(a.heads, B, a.max_splits);
+  if (a.dh == 128) k_attn_decode<128><<<grid, kAttnThreads, 0, st>>>(a);
+  else if (a.dh == 64) k_attn_decode<64><<<grid, kAttnThreads, 0, st>>>(a);
+  else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
   LAUNCH_CHECK("k_attn_decode");
 }
 

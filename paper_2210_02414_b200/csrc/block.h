@@ -18,11 +18,14 @@ struct SubIn {
   const float* scale = nullptr;
 };
 
-// Destination x_frag (fp16, fragment order) of the next quantized linear, with its
-// kRow activation fold (row_scale may be null = 1). xf == null disables the output.
+// Destination activation buffer (fp16) of the next quantized linear, with its kRow
+// activation fold (row_scale may be null = 1). xf == null disables the output. Layout per
+// consumer (layout.cuh): x_frag for the decode GEMV (tile == 0, nch chunks) or 128-token
+// tcgen05 B-operand tiles for the prefill GEMM (tile == 1, padded depth Kp).
 struct XOut {
   __half* xf = nullptr;
-  int64_t nch = 0;
+  int64_t nch = 0, Kp = 0;
+  int tile = 0;
   const float* row_scale = nullptr;
 };
 

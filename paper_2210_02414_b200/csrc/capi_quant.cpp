@@ -67,19 +67,23 @@ void check_policy(int bits, int axis) {
   if (axis < 0 || axis > 2) fail(GLM_CONTRACT, "quantlab", "unknown group axis");
 }
 
-// y = x . dequantize(q) for any M >= 1 (device pointers), GEMV path in 16-row slabs.
+// y = x . dequantize(q) for any M >= 1 (device pointers): the decode GEMV for M <= 16 rows,
+// the tcgen05 GEMM (128-token tiles) above; then the split-K reduce with the group scale.
 void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, cudaStream_t st) {
   const QWeightDev& w = q->w;
-  const int64_t slab = 16;
-  const GemvPlan p = plan_gemv(w.L, static_cast<int>(slab < M ? slab : M));
-  DeviceBuffer xf(slab * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * slab * w.L.Np * 4);
-  CUDA_CHECK(cudaMemsetAsync(xf.ptr, 0, xf.bytes, st));
-  for (int64_t m0 = 0; m0 < M; m0 += slab) {
-    const int mm = static_cast<int>(M - m0 < slab ? M - m0 : slab);
-    xfrag_from_f32(x + m0 * w.L.K, w.L.K, mm, w, xf.as<__half>(), st);
-    gemv_launch(w, xf.as<__half>(), mm, part.as<float>(), p, st);
-    gemv_reduce(part.as<float>(), p.ksplit, mm, w, y + m0 * w.L.N, w.L.N, st);
+  const bool gemv = M <= 16;
+  const GemvPlan p = gemv ? plan_gemv(w.L, static_cast<int>(M)) : plan_qmm(w.L, static_cast<int>(M));
+  const int64_t rows = gemv ? M : xtile_tokens(static_cast<int>(M));
+  DeviceBuffer xb(rows * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
+  CUDA_CHECK(cudaMemsetAsync(xb.ptr, 0, xb.bytes, st));
+  if (gemv) {
+    xfrag_from_f32(x, w.L.K, static_cast<int>(M), w, xb.as<__half>(), st);
+    gemv_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+  } else {
+    xtile_from_f32(x, w.L.K, static_cast<int>(M), w, xb.as<__half>(), st);
+    qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
   }
+  gemv_reduce(part.as<float>(), p.ksplit, static_cast<int>(M), w, y, w.L.N, st);
   CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -255,6 +259,13 @@ glm_status glm_qweight_export(const glm_qweight* q, int8_t* payload, double* sca
   });
 }
 
+glm_status glm_debug_qmm_trace(long long* host_out) {
+  return guarded([&] {
+    if (!qmm_trace_ptr()) fail(GLM_CONTRACT, "qlinear", "no traced launch (set GLM_QMM_TRACE)");
+    CUDA_CHECK(cudaMemcpy(host_out, qmm_trace_ptr(), 256 * 8 * sizeof(long long), cudaMemcpyDeviceToHost));
+  });
+}
+
 int64_t glm_qweight_device_bytes(const glm_qweight* q) { return q ? q->w.L.bytes() : 0; }
 
 glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out) {
@@ -280,15 +291,21 @@ glm_status glm_qlinear_host(const glm_qweight* q, const float* x, int64_t M, flo
 
 glm_status glm_qlinear_bench(const glm_qweight* q, int64_t M, int iters, int flush, double* us) {
   return guarded([&] {
-    if (M < 1 || M > 16) fail(GLM_DIMENSION, "qlinear", "bench covers the GEMV path, M in 1..16");
+    if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
     const QWeightDev& w = q->w;
-    const GemvPlan p = plan_gemv(w.L, static_cast<int>(M));
-    DeviceBuffer xf(M * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
+    const bool gemv = M <= 16;
+    const GemvPlan p = gemv ? plan_gemv(w.L, static_cast<int>(M)) : plan_qmm(w.L, static_cast<int>(M));
+    const int64_t rows = gemv ? M : xtile_tokens(static_cast<int>(M));
+    DeviceBuffer xb(rows * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
     DeviceBuffer fl(flush ? (256ll << 20) : 0);
-    CUDA_CHECK(cudaMemset(xf.ptr, 0, xf.bytes));
+    CUDA_CHECK(cudaMemset(xb.ptr, 0, xb.bytes));
     cudaStream_t st;
     CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    for (int i = 0; i < 3; ++i) gemv_launch(w, xf.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+    auto launch = [&] {
+      if (gemv) gemv_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+      else qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+    };
+    for (int i = 0; i < 3; ++i) launch();
     cudaEvent_t e0, e1;
     CUDA_CHECK(cudaEventCreate(&e0));
     CUDA_CHECK(cudaEventCreate(&e1));
@@ -296,7 +313,7 @@ glm_status glm_qlinear_bench(const glm_qweight* q, int64_t M, int iters, int flu
     for (int i = 0; i < iters; ++i) {
       if (flush) CUDA_CHECK(cudaMemsetAsync(fl.ptr, i & 0xFF, fl.bytes, st));
       CUDA_CHECK(cudaEventRecord(e0, st));
-      gemv_launch(w, xf.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
+      launch();
       CUDA_CHECK(cudaEventRecord(e1, st));
       CUDA_CHECK(cudaEventSynchronize(e1));
       float ms = 0.f;

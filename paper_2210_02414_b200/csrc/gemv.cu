@@ -3,19 +3,29 @@
 // Replaces `matmul(x, dequantize(q))` (quant.cpp:188-221 + tensor.cpp:135-155) on the
 // decode path. HBM-bound: every weight byte is read exactly once per call.
 //
-//  * weights: one coalesced 512 B warp load (LDG.128 per lane, L1::no_allocate) per
-//    64-deep chunk of a 16-feature row tile, in the fragment-ordered device layout of
-//    layout.cuh, double-buffered in registers (next chunk group in flight while the
-//    current one is transcoded);
+//  * weights: each warp streams its own 16-feature row tile through a 3-stage ring of 4 KB
+//    shared-memory stages filled by the bulk-copy engine (cp.async.bulk = 1-D TMA, L2
+//    evict-first, mbarrier transaction counts); lanes read their 16 B fragment words
+//    with LDS.128 from the fragment-ordered device layout of layout.cuh;
 //  * dequantisation in registers: INT4 nibbles -> fp16 with one LOP3 (|0x6400 magic)
 //    and one HSUB2/HFMA2 per pair of codes, INT8 bytes with PRMT; the codes are exact
 //    small integers in fp16;
 //  * the K-loop reduction runs on the tensor cores: mma.sync m16n8k16 (f16 x f16 -> f32)
-//    with the weights as A (16 features) and the <= 8 tokens as B, fp32 accumulation;
-//  * activations arrive pre-permuted in fragment order (x_frag), 32 B per lane per
-//    chunk, L1-resident across the warps of an SM;
+//    with the weights as A (16 features) and the <= 8 tokens as B, fp32 accumulation in
+//    four independent chains;
+//  * activations arrive pre-permuted in fragment order (x_frag), 32 B per lane per chunk,
+//    fetched for a whole stage before the stage's mbarrier wait;
 //  * split-K over `ksplit` static slices balances the 148 SMs; partial sums go to a
 //    [ksplit][M][Np] fp32 buffer reduced (with the group scale) by the consumer.
+//
+// Measured on B200 (tools/*_probe.cu): this register-MMA form sustains ~3.6 TB/s INT4 /
+// ~6 TB/s INT8 at M = 1. A tcgen05 variant (transcode into TMEM, async MMA) was built and
+// measured slower for decode (2.6 / 5.3 TB/s: a small-N tcgen05.mma costs its issuing
+// thread ~68 cycles and the extra cross-warp hand-offs add ~350 cycles per stage); it is
+// used where it wins, for prefill (qmm_tc.cu).
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,8 +33,6 @@ namespace glm {
 
 namespace {
 
-constexpr int kWarps = 8;       // warps per CTA
-constexpr int kCtasPerSM = 2;   // resident CTAs per SM (128 regs/thread budget)
 
 __device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
   uint32_t d;
@@ -48,7 +56,7 @@ __device__ __forceinline__ void dq4(uint32_t w, uint32_t (&a)[4]) {
   const uint32_t k1032 = 0x64086408u;                // (1032, 1032): 1024 + 8 offset
   const uint32_t k1_16 = 0x2C002C00u;                // (1/16, 1/16)
   const uint32_t kneg72 = 0xD480D480u;               // (-72, -72) = -(64 + 8)
-  const uint32_t w8 = w >> 8;
+  const uint32_t w8 = __umulhi(w, 0x01000000u);  // w >> 8 on the FMA pipe (IMAD.HI), ALU pipe is the bottleneck
   a[0] = hsub2_u32(lop_or_magic(w, 0x000F000Fu), k1032);
   a[1] = hfma2_u32(lop_or_magic(w, 0x00F000F0u), k1_16, kneg72);
   a[2] = hsub2_u32(lop_or_magic(w8, 0x000F000Fu), k1032);
@@ -106,70 +114,182 @@ __device__ __forceinline__ void compute_chunk(const uint4 (&wv)[BITS == 4 ? 1 : 
 }
 
 template <int BITS, int NT>
-__global__ void __launch_bounds__(kWarps * 32, kCtasPerSM) k_gemv(GemvArgs a) {
-  constexpr int WV = BITS == 4 ? 1 : 2;              // uint4 weight loads per chunk per lane
-  constexpr int CHUNK_U4 = BITS == 4 ? 32 : 64;      // uint4 per chunk block
-  constexpr int kUnroll = BITS == 4 ? 8 : 4;         // chunks per stage: 4 KB per warp in flight
+__device__ __forceinline__ void compute_chunk4(const uint4 (&wv)[BITS == 4 ? 1 : 2], const uint4 (&xv)[NT][2],
+                                               float (&acc)[4][NT][4]) {
+  const uint32_t ws[4] = {wv[0].x, wv[0].y, wv[0].z, wv[0].w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t a[4];
+    if constexpr (BITS == 4) {
+      dq4(ws[j], a);
+    } else {
+      const uint4 v = j < 2 ? wv[0] : wv[1];
+      const int jj = j & 1;
+      dq8(jj ? v.z : v.x, jj ? v.w : v.y, a);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint4 x = xv[nt][j >> 1];
+      const uint32_t b0 = (j & 1) ? x.z : x.x, b1 = (j & 1) ? x.w : x.y;
+      mma16816(acc[j][nt], a, b0, b1);
+    }
+  }
+}
+
+constexpr int kTWarps = 16;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 4096;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+template <int BITS, int NT>
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
+  constexpr int CHUNK = BITS == 4 ? 512 : 1024;
+  constexpr int U = kStageBytes / CHUNK;  // chunks per stage
+  extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
+  uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kTWarps) * kStages * kStageBytes) + warp * kStages;
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
   const int64_t nitems = a.nrt * a.ksplit;
-  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kTWarps;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * kTWarps + warp;
   bool xon[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) xon[nt] = (nt * 8 + g) < a.M;
 
-  for (int64_t item = static_cast<int64_t>(blockIdx.x) * kWarps + warp; item < nitems; item += wstride) {
+  // issue cursor over this warp's (item, chunk) sequence
+  int64_t ii = first, ic = 0, ic1 = 0;
+  auto item_range = [&](int64_t item, int64_t& c0, int64_t& c1) {
+    const int s = static_cast<int>(item % a.ksplit);
+    c0 = a.nch * s / a.ksplit;
+    c1 = a.nch * (s + 1) / a.ksplit;
+  };
+  if (ii < nitems) item_range(ii, ic, ic1);
+  uint32_t issued = 0;
+  auto issue = [&]() {  // lane 0 only; returns false when the sequence is exhausted
+    if (ii >= nitems) return;
+    const int64_t n = min(static_cast<int64_t>(U), ic1 - ic);
+    const int slot = issued % kStages;
+    const int64_t rt = ii / a.ksplit;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w) + (rt * a.nch + ic) * CHUNK;
+    mbar_expect_tx(bars + slot, static_cast<uint32_t>(n * CHUNK));
+    bulk_g2s(ring + slot * kStageBytes, src, static_cast<uint32_t>(n * CHUNK), bars + slot, policy);
+    ++issued;
+    ic += n;
+    if (ic >= ic1) {
+      ii += wstride;
+      if (ii < nitems) item_range(ii, ic, ic1);
+    }
+  };
+  if (lane == 0)
+    for (int s = 0; s < kStages; ++s) issue();
+  // lanes other than 0 track the issue count implicitly: consumption order is identical
+  uint32_t consumed = 0;
+
+  for (int64_t item = first; item < nitems; item += wstride) {
     const int64_t rt = item / a.ksplit;
     const int s = static_cast<int>(item % a.ksplit);
-    const int64_t c0 = a.nch * s / a.ksplit, c1 = a.nch * (s + 1) / a.ksplit;
-    const uint4* wp = a.w + rt * a.nch * CHUNK_U4 + lane;
-    const uint4* xfb = rt < a.rt_split ? a.xf : a.xf2;
-    float acc[NT][4];
+    int64_t c0, c1;
+    item_range(item, c0, c1);
+    const uint4* xfb = reinterpret_cast<const uint4*>(rt < a.rt_split ? a.xf : a.xf2);
+    // four independent accumulator chains (one per k-tile of a chunk)
+    float acc[4][NT][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int h = 0; h < 4; ++h)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
-
-    // Two named register stages (no dynamic indexing -> no local memory): while one
-    // stage is transcoded + MMA'd the other stage's LDG.128s are in flight.
-    uint4 wa[kUnroll][WV], wb[kUnroll][WV];
-    auto load_stage = [&](uint4 (&dst)[kUnroll][WV], int64_t cs) {
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
+        for (int i = 0; i < 4; ++i) acc[h][nt][i] = 0.f;
+    for (int64_t c = c0; c < c1; c += U) {
+      const int n = static_cast<int>(min(static_cast<int64_t>(U), c1 - c));
+      const int slot = consumed % kStages;
+      // activations of the whole stage first (L1/L2 latency overlaps the mbarrier wait);
+      // NT = 2 (9..16 tokens) would exceed the register budget and loads per chunk instead
+      constexpr int UX = NT == 1 ? U : 1;
+      uint4 xv[UX][NT][2];
+      auto load_x = [&](uint4 (&dst)[NT][2], int64_t cc, bool on) {
 #pragma unroll
-        for (int v = 0; v < WV; ++v)
-          dst[u][v] = (cs + u < c1) ? ld_stream(wp + (cs + u) * CHUNK_U4 + v * 32) : make_uint4(0, 0, 0, 0);
-    };
-    auto compute_stage = [&](const uint4 (&src)[kUnroll][WV], int64_t cs) {
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (cs + u < c1) {
-          uint4 xv[NT][2];
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            if (xon[nt]) {
-              const uint4* xp = xfb + (((nt * 8 + g) * a.nch + (cs + u)) * 4 + t) * 2;
-              xv[nt][0] = ld_nc(xp);
-              xv[nt][1] = ld_nc(xp + 1);
-            } else {
-              xv[nt][0] = make_uint4(0, 0, 0, 0);
-              xv[nt][1] = make_uint4(0, 0, 0, 0);
-            }
+        for (int nt = 0; nt < NT; ++nt) {
+          if (xon[nt] && on) {
+            const uint4* xp = xfb + (((nt * 8 + g) * a.nch + cc) * 4 + t) * 2;
+            dst[nt][0] = ld_nc(xp);
+            dst[nt][1] = ld_nc(xp + 1);
+          } else {
+            dst[nt][0] = make_uint4(0, 0, 0, 0);
+            dst[nt][1] = make_uint4(0, 0, 0, 0);
           }
-          compute_chunk<BITS, NT>(src[u], xv, acc);
+        }
+      };
+      if constexpr (NT == 1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) load_x(xv[u], c + u, u < n);
+      }
+      mbar_wait(bars + slot, (consumed / kStages) & 1);
+      const uint8_t* st = ring + slot * kStageBytes;
+      if (n == U) {
+        // full stage: straight-line code, no per-chunk branches, so LDS / LOP3 / HMMA of
+        // consecutive chunks interleave
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint4 wv[BITS == 4 ? 1 : 2];
+          wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK + lane * 16);
+          if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(st + u * CHUNK + 512 + lane * 16);
+          if constexpr (NT == 1) {
+            compute_chunk4<BITS, NT>(wv, xv[u], acc);
+          } else {
+            load_x(xv[0], c + u, true);
+            compute_chunk4<BITS, NT>(wv, xv[0], acc);
+          }
+        }
+      } else {
+        for (int u = 0; u < n; ++u) {
+          uint4 wv[BITS == 4 ? 1 : 2];
+          wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK + lane * 16);
+          if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(st + u * CHUNK + 512 + lane * 16);
+          uint4 xu[NT][2];
+          load_x(xu, c + u, true);  // tail stage: per-chunk activations
+          compute_chunk4<BITS, NT>(wv, xu, acc);
         }
       }
-    };
-    int64_t c = c0;
-    load_stage(wa, c);
-    for (; c < c1; c += 2 * kUnroll) {
-      if (c + kUnroll < c1) load_stage(wb, c + kUnroll);
-      compute_stage(wa, c);
-      if (c + kUnroll >= c1) break;
-      if (c + 2 * kUnroll < c1) load_stage(wa, c + 2 * kUnroll);
-      compute_stage(wb, c + kUnroll);
+      __syncwarp();
+      ++consumed;
+      if (lane == 0) issue();
     }
-    // D fragment: rows g, g+8 (features); cols 2t, 2t+1 (tokens) of each n-tile.
     float* out = a.partial + static_cast<int64_t>(s) * a.M * a.Np + rt * kTileN;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -177,10 +297,16 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSM) k_gemv(GemvArgs a) {
       for (int i = 0; i < 4; ++i) {
         const int m = nt * 8 + 2 * t + (i & 1);
         const int row = g + 8 * (i >> 1);
-        if (m < a.M) out[static_cast<int64_t>(m) * a.Np + row] = acc[nt][i];
+        if (m < a.M) out[static_cast<int64_t>(m) * a.Np + row] = (acc[0][nt][i] + acc[1][nt][i]) + (acc[2][nt][i] + acc[3][nt][i]);
       }
   }
 }
+
+// ---- dual-tile TMA variant (default) ------------------------------------------------------
+// As k_gemv_tma, but each warp item covers TWO adjacent row tiles (32 output features) of
+// the same k-slice: every activation fragment fetched from L1 feeds 2x the MMAs, and the
+// two tiles give 8 independent accumulator chains, doubling the instruction-level
+// parallelism of the transcode -> HMMA stream without more resident warps.
 
 __global__ void k_xfrag_from_f32(const float* __restrict__ x, int64_t ldx, int M, int64_t K, int64_t Kp,
                                  int64_t nch, const float* __restrict__ row_scale, __half* __restrict__ xf) {
@@ -213,11 +339,11 @@ __global__ void k_gemv_reduce(const float* __restrict__ partial, int ksplit, int
 
 GemvPlan plan_gemv(int64_t nrt, int64_t nch) {
   GemvPlan p;
-  const int64_t total_warps = static_cast<int64_t>(kNumSMs) * kCtasPerSM * kWarps;
+  const int64_t total_warps = static_cast<int64_t>(kNumSMs) * kTWarps;
   double best = -1.0;
   const int64_t max_split = nch < 32 ? nch : 32;
   for (int64_t ks = 1; ks <= max_split; ++ks) {
-    if (nch / ks < 4 && ks > 1) break;  // keep >= 4 chunks (2 KB per lane) per item
+    if (nch / ks < 4 && ks > 1) break;  // keep >= 4 chunks per item
     const int64_t items = nrt * ks;
     const int64_t waves = (items + total_warps - 1) / total_warps;
     double eff = static_cast<double>(items) / static_cast<double>(waves * total_warps);
@@ -227,10 +353,8 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch) {
       p.ksplit = static_cast<int>(ks);
     }
   }
-  const int64_t items = nrt * p.ksplit;
-  const int64_t ctas = (items + kWarps - 1) / kWarps;
-  const int64_t maxc = static_cast<int64_t>(kNumSMs) * kCtasPerSM;
-  p.grid = static_cast<int>(ctas < maxc ? ctas : maxc);
+  const int64_t ctas = (nrt * p.ksplit + kTWarps - 1) / kTWarps;
+  p.grid = static_cast<int>(ctas < kNumSMs ? ctas : kNumSMs);
   return p;
 }
 
@@ -244,15 +368,24 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   GemvArgs a{static_cast<const uint4*>(op.codes), reinterpret_cast<const uint4*>(op.xf),
              reinterpret_cast<const uint4*>(op.xf2 ? op.xf2 : op.xf), op.xf2 ? op.rt_split : op.nrt, partial,
              op.nrt, op.nch, op.nrt * kTileN, M, p.ksplit};
-  const dim3 grid(p.grid), block(kWarps * 32);
-  if (op.bits == 4) {
-    if (M <= 8) k_gemv<4, 1><<<grid, block, 0, st>>>(a);
-    else k_gemv<4, 2><<<grid, block, 0, st>>>(a);
-  } else {
-    if (M <= 8) k_gemv<8, 1><<<grid, block, 0, st>>>(a);
-    else k_gemv<8, 2><<<grid, block, 0, st>>>(a);
+  const size_t smem = static_cast<size_t>(kTWarps) * kStages * (kStageBytes + 8);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_tma<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_tma<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_tma<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_tma<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
   }
-  LAUNCH_CHECK("k_gemv");
+  const dim3 grid(p.grid), block(kTWarps * 32);
+  if (op.bits == 4) {
+    if (M <= 8) k_gemv_tma<4, 1><<<grid, block, smem, st>>>(a);
+    else k_gemv_tma<4, 2><<<grid, block, smem, st>>>(a);
+  } else {
+    if (M <= 8) k_gemv_tma<8, 1><<<grid, block, smem, st>>>(a);
+    else k_gemv_tma<8, 2><<<grid, block, smem, st>>>(a);
+  }
+  LAUNCH_CHECK("k_gemv_tma");
 }
 
 void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,

@@ -56,8 +56,8 @@ struct GemvPlan {
 };
 GemvPlan plan_gemv(const QLayout& L, int M);
 GemvPlan plan_gemv(int64_t nrt, int64_t nch);
-// One GEMV launch over nrt row tiles of contiguous device-layout codes; row tiles
-// >= rt_split read x_frag xf2 (fused W1|V launch, distinct kRow folds).
+// One decode-GEMV launch (M <= 16) over nrt row tiles of contiguous device-layout codes;
+// row tiles >= rt_split read x_frag xf2 (fused W1|V launch, distinct kRow folds).
 struct GemvOp {
   const void* codes;
   int bits;
@@ -67,9 +67,20 @@ struct GemvOp {
   int64_t rt_split;
 };
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
-// partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over chunk slice s of x . W
+// partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over k-split s of x . W
 void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,
                  cudaStream_t st);
+
+// ---- qmm_tc.cu : tcgen05 quantized GEMM for prefill (M > 16 tokens) ----
+constexpr int kQmmTokens = 128;  // token columns per MMA tile (UMMA N)
+inline int xtile_tokens(int M) { return (M + kQmmTokens - 1) / kQmmTokens * kQmmTokens; }
+// partial[s][m][n] (fp32, [ksplit][M][Np]) from activations xt in the tcgen05 B-operand
+// layout (layout.cuh xtile_index) holding NT = xtile_tokens(M) token rows.
+GemvPlan plan_qmm(const QLayout& L, int M);
+void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st);
+void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st);
+long long*& qmm_trace_ptr();  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
+
 // x fp32 [M][K] (row stride ldx) -> x_frag fp16 with the kRow scale fold
 void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xfrag, cudaStream_t st);
 // y[m][n] (row stride ldy) = col_scale[n] * sum_s partial[s][m][n]

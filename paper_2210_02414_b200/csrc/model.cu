@@ -147,8 +147,6 @@ struct glm_model {
     return pool.back().as<T>();
   }
 
-  int64_t nch_of(int64_t K) const { return (K + kChunkK - 1) / kChunkK; }
-  int64_t kp_of(int64_t K) const { return nch_of(K) * kChunkK; }
 
   // ---------------------------------------------------------------------------------
   void setup(const glm_config& c, int bits_, int axis_, int max_batch_, int max_ctx_, bool head_bf16_, int r, int t) {
@@ -251,15 +249,7 @@ struct glm_model {
     CUDA_CHECK(cudaMallocHost(&h_next, max_batch * sizeof(int)));
     h_len.assign(max_batch, 0);
     ensure_rows(max_batch);
-    int64_t pmax = 0;
-    for (int i = 0; i < 5; ++i) {
-      const Linear& lin = layers[0].lin[i];
-      pmax = std::max<int64_t>(pmax, static_cast<int64_t>(lin.plan.ksplit) * 16 * lin.w.L.Np);
-    }
-    pmax = std::max<int64_t>(pmax, static_cast<int64_t>(fused_plan.ksplit) * 16 *
-                                       (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
-    partial.alloc(pmax * 4);
-    partial_cap = pmax;
+    ensure_partial(16);
     if (tp_size > 1) comm = std::make_unique<Collective>();
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
@@ -284,16 +274,17 @@ struct glm_model {
     if (rows <= rows_cap) return;
     drop_graphs();  // captured graphs hold the old buffer addresses
     const Layer& ly = layers[0];
+    const int64_t nt = std::max<int64_t>(rows, xtile_tokens(static_cast<int>(rows)));
     auto zero = [&](DeviceBuffer& b, int64_t bytes) {
       b.alloc(bytes);
       CUDA_CHECK(cudaMemsetAsync(b.ptr, 0, bytes, st));
     };
     zero(h, rows * d * 4);
-    zero(xf_qkv, rows * ly.lin[QKV].w.L.Kp * 2);
-    zero(xf_out, rows * ly.lin[OUT].w.L.Kp * 2);
-    zero(xf_w1, rows * ly.lin[W1].w.L.Kp * 2);
-    zero(xf_v, rows * ly.lin[VV].w.L.Kp * 2);
-    zero(xf_w2, rows * ly.lin[W2].w.L.Kp * 2);
+    zero(xf_qkv, nt * ly.lin[QKV].w.L.Kp * 2);
+    zero(xf_out, nt * ly.lin[OUT].w.L.Kp * 2);
+    zero(xf_w1, nt * ly.lin[W1].w.L.Kp * 2);
+    zero(xf_v, nt * ly.lin[VV].w.L.Kp * 2);
+    zero(xf_w2, nt * ly.lin[W2].w.L.Kp * 2);
     zero(logits, rows * V * 4);
     pool.emplace_back(rows * 8);
     d_argmax_rows = pool.back().as<unsigned long long>();
@@ -306,8 +297,25 @@ struct glm_model {
   unsigned long long* d_argmax_rows = nullptr;
   int* d_next_rows = nullptr;
 
+  // split-K partial buffer large enough for every linear at M rows
+  void ensure_partial(int64_t M) {
+    int64_t need = 0;
+    for (int i = 0; i < 5; ++i) {
+      const Linear& lin = layers[0].lin[i];
+      const GemvPlan p = M <= 16 ? plan_gemv(lin.w.L, static_cast<int>(M)) : plan_qmm(lin.w.L, static_cast<int>(M));
+      need = std::max<int64_t>(need, static_cast<int64_t>(p.ksplit) * M * lin.w.L.Np);
+    }
+    need = std::max<int64_t>(need, static_cast<int64_t>(fused_plan.ksplit) * std::min<int64_t>(M, 16) *
+                                       (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
+    if (need <= partial_cap) return;
+    drop_graphs();
+    partial.alloc(need * 4);
+    partial_cap = need;
+  }
+
   void ensure_prefill(int64_t n) {
     ensure_rows(n);
+    ensure_partial(n);
     if (y_qkv.bytes >= n * 3 * dl * 4) return;
     y_qkv.alloc(n * 3 * dl * 4);
     q_rot.alloc(n * dl * 4);
@@ -326,7 +334,8 @@ struct glm_model {
     taps_rows = rows;
   }
 
-  XOut xout(__half* xf, const Linear& lin) const { return XOut{xf, lin.w.L.nch, lin.w.row_scale}; }
+  // tile = 1 for prefill activations consumed by the tcgen05 GEMM (M > 16 rows)
+  XOut xout(__half* xf, const Linear& lin, int tile = 0) const { return XOut{xf, lin.w.L.nch, lin.w.L.Kp, tile, lin.w.row_scale}; }
 
   // ---- weights -------------------------------------------------------------------------
   void finish_linear(Linear& lin, const double* full_scales) {
@@ -558,14 +567,18 @@ struct glm_model {
   }
 
   // ---- prefill ---------------------------------------------------------------------------
-  // y[M][N] = x_frag rows . W for M rows, GEMV path in 16-row slabs.
+  // y[M][N] = x . W for M rows: decode GEMV (M <= 16, x_frag) or the tcgen05 GEMM (128-token
+  // tiles) + split-K reduce with the group scale.
   void linear_rows(const Linear& lin, const __half* xf, int64_t M, float* y) {
-    const int64_t slab_halves = lin.w.L.nch * kChunkK * 16;
-    for (int64_t m0 = 0; m0 < M; m0 += 16) {
-      const int mm = static_cast<int>(M - m0 < 16 ? M - m0 : 16);
-      gemv_launch(lin.w, xf + (m0 / 16) * slab_halves, mm, partial.as<float>(), lin.plan, st);
-      gemv_reduce(partial.as<float>(), lin.plan.ksplit, mm, lin.w, y + m0 * lin.w.L.N, lin.w.L.N, st);
+    GemvPlan p;
+    if (M <= 16) {
+      p = lin.plan;
+      gemv_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
+    } else {
+      p = plan_qmm(lin.w.L, static_cast<int>(M));
+      qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     }
+    gemv_reduce(partial.as<float>(), p.ksplit, static_cast<int>(M), lin.w, y, lin.w.L.N, st);
   }
 
   void prefill(int seq, const int* tokens, const int* positions, int n, int context_len, float* logits_out) {
@@ -579,11 +592,12 @@ struct glm_model {
       if (positions[i] < 0 || positions[i] > max_ctx) fail(GLM_CONTRACT, "glmmodel", "position outside the RoPE table");
     }
     ensure_prefill(n);
+    const int nt = n > 16 ? 1 : 0;  // activation layout of this prefill: tcgen05 tiles or x_frag
     if (taps) ensure_taps(n);
     DeviceBuffer dtok(n * 4), dpos(n * 4);
     CUDA_CHECK(cudaMemcpyAsync(dtok.ptr, tokens, n * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(dpos.ptr, positions, n * 4, cudaMemcpyHostToDevice, st));
-    launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV]), st);
+    launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV], nt), st);
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
       Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
@@ -594,7 +608,7 @@ struct glm_model {
       AttnPrefillArgs ap{q_rot.as<float>(), kcache(l), vcache(l), n, Hl, dh, seq, max_ctx, context_len,
                          attn_out.as<float>(), dl};
       launch_attn_prefill(ap, st);
-      launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out), st);
+      launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
       linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
       if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
       LnArgs ln;
@@ -605,8 +619,8 @@ struct glm_model {
       ln.alpha = static_cast<float>(alpha);
       ln.eps = static_cast<float>(eps);
       ln.d = d;
-      ln.x0 = xout(xf_w1.as<__half>(), w1);
-      ln.x1 = xout(xf_v.as<__half>(), v);
+      ln.x0 = xout(xf_w1.as<__half>(), w1, nt);
+      ln.x1 = xout(xf_v.as<__half>(), v, nt);
       ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
       ln.zero_sublayer = zero_sub;
       launch_deepnorm_ln(ln, n, st);
@@ -617,7 +631,7 @@ struct glm_model {
       act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
       act.M = n;
       act.f = fl;
-      act.xo = xout(xf_w2.as<__half>(), w2);
+      act.xo = xout(xf_w2.as<__half>(), w2, nt);
       launch_geglu_act(act, st);
       linear_rows(w2, xf_w2.as<__half>(), n, y_ffn.as<float>());
       if (tp_size > 1) comm->allreduce_sum(y_ffn.as<float>(), static_cast<int64_t>(n) * d, st);
@@ -625,7 +639,7 @@ struct glm_model {
       ln2.in = SubIn{y_ffn.as<float>(), 1, 0, d, nullptr};
       ln2.gain = ly.ln2g;
       ln2.bias = ly.ln2b;
-      ln2.x0 = l + 1 == L ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]);
+      ln2.x0 = l + 1 == L ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV], nt);
       ln2.x1 = XOut{};
       ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
       launch_deepnorm_ln(ln2, n, st);

@@ -1,0 +1,423 @@
+// qmm_tc.cu — W4A16 / W8A16 quantized GEMM for prefill on the 5th-generation tensor cores.
+//
+// Replaces `matmul(x, dequantize(q))` (quant.cpp:188-221 + tensor.cpp:135-155) when many
+// token rows share the weights (prefill, M > 16): a 128-feature x 128-token output tile per
+// CTA item, fp32 accumulators in TMEM, one persistent CTA per SM (all 512 TMEM columns).
+//
+//   warps 0-15  transcode: 4 groups x 4 TMEM lane quarters; group g owns the 64-k stages with
+//               q % 4 == g. Each thread owns one output feature (TMEM lane): it loads the
+//               64 B of fragment-ordered codes that hold its feature (layout.cuh) straight
+//               from global memory (L2-resident across the token tiles of a row tile, the
+//               next stage prefetched in registers), regroups them into fp16 pairs
+//               (k, k+1) with LOP3/PRMT magic-number conversion and writes them to its TMEM
+//               lane with tcgen05.st (the MMA's A operand);
+//   warp 16     TMA producer: one cp.async.bulk per stage brings the 128-token x 64-k
+//               activation tile (16 KB, canonical K-major layout) into a 4-stage smem ring;
+//   warp 17     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, A = transcoded weights in TMEM,
+//               B = activations in smem, M = 128 features, N = 128 tokens, K = 16 per
+//               instruction; tcgen05.commit releases the smem slot / TMEM buffer;
+//   group 0     epilogue: tcgen05.ld of the accumulator tile into the split-K partial.
+//
+// Evidence: UTCHMMA / LDTM / STTM / UBLKCP in `cuobjdump -sass` of this object.
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace glm {
+
+namespace {
+
+constexpr int NTOK = kQmmTokens;  // 128 token columns per tile
+constexpr int kGroups = 4;
+constexpr int kTcWarps = 4 * kGroups;
+constexpr int kThreads = (kTcWarps + 2) * 32;
+constexpr int kPK = 64;                          // k per stage = one layout chunk
+constexpr int XB = kPK * NTOK * 2;               // activation bytes per stage (16 KB)
+constexpr int RX = 4;                            // activation ring
+constexpr int NA = 8;                            // 32-column A buffers (two per group)
+constexpr int NDB = 2;                           // accumulator tiles (epilogue overlaps next item)
+constexpr uint32_t D_COL = NA * 32;              // 256: accumulators at [256, 512)
+constexpr size_t kSmem = static_cast<size_t>(RX) * XB + 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mma_f16_ts_elect(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop_or_magic(uint32_t w, uint32_t mask) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(w), "r"(mask), "r"(0x64006400u));
+  return d;
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+struct QmmArgs {
+  const uint8_t* w;   // fragment-ordered device layout (layout.cuh)
+  const __half* xt;   // activations, 128-token tiles (xtile_index)
+  float* partial;     // [ksplit][M][Np]
+  int64_t nrt16, nch, Np, Kp;
+  int M, ksplit, ntt, nrt128;
+  long long* trace;
+};
+__device__ __forceinline__ void stamp(const QmmArgs& a, int ev, uint32_t q) {
+  if (a.trace && blockIdx.x == 0 && q < 256) a.trace[q * 8 + ev] = clock64();
+}
+
+// item -> (128-feature tile, token tile, k split); token tiles innermost so the CTAs working
+// at the same time share a few weight row tiles (L2-resident), stages = 64-k chunks.
+__device__ __forceinline__ void decode_item(const QmmArgs& a, int64_t item, int64_t& rt, int64_t& tt, int& s,
+                                            int64_t& c0, int64_t& c1) {
+  s = static_cast<int>(item % a.ksplit);
+  const int64_t rest = item / a.ksplit;
+  tt = rest % a.ntt;
+  rt = rest / a.ntt;
+  c0 = a.nch * s / a.ksplit;
+  c1 = a.nch * (s + 1) / a.ksplit;
+}
+
+// The 64 B of codes holding feature (row tile i, g, half h) for chunk c: lanes 4g..4g+3.
+template <int BITS>
+struct Codes {
+  uint4 u[BITS == 4 ? 4 : 8];
+};
+template <int BITS>
+__device__ __forceinline__ void load_codes(const QmmArgs& a, int64_t rt16, int64_t c, int g, Codes<BITS>& cd) {
+  constexpr int CB = BITS == 4 ? 512 : 1024;
+  const uint4* base = reinterpret_cast<const uint4*>(a.w + (rt16 * a.nch + c) * CB + g * 64);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) cd.u[t] = __ldg(base + t);
+  if constexpr (BITS == 8) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cd.u[4 + t] = __ldg(base + 32 + t);  // k-tiles 2,3 at +512 B
+  }
+}
+
+// Regroup this feature's codes into 32 fp16 pairs (k = 2c, 2c+1 of the chunk, c = column).
+template <int BITS>
+__device__ __forceinline__ void transcode(const Codes<BITS>& cd, int h, uint32_t (&r)[32]) {
+  if constexpr (BITS == 4) {
+    // word j of lane t: nibbles (h, h+4) = k (2t, 2t+1), (h+2, h+6) = k (2t+8, 2t+9) of k-tile j
+    const uint32_t k1032 = 0x64086408u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t ws[4] = {cd.u[t].x, cd.u[t].y, cd.u[t].z, cd.u[t].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t w = ws[j] >> (4 * h);
+        r[8 * j + t] = hsub2_u32(lop_or_magic(w, 0x000F000Fu), k1032);
+        r[8 * j + 4 + t] = hsub2_u32(lop_or_magic(w >> 8, 0x000F000Fu), k1032);
+      }
+    }
+  } else {
+    // k-tile j of lane t: word pair (wd0, wd1); bytes (2h, 2h+1) of wd0 = k (2t, 2t+1),
+    // of wd1 = k (2t+8, 2t+9)
+    const uint32_t k1152 = 0x64806480u;
+    const uint32_t sel = h ? 0x4342u : 0x4140u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 v = cd.u[(j >> 1) * 4 + t];
+        const uint32_t wd0 = (j & 1) ? v.z : v.x, wd1 = (j & 1) ? v.w : v.y;
+        r[8 * j + t] = hsub2_u32(__byte_perm(wd0, 0x64646464u, sel), k1152);
+        r[8 * j + 4 + t] = hsub2_u32(__byte_perm(wd1, 0x64646464u, sel), k1152);
+      }
+    }
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* xring = smem;
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(RX) * XB);
+  uint64_t* xempty = xfull + RX;
+  uint64_t* a_full = xempty + RX;
+  uint64_t* a_empty = a_full + NA;
+  uint64_t* d_full = a_empty + NA;
+  uint64_t* d_empty = d_full + NDB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + NDB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < RX; ++i) {
+      mbar_init(xfull + i, 1);
+      mbar_init(xempty + i, 1);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(a_full + i, 4);
+      mbar_init(a_empty + i, 1);
+    }
+    for (int i = 0; i < NDB; ++i) {
+      mbar_init(d_full + i, 1);
+      mbar_init(d_empty + i, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int64_t nitems = static_cast<int64_t>(a.nrt128) * a.ntt * a.ksplit;
+
+  if (warp == kTcWarps) {
+    // ---------------- TMA producer: activation tiles ----------------
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      uint32_t q = 0;
+      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int64_t rt, tt, c0, c1;
+        int s;
+        decode_item(a, item, rt, tt, s, c0, c1);
+        for (int64_t c = c0; c < c1; ++c, ++q) {
+          const int xs = q % RX;
+          mbar_wait(xempty + xs, ((q / RX) & 1) ^ 1);
+          mbar_expect_tx(xfull + xs, XB);
+          bulk_g2s(xring + xs * XB, a.xt + tt * a.Kp * NTOK + c * kPK * NTOK, XB, xfull + xs, pol);
+          stamp(a, 5, q);
+        }
+      }
+    }
+  } else if (warp == kTcWarps + 1) {
+    // ---------------- MMA issuer (whole warp converged; elect.sync issues) ----------------
+    const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(NTOK >> 3) << 17) | (8u << 24);
+    const uint64_t desc_hi = (static_cast<uint64_t>((NTOK * 16) >> 4) << 16) |
+                             (static_cast<uint64_t>(128 >> 4) << 32) | (1ull << 46);
+    const uint32_t x0 = smem_u32(xring);
+    uint32_t q = 0, it = 0;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+      int64_t rt, tt, c0, c1;
+      int s;
+      decode_item(a, item, rt, tt, s, c0, c1);
+      const int db = it % NDB;
+      mbar_wait(d_empty + db, ((it / NDB) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tbase + D_COL + db * NTOK;
+      for (int64_t c = c0; c < c1; ++c, ++q) {
+        const int xs = q % RX, ab = q % NA;
+        mbar_wait(xfull + xs, (q / RX) & 1);
+        mbar_wait(a_full + ab, (q / NA) & 1);
+        tc_fence_after();
+        if (lane == 0) stamp(a, 3, q);
+        const uint64_t dbase = desc_hi | static_cast<uint64_t>(((x0 + xs * XB) >> 4) & 0x3FFF);
+#pragma unroll
+        for (int ks = 0; ks < kPK / 16; ++ks)
+          mma_f16_ts_elect(dcol, tbase + ab * 32 + ks * 8, dbase + ((ks * NTOK * 32) >> 4), idesc,
+                           (c > c0 || ks > 0) ? 1u : 0u);
+        tc_commit_elect(xempty + xs);
+        tc_commit_elect(a_empty + ab);
+        __syncwarp();
+      }
+      tc_commit_elect(d_full + db);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- transcode (+ epilogue on group 0) ----------------
+    const int quarter = warp & 3, group = warp >> 2;
+    const int row = quarter * 32 + lane;              // TMEM lane = feature in the 128 tile
+    const int i16 = row >> 4, g = row & 7, h = (row >> 3) & 1;
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
+    uint32_t q = 0, it = 0;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+      int64_t rt, tt, c0, c1;
+      int s;
+      decode_item(a, item, rt, tt, s, c0, c1);
+      const int64_t rt16 = rt * 8 + i16;
+      // first owned stage of this item, then prefetch one owned stage ahead
+      int64_t c = c0 + ((group - static_cast<int>(q % kGroups)) + kGroups) % kGroups;
+      uint32_t qq = q + static_cast<uint32_t>(c - c0);
+      Codes<BITS> cur;
+      if (c < c1) load_codes<BITS>(a, rt16, c, g, cur);
+      for (; c < c1; c += kGroups, qq += kGroups) {
+        Codes<BITS> nxt;
+        if (c + kGroups < c1) load_codes<BITS>(a, rt16, c + kGroups, g, nxt);
+        const int ab = qq % NA;
+        uint32_t r[32];
+        transcode<BITS>(cur, h, r);
+        mbar_wait(a_empty + ab, ((qq / NA) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st16(lane_base + ab * 32, r);
+        tmem_st16(lane_base + ab * 32 + 16, r + 16);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (warp == 0 && lane == 0) stamp(a, 2, qq);
+        if (lane == 0) mbar_arrive(a_full + ab);
+        cur = nxt;
+      }
+      q += static_cast<uint32_t>(c1 - c0);
+      if (group == 0) {
+        const int db = it % NDB;
+        mbar_wait(d_full + db, (it / NDB) & 1);
+        tc_fence_after();
+        float* out = a.partial + static_cast<int64_t>(s) * a.M * a.Np + rt * 128 + row;
+#pragma unroll 1
+        for (int c16 = 0; c16 < NTOK; c16 += 16) {
+          uint32_t v[16];
+          tmem_ld16(lane_base + D_COL + db * NTOK + c16, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            const int64_t tok = tt * NTOK + c16 + m;
+            if (tok < a.M) out[tok * a.Np] = __uint_as_float(v[m]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty + db);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+__global__ void k_xtile_from_f32(const float* __restrict__ x, int64_t ldx, int M, int64_t K, int64_t Kp, int NT,
+                                 const float* __restrict__ row_scale, __half* __restrict__ xt) {
+  const int64_t pairs = static_cast<int64_t>(NT) * (Kp / 2);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / (Kp / 2));
+    const int64_t k = (i % (Kp / 2)) * 2;
+    const float v0 = (m < M && k < K) ? x[m * ldx + k] * row_scale[k] : 0.f;
+    const float v1 = (m < M && k + 1 < K) ? x[m * ldx + k + 1] * row_scale[k + 1] : 0.f;
+    *reinterpret_cast<__half2*>(xt + xtile_index(Kp, m, k)) = __floats2half2_rn(v0, v1);
+  }
+}
+
+}  // namespace
+
+long long*& qmm_trace_ptr() {
+  static long long* p = nullptr;
+  return p;
+}
+
+GemvPlan plan_qmm(const QLayout& L, int M) {
+  GemvPlan p;
+  const int64_t ntt = (M + NTOK - 1) / NTOK, nrt128 = L.Np / 128;
+  const int64_t workers = kNumSMs;
+  double best = -1.0;
+  const int64_t max_split = L.nch < 16 ? L.nch : 16;
+  for (int64_t ks = 1; ks <= max_split; ++ks) {
+    if (L.nch / ks < 8 && ks > 1) break;
+    const int64_t items = ntt * nrt128 * ks;
+    const int64_t waves = (items + workers - 1) / workers;
+    double eff = static_cast<double>(items) / static_cast<double>(waves * workers) - 0.01 * static_cast<double>(ks);
+    if (eff > best + 1e-9) {
+      best = eff;
+      p.ksplit = static_cast<int>(ks);
+    }
+  }
+  const int64_t items = ntt * nrt128 * p.ksplit;
+  p.grid = static_cast<int>(items < workers ? items : workers);
+  return p;
+}
+
+void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st) {
+  if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
+  if (w.L.Np % 128 || w.L.Kp % 64) fail(GLM_DIMENSION, "qlinear", "layout not padded for the tcgen05 path");
+  QmmArgs a;
+  a.w = static_cast<const uint8_t*>(w.codes);
+  a.xt = xt;
+  a.partial = partial;
+  a.nrt16 = w.L.nrt;
+  a.nch = w.L.nch;
+  a.Np = w.L.Np;
+  a.Kp = w.L.Kp;
+  a.M = M;
+  a.ksplit = p.ksplit;
+  a.ntt = (M + NTOK - 1) / NTOK;
+  a.nrt128 = static_cast<int>(w.L.Np / 128);
+  a.trace = nullptr;
+  static long long* trace_buf = nullptr;
+  if (getenv("GLM_QMM_TRACE")) {
+    if (!trace_buf) CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8 * sizeof(long long)));
+    CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 256 * 8 * sizeof(long long), st));
+    a.trace = trace_buf;
+    qmm_trace_ptr() = trace_buf;
+  }
+  static bool attr[2] = {false, false};
+  const int bi = w.L.bits == 4 ? 0 : 1;
+  if (!attr[bi]) {
+    if (bi == 0) CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
+    else CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
+    attr[bi] = true;
+  }
+  if (bi == 0) k_qmm_tc<4><<<p.grid, kThreads, kSmem, st>>>(a);
+  else k_qmm_tc<8><<<p.grid, kThreads, kSmem, st>>>(a);
+  LAUNCH_CHECK("k_qmm_tc");
+}
+
+void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st) {
+  const int NT = xtile_tokens(M);
+  const int64_t pairs = static_cast<int64_t>(NT) * (w.L.Kp / 2);
+  const int grid = static_cast<int>(std::min<int64_t>((pairs + 255) / 256, 148 * 16));
+  k_xtile_from_f32<<<grid, 256, 0, st>>>(x, ldx, M, w.L.K, w.L.Kp, NT, w.row_scale, xt);
+  LAUNCH_CHECK("k_xtile_from_f32");
+}
+
+}  // namespace glm

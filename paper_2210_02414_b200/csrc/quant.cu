@@ -153,37 +153,18 @@ struct RepackMap {
 
 __global__ void k_repack(const int8_t* __restrict__ payload, QLayout L, RepackMap mp, uint32_t* __restrict__ out) {
   const int64_t words = L.bytes() / 4;
+  const int per = L.bits == 4 ? 8 : 4;
   for (int64_t wi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; wi < words;
        wi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t byte0 = wi * 4;
-    const int64_t blk = byte0 / L.chunk_bytes();
-    const int64_t rt = blk / L.nch, c = blk % L.nch;
-    int inblk = static_cast<int>(byte0 % L.chunk_bytes());
     uint32_t word = 0;
-    if (L.bits == 4) {
-      const int lane = inblk / 16, j = (inblk % 16) / 4;
-      const int g = lane >> 2, t = lane & 3;
-      for (int p = 0; p < 8; ++p) {
-        const int r = p & 3, hi = p >> 2;
-        const int64_t n = rt * kTileN + g + 8 * (r & 1);
-        const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
-        const int code =
-            (k < L.K && n < L.N) ? canonical_code(payload, (mp.row_offset + k) * mp.Nfull + mp.col(n), 4) : 0;
-        word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * p);
-      }
-    } else {
-      const int half = inblk / 512;
-      inblk %= 512;
-      const int lane = inblk / 16, jj = (inblk % 16) / 8, wd = (inblk % 8) / 4;
-      const int g = lane >> 2, t = lane & 3, j = half * 2 + jj;
-      for (int b = 0; b < 4; ++b) {
-        const int r = wd * 2 + (b >> 1), hi = b & 1;
-        const int64_t n = rt * kTileN + g + 8 * (r & 1);
-        const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
-        const int code =
-            (k < L.K && n < L.N) ? canonical_code(payload, (mp.row_offset + k) * mp.Nfull + mp.col(n), 8) : 0;
-        word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * b);
-      }
+    for (int e = 0; e < per; ++e) {
+      int64_t k, n;
+      layout_element(L, wi * 4 + (L.bits == 4 ? e / 2 : e), L.bits == 4 ? e & 1 : 0, &k, &n);
+      const int code = (k < L.K && n < L.N)
+                           ? canonical_code(payload, (mp.row_offset + k) * mp.Nfull + mp.col(n), L.bits)
+                           : 0;
+      if (L.bits == 4) word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * e);
+      else word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * e);
     }
     out[wi] = word;
   }
@@ -338,45 +319,21 @@ __global__ void k_gen_codes(GenSpec g, ShardMap sm, QLayout L, int axis, const d
                             uint32_t* __restrict__ out) {
   const int64_t words = L.bytes() / 4;
   const double cap = static_cast<double>((1 << (L.bits - 1)) - 1);
+  const int per = L.bits == 4 ? 8 : 4;
   for (int64_t wi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; wi < words;
        wi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t byte0 = wi * 4;
-    const int64_t blk = byte0 / L.chunk_bytes();
-    const int64_t rt = blk / L.nch, c = blk % L.nch;
-    int inblk = static_cast<int>(byte0 % L.chunk_bytes());
     uint32_t word = 0;
-    const int nvals = L.bits == 4 ? 8 : 4;
-    int half = 0, lane, j, wd = 0;
-    if (L.bits == 4) {
-      lane = inblk / 16;
-      j = (inblk % 16) / 4;
-    } else {
-      half = inblk / 512;
-      inblk %= 512;
-      lane = inblk / 16;
-      j = half * 2 + (inblk % 16) / 8;
-      wd = (inblk % 8) / 4;
-    }
-    const int gg = lane >> 2, t = lane & 3;
-    for (int p = 0; p < nvals; ++p) {
-      int r, hi;
-      if (L.bits == 4) {
-        r = p & 3;
-        hi = p >> 2;
-      } else {
-        r = wd * 2 + (p >> 1);
-        hi = p & 1;
-      }
-      const int64_t n = rt * kTileN + gg + 8 * (r & 1);
-      const int64_t k = c * kChunkK + j * 16 + 2 * t + 8 * (r >> 1) + hi;
+    for (int e = 0; e < per; ++e) {
+      int64_t k, n;
+      layout_element(L, wi * 4 + (L.bits == 4 ? e / 2 : e), L.bits == 4 ? e & 1 : 0, &k, &n);
       int code = 0;
       if (k < L.K && n < L.N) {
         const int64_t fk = sm.row(k), fn = sm.col(n);
         const double s = scales[axis == GLM_AXIS_ROW ? fk : fn];
         if (s != 0.0) code = round_code(gen_value(g, fk, fn) / s, cap);
       }
-      if (L.bits == 4) word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * p);
-      else word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * p);
+      if (L.bits == 4) word |= static_cast<uint32_t>((code + 8) & 0xF) << (4 * e);
+      else word |= static_cast<uint32_t>((code + 128) & 0xFF) << (8 * e);
     }
     out[wi] = word;
   }

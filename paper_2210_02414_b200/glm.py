@@ -85,6 +85,7 @@ SIGNATURES = {
     "glm_qweight_export": (I32, [P, P, P]),
     "glm_qweight_device_bytes": (I64, [P]),
     "glm_qweight_device_copy": (I32, [P, P]),
+    "glm_debug_qmm_trace": (I32, [P]),
     "glm_qlinear": (I32, [P, P, I64, P, P]),
     "glm_qlinear_host": (I32, [P, P, I64, P]),
     "glm_qlinear_bench": (I32, [P, I64, I32, I32, C.POINTER(D)]),

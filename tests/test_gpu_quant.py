@@ -124,11 +124,12 @@ def test_qweight_export_round_trip_and_layout(bits, axis):
     ql = glm.QLinear.from_payload(q)
     e = ql.export()
     assert np.array_equal(e["payload"], q["payload"]) and np.array_equal(e["scales"], q["scales"])
-    # the device layout places code(k, n) where layout.cuh says
+    # the device layout places code(k, n) where layout.cuh says: 16-feature row tiles x
+    # 64-k chunks in mma.sync fragment order (Np/Kp padded to 128)
     dev = ql.device_bytes()
     codes = O.codes_of(q).reshape(K, N)
-    nch, chunk = (K + 63) // 64, (512 if bits == 4 else 1024)
-    for k, n in [(0, 0), (1, 0), (0, 1), (9, 8), (63, 15), (64, 16), (K - 1, N - 1), (130, 77)]:
+    nch, chunk = ((K + 127) // 128 * 128) // 64, (512 if bits == 4 else 1024)
+    for k, n in [(0, 0), (1, 0), (0, 1), (9, 8), (63, 15), (64, 16), (K - 1, N - 1), (130, 77), (31, 89), (199, 64)]:
         rt, c, row, kk = n // 16, k // 64, n % 16, k % 64
         g, rsel, j, kc = row & 7, row >> 3, kk >> 4, kk & 15
         hi, t, r = kc & 1, (kc & 7) >> 1, rsel | ((kc >> 3) << 1)
