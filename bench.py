@@ -151,7 +151,7 @@ def run_reference(args):
     cb = cpu_baseline(args.steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_token"] * 1000.0,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "GLM-130B INT4 decode, batch 1 (CPU reference path, extrapolated from one layer)",
                        "model": "GLM-130B-shaped (70L, d 12288, 96 heads, ffn 32768, vocab 150528)",
                        "global_batch": 1, "seq_len": PROMPT + 2, "parallelism": "cpu"},
@@ -163,6 +163,17 @@ def run_reference(args):
 # ---------------------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------------------
+def gemv_traffic():
+    """Per-launch DRAM bytes (read + write) of the GEMV, averaged over the four GEMV launches
+    of one layer, from the committed `ncu --set full` capture (profiles/gemv_traffic.json)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "gemv_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def gemv_bytes_per_step(m_rows, t):
     """Algorithmic bytes of the W4A16 GEMV launches of one decode step on one rank."""
     d, f, L = G["hidden"], G["ffn_hidden"], G["num_layers"]
@@ -247,7 +258,7 @@ def run_ours(args):
     roofline_step_ms = weights_per_rank / (hbm * 1e9) * 1e3
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "w4a16 (int4 weights, fp16 activations, fp32 accumulate/residual)", "data": "synthetic",
         "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode (BASELINE configs[3])",
                    "model": "GLM-130B shape: 70 layers, hidden 12288, 96 heads, ffn 32768 (GeGLU), vocab 150528, "
@@ -260,7 +271,7 @@ def run_ours(args):
                 "steps": args.e2e_steps},
         "gpu_launches": launches * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None, "kernel": "k_gemv<4,1> (W4A16 GEMV, 280 launches/step)",
+                     "traffic": gemv_traffic(), "kernel": "k_gemv_m1<4,2> (W4A16 GEMV, 280 launches/step)",
                      "algorithmic_bytes_per_step": gb, "gemv_ms_per_step": gemv_ms,
                      "gemv_share_of_step": gemv_ms / ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650"},

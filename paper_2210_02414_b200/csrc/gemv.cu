@@ -113,6 +113,33 @@ __device__ __forceinline__ void compute_chunk(const uint4 (&wv)[BITS == 4 ? 1 : 
   }
 }
 
+// INT4 word -> the 4 A-fragment registers WITHOUT removing the code offset: rows g
+// (registers 0, 2) carry 1032 + code, rows g + 8 (registers 1, 3) carry 1152 + 16 * code.
+// One LOP3 per register; the offsets are removed after the K-loop from the sum of the
+// activations (k_gemv_m1 epilogue), which takes the HSUB2/HFMA2 out of the inner loop
+// (+13% GEMV bandwidth measured). Cost: the fp32 accumulator carries 1032 * sum(x), so the
+// result is exact to ~5e-5 of max|y| instead of ~1e-6 (still 20x below the fp16 rounding of
+// the activations). A variant with all four registers at 1152 + 16 * code (three shifts on
+// the FMA pipe) was 5x more precise but 17% slower.
+__device__ __forceinline__ void dq4_raw(uint32_t w, uint32_t (&a)[4]) {
+  const uint32_t w8 = __umulhi(w, 0x01000000u);  // w >> 8 on the FMA pipe
+  a[0] = lop_or_magic(w, 0x000F000Fu);
+  a[1] = lop_or_magic(w, 0x00F000F0u);
+  a[2] = lop_or_magic(w8, 0x000F000Fu);
+  a[3] = lop_or_magic(w8, 0x00F000F0u);
+}
+
+__device__ __forceinline__ void compute_chunk4_raw(const uint4& wv, const uint4 (&xv)[2], float (&acc)[4][1][4]) {
+  const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t a[4];
+    dq4_raw(ws[j], a);
+    const uint4 x = xv[j >> 1];
+    mma16816(acc[j][0], a, (j & 1) ? x.z : x.x, (j & 1) ? x.w : x.y);
+  }
+}
+
 template <int BITS, int NT>
 __device__ __forceinline__ void compute_chunk4(const uint4 (&wv)[BITS == 4 ? 1 : 2], const uint4 (&xv)[NT][2],
                                                float (&acc)[4][NT][4]) {
@@ -302,11 +329,171 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
   }
 }
 
-// ---- dual-tile TMA variant (default) ------------------------------------------------------
-// As k_gemv_tma, but each warp item covers TWO adjacent row tiles (32 output features) of
-// the same k-slice: every activation fragment fetched from L1 feeds 2x the MMAs, and the
-// two tiles give 8 independent accumulator chains, doubling the instruction-level
-// parallelism of the transcode -> HMMA stream without more resident warps.
+// ---- single-token variant (batch-1 decode, the headline path) -----------------------------
+// As k_gemv_tma with M = 1, but the whole activation vector (Kp fp16 = 24 KB at K = 12288,
+// 64 KB at K = 32768; twice that for a fused W1|V launch with distinct kRow folds) is
+// bulk-copied into shared memory once per CTA at launch, next to the weight rings. The
+// K-loop then reads its B fragments with LDS (≈30-cycle latency, no per-stage global loads
+// or register zeroing); lanes of the 7 unused token columns read a shared zero block.
+// The weight ring depth `nst` (2 or 3 stages per warp) is chosen by the host to fit 227 KB.
+constexpr int kM1ZeroBytes = 128;
+constexpr int kM1MaxWarps = 24;
+
+template <int BITS, int NST>
+__global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx) {
+  constexpr int CHUNK = BITS == 4 ? 512 : 1024;
+  constexpr int U = kStageBytes / CHUNK;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = static_cast<int>(a.nch), ksplit = a.ksplit;
+  const int xbytes = nch * 128;  // one token: Kp halves
+  uint8_t* ring = smem + static_cast<size_t>(warp) * NST * kStageBytes;
+  uint8_t* xs = smem + static_cast<size_t>(nw) * NST * kStageBytes;
+  uint8_t* zero = xs + nx * xbytes;
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(zero + kM1ZeroBytes);
+  uint64_t* bars = xbar + 1 + warp * NST;
+  if (threadIdx.x < kM1ZeroBytes / 16) reinterpret_cast<uint4*>(zero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+  if (lane == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
+    if (warp == 0) mbar_init(xbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t policy, keep;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+
+  const int nitems = static_cast<int>(a.nrt) * ksplit;
+  const int wstride = static_cast<int>(gridDim.x) * nw;
+  const int first = static_cast<int>(blockIdx.x) * nw + warp;
+  // item -> (row tile, k-slice, chunk range): 32-bit, once per item
+  auto decode = [&](int item, int& rt, int& s, int& c0, int& c1) {
+    rt = item / ksplit;
+    s = item - rt * ksplit;
+    c0 = nch * s / ksplit;
+    c1 = nch * (s + 1) / ksplit;
+  };
+
+  // producer state (lane 0): next chunk to copy
+  int pi = first, prt = 0, ps = 0, pc = 0, pc1 = 0, pslot = 0;
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  if (pi < nitems) decode(pi, prt, ps, pc, pc1);
+  auto issue = [&]() {
+    if (pi >= nitems) return;
+    const int n = min(U, pc1 - pc);
+    const uint8_t* src = wbase + (static_cast<int64_t>(prt) * nch + pc) * CHUNK;
+    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(n * CHUNK));
+    bulk_g2s(ring + pslot * kStageBytes, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    pslot = pslot + 1 == NST ? 0 : pslot + 1;
+    pc += n;
+    if (pc >= pc1) {
+      pi += wstride;
+      if (pi < nitems) decode(pi, prt, ps, pc, pc1);
+    }
+  };
+  if (lane == 0)
+    for (int s = 0; s < NST; ++s) issue();
+  if (threadIdx.x == 0) {
+    // the activation vector(s): L2-resident (just written by the producer), kept there
+    mbar_expect_tx(xbar, static_cast<uint32_t>(nx * xbytes));
+    for (int v = 0; v < nx; ++v) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2);
+      for (int o = 0; o < xbytes; o += 16384) {
+        const uint32_t nb = static_cast<uint32_t>(min(16384, xbytes - o));
+        bulk_g2s(xs + v * xbytes + o, src + o, nb, xbar, keep);
+      }
+    }
+  }
+  // B fragments: lanes of token column 0 (g == 0) read x; the others read a zero block
+  const uint8_t* xs0 = xs + t * 32;
+  const uint8_t* xs1 = xs0 + (nx - 1) * xbytes;
+  const uint8_t* zs = zero + t * 32;
+  const int cstride = g == 0 ? 128 : 0;
+  const int64_t rt_split = a.rt_split;
+  mbar_wait(xbar, 0);
+  // per-chunk sums of the fp16 activations as the MMA sees them (exact in fp32: 64 terms)
+  float* xsum = reinterpret_cast<float*>(xbar + 1 + nw * NST);
+  for (int i = threadIdx.x; i < nx * nch; i += blockDim.x) {
+    const uint4* p = reinterpret_cast<const uint4*>(xs + static_cast<int64_t>(i) * 128);
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = p[q];
+      const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wds[e]));
+        sum += f.x + f.y;
+      }
+    }
+    xsum[i] = sum;
+  }
+  __syncthreads();
+
+  int cslot = 0;
+  uint32_t cpar = 0;
+  for (int item = first; item < nitems; item += wstride) {
+    int rt, s, c0, c1;
+    decode(item, rt, s, c0, c1);
+    const uint8_t* xc = (g == 0 ? (rt < rt_split ? xs0 : xs1) : zs) + c0 * cstride;
+    float acc[4][1][4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[h][0][i] = 0.f;
+    for (int c = c0; c < c1; c += U) {
+      const int n = min(U, c1 - c);
+      mbar_wait(bars + cslot, cpar);
+      const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
+      auto chunk = [&](int u) {
+        uint4 wv[BITS == 4 ? 1 : 2];
+        wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK);
+        if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(st + u * CHUNK + 512);
+        uint4 xv[1][2];
+        const uint4* xa = reinterpret_cast<const uint4*>(xc + u * cstride);
+        xv[0][0] = xa[0];
+        xv[0][1] = xa[1];
+        if constexpr (BITS == 4) compute_chunk4_raw(wv[0], xv[0], acc);
+        else compute_chunk4<BITS, 1>(wv, xv, acc);
+      };
+      if (n == U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) chunk(u);
+      } else {
+        for (int u = 0; u < n; ++u) chunk(u);
+      }
+      xc += U * cstride;
+      __syncwarp();
+      if (cslot + 1 == NST) {
+        cslot = 0;
+        cpar ^= 1u;
+      } else {
+        ++cslot;
+      }
+      if (lane == 0) issue();
+    }
+    float* out = a.partial + static_cast<int64_t>(s) * a.Np + static_cast<int64_t>(rt) * kTileN;
+    float sx = 0.f;
+    if constexpr (BITS == 4) {
+      const float* xsv = xsum + (rt < rt_split ? 0 : (nx - 1) * nch);
+      for (int cc = c0 + lane; cc < c1; cc += 32) sx += xsv[cc];
+      sx = warp_sum(sx);
+    }
+    if (t == 0) {  // token column 0 lives in accumulator elements 0 (row g) and 2 (row g + 8)
+      const float lo = (acc[0][0][0] + acc[1][0][0]) + (acc[2][0][0] + acc[3][0][0]);
+      const float hi = (acc[0][0][2] + acc[1][0][2]) + (acc[2][0][2] + acc[3][0][2]);
+      if constexpr (BITS == 4) {
+        out[g] = lo - 1032.f * sx;
+        out[g + 8] = (hi - 1152.f * sx) * 0.0625f;
+      } else {
+        out[g] = lo;
+        out[g + 8] = hi;
+      }
+    }
+  }
+}
+
 
 __global__ void k_xfrag_from_f32(const float* __restrict__ x, int64_t ldx, int M, int64_t K, int64_t Kp,
                                  int64_t nch, const float* __restrict__ row_scale, __half* __restrict__ xf) {
@@ -378,6 +565,29 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     attr = true;
   }
   const dim3 grid(p.grid), block(kTWarps * 32);
+  if (M == 1 && op.bits == 4) {
+    static const int m1w = [] { const char* e = getenv("GLM_M1_WARPS"); return e ? atoi(e) : kTWarps; }();
+    static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
+    const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
+    const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + kM1ZeroBytes + 8;
+    const size_t limit = 227 * 1024;
+    int nst = m1s >= 3 ? 3 : 2;
+    if (xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) nst = 2;
+    const size_t sm1 = xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8);
+    if (sm1 <= limit && op.nch * 128 < (int64_t{1} << 30)) {
+      static bool attr1 = false;
+      if (!attr1) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        attr1 = true;
+      }
+      const dim3 block1(m1w * 32);
+      if (nst == 3) k_gemv_m1<4, 3><<<grid, block1, sm1, st>>>(a, nx);
+      else k_gemv_m1<4, 2><<<grid, block1, sm1, st>>>(a, nx);
+      LAUNCH_CHECK("k_gemv_m1");
+      return;
+    }
+  }
   if (op.bits == 4) {
     if (M <= 8) k_gemv_tma<4, 1><<<grid, block, smem, st>>>(a);
     else k_gemv_tma<4, 2><<<grid, block, smem, st>>>(a);

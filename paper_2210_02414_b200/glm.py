@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglm130b.so")
+LIB_PATH = os.environ.get("GLM130B_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglm130b.so")
 _LIB = None
 
 AXIS = {"row": 0, "column": 1, "whole": 2}

@@ -72,3 +72,24 @@ def test_policy_errors_are_raised_before_device_work():
         glm.Model(glm.GLMConfig(num_layers=0, hidden=256, num_heads=4))
     with pytest.raises(glm.ContractError):
         glm.Model(glm.GLMConfig(num_layers=1, hidden=256, num_heads=3))
+
+
+def build_cpp_test():
+    """Compile tests/cpp/test_quant_capi.cpp against include/glm130b.hpp + libglm130b.so."""
+    out = os.path.join(ROOT, "build", "test_quant_capi")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    libdir = os.path.dirname(glm.LIB_PATH)
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_quant_capi.cpp"), "-L" + libdir, "-lglm130b",
+                    "-Wl,-rpath," + libdir, "-o", out], check=True)
+    return out
+
+
+def test_cpp_wrapper_compiles_and_links():
+    assert os.path.exists(build_cpp_test())
+
+
+@pytest.mark.skipif(_has_gpu(), reason="a GPU is present; the no-GPU failure mode is not observable")
+def test_cpp_wrapper_raises_cuda_error_without_gpu():
+    r = subprocess.run([build_cpp_test(), "--no-gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -3,8 +3,11 @@ y = x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155).
 
 Two bars: (1) exact-arithmetic check against a float64 evaluation of the kernel's own
 contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only fp32
-accumulation error remains, <= 2e-6 relative; (2) the reference check against the oracle's
-float64 x . dequantize(q), max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
+accumulation error remains: <= 2e-6 of max|y|, except the single-token INT4 kernel, which
+accumulates offset-binary codes (1032 + code) and removes 1032 * sum(x) afterwards, so its
+fp32 accumulator carries the larger offset term: <= 2e-4 of max|y| (gemv.cu, dq4_raw);
+(2) the reference check against the oracle's float64 x . dequantize(q),
+max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
 import numpy as np
 import pytest
 
@@ -12,6 +15,10 @@ from oracle import pyoracle as O
 from paper_2210_02414_b200 import glm
 
 pytestmark = pytest.mark.gpu
+
+
+def contract_tol(M, bits):
+    return 2e-4 if (M == 1 and bits == 4) else 2e-6
 
 
 def kernel_contract(x, q):
@@ -45,7 +52,7 @@ def test_qlinear_matches_contract_and_oracle(bits, axis, K, N):
         x = rng.normal(0, 1, size=(M, K))
         y = lin(x).astype(np.float64)
         c = kernel_contract(x, q)
-        assert np.abs(y - c).max() <= 2e-6 * np.abs(c).max() + 1e-30, (M, np.abs(y - c).max())
+        assert np.abs(y - c).max() <= contract_tol(M, bits) * np.abs(c).max() + 1e-30, (M, np.abs(y - c).max())
         ref = x @ O.dequantize(q)
         assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
 
@@ -58,10 +65,11 @@ def test_qlinear_glm130b_k_dimension_with_split_k():
     for bits, axis in ((4, "column"), (8, "row")):
         q = glm.quantize_absmax(w, bits, axis)
         lin = glm.QLinear.from_payload(q)
-        x = rng.normal(0, 1, size=(2, K))
-        y = lin(x).astype(np.float64)
-        c = kernel_contract(x, q)
-        assert np.abs(y - c).max() <= 2e-6 * np.abs(c).max()
+        for M in (1, 2):
+            x = rng.normal(0, 1, size=(M, K))
+            y = lin(x).astype(np.float64)
+            c = kernel_contract(x, q)
+            assert np.abs(y - c).max() <= contract_tol(M, bits) * np.abs(c).max()
 
 
 def test_qlinear_quantize_handle_equals_payload_handle():
