@@ -7,6 +7,7 @@
 // scale fold, so no separate activation-formatting pass exists on the decode path.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "block.h"
@@ -21,6 +22,7 @@ constexpr float kInvSqrt2 = 0.70710678118654752440f;
 // Sum over ksplit partials of element n of row m, times the group scale.
 __device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t n) {
   float acc = 0.f;
+#pragma unroll 4
   for (int s = 0; s < in.ksplit; ++s) acc += in.p[static_cast<int64_t>(s) * in.split_stride + m * in.ld + n];
   return in.scale ? acc * in.scale[n] : acc;
 }
@@ -53,6 +55,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 template <typename ET>
 __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restrict__ tokens, int M,
                         float* __restrict__ h, XOut xo) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int64_t row = tokens[m];
   for (int64_t k = 2 * threadIdx.x; k < d; k += 2 * blockDim.x) {
@@ -76,41 +80,59 @@ __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restri
 // exchanged through distributed shared memory (DSMEM), so a 12288-wide row is spread over
 // 8 SMs instead of serialising its L2 latency on one.
 constexpr int kLnCluster = 8;
-constexpr int kLnThreads = 256;
-constexpr int kLnPairs = 4;  // pairs per thread: d <= 2 * 4 * 256 * 8 = 16384
+constexpr int kLnThreads = 384;
+constexpr int kLnPairs = 4;  // pairs per thread: d <= 2 * 4 * 384 * 8 = 24576
 
-__device__ __forceinline__ float cluster_sum(float v, float* red, float* slot) {
+// Cluster-wide sum of (a, b): CTA partials go to shared memory, then after one cluster
+// barrier every warp reads the kLnCluster remote partials in parallel (one lane each).
+__device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* slot) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  v = warp_sum(v);
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int i = 0; i < kLnThreads / 32; ++i) s += red[i];
-    *slot = s;
+  if (w == 0) {
+    float2 t = l < kLnThreads / 32 ? red[l] : make_float2(0.f, 0.f);
+    t.x = warp_sum(t.x);
+    t.y = warp_sum(t.y);
+    if (l == 0) *slot = t;
   }
   cluster.sync();
-  float tot = 0.f;
-  for (int r = 0; r < kLnCluster; ++r) tot += *cluster.map_shared_rank(slot, r);  // fixed order
-  cluster.sync();
-  return tot;
+  float2 r = l < kLnCluster ? *cluster.map_shared_rank(slot, l) : make_float2(0.f, 0.f);
+  // fixed-order (butterfly) combine: identical on every CTA and every run
+  r.x = warp_sum(r.x);
+  r.y = warp_sum(r.y);
+  cluster.sync();  // no CTA leaves while its slot may still be read
+  return r;
 }
 
 __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
-  __shared__ float red[kLnThreads / 32];
-  __shared__ float slot;
+  __shared__ float2 red[kLnThreads / 32];
+  __shared__ float2 slot;
   namespace cg = cooperative_groups;
   const int rank = static_cast<int>(cg::this_cluster().block_rank());
   const int m = blockIdx.x / kLnCluster;
   const int64_t npairs = a.d / 2;
   const int64_t per = (npairs + kLnCluster - 1) / kLnCluster;
   const int64_t p0 = rank * per, p1 = min(npairs, p0 + per);
+  // parameters do not depend on the predecessor: fetch them before waiting on it
+  float2 gn[kLnPairs], bs[kLnPairs];
+#pragma unroll
+  for (int i = 0; i < kLnPairs; ++i) {
+    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    if (p < p1) {
+      gn[i] = *reinterpret_cast<const float2*>(a.gain + 2 * p);
+      bs[i] = *reinterpret_cast<const float2*>(a.bias + 2 * p);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
   const float* __restrict__ hrow = a.h + static_cast<int64_t>(m) * a.d;
   float2 z[kLnPairs];
-  float sum = 0.f;
-  // issue every load of the slice first (partials of all splits + residual)
+  float2 acc = make_float2(0.f, 0.f);
+  // every load of the slice first (partials of all splits + residual)
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
@@ -133,25 +155,23 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
       const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
       z[i] = make_float2(a.alpha * hv.x + y.x, a.alpha * hv.y + y.y);
       if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + n) = y;
-      sum += z[i].x + z[i].y;
+      acc.x += z[i].x + z[i].y;
+      acc.y += z[i].x * z[i].x + z[i].y * z[i].y;
     }
   }
-  const float mean = cluster_sum(sum, red, &slot) / static_cast<float>(a.d);
-  float sq = 0.f;
-#pragma unroll
-  for (int i = 0; i < kLnPairs; ++i) {
-    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
-    if (p < p1) sq += (z[i].x - mean) * (z[i].x - mean) + (z[i].y - mean) * (z[i].y - mean);
-  }
-  const float var = cluster_sum(sq, red, &slot) / static_cast<float>(a.d);  // biased (tensor.cpp:267)
+  // one cluster reduction of (sum, sum of squares); biased variance (tensor.cpp:267)
+  const float2 tot = cluster_sum2(acc, red, &slot);
+  const float inv_d = 1.f / static_cast<float>(a.d);
+  const float mean = tot.x * inv_d;
+  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);
   const float rstd = rsqrtf(var + a.eps);
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
     if (p < p1) {
       const int64_t n = 2 * p;
-      const float o0 = (z[i].x - mean) * rstd * a.gain[n] + a.bias[n];
-      const float o1 = (z[i].y - mean) * rstd * a.gain[n + 1] + a.bias[n + 1];
+      const float o0 = (z[i].x - mean) * rstd * gn[i].x + bs[i].x;
+      const float o1 = (z[i].y - mean) * rstd * gn[i].y + bs[i].y;
       *reinterpret_cast<float2*>(a.h + static_cast<int64_t>(m) * a.d + n) = make_float2(o0, o1);
       store_xfrag_pair(a.x0, m, n, o0, o1);
       store_xfrag_pair(a.x1, m, n, o0, o1);
@@ -161,6 +181,8 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
 
 // ---- GeGLU activation: gelu(x W1) * (x V) (model.cpp:133-135, tensor.cpp:313-318) --------
 __global__ void k_geglu_act(ActArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t pairs = static_cast<int64_t>(a.M) * (a.f / 2);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -187,12 +209,17 @@ __global__ void k_geglu_act(ActArgs a) {
 constexpr int kAttnThreads = 128;
 constexpr int kSplitKeys = 64;
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
-  constexpr int LPK = DH / 32;          // lanes per key in the score phase
-  constexpr int KPW = 32 / LPK;         // keys per warp iteration
   constexpr int NW = kAttnThreads / 32;
   constexpr int FPL = DH / 32;          // features per lane in the PV phase
+  __shared__ __align__(128) __half kst[kSplitKeys * DH];  // this split's keys / values
+  __shared__ __align__(128) __half vst[kSplitKeys * DH];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ float q[DH];
   __shared__ float p[kSplitKeys];
   __shared__ float red[NW];
@@ -200,6 +227,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   __shared__ int last;
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // cache length / position were written by earlier steps (complete before our predecessor ran)
   const int len = a.cache_len[b];
   const int total = len + 1;
   const int k0 = split * kSplitKeys, k1 = min(total, k0 + kSplitKeys);
@@ -208,50 +236,80 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (DH + 2);
+  // The cached keys/values of this split do not depend on the qkv GEMV still running ahead
+  // of us: bulk-copy them into shared memory before the programmatic-dependency wait.
+  const int n_old = max(0, min(k1, len) - k0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (n_old > 0) {
+      const uint32_t bytes = static_cast<uint32_t>(n_old) * DH * 2;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(2 * bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(kst)),
+                   "l"(kc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&bar))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(vst)),
+                   "l"(vc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&bar))
+                   : "memory");
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
 
   if (k0 < total) {
     const bool has_new = (len >= k0 && len < k1);
-    for (int j = threadIdx.x; j < DH / 2; j += kAttnThreads) {
-      const float2 cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + j];  // (cos, sin), tensor.cpp:357-363
-      const int64_t fq = static_cast<int64_t>(head) * DH + 2 * j;
-      const float qa = reduce_partial(a.qkv, b, fq), qb = reduce_partial(a.qkv, b, fq + 1);
-      q[2 * j] = (cs.x * qa - cs.y * qb) * inv_sqrt;
-      q[2 * j + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
-      if (has_new) {
+    // q pairs on threads [0, DH/2), the new key/value pair on threads [DH/2, DH)
+    for (int j = threadIdx.x; j < DH; j += kAttnThreads) {
+      const int jj = j < DH / 2 ? j : j - DH / 2;
+      const float2 cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + jj];  // (cos, sin), tensor.cpp:357-363
+      const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jj;
+      if (j < DH / 2) {
+        const float qa = reduce_partial(a.qkv, b, fq), qb = reduce_partial(a.qkv, b, fq + 1);
+        q[2 * jj] = (cs.x * qa - cs.y * qb) * inv_sqrt;
+        q[2 * jj + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
+      } else if (has_new) {
         const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
         const float ka = reduce_partial(a.qkv, b, fk), kb = reduce_partial(a.qkv, b, fk + 1);
-        *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * j) =
-            __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
         const float va = reduce_partial(a.qkv, b, fv), vb = reduce_partial(a.qkv, b, fv + 1);
-        *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * j) = __floats2half2_rn(va, vb);
+        const __half2 kh = __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
+        const __half2 vh = __floats2half2_rn(va, vb);
+        *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jj) = kh;
+        *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * jj) = vh;
+        *reinterpret_cast<__half2*>(kst + (len - k0) * DH + 2 * jj) = kh;
+        *reinterpret_cast<__half2*>(vst + (len - k0) * DH + 2 * jj) = vh;
       }
     }
+    if (n_old > 0) {
+      asm volatile(
+          "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W_%=;\n}\n" ::"r"(
+              smem_addr(&bar))
+          : "memory");
+    }
     __syncthreads();
-    // ---- scores ----
-    const int sub = lane % LPK, kin = lane / LPK;
-    float qr[32];
+    // ---- scores: DH/8 lanes per key, one 16 B shared load each (a key row is read as
+    // contiguous 16 B columns, so the 32 lanes hit distinct banks) ----
+    constexpr int LPK2 = DH / 8, KPW2 = 32 / LPK2;
+    const int sub = lane % LPK2, kin = lane / LPK2;
+    float qr[8];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) qr[i] = q[sub * 32 + i];
-    for (int s0 = k0 + warp * KPW; s0 < k1; s0 += NW * KPW) {
+    for (int i = 0; i < 8; ++i) qr[i] = q[sub * 8 + i];
+    for (int s0 = k0 + warp * KPW2; s0 < k1; s0 += NW * KPW2) {
       const int s = s0 + kin;
       float acc = 0.f;
       if (s < k1) {
-        const uint4* kr = reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(s) * DH + sub * 32);
-        uint4 kv[4];
+        const uint4 kv = *reinterpret_cast<const uint4*>(kst + (s - k0) * DH + sub * 8);
+        const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) kv[i] = kr[i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t w4[4] = {kv[i].x, kv[i].y, kv[i].z, kv[i].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
-            acc += qr[i * 8 + 2 * e] * f.x + qr[i * 8 + 2 * e + 1] * f.y;
-          }
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+          acc += qr[2 * e] * f.x + qr[2 * e + 1] * f.y;
         }
       }
 #pragma unroll
-      for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      for (int o = LPK2 / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (sub == 0 && s < k1) p[s - k0] = acc;
     }
     __syncthreads();
@@ -288,7 +346,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * NW;
         if (s < k1) {
-          const __half* vr = vc + static_cast<int64_t>(s) * DH + lane * FPL;
+          const __half* vr = vst + (s - k0) * DH + lane * FPL;
           if constexpr (FPL == 4) vv[u] = *reinterpret_cast<const uint2*>(vr);
           else vv[u] = make_uint2(*reinterpret_cast<const uint32_t*>(vr), 0u);
         }
@@ -362,6 +420,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 
 // Cache length bookkeeping after a decode step (kept on the device for CUDA graphs).
 __global__ void k_advance(int* __restrict__ cache_len, int B) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) cache_len[b] += 1;
 }
@@ -525,6 +585,8 @@ __device__ __forceinline__ void head_rows(const HeadArgs& a, const float* hs, in
 
 template <typename ET>
 __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float hs[];  // [kHeadRowsPerGroup][d]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m0 = 0; m0 < a.M; m0 += kHeadRowsPerGroup) {
@@ -543,6 +605,8 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
 }
 
 __global__ void k_argmax_finish(unsigned long long* __restrict__ keys, int* __restrict__ tokens, int M) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m < M) {
     tokens[m] = static_cast<int>(~static_cast<uint32_t>(keys[m] & 0xFFFFFFFFull));
@@ -559,19 +623,19 @@ int grid_for(int64_t n, int threads, int cap = 148 * 16) {
 
 void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
                   cudaStream_t st) {
-  if (bf16) k_embed<__nv_bfloat16><<<M, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
-  else k_embed<float><<<M, 256, 0, st>>>(static_cast<const float*>(E), d, tokens, M, h, xo);
+  if (bf16) launch_k(k_embed<__nv_bfloat16>, dim3(M), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
+  else launch_k(k_embed<float>, dim3(M), dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
   LAUNCH_CHECK("k_embed");
 }
 
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   if (a.d > 2ll * kLnPairs * kLnThreads * kLnCluster || a.d % 2) fail(GLM_DIMENSION, "glmmodel", "hidden unsupported by LN kernel");
-  k_deepnorm_ln<<<M * kLnCluster, kLnThreads, 0, st>>>(a);
+  launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
   LAUNCH_CHECK("k_deepnorm_ln");
 }
 
 void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
-  k_geglu_act<<<grid_for(static_cast<int64_t>(a.M) * (a.f / 2), 256), 256, 0, st>>>(a);
+  launch_k(k_geglu_act, dim3(grid_for(static_cast<int64_t>(a.M) * (a.f / 2), 128)), dim3(128), 0, st, a);
   LAUNCH_CHECK("k_geglu_act");
 }
 
@@ -579,14 +643,14 @@ int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplit
 
 void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st) {
   const dim3 grid(a.heads, B, a.max_splits);
-  if (a.dh == 128) k_attn_decode<128><<<grid, kAttnThreads, 0, st>>>(a);
-  else if (a.dh == 64) k_attn_decode<64><<<grid, kAttnThreads, 0, st>>>(a);
+  if (a.dh == 128) launch_k(k_attn_decode<128>, grid, dim3(kAttnThreads), 0, st, a);
+  else if (a.dh == 64) launch_k(k_attn_decode<64>, grid, dim3(kAttnThreads), 0, st, a);
   else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
   LAUNCH_CHECK("k_attn_decode");
 }
 
 void launch_advance(int* cache_len, int B, cudaStream_t st) {
-  k_advance<<<1, 32, 0, st>>>(cache_len, B);
+  launch_k(k_advance, dim3(1), dim3(32), 0, st, cache_len, B);
   LAUNCH_CHECK("k_advance");
 }
 
@@ -608,7 +672,7 @@ void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XO
 }
 
 void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(kHeadRowsPerGroup) * a.d * sizeof(float);
+  const size_t smem = static_cast<size_t>(a.M < kHeadRowsPerGroup ? a.M : kHeadRowsPerGroup) * a.d * sizeof(float);
   static bool attr_set[2] = {false, false};
   if (!attr_set[bf16]) {
     if (bf16) CUDA_CHECK(cudaFuncSetAttribute(k_head<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -617,14 +681,15 @@ void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
   }
   if (smem > 227 * 1024) fail(GLM_DIMENSION, "glmmodel", "hidden too large for head kernel");
   if (a.d % 256 != 0) fail(GLM_DIMENSION, "glmmodel", "head kernel needs hidden % 256 == 0");
-  const int grid = kNumSMs * (smem > 110 * 1024 ? 1 : 2);
-  if (bf16) k_head<__nv_bfloat16><<<grid, kHeadThreads, smem, st>>>(a);
-  else k_head<float><<<grid, kHeadThreads, smem, st>>>(a);
+  const int per_sm = static_cast<int>(std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
+  const int grid = kNumSMs * (per_sm < 1 ? 1 : per_sm);
+  if (bf16) launch_k(k_head<__nv_bfloat16>, dim3(grid), dim3(kHeadThreads), smem, st, a);
+  else launch_k(k_head<float>, dim3(grid), dim3(kHeadThreads), smem, st, a);
   LAUNCH_CHECK("k_head");
 }
 
 void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st) {
-  k_argmax_finish<<<grid_for(M, 32), 32, 0, st>>>(keys, tokens, M);
+  launch_k(k_argmax_finish, dim3(grid_for(M, 32)), dim3(32), 0, st, keys, tokens, M);
   LAUNCH_CHECK("k_argmax_finish");
 }
 

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // capi_quant.cpp — C ABI for quantization and the quantized linear (include/glm130b.h).
 #include <cuda_runtime.h>
 
@@ -14,6 +15,14 @@ namespace glm {
 
 thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GLM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int64_t group_count(int64_t rows, int64_t cols, int axis) {
   return axis == GLM_AXIS_ROW ? rows : axis == GLM_AXIS_COLUMN ? cols : 1;

@@ -7,6 +7,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "glm130b.h"
 
@@ -51,6 +52,30 @@ glm_status guarded(F&& f) {
 
 constexpr int kNumSMs = 148;
 
+// Programmatic dependent launch (PDL) for the decode chain: every kernel of the step is
+// launched with programmaticStreamSerialization, so kernel k+1 may become resident while
+// kernel k runs. Each kernel calls pdl_wait() before touching anything its predecessor
+// writes (griddepcontrol.wait: predecessor complete, its memory visible) and pdl_trigger()
+// only AFTER that wait, so at most one kernel runs ahead (no resource deadlock). Work that
+// depends on nothing (e.g. the GEMV's weight prefetch) goes before the wait.
+// GLM_PDL=0 launches everything with plain stream order (A/B switch).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
@@ -82,6 +107,9 @@ __device__ __forceinline__ uint4 ld_nc(const uint4* p) {
                : "l"(p));
   return r;
 }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #endif  // __CUDACC__
 

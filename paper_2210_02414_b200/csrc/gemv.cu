@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
   };
   if (lane == 0)
     for (int s = 0; s < kStages; ++s) issue();
+  // weights never change during decode: their prefetch runs ahead of the predecessor kernel
+  pdl_wait();
+  pdl_trigger();
   // lanes other than 0 track the issue count implicitly: consumption order is identical
   uint32_t consumed = 0;
 
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
 // The weight ring depth `nst` (2 or 3 stages per warp) is chosen by the host to fit 227 KB.
 constexpr int kM1ZeroBytes = 128;
 constexpr int kM1MaxWarps = 24;
+constexpr int kM1DefaultWarps = 16;
 
 template <int BITS, int NST>
 __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx) {
@@ -394,6 +398,9 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   };
   if (lane == 0)
     for (int s = 0; s < NST; ++s) issue();
+  // weights never change during decode: their prefetch runs ahead of the predecessor kernel
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     // the activation vector(s): L2-resident (just written by the producer), kept there
     mbar_expect_tx(xbar, static_cast<uint32_t>(nx * xbytes));
@@ -524,9 +531,19 @@ __global__ void k_gemv_reduce(const float* __restrict__ partial, int ksplit, int
 
 }  // namespace
 
-GemvPlan plan_gemv(int64_t nrt, int64_t nch) {
+int m1_warps() {
+  static const int w = [] {
+    const char* e = getenv("GLM_M1_WARPS");
+    const int v = e ? atoi(e) : kM1DefaultWarps;
+    return v < 4 ? 4 : (v > kM1MaxWarps ? kM1MaxWarps : v);
+  }();
+  return w;
+}
+
+GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits) {
   GemvPlan p;
-  const int64_t total_warps = static_cast<int64_t>(kNumSMs) * kTWarps;
+  p.warps = (M == 1 && bits == 4) ? m1_warps() : kTWarps;
+  const int64_t total_warps = static_cast<int64_t>(kNumSMs) * p.warps;
   double best = -1.0;
   const int64_t max_split = nch < 32 ? nch : 32;
   for (int64_t ks = 1; ks <= max_split; ++ks) {
@@ -540,15 +557,12 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch) {
       p.ksplit = static_cast<int>(ks);
     }
   }
-  const int64_t ctas = (nrt * p.ksplit + kTWarps - 1) / kTWarps;
+  const int64_t ctas = (nrt * p.ksplit + p.warps - 1) / p.warps;
   p.grid = static_cast<int>(ctas < kNumSMs ? ctas : kNumSMs);
   return p;
 }
 
-GemvPlan plan_gemv(const QLayout& L, int M) {
-  (void)M;
-  return plan_gemv(L.nrt, L.nch);
-}
+GemvPlan plan_gemv(const QLayout& L, int M) { return plan_gemv(L.nrt, L.nch, M, L.bits); }
 
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st) {
   if (M < 1 || M > 16) fail(GLM_DIMENSION, "qlinear", "GEMV path takes 1..16 rows, got " + std::to_string(M));
@@ -566,13 +580,14 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   }
   const dim3 grid(p.grid), block(kTWarps * 32);
   if (M == 1 && op.bits == 4) {
-    static const int m1w = [] { const char* e = getenv("GLM_M1_WARPS"); return e ? atoi(e) : kTWarps; }();
     static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
     const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
     const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + kM1ZeroBytes + 8;
     const size_t limit = 227 * 1024;
     int nst = m1s >= 3 ? 3 : 2;
+    int m1w = p.warps;  // the plan's warps if the rings fit next to x, else fewer
     if (xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) nst = 2;
+    while (m1w > 8 && xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) --m1w;
     const size_t sm1 = xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8);
     if (sm1 <= limit && op.nch * 128 < (int64_t{1} << 30)) {
       static bool attr1 = false;
@@ -582,18 +597,18 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
         attr1 = true;
       }
       const dim3 block1(m1w * 32);
-      if (nst == 3) k_gemv_m1<4, 3><<<grid, block1, sm1, st>>>(a, nx);
-      else k_gemv_m1<4, 2><<<grid, block1, sm1, st>>>(a, nx);
+      if (nst == 3) launch_k(k_gemv_m1<4, 3>, grid, block1, sm1, st, a, nx);
+      else launch_k(k_gemv_m1<4, 2>, grid, block1, sm1, st, a, nx);
       LAUNCH_CHECK("k_gemv_m1");
       return;
     }
   }
   if (op.bits == 4) {
-    if (M <= 8) k_gemv_tma<4, 1><<<grid, block, smem, st>>>(a);
-    else k_gemv_tma<4, 2><<<grid, block, smem, st>>>(a);
+    if (M <= 8) launch_k(k_gemv_tma<4, 1>, grid, block, smem, st, a);
+    else launch_k(k_gemv_tma<4, 2>, grid, block, smem, st, a);
   } else {
-    if (M <= 8) k_gemv_tma<8, 1><<<grid, block, smem, st>>>(a);
-    else k_gemv_tma<8, 2><<<grid, block, smem, st>>>(a);
+    if (M <= 8) launch_k(k_gemv_tma<8, 1>, grid, block, smem, st, a);
+    else launch_k(k_gemv_tma<8, 2>, grid, block, smem, st, a);
   }
   LAUNCH_CHECK("k_gemv_tma");
 }

@@ -53,9 +53,11 @@ struct QWeightDev {
 struct GemvPlan {
   int ksplit = 1;
   int grid = 1;
+  int warps = 16;  // warps per CTA the split-K balance was computed for
 };
+// Split-K plan for an M-row GEMV; the single-token INT4 kernel runs more warps per SM.
 GemvPlan plan_gemv(const QLayout& L, int M);
-GemvPlan plan_gemv(int64_t nrt, int64_t nch);
+GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits);
 // One decode-GEMV launch (M <= 16) over nrt row tiles of contiguous device-layout codes;
 // row tiles >= rt_split read x_frag xf2 (fused W1|V launch, distinct kRow folds).
 struct GemvOp {

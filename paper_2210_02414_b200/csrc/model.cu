@@ -31,7 +31,8 @@ namespace {
 
 struct Linear {
   QWeightDev w;
-  GemvPlan plan;
+  GemvPlan plan1, planN;  // decode GEMV plans for 1 and 2..16 rows
+  const GemvPlan& plan(int M) const { return M == 1 ? plan1 : planN; }
   int64_t Kfull = 0, Nfull = 0;
   ShardSpec shard{};
   bool loaded = false;
@@ -75,6 +76,8 @@ __global__ void k_gen_table(uint64_t seed, uint32_t id, int64_t rows, int64_t co
 
 // After a decode step: the greedy token becomes the next input, positions advance.
 __global__ void k_feed(const int* __restrict__ next, int* __restrict__ tokens, int* __restrict__ positions, int B) {
+  pdl_wait();
+  pdl_trigger();
   const int b = threadIdx.x;
   if (b < B) {
     tokens[b] = next[b];
@@ -201,7 +204,8 @@ struct glm_model {
         lin.w.col_scale = alloc<float>(lin.w.L.Np);
         lin.w.row_scale = alloc<float>(lin.w.L.Kp);
         lin.w.scales64 = alloc<double>(lin.w.nscales);
-        lin.plan = plan_gemv(lin.w.L, 1);
+        lin.plan1 = plan_gemv(lin.w.L, 1);
+        lin.planN = plan_gemv(lin.w.L, 2);
       };
       mk(ly.lin[QKV], d, 3 * d, d, 3 * dl, ShardSpec{d, dl, static_cast<int64_t>(r) * dl, 0});
       mk(ly.lin[OUT], d, d, dl, d, ShardSpec{d, d, 0, static_cast<int64_t>(r) * dl});
@@ -222,7 +226,8 @@ struct glm_model {
       k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln1g, d, 1.f);
       k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln2g, d, 1.f);
     }
-    fused_plan = plan_gemv(layers[0].lin[W1].w.L.nrt + layers[0].lin[VV].w.L.nrt, layers[0].lin[W1].w.L.nch);
+    for (int M : {1, 2})
+      fused_plans[M - 1] = plan_gemv(layers[0].lin[W1].w.L.nrt + layers[0].lin[VV].w.L.nrt, layers[0].lin[W1].w.L.nch, M, bits);
     E = head_bf16 ? static_cast<void*>(alloc<__nv_bfloat16>(static_cast<int64_t>(V) * d))
                   : static_cast<void*>(alloc<float>(static_cast<int64_t>(V) * d));
     // RoPE table in double -> float (tensor.cpp:335-341: theta_j = 10000^(-2j/dh))
@@ -254,7 +259,8 @@ struct glm_model {
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
 
-  GemvPlan fused_plan;
+  GemvPlan fused_plans[2];
+  const GemvPlan& fused_plan(int M) const { return fused_plans[M == 1 ? 0 : 1]; }
 
   static int default_ffn(int hidden, int heads) {  // model.cpp:30-37
     if ((8 * hidden) % 3 == 0) return (8 * hidden) / 3;
@@ -305,8 +311,13 @@ struct glm_model {
       const GemvPlan p = M <= 16 ? plan_gemv(lin.w.L, static_cast<int>(M)) : plan_qmm(lin.w.L, static_cast<int>(M));
       need = std::max<int64_t>(need, static_cast<int64_t>(p.ksplit) * M * lin.w.L.Np);
     }
-    need = std::max<int64_t>(need, static_cast<int64_t>(fused_plan.ksplit) * std::min<int64_t>(M, 16) *
-                                       (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
+    for (int mm : {1, 2})
+      need = std::max<int64_t>(need, static_cast<int64_t>(fused_plans[mm - 1].ksplit) * std::min<int64_t>(M, 16) *
+                                         (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
+    for (int i = 0; i < 5; ++i)
+      for (int mm : {1, 2})
+        need = std::max<int64_t>(need, static_cast<int64_t>(layers[0].lin[i].plan(mm).ksplit) * std::min<int64_t>(M, 16) *
+                                           layers[0].lin[i].w.L.Np);
     if (need <= partial_cap) return;
     drop_graphs();
     partial.alloc(need * 4);
@@ -435,9 +446,9 @@ struct glm_model {
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
       Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
-      gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan, st);
+      gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan(B), st);
       AttnDecodeArgs aa;
-      aa.qkv = SubIn{partial.as<float>(), qkv.plan.ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
+      aa.qkv = SubIn{partial.as<float>(), qkv.plan(B).ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
       aa.d_local = dl;
       aa.heads = Hl;
       aa.dh = dh;
@@ -453,9 +464,9 @@ struct glm_model {
       aa.xo = xout(xf_out.as<__half>(), out);
       aa.out = nullptr;
       launch_attn_decode(aa, B, st);
-      gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan, st);
+      gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
       LnArgs ln;
-      ln.in = row_parallel_out(out, out.plan, B);
+      ln.in = row_parallel_out(out, out.plan(B), B);
       ln.h = h.as<float>();
       ln.gain = ly.ln1g;
       ln.bias = ly.ln1b;
@@ -468,18 +479,18 @@ struct glm_model {
       ln.zero_sublayer = zero_sub;
       launch_deepnorm_ln(ln, B, st);
       GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(), xf_v.as<__half>(), w1.w.L.nrt};
-      gemv_launch(op, B, partial.as<float>(), fused_plan, st);
+      gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
       ActArgs act;
       const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
-      act.w1 = SubIn{partial.as<float>(), fused_plan.ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
-      act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan.ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
+      act.w1 = SubIn{partial.as<float>(), fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
+      act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
       act.M = B;
       act.f = fl;
       act.xo = xout(xf_w2.as<__half>(), w2);
       launch_geglu_act(act, st);
-      gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan, st);
+      gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan(B), st);
       LnArgs ln2 = ln;
-      ln2.in = row_parallel_out(w2, w2.plan, B);
+      ln2.in = row_parallel_out(w2, w2.plan(B), B);
       ln2.gain = ly.ln2g;
       ln2.bias = ly.ln2b;
       const bool last = l + 1 == L;
@@ -492,7 +503,7 @@ struct glm_model {
     launches += enqueue_head(B, logits.as<float>());
     launch_argmax_finish(d_argmax, d_next, B, st);
     launch_advance(d_len, B, st);
-    k_feed<<<1, 32, 0, st>>>(d_next, d_tokens, d_positions, B);
+    launch_k(k_feed, dim3(1), dim3(32), 0, st, d_next, d_tokens, d_positions, B);
     LAUNCH_CHECK("k_feed");
     return launches + 3;
   }
@@ -572,7 +583,7 @@ struct glm_model {
   void linear_rows(const Linear& lin, const __half* xf, int64_t M, float* y) {
     GemvPlan p;
     if (M <= 16) {
-      p = lin.plan;
+      p = lin.plan(static_cast<int>(M));
       gemv_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     } else {
       p = plan_qmm(lin.w.L, static_cast<int>(M));
@@ -847,12 +858,12 @@ glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup
       CUDA_CHECK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
       for (int l = 0; l < m->L; ++l) {
         Layer& ly = m->layers[l];
-        gemv_launch(ly.lin[QKV].w, m->xf_qkv.as<__half>(), batch, m->partial.as<float>(), ly.lin[QKV].plan, m->st);
-        gemv_launch(ly.lin[OUT].w, m->xf_out.as<__half>(), batch, m->partial.as<float>(), ly.lin[OUT].plan, m->st);
+        gemv_launch(ly.lin[QKV].w, m->xf_qkv.as<__half>(), batch, m->partial.as<float>(), ly.lin[QKV].plan(batch), m->st);
+        gemv_launch(ly.lin[OUT].w, m->xf_out.as<__half>(), batch, m->partial.as<float>(), ly.lin[OUT].plan(batch), m->st);
         GemvOp op{ly.lin[W1].w.codes, m->bits, ly.lin[W1].w.L.nrt + ly.lin[VV].w.L.nrt, ly.lin[W1].w.L.nch,
                   m->xf_w1.as<__half>(), m->xf_v.as<__half>(), ly.lin[W1].w.L.nrt};
-        gemv_launch(op, batch, m->partial.as<float>(), m->fused_plan, m->st);
-        gemv_launch(ly.lin[W2].w, m->xf_w2.as<__half>(), batch, m->partial.as<float>(), ly.lin[W2].plan, m->st);
+        gemv_launch(op, batch, m->partial.as<float>(), m->fused_plan(batch), m->st);
+        gemv_launch(ly.lin[W2].w, m->xf_w2.as<__half>(), batch, m->partial.as<float>(), ly.lin[W2].plan(batch), m->st);
       }
       CUDA_CHECK(cudaStreamEndCapture(m->st, &g));
       cudaGraphExec_t gx;
