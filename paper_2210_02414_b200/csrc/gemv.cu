@@ -337,9 +337,8 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
 // 64 KB at K = 32768; twice that for a fused W1|V launch with distinct kRow folds) is
 // bulk-copied into shared memory once per CTA at launch, next to the weight rings. The
 // K-loop then reads its B fragments with LDS (≈30-cycle latency, no per-stage global loads
-// or register zeroing); lanes of the 7 unused token columns read a shared zero block.
+// or register zeroing).
 // The weight ring depth `nst` (2 or 3 stages per warp) is chosen by the host to fit 227 KB.
-constexpr int kM1ZeroBytes = 128;
 constexpr int kM1MaxWarps = 24;
 constexpr int kM1DefaultWarps = 16;
 
@@ -354,10 +353,8 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   const int xbytes = nch * 128;  // one token: Kp halves
   uint8_t* ring = smem + static_cast<size_t>(warp) * NST * kStageBytes;
   uint8_t* xs = smem + static_cast<size_t>(nw) * NST * kStageBytes;
-  uint8_t* zero = xs + nx * xbytes;
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(zero + kM1ZeroBytes);
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * xbytes);
   uint64_t* bars = xbar + 1 + warp * NST;
-  if (threadIdx.x < kM1ZeroBytes / 16) reinterpret_cast<uint4*>(zero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   if (lane == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
     if (warp == 0) mbar_init(xbar, 1);
@@ -412,29 +409,33 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
       }
     }
   }
-  // B fragments: lanes of token column 0 (g == 0) read x; the others read a zero block
+  // B fragments: every token column gets the same activation vector (lane (g, t) reads the
+  // fragment of column 0 whatever g is), so the MMA computes 8 identical result columns and
+  // only column 0 is stored: no zero-fill, no per-lane address selection, and the 8 lanes
+  // reading one address are served by a single shared-memory broadcast.
   const uint8_t* xs0 = xs + t * 32;
   const uint8_t* xs1 = xs0 + (nx - 1) * xbytes;
-  const uint8_t* zs = zero + t * 32;
-  const int cstride = g == 0 ? 128 : 0;
+  constexpr int cstride = 128;
   const int64_t rt_split = a.rt_split;
   mbar_wait(xbar, 0);
   // per-chunk sums of the fp16 activations as the MMA sees them (exact in fp32: 64 terms)
   float* xsum = reinterpret_cast<float*>(xbar + 1 + nw * NST);
-  for (int i = threadIdx.x; i < nx * nch; i += blockDim.x) {
-    const uint4* p = reinterpret_cast<const uint4*>(xs + static_cast<int64_t>(i) * 128);
+  // 8 lanes per 128-byte chunk, one 16-byte load each, 3-step shuffle reduction
+  for (int i0 = 0; i0 < nx * nch; i0 += blockDim.x >> 3) {  // warp-uniform trip count
+    const int i = i0 + (threadIdx.x >> 3);
+    const uint4 v = i < nx * nch ? reinterpret_cast<const uint4*>(xs + static_cast<int64_t>(i) * 128)[threadIdx.x & 7]
+                                 : make_uint4(0, 0, 0, 0);
+    const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
     float sum = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint4 v = p[q];
-      const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wds[e]));
-        sum += f.x + f.y;
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wds[e]));
+      sum += f.x + f.y;
     }
-    xsum[i] = sum;
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+    if ((threadIdx.x & 7) == 0 && i < nx * nch) xsum[i] = sum;
   }
   __syncthreads();
 
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   for (int item = first; item < nitems; item += wstride) {
     int rt, s, c0, c1;
     decode(item, rt, s, c0, c1);
-    const uint8_t* xc = (g == 0 ? (rt < rt_split ? xs0 : xs1) : zs) + c0 * cstride;
+    const uint8_t* xc = (rt < rt_split ? xs0 : xs1) + c0 * cstride;
     float acc[4][1][4];
 #pragma unroll
     for (int h = 0; h < 4; ++h)
@@ -582,7 +583,7 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   if (M == 1 && op.bits == 4) {
     static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
     const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
-    const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + kM1ZeroBytes + 8;
+    const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + 8;
     const size_t limit = 227 * 1024;
     int nst = m1s >= 3 ? 3 : 2;
     int m1w = p.warps;  // the plan's warps if the rings fit next to x, else fewer
