@@ -27,12 +27,6 @@ __device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t 
   return in.scale ? acc * in.scale[n] : acc;
 }
 
-__device__ __forceinline__ void store_xfrag_pair(const XOut& xo, int m, int64_t k, float v0, float v1) {
-  if (!xo.xf) return;
-  const float s0 = xo.row_scale ? xo.row_scale[k] : 1.f, s1 = xo.row_scale ? xo.row_scale[k + 1] : 1.f;
-  const int64_t idx = xo.tile ? xtile_index(xo.Kp, m, k) : xfrag_index(xo.nch, m, k);
-  *reinterpret_cast<__half2*>(xo.xf + idx) = __floats2half2_rn(v0 * s0, v1 * s1);
-}
 
 template <int NT>
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -200,27 +194,25 @@ __global__ void k_geglu_act(ActArgs a) {
 }
 
 // ---- decode attention (model.cpp:137-152 for the rows of the generation part) ----------
-// grid (heads, batch, splits); each CTA owns kSplitKeys keys of its sequence's cache.
-// Scores: DH/32 lanes per key, each lane a 32-feature slice (4 x LDG.128 in flight), the
-// dot reduced with DH/32-lane shuffles. P.V: lanes own DH/32 features, keys strided over
-// warps and unrolled so 8 independent V-row loads are in flight. The CTA holding the new
-// slot also rotates/stores the new k, v; the last CTA of a (head, batch) merges the
-// splits in split order (deterministic), writing out_proj's x_frag.
-constexpr int kAttnThreads = 128;
-constexpr int kSplitKeys = 64;
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
+// grid (heads, batch, splits); each CTA owns kSplitKeys consecutive keys of its sequence's
+// cache, so up to kSplitKeys cached tokens need no cross-CTA merge at all. Before the
+// programmatic-dependency wait (the qkv GEMV is still running) the CTA prefetches its
+// cached K/V rows into L2; after it, q (and the new k, v) are reduced from the GEMV's
+// split-K partials and rotated (RoPE), scores use DH/8 lanes per key (one 16-byte load
+// each), softmax is fp32, P.V has lanes own DH/32 features with 8 independent row loads in
+// flight, and the new key/value enter from shared memory. With several splits, the last
+// CTA of a (head, batch) merges them in split order (deterministic).
+constexpr int kAttnThreads = 256;
+constexpr int kSplitKeys = 256;
 
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
   constexpr int NW = kAttnThreads / 32;
   constexpr int FPL = DH / 32;          // features per lane in the PV phase
-  __shared__ __align__(128) __half kst[kSplitKeys * DH];  // this split's keys / values
-  __shared__ __align__(128) __half vst[kSplitKeys * DH];
-  __shared__ __align__(8) uint64_t bar;
+  constexpr int LPK = DH / 8, KPW = 32 / LPK;
   __shared__ float q[DH];
+  __shared__ __align__(16) __half knew[DH];
+  __shared__ __align__(16) __half vnew[DH];
   __shared__ float p[kSplitKeys];
   __shared__ float red[NW];
   __shared__ float opart[NW][DH];
@@ -231,29 +223,19 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   const int len = a.cache_len[b];
   const int total = len + 1;
   const int k0 = split * kSplitKeys, k1 = min(total, k0 + kSplitKeys);
+  const int kold = min(k1, len);  // cached keys of this split: [k0, kold)
   const int pos = a.positions[b];
   const float inv_sqrt = rsqrtf(static_cast<float>(DH));
   __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (DH + 2);
-  // The cached keys/values of this split do not depend on the qkv GEMV still running ahead
-  // of us: bulk-copy them into shared memory before the programmatic-dependency wait.
-  const int n_old = max(0, min(k1, len) - k0);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (n_old > 0) {
-      const uint32_t bytes = static_cast<uint32_t>(n_old) * DH * 2;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(2 * bytes)
-                   : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_addr(kst)),
-                   "l"(kc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&bar))
-                   : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_addr(vst)),
-                   "l"(vc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&bar))
-                   : "memory");
+  {
+    // warm L2 with this split's cached rows (independent of the running qkv GEMV)
+    constexpr int LPR = DH * 2 / 128;  // 128-byte lines per row
+    for (int i = threadIdx.x; i < (kold - k0) * LPR; i += kAttnThreads) {
+      const int64_t off = static_cast<int64_t>(k0) * DH + static_cast<int64_t>(i) * 64;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(kc + off));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vc + off));
     }
   }
   pdl_wait();
@@ -262,7 +244,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   if (k0 < total) {
     const bool has_new = (len >= k0 && len < k1);
     // q pairs on threads [0, DH/2), the new key/value pair on threads [DH/2, DH)
-    for (int j = threadIdx.x; j < DH; j += kAttnThreads) {
+    if (threadIdx.x < DH) {
+      const int j = threadIdx.x;
       const int jj = j < DH / 2 ? j : j - DH / 2;
       const float2 cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + jj];  // (cos, sin), tensor.cpp:357-363
       const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jj;
@@ -278,39 +261,43 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
         const __half2 vh = __floats2half2_rn(va, vb);
         *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jj) = kh;
         *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * jj) = vh;
-        *reinterpret_cast<__half2*>(kst + (len - k0) * DH + 2 * jj) = kh;
-        *reinterpret_cast<__half2*>(vst + (len - k0) * DH + 2 * jj) = vh;
+        *reinterpret_cast<__half2*>(knew + 2 * jj) = kh;
+        *reinterpret_cast<__half2*>(vnew + 2 * jj) = vh;
       }
     }
-    if (n_old > 0) {
-      asm volatile(
-          "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W_%=;\n}\n" ::"r"(
-              smem_addr(&bar))
-          : "memory");
-    }
     __syncthreads();
-    // ---- scores: DH/8 lanes per key, one 16 B shared load each (a key row is read as
-    // contiguous 16 B columns, so the 32 lanes hit distinct banks) ----
-    constexpr int LPK2 = DH / 8, KPW2 = 32 / LPK2;
-    const int sub = lane % LPK2, kin = lane / LPK2;
+    // ---- scores: LPK lanes per key, one 16-byte load each ----
+    const int sub = lane % LPK, kin = lane / LPK;
     float qr[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) qr[i] = q[sub * 8 + i];
-    for (int s0 = k0 + warp * KPW2; s0 < k1; s0 += NW * KPW2) {
-      const int s = s0 + kin;
+    auto dot8 = [&](uint4 kv) {
+      const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
       float acc = 0.f;
-      if (s < k1) {
-        const uint4 kv = *reinterpret_cast<const uint4*>(kst + (s - k0) * DH + sub * 8);
-        const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
-          acc += qr[2 * e] * f.x + qr[2 * e + 1] * f.y;
-        }
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+        acc += qr[2 * e] * f.x + qr[2 * e + 1] * f.y;
+      }
+      return acc;
+    };
+    constexpr int SU = 4;  // key groups in flight per warp
+    for (int s0 = k0 + warp * KPW; s0 < k1; s0 += NW * KPW * SU) {
+      uint4 kv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int s = s0 + u * NW * KPW + kin;
+        kv[u] = s < kold ? ld_nc(reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(s) * DH + sub * 8))
+                         : (s == len ? *reinterpret_cast<const uint4*>(knew + sub * 8) : make_uint4(0, 0, 0, 0));
       }
 #pragma unroll
-      for (int o = LPK2 / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (sub == 0 && s < k1) p[s - k0] = acc;
+      for (int u = 0; u < SU; ++u) {
+        const int s = s0 + u * NW * KPW + kin;
+        float acc = dot8(kv[u]);
+#pragma unroll
+        for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sub == 0 && s < k1) p[s - k0] = acc;
+      }
     }
     __syncthreads();
     // ---- softmax over the split (fp32) ----
@@ -345,8 +332,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * NW;
+        const __half* vr = s < kold ? vc + static_cast<int64_t>(s) * DH + lane * FPL : vnew + lane * FPL;
         if (s < k1) {
-          const __half* vr = vst + (s - k0) * DH + lane * FPL;
           if constexpr (FPL == 4) vv[u] = *reinterpret_cast<const uint2*>(vr);
           else vv[u] = make_uint2(*reinterpret_cast<const uint32_t*>(vr), 0u);
         }
@@ -370,6 +357,25 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
     for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
     __syncthreads();
+    if (gridDim.z == 1) {
+      // single split: normalise and hand the row to out_proj directly
+      const float inv = 1.f / sum;
+      for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kAttnThreads) {
+        float o0 = 0.f, o1 = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          o0 += opart[w][2 * c2];
+          o1 += opart[w][2 * c2 + 1];
+        }
+        const int64_t k = static_cast<int64_t>(head) * DH + 2 * c2;
+        store_xfrag_pair(a.xo, b, k, o0 * inv, o1 * inv);
+        if (a.out) {
+          a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0 * inv;
+          a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
+        }
+      }
+      return;
+    }
     for (int c = threadIdx.x; c < DH; c += kAttnThreads) {
       float acc = 0.f;
 #pragma unroll

@@ -29,6 +29,17 @@ struct XOut {
   const float* row_scale = nullptr;
 };
 
+#if defined(__CUDACC__)
+// Store the pair (k, k+1) of row m into the consumer's activation buffer (fp16, with the
+// consumer's kRow fold).
+__device__ __forceinline__ void store_xfrag_pair(const XOut& xo, int m, int64_t k, float v0, float v1) {
+  if (!xo.xf) return;
+  const float s0 = xo.row_scale ? xo.row_scale[k] : 1.f, s1 = xo.row_scale ? xo.row_scale[k + 1] : 1.f;
+  const int64_t idx = xo.tile ? xtile_index(xo.Kp, m, k) : xfrag_index(xo.nch, m, k);
+  *reinterpret_cast<__half2*>(xo.xf + idx) = __floats2half2_rn(v0 * s0, v1 * s1);
+}
+#endif
+
 struct LnArgs {
   SubIn in;
   float* h;                 // [M][d] residual in / LN output out

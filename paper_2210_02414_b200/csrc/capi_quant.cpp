@@ -16,6 +16,11 @@ namespace glm {
 thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
 
+bool sync_launch_debug() {
+  static const bool on = std::getenv("GLM_SYNC_LAUNCH") != nullptr;
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("GLM_PDL");

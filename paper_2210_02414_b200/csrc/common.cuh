@@ -29,7 +29,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(GLM_CUDA, "cuda", std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CUDA_CHECK(x) ::glm::cuda_check((x), #x)
-#define LAUNCH_CHECK(what) ::glm::cuda_check(cudaGetLastError(), what)
+// GLM_SYNC_LAUNCH=1 (debugging, with GLM_EAGER=1): synchronise after every launch so a
+// device fault is attributed to the kernel that caused it.
+bool sync_launch_debug();
+inline void launch_check(const char* what) {
+  cuda_check(cudaGetLastError(), what);
+  if (sync_launch_debug()) cuda_check(cudaDeviceSynchronize(), what);
+}
+#define LAUNCH_CHECK(what) ::glm::launch_check(what)
 
 void set_last_error(const std::string& s);
 
@@ -61,19 +68,36 @@ constexpr int kNumSMs = 148;
 // GLM_PDL=0 launches everything with plain stream order (A/B switch).
 bool pdl_enabled();
 
+// `coop` adds the cooperative attribute: the launch fails instead of deadlocking if the
+// grid cannot be fully co-resident (kernels with a grid-wide barrier).
 template <typename... KArgs, typename... Args>
-inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+inline void launch_k_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool coop,
+                        Args&&... args) {
+  static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (coop) {
+    at[n].id = cudaLaunchAttributeCooperative;
+    at[n].val.cooperative = 1;
+    ++n;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  launch_k_ex(kernel, grid, block, smem, st, false, std::forward<Args>(args)...);
 }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

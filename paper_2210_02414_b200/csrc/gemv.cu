@@ -343,7 +343,7 @@ constexpr int kM1MaxWarps = 24;
 constexpr int kM1DefaultWarps = 16;
 
 template <int BITS, int NST>
-__global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx) {
+__global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx, int early) {
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
   constexpr int U = kStageBytes / CHUNK;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -393,11 +393,14 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
       if (pi < nitems) decode(pi, prt, ps, pc, pc1);
     }
   };
+  // weights never change during decode: `early` stages are fetched ahead of the
+  // predecessor kernel (programmatic dependent launch), the rest after it completes
   if (lane == 0)
-    for (int s = 0; s < NST; ++s) issue();
-  // weights never change during decode: their prefetch runs ahead of the predecessor kernel
+    for (int s = 0; s < early && s < NST; ++s) issue();
   pdl_wait();
   pdl_trigger();
+  if (lane == 0)
+    for (int s = early; s < NST; ++s) issue();
   if (threadIdx.x == 0) {
     // the activation vector(s): L2-resident (just written by the producer), kept there
     mbar_expect_tx(xbar, static_cast<uint32_t>(nx * xbytes));
@@ -584,7 +587,7 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
     const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
     const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + 8;
-    const size_t limit = 227 * 1024;
+    const size_t limit = 227 * 1024 - 1024;  // leave room for the static shared memory
     int nst = m1s >= 3 ? 3 : 2;
     int m1w = p.warps;  // the plan's warps if the rings fit next to x, else fewer
     if (xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) nst = 2;
@@ -598,8 +601,9 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
         attr1 = true;
       }
       const dim3 block1(m1w * 32);
-      if (nst == 3) launch_k(k_gemv_m1<4, 3>, grid, block1, sm1, st, a, nx);
-      else launch_k(k_gemv_m1<4, 2>, grid, block1, sm1, st, a, nx);
+      static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
+      if (nst == 3) launch_k(k_gemv_m1<4, 3>, grid, block1, sm1, st, a, nx, early);
+      else launch_k(k_gemv_m1<4, 2>, grid, block1, sm1, st, a, nx, early);
       LAUNCH_CHECK("k_gemv_m1");
       return;
     }

@@ -6,6 +6,7 @@
 
 #include "glm130b.h"
 #include "layout.cuh"
+#include "block.h"
 
 namespace glm {
 
@@ -68,6 +69,7 @@ struct GemvOp {
   const __half* xf2;
   int64_t rt_split;
 };
+
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
 // partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over k-split s of x . W
 void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,

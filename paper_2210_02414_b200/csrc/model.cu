@@ -117,6 +117,7 @@ struct glm_model {
   unsigned long long* d_argmax = nullptr;
   float* attn_part = nullptr;
   int* attn_ctr = nullptr;
+
   int attn_splits = 1;
   std::vector<int> h_len;
 
@@ -566,7 +567,9 @@ struct glm_model {
     }
     CUDA_CHECK(cudaMemcpyAsync(d_tokens, h_tokens, B * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(d_positions, h_positions, B * sizeof(int), cudaMemcpyHostToDevice, st));
-    CUDA_CHECK(cudaGraphLaunch(graph_for(B), st));
+    static const bool eager = getenv("GLM_EAGER") != nullptr;  // debugging: no graph
+    if (eager) enqueue_decode(B);
+    else CUDA_CHECK(cudaGraphLaunch(graph_for(B), st));
     if (logits_out) CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(B) * V * 4, cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaMemcpyAsync(h_next, d_next, B * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
