@@ -202,13 +202,9 @@ def run_ours(args):
     m = glm.Model(cfg, bits=4, axis="column", max_batch=B, max_ctx=max_ctx, head_bf16=True, tp_rank=rank,
                   tp_size=world)
     if world > 1:
-        uid = np.zeros(128, np.uint8)
-        if rank == 0:
-            glm._check(glm.lib().glm_tp_unique_id(glm._p(uid)))
-        t = torch.from_numpy(uid).cuda()
-        dist.broadcast(t, 0)
-        uid = t.cpu().numpy()
-        glm._check(glm.lib().glm_model_init_comm(m.h, glm._p(uid)))
+        uid = [glm.tp_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        m.init_comm(uid[0])
     m.init_synthetic(args.seed)
     init_s = time.time() - t0
     rng = np.random.default_rng(1234)

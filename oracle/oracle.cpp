@@ -456,6 +456,7 @@ void shape_of(const or_params* p, int which, int64_t& r, int64_t& c) {
     case OR_W1: case OR_V: r = d; c = f; return;
     case OR_W2: r = f; c = d; return;
     case OR_EMBED: r = p->cfg.vocab; c = d; return;
+    case 5: case 6: r = 1; c = d; return;  // LN gains (biases are zero at init, model.cpp:92-95)
   }
   fail(OR_CONTRACT, "oracle", "unknown tensor slot");
 }

@@ -289,6 +289,14 @@ def gmask_layout(prefix_len, n_gen):
     return pos, P + 1
 
 
+def tp_unique_id() -> bytes:
+    """128-byte NCCL unique id (glm_tp_unique_id); rank 0 creates it, every rank passes it
+    to Model.init_comm."""
+    uid = np.zeros(128, np.uint8)
+    _check(lib().glm_tp_unique_id(_p(uid)))
+    return uid.tobytes()
+
+
 class Model:
     """GLM model on the B200: quantized linears, fp32 residual stream, KV cache."""
 
@@ -308,6 +316,13 @@ class Model:
         if getattr(self, "h", None) and _LIB is not None:
             _LIB.glm_model_destroy(self.h)
             self.h = None
+
+    def init_comm(self, unique_id: bytes):
+        """Join the tensor-parallel group (NCCL over NVLink); no-op at tp_size == 1."""
+        uid = np.frombuffer(bytes(unique_id), np.uint8).copy()
+        if uid.size != 128:
+            raise ContractError("[glmmodel] NCCL unique id must be 128 bytes")
+        _check(lib().glm_model_init_comm(self.h, _p(uid)))
 
     # -- weights --
     def set_embedding(self, e):
