@@ -456,50 +456,201 @@ __global__ void k_rope_store(RopeStoreArgs a) {
   }
 }
 
-constexpr int kPfRows = 16;      // query rows per CTA
-constexpr int kPfThreads = 256;
+// Tensor-core flash attention for prefill (FA2 schedule on mma.sync.m16n8k16, fp16 in,
+// fp32 accumulate): a CTA owns 64 query rows of one head (16 per warp), streams 64-key
+// blocks of K and V through double-buffered shared memory (cp.async), keeps S = Q K^T,
+// the online-softmax state and O in registers, and feeds P straight from the S
+// accumulators into the P.V MMA. Key blocks wholly invisible to the CTA's rows are never
+// loaded; the gMASK rule j < max(C, i + 1) is applied element-wise only on blocks that
+// straddle it. exp2 with log2(e) folded into the Q scale (same softmax).
+constexpr int kFaRows = 64, kFaKeys = 64, kFaThreads = 128;
 
-__global__ void __launch_bounds__(kPfThreads) k_attn_prefill(AttnPrefillArgs a) {
-  // Two-pass over keys in fp32 with online softmax per query row. One warp per query row.
-  extern __shared__ float sm[];
-  const int head = blockIdx.y, i0 = blockIdx.x * kPfRows;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kFaThreads) k_attn_prefill_tc(AttnPrefillArgs a) {
+  constexpr int LDS = DH + 8;  // padded row (halves): ldmatrix rows land in distinct banks
+  extern __shared__ __align__(16) __half fsm[];
+  __half* Qs = fsm;                        // [64][LDS]
+  __half* Ks = Qs + kFaRows * LDS;         // [2][64][LDS]
+  __half* Vs = Ks + 2 * kFaKeys * LDS;     // [2][64][LDS]
+  const int head = blockIdx.y, i0 = blockIdx.x * kFaRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int dh = a.dh;
-  const float inv_sqrt = rsqrtf(static_cast<float>(dh));
-  const __half* kc = a.kcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * dh;
-  const __half* vc = a.vcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * dh;
-  float* qs = sm + warp * dh;  // this warp's q row
-  for (int r = warp; r < kPfRows; r += kPfThreads / 32) {
+  const int g = lane >> 2, t = lane & 3;
+  const int n = a.n, C = a.context_len;
+  const __half* kc = a.kcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * DH;
+  const __half* vc = a.vcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * DH;
+  // keys visible to some row of this block: j < max(C, i0 + 64) (and j < n)
+  const int kend = min(n, max(C, i0 + kFaRows));
+  const int nblk = (kend + kFaKeys - 1) / kFaKeys;
+  auto load_kv = [&](int blk, int buf) {
+    const int j0 = blk * kFaKeys;
+    constexpr int CPR = DH / 8;  // 16-byte chunks per row
+    for (int c = threadIdx.x; c < kFaKeys * CPR; c += kFaThreads) {
+      const int r = c / CPR, cc = (c % CPR) * 8;
+      const int j = j0 + r;
+      const bool ok = j < kend;
+      const int64_t off = static_cast<int64_t>(ok ? j : 0) * DH + cc;
+      cp_async16(Ks + (buf * kFaKeys + r) * LDS + cc, kc + off, ok);
+      cp_async16(Vs + (buf * kFaKeys + r) * LDS + cc, vc + off, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  load_kv(0, 0);
+  // Q (fp32, rotated) -> fp16, pre-scaled by log2(e) / sqrt(dh)
+  const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(DH));
+  for (int c = threadIdx.x; c < kFaRows * DH / 2; c += kFaThreads) {
+    const int r = c / (DH / 2), cc = (c % (DH / 2)) * 2;
     const int i = i0 + r;
-    if (i >= a.n) break;
-    for (int c = lane; c < dh; c += 32) qs[c] = a.q[(static_cast<int64_t>(head) * a.n + i) * dh + c] * inv_sqrt;
-    __syncwarp();
-    const int nkeys = max(a.context_len, i + 1) < a.n ? max(a.context_len, i + 1) : a.n;
-    // online softmax; lane owns features c = lane + 32*t
-    float mrun = -FLT_MAX, lrun = 0.f;
-    float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // dh <= 256
-    for (int s = 0; s < nkeys; ++s) {
-      const __half* kr = kc + static_cast<int64_t>(s) * dh;
-      float acc = 0.f;
-      for (int c = lane; c < dh; c += 32) acc += qs[c] * __half2float(kr[c]);
-      acc = warp_sum(acc);
-      const float mnew = fmaxf(mrun, acc);
-      const float corr = __expf(mrun - mnew), e = __expf(acc - mnew);
-      lrun = lrun * corr + e;
-      const __half* vr = vc + static_cast<int64_t>(s) * dh;
+    float2 v = make_float2(0.f, 0.f);
+    if (i < n) v = *reinterpret_cast<const float2*>(a.q + (static_cast<int64_t>(head) * n + i) * DH + cc);
+    *reinterpret_cast<__half2*>(Qs + r * LDS + cc) = __floats2half2_rn(v.x * qs, v.y * qs);
+  }
+  __syncthreads();
+  uint32_t qa[DH / 16][4];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int c = lane + 32 * t;
-        if (c < dh) o[t] = o[t] * corr + e * __half2float(vr[c]);
+  for (int kt = 0; kt < DH / 16; ++kt)
+    ldsm_x4(qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3],
+            Qs + (warp * 16 + (lane & 15)) * LDS + kt * 16 + (lane >> 4) * 8);
+  float o[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int rowA = i0 + warp * 16 + g, rowB = rowA + 8;
+  const int limA = max(C, rowA + 1), limB = max(C, rowB + 1);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int buf = blk & 1;
+    if (blk + 1 < nblk) {
+      load_kv(blk + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const __half* Kb = Ks + buf * kFaKeys * LDS;
+    const __half* Vb = Vs + buf * kFaKeys * LDS;
+    // ---- S = Q K^T (16 x 64 per warp) ----
+    float sc[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+    for (int kt = 0; kt < DH / 16; ++kt) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {  // pairs of key n-tiles
+        uint32_t b0, b1, b2, b3;
+        const int mi = lane >> 3;
+        ldsm_x4(b0, b1, b2, b3, Kb + (np * 16 + (mi >> 1) * 8 + (lane & 7)) * LDS + kt * 16 + (mi & 1) * 8);
+        mma_f16(sc[2 * np], qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3], b0, b1);
+        mma_f16(sc[2 * np + 1], qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3], b2, b3);
       }
-      mrun = mnew;
+    }
+    // ---- gMASK visibility on blocks that straddle it ----
+    const int j0 = blk * kFaKeys;
+    if (j0 + kFaKeys > min(limA, limB) || j0 + kFaKeys > n) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = j0 + nt * 8 + 2 * t + (e & 1);
+          const int lim = (e >> 1) ? limB : limA;
+          if (j >= lim || j >= n) sc[nt][e] = -INFINITY;
+        }
+    }
+    // ---- online softmax (rows g and g + 8 of the warp's 16) ----
+    float bm[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      bm[0] = fmaxf(bm[0], fmaxf(sc[nt][0], sc[nt][1]));
+      bm[1] = fmaxf(bm[1], fmaxf(sc[nt][2], sc[nt][3]));
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int c = lane + 32 * t;
-      if (c < dh) a.out[static_cast<int64_t>(i) * a.ldout + static_cast<int64_t>(head) * dh + c] = o[t] / lrun;
+    for (int r = 0; r < 2; ++r) {
+      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 1));
+      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 2));
     }
-    __syncwarp();
+    float corr[2], mnew[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mnew[r] = fmaxf(mrow[r], bm[r]);
+      corr[r] = exp2f(mrow[r] - mnew[r]);  // 0 on the first block (mrow = -inf)
+      mrow[r] = mnew[r];
+      lrow[r] *= corr[r];
+    }
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) {
+      o[i][0] *= corr[0];
+      o[i][1] *= corr[0];
+      o[i][2] *= corr[1];
+      o[i][3] *= corr[1];
+    }
+    uint32_t pa[4][4];  // P as the A operand of P.V, one k-tile per 16 keys
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(sc[nt][0] - mnew[0]), p1 = exp2f(sc[nt][1] - mnew[0]);
+      const float p2 = exp2f(sc[nt][2] - mnew[1]), p3 = exp2f(sc[nt][3] - mnew[1]);
+      lrow[0] += p0 + p1;
+      lrow[1] += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_h2(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_h2(p2, p3);
+    }
+    // ---- O += P V ----
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+      for (int dp = 0; dp < DH / 16; ++dp) {  // pairs of dh n-tiles
+        uint32_t b0, b1, b2, b3;
+        const int mi = lane >> 3;
+        ldsm_x4_t(b0, b1, b2, b3, Vb + (kk * 16 + (mi & 1) * 8 + (lane & 7)) * LDS + dp * 16 + (mi >> 1) * 8);
+        mma_f16(o[2 * dp], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+        mma_f16(o[2 * dp + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled two blocks later
+  }
+  // ---- normalise and store ----
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+  const float inv0 = 1.f / lrow[0], inv1 = 1.f / lrow[1];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) {
+    const int c = head * DH + i * 8 + 2 * t;
+    if (rowA < n)
+      *reinterpret_cast<float2*>(a.out + static_cast<int64_t>(rowA) * a.ldout + c) =
+          make_float2(o[i][0] * inv0, o[i][1] * inv0);
+    if (rowB < n)
+      *reinterpret_cast<float2*>(a.out + static_cast<int64_t>(rowB) * a.ldout + c) =
+          make_float2(o[i][2] * inv1, o[i][3] * inv1);
   }
 }
 
@@ -666,10 +817,16 @@ void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
 }
 
 void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st) {
-  if (a.dh > 256) fail(GLM_DIMENSION, "glmmodel", "head dim > 256 unsupported");
-  const size_t smem = (kPfThreads / 32) * a.dh * sizeof(float);
-  k_attn_prefill<<<dim3((a.n + kPfRows - 1) / kPfRows, a.heads), kPfThreads, smem, st>>>(a);
-  LAUNCH_CHECK("k_attn_prefill");
+  const dim3 grid((a.n + kFaRows - 1) / kFaRows, a.heads);
+  auto go = [&](auto kernel, int dh) {
+    const size_t smem = static_cast<size_t>(kFaRows + 4 * kFaKeys) * (dh + 8) * sizeof(__half);
+    CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kernel<<<grid, kFaThreads, smem, st>>>(a);
+  };
+  if (a.dh == 128) go(k_attn_prefill_tc<128>, 128);
+  else if (a.dh == 64) go(k_attn_prefill_tc<64>, 64);
+  else fail(GLM_DIMENSION, "glmmodel", "prefill attention supports head_dim 64 or 128");
+  LAUNCH_CHECK("k_attn_prefill_tc");
 }
 
 void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st) {

@@ -219,3 +219,24 @@ def test_contract_errors(int8_row):
         m.decode_step([999], [0])
     m.prefill(PREFIX[:10], list(range(10)), logits=False)
     assert m.cached_length() == 10
+
+
+@pytest.mark.parametrize("prefix_len,gen", [(200, 0), (150, 60), (63, 2)])
+def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
+    """Tensor-core flash prefill (block.cu k_attn_prefill_tc) at head_dim 128 over several
+    64-key blocks: bidirectional prefix, causal generation rows, and a context length that
+    straddles block boundaries (j < max(C, i + 1), corruption.cpp:338-367)."""
+    p, m, _ = build(4, "column", layers=2, hidden=256, heads=2, vocab=300, seed=9, max_ctx=320)
+    rng = np.random.default_rng(prefix_len)
+    prefix = [int(v) for v in rng.integers(6, 290, size=prefix_len)]
+    gen_toks = [int(v) for v in rng.integers(6, 290, size=gen)]
+    sample = O.gmask_sample(prefix, gen_toks)
+    ref, at, ft, zero = oracle_rows(p, sample)
+    m.reset()
+    m.enable_taps(True)
+    lg = m.prefill(sample["tokens"], sample["positions"], sample["context_length"])
+    pa, pf = m.taps(sample["n"])
+    m.enable_taps(False)
+    check_taps(pa, at)
+    check_taps(pf, ft)
+    check_logits(lg.astype(np.float64), ref, zero)
