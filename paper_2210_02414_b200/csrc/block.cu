@@ -761,6 +761,106 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
   }
 }
 
+// Tensor-core head for 2..16 rows (bf16 table): logits = h E^T on mma.sync.m16n8k16.bf16.
+// A warp owns 16 vocab rows; per 32-wide k block each lane loads 16 contiguous bytes of
+// two E rows (A) and of one h row per 8-token tile (B). The k order inside the block is
+// permuted identically for A and B (lane t's bytes 8t..8t+7 feed k-tile halves), so every
+// load is a plain 16-byte vector load and the dot products are unchanged.
+template <int NTT>
+__global__ void __launch_bounds__(kHeadThreads) k_head_tc(HeadArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* E = static_cast<const __nv_bfloat16*>(a.E);
+  const int64_t ntile = (a.vocab_local + 15) / 16;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kHeadThreads / 32);
+  for (int m0 = 0; m0 < a.M; m0 += 8 * NTT) {
+    const int mg = min(8 * NTT, a.M - m0);
+    unsigned long long best[NTT][2];
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt) best[nt][0] = best[nt][1] = 0ull;
+    // token rows of this lane's B fragments (duplicates beyond the batch are discarded)
+    const __nv_bfloat16* hrow[NTT];
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt) hrow[nt] = a.hb + static_cast<int64_t>(m0 + min(nt * 8 + g, mg - 1)) * a.d + 8 * t;
+    for (int64_t tile = static_cast<int64_t>(blockIdx.x) * (kHeadThreads / 32) + warp; tile < ntile; tile += nwarps) {
+      const int64_t v0 = tile * 16;
+      const int64_t va = min(v0 + g, a.vocab_local - 1), vb = min(v0 + g + 8, a.vocab_local - 1);
+      const uint4* ea = reinterpret_cast<const uint4*>(E + (a.vocab_offset + va) * a.d + 8 * t);
+      const uint4* eb = reinterpret_cast<const uint4*>(E + (a.vocab_offset + vb) * a.d + 8 * t);
+      float acc[NTT][4];
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+      constexpr int U = 4;  // 32-wide k blocks in flight
+      for (int64_t k0 = 0; k0 < a.d; k0 += 32 * U) {
+        uint4 ra[U], rb[U], rh[U][NTT];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t kb = (k0 + 32 * u) / 8;
+          const bool ok = k0 + 32 * u < a.d;
+          ra[u] = ok ? ld_stream(ea + kb) : make_uint4(0, 0, 0, 0);
+          rb[u] = ok ? ld_stream(eb + kb) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int nt = 0; nt < NTT; ++nt)
+            rh[u][nt] = ok ? *reinterpret_cast<const uint4*>(hrow[nt] + k0 + 32 * u) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int nt = 0; nt < NTT; ++nt) {
+            // k-tile 0: bytes 0..7 of each 16-byte group, k-tile 1: bytes 8..15
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};"
+                : "+f"(acc[nt][0]), "+f"(acc[nt][1]), "+f"(acc[nt][2]), "+f"(acc[nt][3])
+                : "r"(ra[u].x), "r"(rb[u].x), "r"(ra[u].y), "r"(rb[u].y), "r"(rh[u][nt].x), "r"(rh[u][nt].y));
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};"
+                : "+f"(acc[nt][0]), "+f"(acc[nt][1]), "+f"(acc[nt][2]), "+f"(acc[nt][3])
+                : "r"(ra[u].z), "r"(rb[u].z), "r"(ra[u].w), "r"(rb[u].w), "r"(rh[u][nt].z), "r"(rh[u][nt].w));
+          }
+      }
+      // acc[nt][0..1]: vocab row v0+g, tokens nt*8+2t+{0,1}; acc[nt][2..3]: row v0+g+8
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int m = nt * 8 + 2 * t + (e & 1);
+          const int64_t v = v0 + g + 8 * (e >> 1);
+          if (m < mg && v < a.vocab_local) {
+            if (a.logits) a.logits[static_cast<int64_t>(m0 + m) * a.ld_logits + a.vocab_offset + v] = acc[nt][e];
+            const unsigned long long key = argmax_key(acc[nt][e], static_cast<int>(a.vocab_offset + v));
+            best[nt][e & 1] = key > best[nt][e & 1] ? key : best[nt][e & 1];
+          }
+        }
+    }
+    // reduce each token's best over the 8 lanes (g) that hold it, then one atomic per token
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        unsigned long long b = best[nt][e];
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+          b = ob > b ? ob : b;
+        }
+        const int m = nt * 8 + 2 * t + e;
+        if (g == 0 && m < mg && b) atomicMax(a.argmax + m0 + m, b);
+      }
+  }
+}
+
+__global__ void k_rows_to_bf16(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 2; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x * 2)
+    *reinterpret_cast<__nv_bfloat162*>(y + i) = __floats2bfloat162_rn(x[i], x[i + 1]);
+}
+
 __global__ void k_argmax_finish(unsigned long long* __restrict__ keys, int* __restrict__ tokens, int M) {
   pdl_wait();
   pdl_trigger();
@@ -844,6 +944,18 @@ void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
   }
   if (smem > 227 * 1024) fail(GLM_DIMENSION, "glmmodel", "hidden too large for head kernel");
   if (a.d % 256 != 0) fail(GLM_DIMENSION, "glmmodel", "head kernel needs hidden % 256 == 0");
+  if (bf16 && a.M > 1 && a.hb) {
+    // batched rows: tensor cores on a bf16 copy of h
+    const int64_t n = static_cast<int64_t>(a.M) * a.d;
+    launch_k(k_rows_to_bf16, dim3(static_cast<unsigned>(std::min<int64_t>((n / 2 + 255) / 256, 1184))), dim3(256), 0, st,
+             a.h, a.hb, n);
+    LAUNCH_CHECK("k_rows_to_bf16");
+    const int grid_tc = kNumSMs * 8;
+    if (a.M <= 8) launch_k(k_head_tc<1>, dim3(grid_tc), dim3(kHeadThreads), 0, st, a);
+    else launch_k(k_head_tc<2>, dim3(grid_tc), dim3(kHeadThreads), 0, st, a);
+    LAUNCH_CHECK("k_head_tc");
+    return;
+  }
   const int per_sm = static_cast<int>(std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
   const int grid = kNumSMs * (per_sm < 1 ? 1 : per_sm);
   if (bf16) launch_k(k_head<__nv_bfloat16>, dim3(grid), dim3(kHeadThreads), smem, st, a);

@@ -98,6 +98,7 @@ struct HeadArgs {
   float* logits;            // optional [M][ld_logits], written at column vocab_offset + v
   int64_t ld_logits;
   unsigned long long* argmax;  // [M] packed (value, ~index), zero-initialised
+  __nv_bfloat16* hb = nullptr;  // [M][d] scratch: bf16 copy of h for the tensor-core head
 };
 
 void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,

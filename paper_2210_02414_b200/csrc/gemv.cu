@@ -332,6 +332,167 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
   }
 }
 
+// ---- multi-token variant (2..16 tokens: batched decode) ----------------------------------
+// At M tokens every weight fragment feeds NT = ceil(M/8) MMAs, and the activations, not the
+// weights, dominate on-chip traffic if each warp fetches its own: a CTA therefore works on
+// CTA-items = (16 consecutive row tiles, one k-slice), one row tile per warp, and the M
+// activation rows of the k-slice are bulk-copied once per CTA-item into a double-buffered
+// shared-memory slice (next item's slice in flight while the current one is consumed).
+// Weights stream through the per-warp TMA rings exactly as in the other variants.
+constexpr int kMkStages = 2;
+constexpr int kMkSliceBytes = 48 * 1024;  // one activation-slice buffer (all x vectors, all tokens)
+
+template <int BITS, int NT>
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx) {
+  constexpr int CHUNK = BITS == 4 ? 512 : 1024;
+  constexpr int U = kStageBytes / CHUNK;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = static_cast<int>(a.nch), ksplit = a.ksplit, M = a.M;
+  const int nrt = static_cast<int>(a.nrt);
+  uint8_t* ring = smem + static_cast<size_t>(warp) * kMkStages * kStageBytes;
+  uint8_t* xbuf = smem + static_cast<size_t>(kTWarps) * kMkStages * kStageBytes;  // [2][kMkSliceBytes]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * kMkSliceBytes);          // [2]
+  uint64_t* bars = xbar + 2 + warp * kMkStages;
+  if (lane == 0) {
+    for (int q = 0; q < kMkStages; ++q) mbar_init(bars + q, 1);
+    if (warp == 0) {
+      mbar_init(xbar, 1);
+      mbar_init(xbar + 1, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t policy, keep;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const int ngroups = (nrt + kTWarps - 1) / kTWarps;
+  const int nitems = ngroups * ksplit;
+  auto slice = [&](int s, int& c0, int& c1) {
+    c0 = nch * s / ksplit;
+    c1 = nch * (s + 1) / ksplit;
+  };
+  // weight producer (lane 0 of each warp) walks this CTA's items in consumption order
+  int pj = blockIdx.x, pc = 0, pc1 = 0, prt = -1, pslot = 0;
+  auto pitem = [&]() {  // position the producer on item pj (skipping items where this warp idles)
+    while (pj < nitems) {
+      prt = (pj / ksplit) * kTWarps + warp;
+      slice(pj % ksplit, pc, pc1);
+      if (prt < nrt) return;
+      pj += gridDim.x;
+    }
+  };
+  pitem();
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  auto issue = [&]() {
+    if (pj >= nitems) return;
+    const int n = min(U, pc1 - pc);
+    const uint8_t* src = wbase + (static_cast<int64_t>(prt) * nch + pc) * CHUNK;
+    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(n * CHUNK));
+    bulk_g2s(ring + pslot * kStageBytes, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    pslot = pslot + 1 == kMkStages ? 0 : pslot + 1;
+    pc += n;
+    if (pc >= pc1) {
+      pj += gridDim.x;
+      pitem();
+    }
+  };
+  if (lane == 0)
+    for (int q = 0; q < kMkStages; ++q) issue();
+  pdl_wait();
+  pdl_trigger();
+  // activation slices: buffer b holds [nx][M][chunks of the slice][128 B]
+  auto load_x = [&](int local, int item) {
+    int c0, c1;
+    slice(item % ksplit, c0, c1);
+    const int nck = c1 - c0;
+    const int b = local & 1;
+    mbar_expect_tx(xbar + b, static_cast<uint32_t>(nx * M * nck * 128));
+    for (int v = 0; v < nx; ++v)
+      for (int m = 0; m < M; ++m) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2) +
+                             (static_cast<int64_t>(m) * nch + c0) * 128;
+        bulk_g2s(xbuf + b * kMkSliceBytes + ((v * M + m) * nck) * 128, src, static_cast<uint32_t>(nck * 128), xbar + b,
+                 keep);
+      }
+  };
+  if (threadIdx.x == 0) {
+    if (static_cast<int>(blockIdx.x) < nitems) load_x(0, blockIdx.x);
+    if (static_cast<int>(blockIdx.x + gridDim.x) < nitems) load_x(1, blockIdx.x + gridDim.x);
+  }
+  int cslot = 0;
+  uint32_t cpar = 0;
+  int local = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
+    const int s = item % ksplit;
+    const int rt = (item / ksplit) * kTWarps + warp;
+    int c0, c1;
+    slice(s, c0, c1);
+    const int nck = c1 - c0;
+    const int b = local & 1;
+    mbar_wait(xbar + b, (local >> 1) & 1);
+    if (rt < nrt) {
+      const int v = rt < a.rt_split ? 0 : nx - 1;
+      const uint8_t* xrow[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        xrow[nt] = xbuf + b * kMkSliceBytes + ((v * M + min(nt * 8 + g, M - 1)) * nck) * 128 + t * 32;
+      float acc[4][NT][4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[h][nt][i] = 0.f;
+      for (int c = 0; c < nck; c += U) {
+        const int n = min(U, nck - c);
+        mbar_wait(bars + cslot, cpar);
+        const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
+        auto chunk = [&](int u) {
+          uint4 wv[BITS == 4 ? 1 : 2];
+          wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK);
+          if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(st + u * CHUNK + 512);
+          uint4 xv[NT][2];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint4* xa = reinterpret_cast<const uint4*>(xrow[nt] + (c + u) * 128);
+            xv[nt][0] = xa[0];
+            xv[nt][1] = xa[1];
+          }
+          compute_chunk4<BITS, NT>(wv, xv, acc);
+        };
+        if (n == U) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) chunk(u);
+        } else {
+          for (int u = 0; u < n; ++u) chunk(u);
+        }
+        __syncwarp();
+        if (cslot + 1 == kMkStages) {
+          cslot = 0;
+          cpar ^= 1u;
+        } else {
+          ++cslot;
+        }
+        if (lane == 0) issue();
+      }
+      float* out = a.partial + static_cast<int64_t>(s) * M * a.Np + static_cast<int64_t>(rt) * kTileN;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int m = nt * 8 + 2 * t + (i & 1);
+          const int row = g + 8 * (i >> 1);
+          if (m < M)
+            out[static_cast<int64_t>(m) * a.Np + row] = (acc[0][nt][i] + acc[1][nt][i]) + (acc[2][nt][i] + acc[3][nt][i]);
+        }
+    }
+    __syncthreads();  // every warp is done with activation buffer b
+    if (threadIdx.x == 0 && item + 2 * static_cast<int>(gridDim.x) < nitems) load_x(local + 2, item + 2 * gridDim.x);
+  }
+}
+
 // ---- single-token variant (batch-1 decode, the headline path) -----------------------------
 // As k_gemv_tma with M = 1, but the whole activation vector (Kp fp16 = 24 KB at K = 12288,
 // 64 KB at K = 32768; twice that for a fused W1|V launch with distinct kRow folds) is
@@ -544,8 +705,29 @@ int m1_warps() {
   return w;
 }
 
-GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits) {
+GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
   GemvPlan p;
+  if (M >= 2) {
+    // multi-token kernel: CTA-items of 16 row tiles x one k-slice; the slice of all M
+    // activation rows (nx vectors) must fit one shared-memory buffer
+    p.warps = kTWarps;
+    const int64_t kmax = std::max<int64_t>(1, kMkSliceBytes / (static_cast<int64_t>(nx) * M * 128));
+    const int64_t ks_min = (nch + kmax - 1) / kmax;
+    const int64_t ngroups = (nrt + kTWarps - 1) / kTWarps;
+    double best = -1.0;
+    for (int64_t ks = ks_min; ks <= std::min<int64_t>(nch, ks_min + 24); ++ks) {
+      const int64_t items = ngroups * ks;
+      const int64_t waves = (items + kNumSMs - 1) / kNumSMs;
+      const double eff = static_cast<double>(items) / static_cast<double>(waves * kNumSMs) - 0.004 * static_cast<double>(ks);
+      if (eff > best + 1e-9) {
+        best = eff;
+        p.ksplit = static_cast<int>(ks);
+      }
+    }
+    const int64_t items = ngroups * p.ksplit;
+    p.grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
+    return p;
+  }
   p.warps = (M == 1 && bits == 4) ? m1_warps() : kTWarps;
   const int64_t total_warps = static_cast<int64_t>(kNumSMs) * p.warps;
   double best = -1.0;
@@ -566,13 +748,39 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits) {
   return p;
 }
 
-GemvPlan plan_gemv(const QLayout& L, int M) { return plan_gemv(L.nrt, L.nch, M, L.bits); }
+GemvPlan plan_gemv(const QLayout& L, int M) { return plan_gemv(L.nrt, L.nch, M, L.bits, 1); }
 
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st) {
   if (M < 1 || M > 16) fail(GLM_DIMENSION, "qlinear", "GEMV path takes 1..16 rows, got " + std::to_string(M));
   GemvArgs a{static_cast<const uint4*>(op.codes), reinterpret_cast<const uint4*>(op.xf),
              reinterpret_cast<const uint4*>(op.xf2 ? op.xf2 : op.xf), op.xf2 ? op.rt_split : op.nrt, partial,
              op.nrt, op.nch, op.nrt * kTileN, M, p.ksplit};
+  if (M >= 2) {
+    const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
+    const int64_t slice_max = (op.nch + p.ksplit - 1) / p.ksplit;
+    if (slice_max * 128 * M * nx > kMkSliceBytes || p.warps != kTWarps)
+      fail(GLM_CONTRACT, "qlinear", "GEMV plan does not match the multi-token kernel (plan for this M and x count)");
+    const size_t smem1 = static_cast<size_t>(kTWarps) * kMkStages * kStageBytes + 2 * kMkSliceBytes +
+                         (2 + kTWarps * kMkStages) * 8;
+    static bool attr_mk = false;
+    if (!attr_mk) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+      attr_mk = true;
+    }
+    const dim3 gridm(p.grid), blockm(kTWarps * 32);
+    if (op.bits == 4) {
+      if (M <= 8) launch_k(k_gemv_mk<4, 1>, gridm, blockm, smem1, st, a, nx);
+      else launch_k(k_gemv_mk<4, 2>, gridm, blockm, smem1, st, a, nx);
+    } else {
+      if (M <= 8) launch_k(k_gemv_mk<8, 1>, gridm, blockm, smem1, st, a, nx);
+      else launch_k(k_gemv_mk<8, 2>, gridm, blockm, smem1, st, a, nx);
+    }
+    LAUNCH_CHECK("k_gemv_mk");
+    return;
+  }
   const size_t smem = static_cast<size_t>(kTWarps) * kStages * (kStageBytes + 8);
   static bool attr = false;
   if (!attr) {

@@ -58,7 +58,8 @@ struct GemvPlan {
 };
 // Split-K plan for an M-row GEMV; the single-token INT4 kernel runs more warps per SM.
 GemvPlan plan_gemv(const QLayout& L, int M);
-GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits);
+// nx: activation vectors the launch reads (2 for a fused W1|V launch with distinct kRow folds)
+GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx = 1);
 // One decode-GEMV launch (M <= 16) over nrt row tiles of contiguous device-layout codes;
 // row tiles >= rt_split read x_frag xf2 (fused W1|V launch, distinct kRow folds).
 struct GemvOp {

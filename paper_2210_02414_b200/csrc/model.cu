@@ -31,8 +31,8 @@ namespace {
 
 struct Linear {
   QWeightDev w;
-  GemvPlan plan1, planN;  // decode GEMV plans for 1 and 2..16 rows
-  const GemvPlan& plan(int M) const { return M == 1 ? plan1 : planN; }
+  GemvPlan plans[17];  // decode GEMV plan per row count 1..16
+  const GemvPlan& plan(int M) const { return plans[M < 1 ? 1 : (M > 16 ? 16 : M)]; }
   int64_t Kfull = 0, Nfull = 0;
   ShardSpec shard{};
   bool loaded = false;
@@ -123,7 +123,7 @@ struct glm_model {
 
   // row buffers (grown for prefill)
   int64_t rows_cap = 0;
-  DeviceBuffer h, xf_qkv, xf_out, xf_w1, xf_v, xf_w2, logits, taps_attn, taps_ffn;
+  DeviceBuffer h, h_bf16, xf_qkv, xf_out, xf_w1, xf_v, xf_w2, logits, taps_attn, taps_ffn;
   DeviceBuffer y_qkv, q_rot, attn_out, y_out, y_a, y_b, y_ffn, ar_buf;
   DeviceBuffer partial;
   int64_t partial_cap = 0;
@@ -205,8 +205,7 @@ struct glm_model {
         lin.w.col_scale = alloc<float>(lin.w.L.Np);
         lin.w.row_scale = alloc<float>(lin.w.L.Kp);
         lin.w.scales64 = alloc<double>(lin.w.nscales);
-        lin.plan1 = plan_gemv(lin.w.L, 1);
-        lin.planN = plan_gemv(lin.w.L, 2);
+        for (int M = 1; M <= 16; ++M) lin.plans[M] = plan_gemv(lin.w.L, M);
       };
       mk(ly.lin[QKV], d, 3 * d, d, 3 * dl, ShardSpec{d, dl, static_cast<int64_t>(r) * dl, 0});
       mk(ly.lin[OUT], d, d, dl, d, ShardSpec{d, d, 0, static_cast<int64_t>(r) * dl});
@@ -227,8 +226,9 @@ struct glm_model {
       k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln1g, d, 1.f);
       k_fill<<<grid_of(d), 256, 0, st>>>(ly.ln2g, d, 1.f);
     }
-    for (int M : {1, 2})
-      fused_plans[M - 1] = plan_gemv(layers[0].lin[W1].w.L.nrt + layers[0].lin[VV].w.L.nrt, layers[0].lin[W1].w.L.nch, M, bits);
+    for (int M = 1; M <= 16; ++M)
+      fused_plans[M] = plan_gemv(layers[0].lin[W1].w.L.nrt + layers[0].lin[VV].w.L.nrt, layers[0].lin[W1].w.L.nch, M,
+                                 bits, axis == GLM_AXIS_ROW ? 2 : 1);
     E = head_bf16 ? static_cast<void*>(alloc<__nv_bfloat16>(static_cast<int64_t>(V) * d))
                   : static_cast<void*>(alloc<float>(static_cast<int64_t>(V) * d));
     // RoPE table in double -> float (tensor.cpp:335-341: theta_j = 10000^(-2j/dh))
@@ -260,8 +260,8 @@ struct glm_model {
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
 
-  GemvPlan fused_plans[2];
-  const GemvPlan& fused_plan(int M) const { return fused_plans[M == 1 ? 0 : 1]; }
+  GemvPlan fused_plans[17];
+  const GemvPlan& fused_plan(int M) const { return fused_plans[M < 1 ? 1 : (M > 16 ? 16 : M)]; }
 
   static int default_ffn(int hidden, int heads) {  // model.cpp:30-37
     if ((8 * hidden) % 3 == 0) return (8 * hidden) / 3;
@@ -293,6 +293,7 @@ struct glm_model {
     zero(xf_v, nt * ly.lin[VV].w.L.Kp * 2);
     zero(xf_w2, nt * ly.lin[W2].w.L.Kp * 2);
     zero(logits, rows * V * 4);
+    zero(h_bf16, rows * d * 2);
     pool.emplace_back(rows * 8);
     d_argmax_rows = pool.back().as<unsigned long long>();
     CUDA_CHECK(cudaMemsetAsync(d_argmax_rows, 0, rows * 8, st));
@@ -312,13 +313,13 @@ struct glm_model {
       const GemvPlan p = M <= 16 ? plan_gemv(lin.w.L, static_cast<int>(M)) : plan_qmm(lin.w.L, static_cast<int>(M));
       need = std::max<int64_t>(need, static_cast<int64_t>(p.ksplit) * M * lin.w.L.Np);
     }
-    for (int mm : {1, 2})
-      need = std::max<int64_t>(need, static_cast<int64_t>(fused_plans[mm - 1].ksplit) * std::min<int64_t>(M, 16) *
+    for (int mm = 1; mm <= std::min<int64_t>(M, 16); ++mm) {
+      need = std::max<int64_t>(need, static_cast<int64_t>(fused_plans[mm].ksplit) * mm *
                                          (layers[0].lin[W1].w.L.Np + layers[0].lin[VV].w.L.Np));
-    for (int i = 0; i < 5; ++i)
-      for (int mm : {1, 2})
-        need = std::max<int64_t>(need, static_cast<int64_t>(layers[0].lin[i].plan(mm).ksplit) * std::min<int64_t>(M, 16) *
+      for (int i = 0; i < 5; ++i)
+        need = std::max<int64_t>(need, static_cast<int64_t>(layers[0].lin[i].plan(mm).ksplit) * mm *
                                            layers[0].lin[i].w.L.Np);
+    }
     if (need <= partial_cap) return;
     drop_graphs();
     partial.alloc(need * 4);
@@ -475,11 +476,12 @@ struct glm_model {
       ln.eps = static_cast<float>(eps);
       ln.d = d;
       ln.x0 = xout(xf_w1.as<__half>(), w1);
-      ln.x1 = xout(xf_v.as<__half>(), v);
+      ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v) : XOut{};  // W1 and V share x unless kRow
       ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
       ln.zero_sublayer = zero_sub;
       launch_deepnorm_ln(ln, B, st);
-      GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(), xf_v.as<__half>(), w1.w.L.nrt};
+      GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
+                axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
       gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
       ActArgs act;
       const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
@@ -520,6 +522,7 @@ struct glm_model {
     ha.logits = logit_out;
     ha.ld_logits = V;
     ha.argmax = d_argmax;
+    ha.hb = h_bf16.as<__nv_bfloat16>();
     launch_head(ha, head_bf16, st);
     if (tp_size > 1) {
       comm->allreduce_max_u64(d_argmax, M, st);
@@ -864,7 +867,8 @@ glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup
         gemv_launch(ly.lin[QKV].w, m->xf_qkv.as<__half>(), batch, m->partial.as<float>(), ly.lin[QKV].plan(batch), m->st);
         gemv_launch(ly.lin[OUT].w, m->xf_out.as<__half>(), batch, m->partial.as<float>(), ly.lin[OUT].plan(batch), m->st);
         GemvOp op{ly.lin[W1].w.codes, m->bits, ly.lin[W1].w.L.nrt + ly.lin[VV].w.L.nrt, ly.lin[W1].w.L.nch,
-                  m->xf_w1.as<__half>(), m->xf_v.as<__half>(), ly.lin[W1].w.L.nrt};
+                  m->xf_w1.as<__half>(), m->axis == GLM_AXIS_ROW ? m->xf_v.as<__half>() : m->xf_w1.as<__half>(),
+                  ly.lin[W1].w.L.nrt};
         gemv_launch(op, batch, m->partial.as<float>(), m->fused_plan(batch), m->st);
         gemv_launch(ly.lin[W2].w, m->xf_w2.as<__half>(), batch, m->partial.as<float>(), ly.lin[W2].plan(batch), m->st);
       }

@@ -240,3 +240,34 @@ def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
     check_taps(pa, at)
     check_taps(pf, ft)
     check_logits(lg.astype(np.float64), ref, zero)
+
+
+@pytest.mark.parametrize("batch", [2, 9, 16])
+def test_batched_decode_bf16_head_tensor_cores(batch):
+    """Batched decode with the bf16 tied head (block.cu k_head_tc, h rounded to bf16): the
+    logits of every sequence match its own single-sequence decode (fp32-h head) within the
+    bf16 rounding of h, and greedy tokens agree wherever the top-2 margin exceeds it."""
+    cfg = glm.GLMConfig(num_layers=2, hidden=256, num_heads=2, vocab=1000)
+    mb = glm.Model(cfg, bits=4, axis="column", max_batch=batch, max_ctx=64, head_bf16=True)
+    ms = glm.Model(cfg, bits=4, axis="column", max_batch=1, max_ctx=64, head_bf16=True)
+    mb.init_synthetic(3)
+    ms.init_synthetic(3)
+    rng = np.random.default_rng(batch)
+    prefixes = [[int(v) for v in rng.integers(6, 990, size=int(rng.integers(5, 30)))] for _ in range(batch)]
+    for b, pre in enumerate(prefixes):
+        pos, C = glm.gmask_layout(len(pre), 0)
+        mb.prefill(pre + [2], pos[:C], C, seq=b, logits=False)
+    toks = [3] * batch
+    poss = [len(pre) for pre in prefixes]
+    nb, lb = mb.decode_step(toks, poss)
+    for b, pre in enumerate(prefixes):
+        ms.reset()
+        pos, C = glm.gmask_layout(len(pre), 0)
+        ms.prefill(pre + [2], pos[:C], C, logits=False)
+        ns, ls = ms.decode_step([3], [len(pre)])
+        err = np.abs(lb[b] - ls[0]).max()
+        scale = np.abs(ls[0]).max()
+        assert err <= 1e-2 * scale, (b, err, scale)
+        top = np.sort(ls[0])[-2:]
+        if top[1] - top[0] > 4 * err:
+            assert int(nb[b]) == int(ns[0]) == int(np.argmax(ls[0]))

@@ -3,7 +3,7 @@ y = x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155).
 
 Two bars: (1) exact-arithmetic check against a float64 evaluation of the kernel's own
 contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only fp32
-accumulation error remains: <= 2e-6 of max|y|, except the single-token INT4 kernel, which
+accumulation error remains: <= 2e-6 of max|y|, except the single-token INT4 GEMV, which
 accumulates offset-binary codes (1032 + code) and removes 1032 * sum(x) afterwards, so its
 fp32 accumulator carries the larger offset term: <= 2e-4 of max|y| (gemv.cu, dq4_raw);
 (2) the reference check against the oracle's float64 x . dequantize(q),
