@@ -108,6 +108,12 @@ glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out);
  * made with the environment variable GLM_QMM_TRACE set. */
 glm_status glm_debug_qmm_trace(long long* host_out);
 
+/* Diagnostics: device timeline. While a trace runs, thread 0 of every CTA of the decode
+ * kernels appends (globaltimer ns, tag << 32 | block << 8 | smid) pairs; stop copies up to
+ * `capacity` pairs (2 * capacity uint64) to host_out and returns the count. */
+glm_status glm_debug_trace_start(int64_t capacity);
+glm_status glm_debug_trace_stop(uint64_t* host_out, int64_t capacity, int64_t* count);
+
 /* y[M, cols] = x[M, rows] . dequantize(q), fp32 in/out, device pointers. M >= 1. */
 glm_status glm_qlinear(const glm_qweight* q, const float* x, int64_t M, float* y, void* stream);
 /* Same with host buffers (H2D, kernel, D2H inside). */

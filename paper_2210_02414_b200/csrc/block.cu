@@ -15,9 +15,15 @@
 
 namespace glm {
 
+GLM_TRACE_TU(block)
+
 namespace {
 
 constexpr float kInvSqrt2 = 0.70710678118654752440f;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
 // Sum over ksplit partials of element n of row m, times the group scale.
 __device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t n) {
@@ -77,9 +83,10 @@ constexpr int kLnCluster = 8;
 constexpr int kLnThreads = 384;
 constexpr int kLnPairs = 4;  // pairs per thread: d <= 2 * 4 * 384 * 8 = 24576
 
-// Cluster-wide sum of (a, b): CTA partials go to shared memory, then after one cluster
-// barrier every warp reads the kLnCluster remote partials in parallel (one lane each).
-__device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* slot) {
+// Cluster-wide sum of (a, b): each CTA pushes its partial into slot[rank] of every CTA of
+// the cluster (distributed shared memory stores), one cluster barrier (release/acquire),
+// then every CTA sums its local slots in rank order: identical on every CTA and every run.
+__device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* slots) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   v.x = warp_sum(v.x);
@@ -91,70 +98,90 @@ __device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* sl
     float2 t = l < kLnThreads / 32 ? red[l] : make_float2(0.f, 0.f);
     t.x = warp_sum(t.x);
     t.y = warp_sum(t.y);
-    if (l == 0) *slot = t;
+    const unsigned rank = cluster.block_rank();
+    if (l < kLnCluster) *cluster.map_shared_rank(slots + rank, l) = t;
   }
   cluster.sync();
-  float2 r = l < kLnCluster ? *cluster.map_shared_rank(slot, l) : make_float2(0.f, 0.f);
-  // fixed-order (butterfly) combine: identical on every CTA and every run
-  r.x = warp_sum(r.x);
-  r.y = warp_sum(r.y);
-  cluster.sync();  // no CTA leaves while its slot may still be read
+  float2 r = make_float2(0.f, 0.f);
+  for (int i = 0; i < kLnCluster; ++i) {
+    r.x += slots[i].x;
+    r.y += slots[i].y;
+  }
   return r;
 }
 
 __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
+  trace_point(20);
   __shared__ float2 red[kLnThreads / 32];
-  __shared__ float2 slot;
+  __shared__ float2 slots[kLnCluster];
   namespace cg = cooperative_groups;
   const int rank = static_cast<int>(cg::this_cluster().block_rank());
   const int m = blockIdx.x / kLnCluster;
   const int64_t npairs = a.d / 2;
   const int64_t per = (npairs + kLnCluster - 1) / kLnCluster;
   const int64_t p0 = rank * per, p1 = min(npairs, p0 + per);
-  // parameters do not depend on the predecessor: fetch them before waiting on it
-  float2 gn[kLnPairs], bs[kLnPairs];
+  // everything that does not depend on the predecessor GEMV (LN parameters, the scale
+  // vector, the residual written two kernels ago) is fetched before waiting on it
+  const float* __restrict__ hrow = a.h + static_cast<int64_t>(m) * a.d;
+  float2 gn[kLnPairs], bs[kLnPairs], sc[kLnPairs], hv[kLnPairs];
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
     if (p < p1) {
       gn[i] = *reinterpret_cast<const float2*>(a.gain + 2 * p);
       bs[i] = *reinterpret_cast<const float2*>(a.bias + 2 * p);
+      sc[i] = a.in.scale ? *reinterpret_cast<const float2*>(a.in.scale + 2 * p) : make_float2(1.f, 1.f);
+      hv[i] = *reinterpret_cast<const float2*>(hrow + 2 * p);
     }
   }
   pdl_wait();
   pdl_trigger();
-  const float* __restrict__ hrow = a.h + static_cast<int64_t>(m) * a.d;
+  trace_point(21);
+  // split-K partials: all loads of the thread issued back to back (4 splits per batch)
+  float2 y[kLnPairs];
+#pragma unroll
+  for (int i = 0; i < kLnPairs; ++i) y[i] = make_float2(0.f, 0.f);
+  if (!a.zero_sublayer) {
+    for (int s0 = 0; s0 < a.in.ksplit; s0 += 4) {
+      float2 v[4][kLnPairs];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < kLnPairs; ++i) {
+          const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+          v[u][i] = (s0 + u < a.in.ksplit && p < p1)
+                        ? *reinterpret_cast<const float2*>(a.in.p + static_cast<int64_t>(s0 + u) * a.in.split_stride +
+                                                           m * a.in.ld + 2 * p)
+                        : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < kLnPairs; ++i) {
+          y[i].x += v[u][i].x;
+          y[i].y += v[u][i].y;
+        }
+    }
+  }
   float2 z[kLnPairs];
   float2 acc = make_float2(0.f, 0.f);
-  // every load of the slice first (partials of all splits + residual)
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
     z[i] = make_float2(0.f, 0.f);
     if (p < p1) {
-      const int64_t n = 2 * p;
-      float2 y = make_float2(0.f, 0.f);
-      if (!a.zero_sublayer) {
-        for (int s = 0; s < a.in.ksplit; ++s) {
-          const float2 v = *reinterpret_cast<const float2*>(a.in.p + static_cast<int64_t>(s) * a.in.split_stride +
-                                                            m * a.in.ld + n);
-          y.x += v.x;
-          y.y += v.y;
-        }
-        if (a.in.scale) {
-          y.x *= a.in.scale[n];
-          y.y *= a.in.scale[n + 1];
-        }
-      }
-      const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
-      z[i] = make_float2(a.alpha * hv.x + y.x, a.alpha * hv.y + y.y);
-      if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + n) = y;
+      y[i].x *= sc[i].x;
+      y[i].y *= sc[i].y;
+      z[i] = make_float2(a.alpha * hv[i].x + y[i].x, a.alpha * hv[i].y + y[i].y);
+      if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + 2 * p) = y[i];
       acc.x += z[i].x + z[i].y;
       acc.y += z[i].x * z[i].x + z[i].y * z[i].y;
     }
   }
   // one cluster reduction of (sum, sum of squares); biased variance (tensor.cpp:267)
-  const float2 tot = cluster_sum2(acc, red, &slot);
+  trace_point(23);
+  const float2 tot = cluster_sum2(acc, red, slots);
+  trace_point(24);
   const float inv_d = 1.f / static_cast<float>(a.d);
   const float mean = tot.x * inv_d;
   const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);
@@ -171,12 +198,15 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
       store_xfrag_pair(a.x1, m, n, o0, o1);
     }
   }
+  trace_point(22);
 }
 
 // ---- GeGLU activation: gelu(x W1) * (x V) (model.cpp:133-135, tensor.cpp:313-318) --------
 __global__ void k_geglu_act(ActArgs a) {
+  trace_point(40);
   pdl_wait();
   pdl_trigger();
+  trace_point(41);
   const int64_t pairs = static_cast<int64_t>(a.M) * (a.f / 2);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -191,6 +221,7 @@ __global__ void k_geglu_act(ActArgs a) {
     }
     store_xfrag_pair(a.xo, m, n, o[0], o[1]);
   }
+  trace_point(42);
 }
 
 // ---- decode attention (model.cpp:137-152 for the rows of the generation part) ----------
@@ -207,16 +238,19 @@ constexpr int kSplitKeys = 256;
 
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
+  trace_point(30);
   constexpr int NW = kAttnThreads / 32;
   constexpr int FPL = DH / 32;          // features per lane in the PV phase
   constexpr int LPK = DH / 8, KPW = 32 / LPK;
   __shared__ float q[DH];
-  __shared__ __align__(16) __half knew[DH];
-  __shared__ __align__(16) __half vnew[DH];
   __shared__ float p[kSplitKeys];
   __shared__ float red[NW];
   __shared__ float opart[NW][DH];
   __shared__ int last;
+  __shared__ __align__(8) uint64_t kvbar;
+  extern __shared__ __align__(128) __half kvs[];  // [2][kSplitKeys][DH]: this split's keys, values
+  __half* kst = kvs;
+  __half* vst = kvs + kSplitKeys * DH;
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cache length / position were written by earlier steps (complete before our predecessor ran)
@@ -229,43 +263,83 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
   float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (DH + 2);
-  {
-    // warm L2 with this split's cached rows (independent of the running qkv GEMV)
-    constexpr int LPR = DH * 2 / 128;  // 128-byte lines per row
-    for (int i = threadIdx.x; i < (kold - k0) * LPR; i += kAttnThreads) {
-      const int64_t off = static_cast<int64_t>(k0) * DH + static_cast<int64_t>(i) * 64;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(kc + off));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(vc + off));
+  // The cached rows of this split do not depend on the running qkv GEMV: one bulk copy
+  // each for K and V into shared memory, issued before the dependency wait.
+  const int n_old = max(0, kold - k0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&kvbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (n_old > 0) {
+      const uint32_t bytes = static_cast<uint32_t>(n_old) * DH * 2;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&kvbar)), "r"(2 * bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(kst)),
+                   "l"(kc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&kvbar))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(vst)),
+                   "l"(vc + static_cast<int64_t>(k0) * DH), "r"(bytes), "r"(smem_addr(&kvbar))
+                   : "memory");
+    }
+  }
+  // RoPE factors and the qkv column scales do not depend on the running GEMV either
+  const int jt = threadIdx.x < DH / 2 ? threadIdx.x : threadIdx.x - DH / 2;
+  float2 cs = make_float2(1.f, 0.f), sq = make_float2(1.f, 1.f), sk = sq, sv = sq;
+  if (threadIdx.x < DH) {
+    cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + jt];  // (cos, sin), tensor.cpp:357-363
+    const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jt;
+    if (a.qkv.scale) {
+      sq = *reinterpret_cast<const float2*>(a.qkv.scale + fq);
+      sk = *reinterpret_cast<const float2*>(a.qkv.scale + a.d_local + fq);
+      sv = *reinterpret_cast<const float2*>(a.qkv.scale + 2 * a.d_local + fq);
     }
   }
   pdl_wait();
   pdl_trigger();
+  trace_point(31);
 
   if (k0 < total) {
     const bool has_new = (len >= k0 && len < k1);
+    auto raw2 = [&](int64_t f) {  // split-K sum of columns (f, f+1), unscaled
+      float2 acc = make_float2(0.f, 0.f);
+      for (int s = 0; s < a.qkv.ksplit; ++s) {
+        const float2 v = *reinterpret_cast<const float2*>(a.qkv.p + static_cast<int64_t>(s) * a.qkv.split_stride +
+                                                          b * a.qkv.ld + f);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      return acc;
+    };
     // q pairs on threads [0, DH/2), the new key/value pair on threads [DH/2, DH)
     if (threadIdx.x < DH) {
       const int j = threadIdx.x;
-      const int jj = j < DH / 2 ? j : j - DH / 2;
-      const float2 cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + jj];  // (cos, sin), tensor.cpp:357-363
+      const int jj = jt;
       const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jj;
       if (j < DH / 2) {
-        const float qa = reduce_partial(a.qkv, b, fq), qb = reduce_partial(a.qkv, b, fq + 1);
+        const float2 qv = raw2(fq);
+        const float qa = qv.x * sq.x, qb = qv.y * sq.y;
         q[2 * jj] = (cs.x * qa - cs.y * qb) * inv_sqrt;
         q[2 * jj + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
       } else if (has_new) {
         const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
-        const float ka = reduce_partial(a.qkv, b, fk), kb = reduce_partial(a.qkv, b, fk + 1);
-        const float va = reduce_partial(a.qkv, b, fv), vb = reduce_partial(a.qkv, b, fv + 1);
+        const float2 kv2 = raw2(fk), vv2 = raw2(fv);
+        const float ka = kv2.x * sk.x, kb = kv2.y * sk.y;
+        const float va = vv2.x * sv.x, vb = vv2.y * sv.y;
         const __half2 kh = __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
         const __half2 vh = __floats2half2_rn(va, vb);
         *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jj) = kh;
         *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * jj) = vh;
-        *reinterpret_cast<__half2*>(knew + 2 * jj) = kh;
-        *reinterpret_cast<__half2*>(vnew + 2 * jj) = vh;
+        *reinterpret_cast<__half2*>(kst + (len - k0) * DH + 2 * jj) = kh;
+        *reinterpret_cast<__half2*>(vst + (len - k0) * DH + 2 * jj) = vh;
       }
     }
+    if (n_old > 0)
+      asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W_%=;\n}\n" ::"r"(
+                       smem_addr(&kvbar))
+                   : "memory");
     __syncthreads();
+    trace_point(33);
     // ---- scores: LPK lanes per key, one 16-byte load each ----
     const int sub = lane % LPK, kin = lane / LPK;
     float qr[8];
@@ -287,8 +361,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         const int s = s0 + u * NW * KPW + kin;
-        kv[u] = s < kold ? ld_nc(reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(s) * DH + sub * 8))
-                         : (s == len ? *reinterpret_cast<const uint4*>(knew + sub * 8) : make_uint4(0, 0, 0, 0));
+        kv[u] = s < k1 ? *reinterpret_cast<const uint4*>(kst + (s - k0) * DH + sub * 8) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
@@ -300,6 +373,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
       }
     }
     __syncthreads();
+    trace_point(34);
     // ---- softmax over the split (fp32) ----
     float mx = -FLT_MAX;
     for (int s = threadIdx.x; s < k1 - k0; s += kAttnThreads) mx = fmaxf(mx, p[s]);
@@ -332,7 +406,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * NW;
-        const __half* vr = s < kold ? vc + static_cast<int64_t>(s) * DH + lane * FPL : vnew + lane * FPL;
+        const __half* vr = vst + (s - k0) * DH + lane * FPL;
         if (s < k1) {
           if constexpr (FPL == 4) vv[u] = *reinterpret_cast<const uint2*>(vr);
           else vv[u] = make_uint2(*reinterpret_cast<const uint32_t*>(vr), 0u);
@@ -357,6 +431,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
     for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
     __syncthreads();
+    trace_point(35);
     if (gridDim.z == 1) {
       // single split: normalise and hand the row to out_proj directly
       const float inv = 1.f / sum;
@@ -374,6 +449,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
           a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
         }
       }
+      trace_point(32);
       return;
     }
     for (int c = threadIdx.x; c < DH; c += kAttnThreads) {
@@ -422,6 +498,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
       a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
     }
   }
+  trace_point(32);
 }
 
 // Cache length bookkeeping after a decode step (kept on the device for CUDA graphs).
@@ -465,9 +542,6 @@ __global__ void k_rope_store(RopeStoreArgs a) {
 // straddle it. exp2 with log2(e) folded into the Q scale (same softmax).
 constexpr int kFaRows = 64, kFaKeys = 64, kFaThreads = 128;
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -742,8 +816,10 @@ __device__ __forceinline__ void head_rows(const HeadArgs& a, const float* hs, in
 
 template <typename ET>
 __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
+  trace_point(50);
   pdl_wait();
   pdl_trigger();
+  trace_point(51);
   extern __shared__ float hs[];  // [kHeadRowsPerGroup][d]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m0 = 0; m0 < a.M; m0 += kHeadRowsPerGroup) {
@@ -759,6 +835,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a) {
       default: head_rows<ET, 4>(a, hs, m0, warp, lane); break;
     }
   }
+  trace_point(52);
 }
 
 // Tensor-core head for 2..16 rows (bf16 table): logits = h E^T on mma.sync.m16n8k16.bf16.
@@ -900,8 +977,16 @@ int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplit
 
 void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st) {
   const dim3 grid(a.heads, B, a.max_splits);
-  if (a.dh == 128) launch_k(k_attn_decode<128>, grid, dim3(kAttnThreads), 0, st, a);
-  else if (a.dh == 64) launch_k(k_attn_decode<64>, grid, dim3(kAttnThreads), 0, st, a);
+  // keys + values of one split staged in shared memory
+  const size_t smem = 2ull * kSplitKeys * a.dh * sizeof(__half);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 128 * 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 64 * 2));
+    attr = true;
+  }
+  if (a.dh == 128) launch_k(k_attn_decode<128>, grid, dim3(kAttnThreads), smem, st, a);
+  else if (a.dh == 64) launch_k(k_attn_decode<64>, grid, dim3(kAttnThreads), smem, st, a);
   else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
   LAUNCH_CHECK("k_attn_decode");
 }

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // capi_quant.cpp — C ABI for quantization and the quantized linear (include/glm130b.h).
 #include <cuda_runtime.h>
@@ -277,6 +278,38 @@ glm_status glm_debug_qmm_trace(long long* host_out) {
   return guarded([&] {
     if (!qmm_trace_ptr()) fail(GLM_CONTRACT, "qlinear", "no traced launch (set GLM_QMM_TRACE)");
     CUDA_CHECK(cudaMemcpy(host_out, qmm_trace_ptr(), 256 * 8 * sizeof(long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+static unsigned long long* g_trace_dev = nullptr;
+
+glm_status glm_debug_trace_start(int64_t capacity) {
+  return guarded([&] {
+    if (capacity < 1) fail(GLM_CONTRACT, "trace", "capacity must be positive");
+    if (g_trace_dev) cudaFree(g_trace_dev);
+    CUDA_CHECK(cudaMalloc(&g_trace_dev, (1 + 2 * capacity) * sizeof(unsigned long long)));
+    CUDA_CHECK(cudaMemset(g_trace_dev, 0, (1 + 2 * capacity) * sizeof(unsigned long long)));
+    trace_bind_gemv(g_trace_dev, capacity);
+    trace_bind_block(g_trace_dev, capacity);
+    trace_bind_model(g_trace_dev, capacity);
+  });
+}
+
+glm_status glm_debug_trace_stop(uint64_t* host_out, int64_t capacity, int64_t* count) {
+  return guarded([&] {
+    if (!g_trace_dev) fail(GLM_CONTRACT, "trace", "no trace running");
+    CUDA_CHECK(cudaDeviceSynchronize());
+    unsigned long long n = 0;
+    CUDA_CHECK(cudaMemcpy(&n, g_trace_dev, sizeof(n), cudaMemcpyDeviceToHost));
+    const int64_t m = std::min<int64_t>(static_cast<int64_t>(n), capacity);
+    if (host_out && m > 0)
+      CUDA_CHECK(cudaMemcpy(host_out, g_trace_dev + 1, 2 * m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (count) *count = m;
+    trace_bind_gemv(nullptr, 0);
+    trace_bind_block(nullptr, 0);
+    trace_bind_model(nullptr, 0);
+    cudaFree(g_trace_dev);
+    g_trace_dev = nullptr;
   });
 }
 

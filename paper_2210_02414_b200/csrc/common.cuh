@@ -132,6 +132,30 @@ __device__ __forceinline__ uint4 ld_nc(const uint4* p) {
   return r;
 }
 
+// Timeline tracer (diagnostics, tools/timeline.py): when a trace buffer is bound, thread 0
+// of every CTA appends (globaltimer ns, tag << 32 | block << 8 | smid) records. Each
+// translation unit has its own symbol, bound by trace_bind_all() (capi_quant.cpp).
+static __device__ unsigned long long* g_trace_buf = nullptr;
+static __device__ unsigned long long g_trace_cap = 0;
+__device__ __forceinline__ void trace_point(unsigned tag) {
+  unsigned long long* buf = g_trace_buf;
+  if (buf == nullptr || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const unsigned long long i = atomicAdd(buf, 1ull);
+  if (i < g_trace_cap) {
+    buf[1 + 2 * i] = t;
+    buf[2 + 2 * i] = (static_cast<unsigned long long>(tag) << 32) | (static_cast<unsigned long long>(blockIdx.x) << 8) | smid;
+  }
+}
+#define GLM_TRACE_TU(name)                                                                   \
+  void trace_bind_##name(unsigned long long* buf, unsigned long long cap) {                  \
+    CUDA_CHECK(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)));                          \
+    CUDA_CHECK(cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap)));                          \
+  }
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

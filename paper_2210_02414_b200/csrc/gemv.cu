@@ -31,6 +31,8 @@
 
 namespace glm {
 
+GLM_TRACE_TU(gemv)
+
 namespace {
 
 
@@ -505,6 +507,7 @@ constexpr int kM1DefaultWarps = 16;
 
 template <int BITS, int NST>
 __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx, int early) {
+  trace_point(10);
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
   constexpr int U = kStageBytes / CHUNK;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -560,6 +563,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
     for (int s = 0; s < early && s < NST; ++s) issue();
   pdl_wait();
   pdl_trigger();
+  trace_point(11);
   if (lane == 0)
     for (int s = early; s < NST; ++s) issue();
   if (threadIdx.x == 0) {
@@ -602,6 +606,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
     if ((threadIdx.x & 7) == 0 && i < nx * nch) xsum[i] = sum;
   }
   __syncthreads();
+  trace_point(12);
 
   int cslot = 0;
   uint32_t cpar = 0;
@@ -664,6 +669,8 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
       }
     }
   }
+  __syncthreads();
+  trace_point(13);
 }
 
 

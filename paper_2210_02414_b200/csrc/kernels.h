@@ -92,4 +92,9 @@ void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __h
 void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, float* y, int64_t ldy,
                  cudaStream_t st);
 
+// diagnostics: bind the timeline trace buffer of each translation unit (common.cuh)
+void trace_bind_gemv(unsigned long long* buf, unsigned long long cap);
+void trace_bind_block(unsigned long long* buf, unsigned long long cap);
+void trace_bind_model(unsigned long long* buf, unsigned long long cap);
+
 }  // namespace glm

@@ -27,6 +27,8 @@
 
 namespace glm {
 
+GLM_TRACE_TU(model)
+
 namespace {
 
 struct Linear {
@@ -348,7 +350,10 @@ struct glm_model {
   }
 
   // tile = 1 for prefill activations consumed by the tcgen05 GEMM (M > 16 rows)
-  XOut xout(__half* xf, const Linear& lin, int tile = 0) const { return XOut{xf, lin.w.L.nch, lin.w.L.Kp, tile, lin.w.row_scale}; }
+  // consumer activation buffer; the kRow fold vector only where it is not all ones
+  XOut xout(__half* xf, const Linear& lin, int tile = 0) const {
+    return XOut{xf, lin.w.L.nch, lin.w.L.Kp, tile, axis == GLM_AXIS_ROW ? lin.w.row_scale : nullptr};
+  }
 
   // ---- weights -------------------------------------------------------------------------
   void finish_linear(Linear& lin, const double* full_scales) {

@@ -91,6 +91,8 @@ SIGNATURES = {
     "glm_qlinear_bench": (I32, [P, I64, I32, I32, C.POINTER(D)]),
     "glm_model_create": (I32, [C.POINTER(_Config), I32, I32, I32, I32, I32, I32, I32, C.POINTER(P)]),
     "glm_model_destroy": (I32, [P]),
+    "glm_debug_trace_start": (I32, [I64]),
+    "glm_debug_trace_stop": (I32, [P, I64, P]),
     "glm_tp_unique_id": (I32, [P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
