@@ -505,18 +505,18 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
 constexpr int kM1MaxWarps = 24;
 constexpr int kM1DefaultWarps = 16;
 
-template <int BITS, int NST>
+template <int BITS, int NST, int SB>
 __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx, int early) {
   trace_point(10);
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
-  constexpr int U = kStageBytes / CHUNK;
+  constexpr int U = SB / CHUNK;  // chunks per stage
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int nch = static_cast<int>(a.nch), ksplit = a.ksplit;
   const int xbytes = nch * 128;  // one token: Kp halves
-  uint8_t* ring = smem + static_cast<size_t>(warp) * NST * kStageBytes;
-  uint8_t* xs = smem + static_cast<size_t>(nw) * NST * kStageBytes;
+  uint8_t* ring = smem + static_cast<size_t>(warp) * NST * SB;
+  uint8_t* xs = smem + static_cast<size_t>(nw) * NST * SB;
   uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * xbytes);
   uint64_t* bars = xbar + 1 + warp * NST;
   if (lane == 0) {
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
     const int n = min(U, pc1 - pc);
     const uint8_t* src = wbase + (static_cast<int64_t>(prt) * nch + pc) * CHUNK;
     mbar_expect_tx(bars + pslot, static_cast<uint32_t>(n * CHUNK));
-    bulk_g2s(ring + pslot * kStageBytes, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    bulk_g2s(ring + pslot * SB, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
     pslot = pslot + 1 == NST ? 0 : pslot + 1;
     pc += n;
     if (pc >= pc1) {
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
     for (int c = c0; c < c1; c += U) {
       const int n = min(U, c1 - c);
       mbar_wait(bars + cslot, cpar);
-      const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
+      const uint8_t* st = ring + cslot * SB + lane * 16;
       auto chunk = [&](int u) {
         uint4 wv[BITS == 4 ? 1 : 2];
         wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK);
@@ -800,25 +800,33 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   const dim3 grid(p.grid), block(kTWarps * 32);
   if (M == 1 && op.bits == 4) {
     static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
+    static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
     const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
     const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + 8;
     const size_t limit = 227 * 1024 - 1024;  // leave room for the static shared memory
     int nst = m1s >= 3 ? 3 : 2;
+    int sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
     int m1w = p.warps;  // the plan's warps if the rings fit next to x, else fewer
-    if (xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) nst = 2;
-    while (m1w > 8 && xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8) > limit) --m1w;
-    const size_t sm1 = xb + static_cast<size_t>(m1w) * nst * (kStageBytes + 8);
+    auto need = [&](int w, int n, int b) { return xb + static_cast<size_t>(w) * n * (b + 8); };
+    if (need(m1w, nst, sb) > limit) nst = 2;
+    while (sb > 4096 && need(m1w, nst, sb) > limit) sb -= 2048;
+    while (m1w > 8 && need(m1w, nst, sb) > limit) --m1w;
+    const size_t sm1 = need(m1w, nst, sb);
+    const dim3 block1(m1w * 32);
     if (sm1 <= limit && op.nch * 128 < (int64_t{1} << 30)) {
       static bool attr1 = false;
       if (!attr1) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 6144>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 3, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
         attr1 = true;
       }
-      const dim3 block1(m1w * 32);
       static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
-      if (nst == 3) launch_k(k_gemv_m1<4, 3>, grid, block1, sm1, st, a, nx, early);
-      else launch_k(k_gemv_m1<4, 2>, grid, block1, sm1, st, a, nx, early);
+      if (nst == 3) launch_k(k_gemv_m1<4, 3, 4096>, grid, block1, sm1, st, a, nx, early);
+      else if (sb == 8192) launch_k(k_gemv_m1<4, 2, 8192>, grid, block1, sm1, st, a, nx, early);
+      else if (sb == 6144) launch_k(k_gemv_m1<4, 2, 6144>, grid, block1, sm1, st, a, nx, early);
+      else launch_k(k_gemv_m1<4, 2, 4096>, grid, block1, sm1, st, a, nx, early);
       LAUNCH_CHECK("k_gemv_m1");
       return;
     }
