@@ -201,25 +201,98 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
   trace_point(22);
 }
 
+// Many-row variant (prefill): one CTA per row, no cluster; the row's pairs are strided over
+// the CTA's threads and the statistics are a CTA reduction (fixed order).
+constexpr int kLnRowThreads = 512;
+
+__global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float2 red[kLnRowThreads / 32];
+  const int m = blockIdx.x;
+  const int64_t npairs = a.d / 2;
+  float* hrow = a.h + static_cast<int64_t>(m) * a.d;
+  float2 acc = make_float2(0.f, 0.f);
+  // pass 1: z = alpha h + y (kept in h), statistics
+  for (int64_t p = threadIdx.x; p < npairs; p += kLnRowThreads) {
+    const int64_t n = 2 * p;
+    float2 y = make_float2(0.f, 0.f);
+    if (!a.zero_sublayer) {
+      for (int s = 0; s < a.in.ksplit; ++s) {
+        const float2 v = *reinterpret_cast<const float2*>(a.in.p + static_cast<int64_t>(s) * a.in.split_stride +
+                                                          m * a.in.ld + n);
+        y.x += v.x;
+        y.y += v.y;
+      }
+      if (a.in.scale) {
+        y.x *= a.in.scale[n];
+        y.y *= a.in.scale[n + 1];
+      }
+    }
+    if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + n) = y;
+    const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
+    const float2 z = make_float2(a.alpha * hv.x + y.x, a.alpha * hv.y + y.y);
+    *reinterpret_cast<float2*>(hrow + n) = z;
+    acc.x += z.x + z.y;
+    acc.y += z.x * z.x + z.y * z.y;
+  }
+  acc.x = warp_sum(acc.x);
+  acc.y = warp_sum(acc.y);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = acc;
+  __syncthreads();
+  float2 tot = make_float2(0.f, 0.f);
+  for (int i = 0; i < kLnRowThreads / 32; ++i) {
+    tot.x += red[i].x;
+    tot.y += red[i].y;
+  }
+  const float inv_d = 1.f / static_cast<float>(a.d);
+  const float mean = tot.x * inv_d;
+  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);  // biased (tensor.cpp:267)
+  const float rstd = rsqrtf(var + a.eps);
+  // pass 2 (same thread -> same pairs, so z is read back from where this thread wrote it)
+  for (int64_t p = threadIdx.x; p < npairs; p += kLnRowThreads) {
+    const int64_t n = 2 * p;
+    const float2 z = *reinterpret_cast<const float2*>(hrow + n);
+    const float o0 = (z.x - mean) * rstd * a.gain[n] + a.bias[n];
+    const float o1 = (z.y - mean) * rstd * a.gain[n + 1] + a.bias[n + 1];
+    *reinterpret_cast<float2*>(hrow + n) = make_float2(o0, o1);
+    store_xfrag_pair(a.x0, m, n, o0, o1);
+    store_xfrag_pair(a.x1, m, n, o0, o1);
+  }
+}
+
 // ---- GeGLU activation: gelu(x W1) * (x V) (model.cpp:133-135, tensor.cpp:313-318) --------
+__device__ __forceinline__ float2 reduce_partial2(const SubIn& in, int m, int64_t n) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 4
+  for (int s = 0; s < in.ksplit; ++s) {
+    const float2 v = *reinterpret_cast<const float2*>(in.p + static_cast<int64_t>(s) * in.split_stride + m * in.ld + n);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  if (in.scale) {
+    acc.x *= in.scale[n];
+    acc.y *= in.scale[n + 1];
+  }
+  return acc;
+}
+
 __global__ void k_geglu_act(ActArgs a) {
   trace_point(40);
   pdl_wait();
   pdl_trigger();
   trace_point(41);
-  const int64_t pairs = static_cast<int64_t>(a.M) * (a.f / 2);
+  const int64_t half = a.f / 2;
+  const int64_t pairs = static_cast<int64_t>(a.M) * half;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int m = static_cast<int>(i / (a.f / 2));
-    const int64_t n = (i % (a.f / 2)) * 2;
-    float o[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float u = reduce_partial(a.w1, m, n + e);
-      const float v = reduce_partial(a.v, m, n + e);
-      o[e] = 0.5f * u * (1.f + erff(u * kInvSqrt2)) * v;
-    }
-    store_xfrag_pair(a.xo, m, n, o[0], o[1]);
+    const int m = static_cast<int>(i / half);
+    const int64_t n = (i % half) * 2;
+    const float2 u = reduce_partial2(a.w1, m, n), v = reduce_partial2(a.v, m, n);
+    const float o0 = 0.5f * u.x * (1.f + erff(u.x * kInvSqrt2)) * v.x;  // tensor.cpp:313-318
+    const float o1 = 0.5f * u.y * (1.f + erff(u.y * kInvSqrt2)) * v.y;
+    store_xfrag_pair(a.xo, m, n, o0, o1);
   }
   trace_point(42);
 }
@@ -964,7 +1037,8 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
 
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   if (a.d > 2ll * kLnPairs * kLnThreads * kLnCluster || a.d % 2) fail(GLM_DIMENSION, "glmmodel", "hidden unsupported by LN kernel");
-  launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
+  if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
+  else launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
   LAUNCH_CHECK("k_deepnorm_ln");
 }
 

@@ -96,6 +96,11 @@ void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, c
     gemv_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
   } else {
     xtile_from_f32(x, w.L.K, static_cast<int>(M), w, xb.as<__half>(), st);
+    if (p.ksplit == 1) {  // the tcgen05 epilogue writes the scaled result directly
+      qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st, y, w.L.N);
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      return;
+    }
     qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
   }
   gemv_reduce(part.as<float>(), p.ksplit, static_cast<int>(M), w, y, w.L.N, st);

@@ -82,7 +82,9 @@ inline int xtile_tokens(int M) { return (M + kQmmTokens - 1) / kQmmTokens * kQmm
 // partial[s][m][n] (fp32, [ksplit][M][Np]) from activations xt in the tcgen05 B-operand
 // layout (layout.cuh xtile_index) holding NT = xtile_tokens(M) token rows.
 GemvPlan plan_qmm(const QLayout& L, int M);
-void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st);
+// y (optional, ksplit == 1): write the scaled result y[M][ldy] directly instead of partials
+void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
+                float* y = nullptr, int64_t ldy = 0);
 void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st);
 long long*& qmm_trace_ptr();  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
 

@@ -598,6 +598,10 @@ struct glm_model {
       gemv_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     } else {
       p = plan_qmm(lin.w.L, static_cast<int>(M));
+      if (p.ksplit == 1) {  // tcgen05 epilogue writes the scaled result: no reduce pass
+        qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st, y, lin.w.L.N);
+        return;
+      }
       qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     }
     gemv_reduce(partial.as<float>(), p.ksplit, static_cast<int>(M), lin.w, y, lin.w.L.N, st);
@@ -642,12 +646,12 @@ struct glm_model {
       ln.eps = static_cast<float>(eps);
       ln.d = d;
       ln.x0 = xout(xf_w1.as<__half>(), w1, nt);
-      ln.x1 = xout(xf_v.as<__half>(), v, nt);
+      ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v, nt) : XOut{};  // W1 and V share x unless kRow
       ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
       ln.zero_sublayer = zero_sub;
       launch_deepnorm_ln(ln, n, st);
       linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
-      linear_rows(v, xf_v.as<__half>(), n, y_b.as<float>());
+      linear_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), n, y_b.as<float>());
       ActArgs act;
       act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
       act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};

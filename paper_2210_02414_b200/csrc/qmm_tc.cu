@@ -110,7 +110,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 struct QmmArgs {
   const uint8_t* w;   // fragment-ordered device layout (layout.cuh)
   const __half* xt;   // activations, 128-token tiles (xtile_index)
-  float* partial;     // [ksplit][M][Np]
+  float* partial;     // [ksplit][M][Np], or the final y [M][ldo] when col_scale is set
+  const float* col_scale;  // non-null (ksplit == 1): write y = acc * col_scale, columns < N
+  int64_t ldo, N;
   int64_t nrt16, nch, Np, Kp;
   int M, ksplit, ntt, nrt128;
   long long* trace;
@@ -310,7 +312,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
         const int db = it % NDB;
         mbar_wait(d_full + db, (it / NDB) & 1);
         tc_fence_after();
-        float* out = a.partial + static_cast<int64_t>(s) * a.M * a.Np + rt * 128 + row;
+        const int64_t col = rt * 128 + row;
+        const bool direct = a.col_scale != nullptr;  // final output, group scale applied here
+        const float cs = direct && col < a.N ? a.col_scale[col] : 1.f;
+        const int64_t ld = direct ? a.ldo : a.Np;
+        float* out = a.partial + (direct ? 0 : static_cast<int64_t>(s) * a.M * a.Np) + col;
+        const bool keep = !direct || col < a.N;
 #pragma unroll 1
         for (int c16 = 0; c16 < NTOK; c16 += 16) {
           uint32_t v[16];
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             const int64_t tok = tt * NTOK + c16 + m;
-            if (tok < a.M) out[tok * a.Np] = __uint_as_float(v[m]);
+            if (tok < a.M && keep) out[tok * ld] = __uint_as_float(v[m]) * cs;
           }
         }
         tc_fence_before();
@@ -366,7 +373,9 @@ GemvPlan plan_qmm(const QLayout& L, int M) {
     if (L.nch / ks < 8 && ks > 1) break;
     const int64_t items = ntt * nrt128 * ks;
     const int64_t waves = (items + workers - 1) / workers;
-    double eff = static_cast<double>(items) / static_cast<double>(waves * workers) - 0.01 * static_cast<double>(ks);
+    // an unsplit K writes the scaled output directly (no partials, no reduce pass)
+    double eff = static_cast<double>(items) / static_cast<double>(waves * workers) - 0.01 * static_cast<double>(ks) -
+                 (ks > 1 ? 0.04 : 0.0);
     if (eff > best + 1e-9) {
       best = eff;
       p.ksplit = static_cast<int>(ks);
@@ -377,13 +386,18 @@ GemvPlan plan_qmm(const QLayout& L, int M) {
   return p;
 }
 
-void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st) {
+void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
+                float* y, int64_t ldy) {
   if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
   if (w.L.Np % 128 || w.L.Kp % 64) fail(GLM_DIMENSION, "qlinear", "layout not padded for the tcgen05 path");
+  if (y && p.ksplit != 1) fail(GLM_CONTRACT, "qlinear", "direct output needs an unsplit K");
   QmmArgs a;
   a.w = static_cast<const uint8_t*>(w.codes);
   a.xt = xt;
-  a.partial = partial;
+  a.partial = y ? y : partial;
+  a.col_scale = y ? w.col_scale : nullptr;
+  a.ldo = ldy;
+  a.N = w.L.N;
   a.nrt16 = w.L.nrt;
   a.nch = w.L.nch;
   a.Np = w.L.Np;
