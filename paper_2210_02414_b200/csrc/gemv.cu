@@ -564,10 +564,9 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   pdl_wait();
   pdl_trigger();
   trace_point(11);
-  if (lane == 0)
-    for (int s = early; s < NST; ++s) issue();
   if (threadIdx.x == 0) {
-    // the activation vector(s): L2-resident (just written by the producer), kept there
+    // the activation vector(s): L2-resident (just written by the producer), kept there;
+    // requested ahead of any weight stage not yet in flight
     mbar_expect_tx(xbar, static_cast<uint32_t>(nx * xbytes));
     for (int v = 0; v < nx; ++v) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2);
@@ -577,6 +576,8 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
       }
     }
   }
+  if (lane == 0)
+    for (int s = early; s < NST; ++s) issue();
   // B fragments: every token column gets the same activation vector (lane (g, t) reads the
   // fragment of column 0 whatever g is), so the MMA computes 8 identical result columns and
   // only column 0 is stored: no zero-fill, no per-lane address selection, and the 8 lanes
