@@ -148,6 +148,8 @@ glm_status glm_model_create(const glm_config* cfg, int bits, glm_axis axis, int 
                             int max_ctx, int head_bf16, int tp_rank, int tp_size,
                             glm_model** out);
 glm_status glm_model_destroy(glm_model* m);
+/* The effective configuration (ffn_hidden / alpha resolved to the reference defaults). */
+glm_status glm_model_get_config(const glm_model* m, glm_config* out);
 /* Tensor parallelism (tp_size > 1): rank 0 calls glm_tp_unique_id, shares the 128 bytes
  * with every rank (e.g. over torch.distributed), then each rank calls
  * glm_model_init_comm before loading weights. No-op at tp_size == 1. */
@@ -159,6 +161,16 @@ glm_status glm_model_init_comm(glm_model* m, const void* unique_id);
  * 7 ln2_gain, 8 ln2_bias; embedding [vocab, d] via glm_model_set_embedding. */
 glm_status glm_model_set_embedding(glm_model* m, const double* embedding);
 glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double* values);
+/* A quantized linear given as the reference's canonical QuantizedMatrix (quant.hpp:26-42:
+ * payload bytes + FP64 scales of the FULL [K, N] matrix, the model's bits/axis, absmax);
+ * stored as this rank's shard without re-quantizing. Wrong lengths -> GLM_FORMAT. */
+glm_status glm_model_set_quantized(glm_model* m, int layer, int which, const int8_t* payload,
+                                   int64_t payload_bytes, const double* scales, int64_t nscales);
+/* load_quantized_model (quant.cpp:450-491): a checkpoint directory written by the reference's
+ * save_quantized_model (manifest.json + GLMT tensors, tensor_io.cpp:68-179). Every file is
+ * validated before device work (GLM_FORMAT on malformed input); absmax checkpoints only. */
+glm_status glm_model_load_quantized(const char* dir, int max_batch, int max_ctx, int head_bf16,
+                                    int tp_rank, int tp_size, glm_model** out);
 /* Synthetic random-init weights of the configured shape, generated and quantized on the
  * GPU with the counter-based generator of DESIGN.md (same stds as model.cpp:69-104). */
 glm_status glm_model_init_synthetic(glm_model* m, uint64_t seed);

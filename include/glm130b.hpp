@@ -200,6 +200,18 @@ class QuantizedModel {
                            tp_rank, tp_size, &m));
     m_.reset(m);
   }
+  // load_quantized_model (quant.cpp:450-491): a checkpoint directory written by the reference
+  static QuantizedModel load_quantized(const std::string& dir, int max_batch = 1, int max_ctx = 2048,
+                                       bool head_bf16 = false, int tp_rank = 0, int tp_size = 1) {
+    glm_model* m = nullptr;
+    check(glm_model_load_quantized(dir.c_str(), max_batch, max_ctx, head_bf16 ? 1 : 0, tp_rank, tp_size, &m));
+    return QuantizedModel(m);
+  }
+  // a canonical QuantizedMatrix of linear `which` (0 qkv .. 4 ffn_w2) of `layer`
+  void set_quantized(int layer, int which, const QuantizedMatrix& q) {
+    check(glm_model_set_quantized(m_.get(), layer, which, q.payload.data(), static_cast<Index>(q.payload.size()),
+                                  q.scales.data(), static_cast<Index>(q.scales.size())));
+  }
   glm_model* handle() const { return m_.get(); }
   void set_embedding(const std::vector<double>& e) { check(glm_model_set_embedding(m_.get(), e.data())); }
   // which: 0 qkv, 1 out_proj, 2 ffn_w1, 3 ffn_v, 4 ffn_w2, 5..8 LN gains/biases (model.hpp:41-65).
@@ -235,6 +247,18 @@ class QuantizedModel {
   void reset() { check(glm_model_reset(m_.get())); }
 
  private:
+  explicit QuantizedModel(glm_model* m) : m_(m) {
+    glm_config c{};
+    check(glm_model_get_config(m, &c));
+    cfg_.num_layers = c.num_layers;
+    cfg_.hidden = c.hidden;
+    cfg_.num_heads = c.num_heads;
+    cfg_.ffn_hidden = c.ffn_hidden;
+    cfg_.vocab = c.vocab;
+    cfg_.init_method_std = c.init_method_std;
+    cfg_.layernorm_eps = c.layernorm_eps;
+    cfg_.deepnorm_alpha = c.deepnorm_alpha;
+  }
   struct Del {
     void operator()(glm_model* p) const { glm_model_destroy(p); }
   };

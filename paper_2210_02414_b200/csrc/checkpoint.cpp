@@ -1,0 +1,336 @@
+// checkpoint.cpp — loads a quantized GLM checkpoint written by the reference
+// (`save_quantized_model`, quant.cpp:409-448; GLMT tensors, tensor_io.cpp:68-179) straight
+// into the B200 model: the canonical payloads and FP64 scales go to the device layout
+// without re-quantizing, so the GPU model holds exactly the reference's QuantizedModel.
+//
+// Directory layout (quant.cpp:409-448):
+//   manifest.json           {"config": {...}, "policy": {"bits","scheme","axis"},
+//                            "matrices": [{"name","bits","scheme","axis","rows","cols"}, ...]}
+//   embedding.glmt          f64 [vocab, hidden]
+//   layer<L>.<m>.codes.glmt i8  [payload bytes]   m in qkv, out_proj, ffn_w1, ffn_v, ffn_w2
+//   layer<L>.<m>.scales.glmt f64 [groups]
+//   layer<L>.ln{1,2}_{gain,bias}.glmt f64 [hidden]
+// Every file is parsed and validated before any device work, so format errors surface as
+// GLM_FORMAT (FormatError) even without a GPU.
+#include <cctype>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "glm130b.h"
+
+namespace glm {
+namespace {
+
+// ---- GLMT (tensor_io.cpp:12-13, 68-140): "GLMT", u8 version 1, u8 dtype (0 f64, 1 f32,
+// 2 i8), u32 rank, u64 dims[rank] (little endian), then the raw payload -----------------
+struct Glmt {
+  int dtype = 0;
+  std::vector<uint64_t> dims;
+  std::vector<double> f64;
+  std::vector<int8_t> i8;
+  uint64_t count() const {
+    uint64_t n = 1;
+    for (uint64_t d : dims) n *= d;
+    return n;
+  }
+};
+
+Glmt read_glmt(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(GLM_FORMAT, "tensor_io", "cannot open " + path);
+  auto bytes = [&](void* dst, size_t n) {
+    in.read(static_cast<char*>(dst), static_cast<std::streamsize>(n));
+    if (static_cast<size_t>(in.gcount()) != n) fail(GLM_FORMAT, "tensor_io", "truncated file " + path);
+  };
+  char magic[4];
+  bytes(magic, 4);
+  if (std::memcmp(magic, "GLMT", 4) != 0) fail(GLM_FORMAT, "tensor_io", "bad magic in " + path);
+  uint8_t version = 0, dtype = 0;
+  bytes(&version, 1);
+  if (version != 1) fail(GLM_FORMAT, "tensor_io", "unsupported version " + std::to_string(version));
+  bytes(&dtype, 1);
+  if (dtype > 2) fail(GLM_FORMAT, "tensor_io", "unknown dtype " + std::to_string(dtype));
+  uint8_t b[8];
+  bytes(b, 4);
+  uint32_t rank = 0;
+  for (int i = 3; i >= 0; --i) rank = (rank << 8) | b[i];
+  if (rank > 64) fail(GLM_FORMAT, "tensor_io", "implausible rank " + std::to_string(rank));
+  Glmt t;
+  t.dtype = dtype;
+  t.dims.resize(rank);
+  for (uint32_t r = 0; r < rank; ++r) {
+    bytes(b, 8);
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+    t.dims[r] = v;
+  }
+  const uint64_t n = t.count();
+  if (dtype == 0) {
+    t.f64.resize(n);
+    bytes(t.f64.data(), n * 8);
+  } else if (dtype == 1) {
+    std::vector<float> f(n);
+    bytes(f.data(), n * 4);
+    t.f64.assign(f.begin(), f.end());
+    t.dtype = 0;
+  } else {
+    t.i8.resize(n);
+    bytes(t.i8.data(), n);
+  }
+  return t;
+}
+
+// ---- minimal JSON (the manifest only needs objects, arrays, strings, numbers, bools) ----
+struct Json {
+  enum Kind { kNull, kBool, kNum, kStr, kArr, kObj } kind = kNull;
+  double num = 0.0;
+  bool b = false;
+  std::string str;
+  std::vector<Json> arr;
+  std::map<std::string, Json> obj;
+  const Json& at(const std::string& k) const {
+    auto it = obj.find(k);
+    if (kind != kObj || it == obj.end()) fail(GLM_FORMAT, "quantlab", "manifest is missing \"" + k + "\"");
+    return it->second;
+  }
+  int as_int() const {
+    if (kind != kNum || num != std::floor(num)) fail(GLM_FORMAT, "quantlab", "manifest field is not an integer");
+    return static_cast<int>(num);
+  }
+  double as_num() const {
+    if (kind != kNum) fail(GLM_FORMAT, "quantlab", "manifest field is not a number");
+    return num;
+  }
+  const std::string& as_str() const {
+    if (kind != kStr) fail(GLM_FORMAT, "quantlab", "manifest field is not a string");
+    return str;
+  }
+};
+
+class JsonParser {
+ public:
+  explicit JsonParser(const std::string& s) : s_(s) {}
+  Json parse() {
+    Json v = value();
+    ws();
+    if (i_ != s_.size()) bad("trailing characters");
+    return v;
+  }
+
+ private:
+  [[noreturn]] void bad(const char* what) {
+    fail(GLM_FORMAT, "quantlab", std::string("manifest.json: ") + what + " at offset " + std::to_string(i_));
+  }
+  void ws() {
+    while (i_ < s_.size() && (s_[i_] == ' ' || s_[i_] == '\n' || s_[i_] == '\r' || s_[i_] == '\t')) ++i_;
+  }
+  char peek() {
+    ws();
+    if (i_ >= s_.size()) bad("unexpected end");
+    return s_[i_];
+  }
+  void expect(char c) {
+    if (peek() != c) bad("unexpected character");
+    ++i_;
+  }
+  Json value() {
+    const char c = peek();
+    Json v;
+    if (c == '{') {
+      v.kind = Json::kObj;
+      ++i_;
+      if (peek() == '}') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        Json k = value();
+        if (k.kind != Json::kStr) bad("object key is not a string");
+        expect(':');
+        v.obj[k.str] = value();
+        if (peek() == ',') {
+          ++i_;
+          continue;
+        }
+        expect('}');
+        return v;
+      }
+    }
+    if (c == '[') {
+      v.kind = Json::kArr;
+      ++i_;
+      if (peek() == ']') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        v.arr.push_back(value());
+        if (peek() == ',') {
+          ++i_;
+          continue;
+        }
+        expect(']');
+        return v;
+      }
+    }
+    if (c == '"') {
+      v.kind = Json::kStr;
+      ++i_;
+      while (i_ < s_.size() && s_[i_] != '"') {
+        if (s_[i_] == '\\') {
+          if (++i_ >= s_.size()) bad("bad escape");
+          const char e = s_[i_];
+          if (e == 'u') {  // \uXXXX: keep ASCII, replace the rest
+            if (i_ + 4 >= s_.size()) bad("bad escape");
+            const int code = std::stoi(s_.substr(i_ + 1, 4), nullptr, 16);
+            v.str.push_back(code < 128 ? static_cast<char>(code) : '?');
+            i_ += 4;
+          } else {
+            v.str.push_back(e == 'n' ? '\n' : e == 't' ? '\t' : e == 'r' ? '\r' : e == 'b' ? '\b' : e == 'f' ? '\f' : e);
+          }
+        } else {
+          v.str.push_back(s_[i_]);
+        }
+        ++i_;
+      }
+      if (i_ >= s_.size()) bad("unterminated string");
+      ++i_;
+      return v;
+    }
+    if (s_.compare(i_, 4, "true") == 0) {
+      v.kind = Json::kBool;
+      v.b = true;
+      i_ += 4;
+      return v;
+    }
+    if (s_.compare(i_, 5, "false") == 0) {
+      v.kind = Json::kBool;
+      i_ += 5;
+      return v;
+    }
+    if (s_.compare(i_, 4, "null") == 0) {
+      i_ += 4;
+      return v;
+    }
+    const size_t start = i_;
+    while (i_ < s_.size() && (std::isdigit(static_cast<unsigned char>(s_[i_])) || std::strchr("+-.eE", s_[i_]))) ++i_;
+    if (start == i_) bad("unexpected character");
+    v.kind = Json::kNum;
+    try {
+      v.num = std::stod(s_.substr(start, i_ - start));
+    } catch (...) {
+      bad("bad number");
+    }
+    return v;
+  }
+  const std::string& s_;
+  size_t i_ = 0;
+};
+
+int axis_from(const std::string& s) {  // to_string(GroupAxis), quant.cpp
+  if (s == "row") return GLM_AXIS_ROW;
+  if (s == "column") return GLM_AXIS_COLUMN;
+  if (s == "whole") return GLM_AXIS_WHOLE;
+  fail(GLM_FORMAT, "quantlab", "unknown group axis \"" + s + "\"");
+}
+
+}  // namespace
+}  // namespace glm
+
+using namespace glm;
+
+extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, int max_ctx, int head_bf16,
+                                               int tp_rank, int tp_size, glm_model** out) {
+  return guarded([&] {
+    if (!dir || !out) fail(GLM_CONTRACT, "quantlab", "null argument");
+    *out = nullptr;
+    const std::string root(dir);
+    std::ifstream in(root + "/manifest.json");
+    if (!in) fail(GLM_FORMAT, "quantlab", "missing manifest.json in " + root);
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    const Json man = JsonParser(text).parse();
+    const Json& jc = man.at("config");
+    glm_config cfg{};
+    cfg.num_layers = jc.at("num_layers").as_int();
+    cfg.hidden = jc.at("hidden").as_int();
+    cfg.num_heads = jc.at("num_heads").as_int();
+    cfg.ffn_hidden = jc.at("ffn_hidden").as_int();
+    cfg.vocab = jc.at("vocab").as_int();
+    cfg.init_method_std = jc.at("init_method_std").as_num();
+    cfg.layernorm_eps = jc.at("layernorm_eps").as_num();
+    cfg.deepnorm_alpha = jc.at("deepnorm_alpha").as_num();
+    const Json& jp = man.at("policy");
+    const int bits = jp.at("bits").as_int();
+    if (jp.at("scheme").as_str() != "absmax")
+      fail(GLM_CONTRACT, "quantlab", "the B200 path runs absmax checkpoints (zeropoint is on the round-2 list)");
+    const int axis = axis_from(jp.at("axis").as_str());
+    std::map<std::string, const Json*> by_name;
+    for (const Json& e : man.at("matrices").arr) by_name[e.at("name").as_str()] = &e;
+
+    // read and validate every tensor before touching the device
+    const int64_t d = cfg.hidden, f = cfg.ffn_hidden, L = cfg.num_layers;
+    const int64_t shapes[5][2] = {{d, 3 * d}, {d, d}, {d, f}, {d, f}, {f, d}};
+    const char* names[5] = {"qkv", "out_proj", "ffn_w1", "ffn_v", "ffn_w2"};
+    const char* vecs[4] = {"ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias"};
+    Glmt emb = read_glmt(root + "/embedding.glmt");
+    if (emb.dtype != 0 || emb.count() != static_cast<uint64_t>(cfg.vocab) * d)
+      fail(GLM_FORMAT, "quantlab", "embedding.glmt must be f64 [vocab, hidden]");
+    std::vector<Glmt> codes, scales, lnv;
+    for (int64_t l = 0; l < L; ++l) {
+      const std::string p = root + "/layer" + std::to_string(l) + ".";
+      for (int w = 0; w < 5; ++w) {
+        const std::string nm = "layer" + std::to_string(l) + "." + names[w];
+        auto it = by_name.find(nm);
+        if (it == by_name.end()) fail(GLM_FORMAT, "quantlab", "manifest has no matrix " + nm);
+        const Json& e = *it->second;
+        if (e.at("bits").as_int() != bits || e.at("scheme").as_str() != "absmax" ||
+            axis_from(e.at("axis").as_str()) != axis)
+          fail(GLM_FORMAT, "quantlab", nm + " does not follow the manifest policy");
+        if (e.at("rows").as_int() != shapes[w][0] || e.at("cols").as_int() != shapes[w][1])
+          fail(GLM_FORMAT, "quantlab", nm + " has the wrong shape for the configured model");
+        codes.push_back(read_glmt(p + names[w] + ".codes.glmt"));
+        scales.push_back(read_glmt(p + names[w] + ".scales.glmt"));
+        const int64_t n = shapes[w][0] * shapes[w][1];
+        const int64_t pb = bits == 4 ? (n + 1) / 2 : n;
+        const int64_t ng = axis == GLM_AXIS_ROW ? shapes[w][0] : axis == GLM_AXIS_COLUMN ? shapes[w][1] : 1;
+        if (codes.back().dtype != 2 || static_cast<int64_t>(codes.back().count()) != pb)
+          fail(GLM_FORMAT, "quantlab", nm + ".codes.glmt payload length does not match");
+        if (scales.back().dtype != 0 || static_cast<int64_t>(scales.back().count()) != ng)
+          fail(GLM_FORMAT, "quantlab", nm + ".scales.glmt group count does not match");
+      }
+      for (int v = 0; v < 4; ++v) {
+        lnv.push_back(read_glmt(p + vecs[v] + ".glmt"));
+        if (lnv.back().dtype != 0 || static_cast<int64_t>(lnv.back().count()) != d)
+          fail(GLM_FORMAT, "quantlab", std::string("layer LN vector ") + vecs[v] + " must be f64 [hidden]");
+      }
+    }
+
+    glm_model* m = nullptr;
+    glm_status s = glm_model_create(&cfg, bits, static_cast<glm_axis>(axis), max_batch, max_ctx, head_bf16, tp_rank,
+                                    tp_size, &m);
+    if (s != GLM_OK) fail(s, "glmmodel", glm_last_error());
+    std::unique_ptr<glm_model, glm_status (*)(glm_model*)> guard(m, glm_model_destroy);
+    auto check = [&](glm_status st) {
+      if (st != GLM_OK) fail(st, "glmmodel", glm_last_error());
+    };
+    check(glm_model_set_embedding(m, emb.f64.data()));
+    for (int64_t l = 0; l < L; ++l) {
+      for (int w = 0; w < 5; ++w) {
+        const Glmt& c = codes[l * 5 + w];
+        const Glmt& sc = scales[l * 5 + w];
+        check(glm_model_set_quantized(m, static_cast<int>(l), w, c.i8.data(), static_cast<int64_t>(c.i8.size()),
+                                      sc.f64.data(), static_cast<int64_t>(sc.f64.size())));
+      }
+      for (int v = 0; v < 4; ++v) check(glm_model_set_tensor(m, static_cast<int>(l), 5 + v, lnv[l * 4 + v].f64.data()));
+    }
+    *out = guard.release();
+  });
+}

@@ -373,6 +373,26 @@ struct glm_model {
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
 
+  // A quantized linear given as the reference's canonical QuantizedMatrix (quant.hpp:26-42):
+  // payload + FP64 scales go to this rank's device layout without re-quantizing.
+  void set_linear_quantized(int l, int which, const int8_t* payload, int64_t payload_bytes, const double* scales,
+                            int64_t nscales) {
+    Linear& lin = layers[l].lin[which];
+    const int64_t K = lin.Kfull, N = lin.Nfull, n = K * N;
+    const int64_t pb = bits == 4 ? (n + 1) / 2 : n;
+    const int64_t ng = axis == GLM_AXIS_ROW ? K : axis == GLM_AXIS_COLUMN ? N : 1;
+    if (payload_bytes != pb) fail(GLM_FORMAT, "quantlab", "payload length does not match the linear's shape and bits");
+    if (nscales != ng) fail(GLM_FORMAT, "quantlab", "scale count does not match the model's group axis");
+    for (int64_t g = 0; g < ng; ++g)
+      if (!std::isfinite(scales[g]) || scales[g] < 0.0) fail(GLM_FORMAT, "quantlab", "scales must be finite and >= 0");
+    DeviceBuffer dp(pb), ds(ng * 8);
+    CUDA_CHECK(cudaMemcpyAsync(dp.ptr, payload, pb, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(ds.ptr, scales, ng * 8, cudaMemcpyHostToDevice, st));
+    repack_shard_device(dp.as<int8_t>(), N, lin.shard, lin.w.L, lin.w.codes, st);
+    finish_linear(lin, ds.as<double>());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
   void set_embedding(const double* e) {
     const int64_t n = static_cast<int64_t>(V) * d;
     DeviceBuffer de(n * 8);
@@ -740,6 +760,24 @@ glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double
     if (which >= 0 && which < 5) m->set_linear_from_host(layer, which, values);
     else if (which >= 5 && which < 9) m->set_vector(layer, which, values);
     else fail(GLM_CONTRACT, "glmmodel", "unknown tensor slot");
+  });
+}
+
+glm_status glm_model_get_config(const glm_model* m, glm_config* out) {
+  return guarded([&] {
+    checked(m);
+    if (!out) fail(GLM_CONTRACT, "glmmodel", "null output");
+    *out = glm_config{m->L, m->d, m->H, m->f, m->V, m->init_std, m->eps, m->alpha};
+  });
+}
+
+glm_status glm_model_set_quantized(glm_model* m, int layer, int which, const int8_t* payload,
+                                   int64_t payload_bytes, const double* scales, int64_t nscales) {
+  return guarded([&] {
+    checked(m);
+    if (layer < 0 || layer >= m->L || which < 0 || which > 4) fail(GLM_CONTRACT, "glmmodel", "bad linear index");
+    if (!payload || !scales) fail(GLM_CONTRACT, "glmmodel", "null payload or scales");
+    m->set_linear_quantized(layer, which, payload, payload_bytes, scales, nscales);
   });
 }
 

@@ -93,6 +93,9 @@ SIGNATURES = {
     "glm_model_destroy": (I32, [P]),
     "glm_debug_trace_start": (I32, [I64]),
     "glm_debug_trace_stop": (I32, [P, I64, P]),
+    "glm_model_set_quantized": (I32, [P, I32, I32, P, I64, P, I64]),
+    "glm_model_get_config": (I32, [P, P]),
+    "glm_model_load_quantized": (I32, [C.c_char_p, I32, I32, I32, I32, I32, P]),
     "glm_tp_unique_id": (I32, [P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
@@ -318,6 +321,32 @@ class Model:
         if getattr(self, "h", None) and _LIB is not None:
             _LIB.glm_model_destroy(self.h)
             self.h = None
+
+    @classmethod
+    def load_quantized(cls, directory, max_batch=1, max_ctx=256, head_bf16=False, tp_rank=0, tp_size=1):
+        """load_quantized_model (quant.cpp:450-491) of a reference checkpoint directory."""
+        h = C.c_void_p()
+        _check(lib().glm_model_load_quantized(os.fsencode(directory), max_batch, max_ctx, int(head_bf16), tp_rank,
+                                              tp_size, C.byref(h)))
+        self = cls.__new__(cls)
+        self.h = h
+        cfg = _Config()
+        import json
+        with open(os.path.join(directory, "manifest.json")) as fh:
+            man = json.load(fh)
+        jc, jp = man["config"], man["policy"]
+        self.cfg = GLMConfig(num_layers=jc["num_layers"], hidden=jc["hidden"], num_heads=jc["num_heads"],
+                             ffn_hidden=jc["ffn_hidden"], vocab=jc["vocab"])
+        self.bits, self.axis = jp["bits"], jp["axis"]
+        self._c = self.cfg.c()
+        del cfg
+        return self
+
+    def set_quantized(self, layer, which, payload, scales):
+        """A canonical QuantizedMatrix (payload int8 bytes, FP64 scales) of linear `which`."""
+        payload = np.ascontiguousarray(payload, np.int8)
+        scales = np.ascontiguousarray(scales, np.float64)
+        _check(lib().glm_model_set_quantized(self.h, layer, which, _p(payload), payload.size, _p(scales), scales.size))
 
     def init_comm(self, unique_id: bytes):
         """Join the tensor-parallel group (NCCL over NVLink); no-op at tp_size == 1."""

@@ -166,8 +166,22 @@ static void no_gpu_contract() {
   CHECK(std::string(glm_version()).find("sm_100a") != std::string::npos);
 }
 
+// load_quantized_model through the C++ wrapper: a reference-format checkpoint directory
+// (written by tests/test_checkpoint.py) serves greedy decode like the constructed model.
+static void load_checkpoint(const char* dir) {
+  QuantizedModel m = QuantizedModel::load_quantized(dir, 1, 64);
+  std::vector<int> toks = {6, 13, 20, 27, 2};
+  std::vector<int> pos = {0, 1, 2, 3, 4};
+  std::vector<float> logits = m.prefill(0, toks, pos, 5, true);
+  CHECK(logits.size() == 5u * 300u);
+  std::vector<int> next = m.decode_step({3}, {4});
+  CHECK(next[0] >= 0 && next[0] < 300);
+}
+
 int main(int argc, char** argv) {
-  if (argc > 1 && std::strcmp(argv[1], "--no-gpu") == 0) {
+  if (argc > 2 && std::strcmp(argv[1], "--checkpoint") == 0) {
+    load_checkpoint(argv[2]);
+  } else if (argc > 1 && std::strcmp(argv[1], "--no-gpu") == 0) {
     no_gpu_contract();
   } else {
     absmax_worked_row();
