@@ -346,3 +346,36 @@ def qlinear_full(x, q):
     _check(lib().or_qlinear_full(_ptr(x), x.shape[0], q["rows"], q["cols"], _ptr(np.ascontiguousarray(q["payload"])),
                                  _ptr(np.ascontiguousarray(q["scales"])), q["bits"], AXIS[q["axis"]], _ptr(y)))
     return y
+
+
+def mask_sample(tokens, spans, permutation, mask_id=1, sop_id=3):
+    """A [MASK] blank-infilling sample laid out as corrupt_mask does (corruption.cpp:190-247):
+    Part A = the text with each span replaced by one [MASK] placeholder (sequential positions),
+    Part B = the spans in `permutation` order, each [sop] + its tokens, every Part-B input
+    carrying its span's placeholder position. spans = [(start, length), ...] sorted by start.
+    Token ids: [MASK] = 1, [sop] = 3 (corruption.hpp:17-19)."""
+    toks, pos, span_id, span_off = [], [], [], []
+    placeholder = []
+    cursor = 0
+    for (start, length) in spans:
+        while cursor < start:
+            toks.append(tokens[cursor]); pos.append(len(toks) - 1); span_id.append(-1); span_off.append(-1)
+            cursor += 1
+        placeholder.append(len(toks))
+        toks.append(mask_id); pos.append(len(toks) - 1); span_id.append(-1); span_off.append(-1)
+        cursor = start + length
+    while cursor < len(tokens):
+        toks.append(tokens[cursor]); pos.append(len(toks) - 1); span_id.append(-1); span_off.append(-1)
+        cursor += 1
+    C = len(toks)
+    rank = [0] * len(spans)
+    for r, s in enumerate(permutation):
+        rank[s] = r
+    for s in permutation:
+        start, length = spans[s]
+        for j in range(length + 1):
+            toks.append(sop_id if j == 0 else tokens[start + j - 1])
+            pos.append(placeholder[s]); span_id.append(s); span_off.append(j)
+    n = len(toks)
+    return dict(n=n, tokens=toks, positions=pos, span_id=span_id, span_offset=span_off, segment=[0] * n,
+                span_rank=rank, context_length=C)
