@@ -271,3 +271,20 @@ def test_batched_decode_bf16_head_tensor_cores(batch):
         top = np.sort(ls[0])[-2:]
         if top[1] - top[0] > 4 * err:
             assert int(nb[b]) == int(ns[0]) == int(np.argmax(ls[0]))
+
+
+def test_unidirectional_forward_is_context_length_zero(int8_row):
+    """The reference's unidirectional variant (model.cpp:156-162, :180-183) is the same
+    visibility predicate with C = 0 (pure causal): prefill(context_length=0) == oracle."""
+    p, m, _ = int8_row
+    sample = O.gmask_sample(PREFIX[:50])
+    sample["unidirectional"] = 1
+    ref, at, ft, zero = oracle_rows(p, sample)
+    m.reset()
+    m.enable_taps(True)
+    lg = m.prefill(sample["tokens"], sample["positions"], 0).astype(np.float64)
+    pa, pf = m.taps(sample["n"])
+    m.enable_taps(False)
+    check_logits(lg, ref, zero)
+    check_taps(pa, at)
+    check_taps(pf, ft)
