@@ -90,6 +90,12 @@ typedef struct glm_qweight glm_qweight;
 /* From the canonical reference payload + FP64 scales (host buffers). Absmax only. */
 glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64_t rows,
                               int64_t cols, int bits, glm_axis axis, glm_qweight** out);
+/* Any scheme: zeropoint weights (quantize_zeropoint, quant.cpp:145-186) run the same
+ * kernels with the zero points applied as a rank-1 epilogue term; zero_points may be NULL
+ * for GLM_ABSMAX. Constant groups (scale 0) follow quant.cpp:209-216. */
+glm_status glm_qweight_create_ex(const int8_t* payload, const double* scales, const double* zero_points,
+                                 int64_t rows, int64_t cols, int bits, glm_scheme scheme, glm_axis axis,
+                                 glm_qweight** out);
 /* Quantize a [rows, cols] weight (host, dtype F64/F32/BF16) straight into a handle. */
 glm_status glm_qweight_quantize(const void* w, glm_dtype dtype, int64_t rows, int64_t cols,
                                 int bits, glm_axis axis, glm_qweight** out);

@@ -139,10 +139,10 @@ inline std::vector<std::int8_t> unpack_int4(const std::vector<std::int8_t>& pack
 class QLinear {
  public:
   explicit QLinear(const QuantizedMatrix& q) : rows_(q.rows), cols_(q.cols) {
-    if (q.scheme != QuantScheme::kAbsmax) throw ContractError("[qlinear] only absmax payloads run on the GPU path");
     glm_qweight* h = nullptr;
-    check(glm_qweight_create(q.payload.data(), q.scales.data(), q.rows, q.cols, q.bits,
-                             static_cast<glm_axis>(q.axis), &h));
+    check(glm_qweight_create_ex(q.payload.data(), q.scales.data(),
+                                q.zero_points.empty() ? nullptr : q.zero_points.data(), q.rows, q.cols, q.bits,
+                                static_cast<glm_scheme>(q.scheme), static_cast<glm_axis>(q.axis), &h));
     h_.reset(h);
   }
   Index rows() const { return rows_; }

@@ -1,3 +1,4 @@
+#include <cmath>
 #include <algorithm>
 #include <cstdlib>
 // capi_quant.cpp — C ABI for quantization and the quantized linear (include/glm130b.h).
@@ -49,8 +50,9 @@ size_t dtype_size(glm_dtype d) {
 
 struct glm_qweight {
   glm::QWeightDev w;
-  glm::DeviceBuffer codes, col_scale, row_scale, scales64;
+  glm::DeviceBuffer codes, col_scale, row_scale, scales64, zvec, zeta;
   int bits = 8;
+  int scheme = GLM_ABSMAX;
 };
 
 namespace glm {
@@ -91,19 +93,25 @@ void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, c
   const int64_t rows = gemv ? M : xtile_tokens(static_cast<int>(M));
   DeviceBuffer xb(rows * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
   CUDA_CHECK(cudaMemsetAsync(xb.ptr, 0, xb.bytes, st));
+  DeviceBuffer ztb(w.zvec ? M * 4 : 0);
+  const float* zt = nullptr;
+  if (w.zvec) {  // zeropoint weights: per-row sums of the activations the MMA sees
+    zp_token_sums(x, w.L.K, static_cast<int>(M), w, ztb.as<float>(), st);
+    zt = ztb.as<float>();
+  }
   if (gemv) {
     xfrag_from_f32(x, w.L.K, static_cast<int>(M), w, xb.as<__half>(), st);
     gemv_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
   } else {
     xtile_from_f32(x, w.L.K, static_cast<int>(M), w, xb.as<__half>(), st);
     if (p.ksplit == 1) {  // the tcgen05 epilogue writes the scaled result directly
-      qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st, y, w.L.N);
+      qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st, y, w.L.N, zt);
       CUDA_CHECK(cudaStreamSynchronize(st));
       return;
     }
     qmm_launch(w, xb.as<__half>(), static_cast<int>(M), part.as<float>(), p, st);
   }
-  gemv_reduce(part.as<float>(), p.ksplit, static_cast<int>(M), w, y, w.L.N, st);
+  gemv_reduce(part.as<float>(), p.ksplit, static_cast<int>(M), w, y, w.L.N, st, zt);
   CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -216,6 +224,48 @@ glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64
         if (c < -7) fail(GLM_CONTRACT, "quantlab", "INT4 code -8 outside [-7, 7]");
     }
     auto q = make_qweight(dp.as<int8_t>(), ds.as<double>(), rows, cols, bits, axis, nullptr);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    *out = q.release();
+  });
+}
+
+glm_status glm_qweight_create_ex(const int8_t* payload, const double* scales, const double* zero_points,
+                                 int64_t rows, int64_t cols, int bits, glm_scheme scheme, glm_axis axis,
+                                 glm_qweight** out) {
+  if (scheme == GLM_ABSMAX) return glm_qweight_create(payload, scales, rows, cols, bits, axis, out);
+  return guarded([&] {
+    check_policy(bits, axis);
+    if (scheme != GLM_ZEROPOINT) fail(GLM_CONTRACT, "quantlab", "unknown quantization scheme");
+    if (!zero_points) fail(GLM_CONTRACT, "quantlab", "zeropoint weights need their zero points");
+    if (rows <= 0 || cols <= 0) fail(GLM_DIMENSION, "qlinear", "empty weight");
+    const int64_t pb = payload_bytes(rows, cols, bits), g = group_count(rows, cols, axis);
+    // s_eff = s, or 1 for constant groups (s == 0: codes 0, value z; quant.cpp:209-216)
+    std::vector<double> seff(g);
+    for (int64_t i = 0; i < g; ++i) {
+      if (!std::isfinite(scales[i]) || !std::isfinite(zero_points[i])) fail(GLM_FORMAT, "quantlab", "non-finite scale");
+      seff[i] = scales[i] == 0.0 ? 1.0 : scales[i];
+    }
+    DeviceBuffer dp(pb), ds(g * 8);
+    CUDA_CHECK(cudaMemcpy(dp.ptr, payload, pb, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(ds.ptr, seff.data(), g * 8, cudaMemcpyHostToDevice));
+    auto q = make_qweight(dp.as<int8_t>(), ds.as<double>(), rows, cols, bits, axis, nullptr);
+    q->scheme = GLM_ZEROPOINT;
+    CUDA_CHECK(cudaMemcpy(q->w.scales64, scales, g * 8, cudaMemcpyHostToDevice));  // export the originals
+    const QLayout& L = q->w.L;
+    std::vector<float> zvec(L.Np, 0.f), zeta(L.Kp, 0.f);
+    double smax = 0.0;
+    for (int64_t i = 0; i < g; ++i) smax = std::max(smax, seff[i]);
+    for (int64_t n = 0; n < cols; ++n)
+      zvec[n] = static_cast<float>(axis == GLM_AXIS_ROW ? smax
+                                   : axis == GLM_AXIS_COLUMN ? seff[n] * zero_points[n]
+                                                             : seff[0] * zero_points[0]);
+    for (int64_t k = 0; k < rows; ++k) zeta[k] = axis == GLM_AXIS_ROW ? static_cast<float>(zero_points[k]) : 1.f;
+    q->zvec.alloc(L.Np * 4);
+    q->zeta.alloc(L.Kp * 4);
+    CUDA_CHECK(cudaMemcpy(q->zvec.ptr, zvec.data(), L.Np * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(q->zeta.ptr, zeta.data(), L.Kp * 4, cudaMemcpyHostToDevice));
+    q->w.zvec = q->zvec.as<float>();
+    q->w.zeta = q->zeta.as<float>();
     CUDA_CHECK(cudaDeviceSynchronize());
     *out = q.release();
   });

@@ -690,7 +690,8 @@ __global__ void k_xfrag_from_f32(const float* __restrict__ x, int64_t ldx, int M
 }
 
 __global__ void k_gemv_reduce(const float* __restrict__ partial, int ksplit, int M, int64_t N, int64_t Np,
-                              const float* __restrict__ col_scale, float* __restrict__ y, int64_t ldy) {
+                              const float* __restrict__ col_scale, float* __restrict__ y, int64_t ldy,
+                              const float* __restrict__ zt, const float* __restrict__ zvec) {
   const int64_t total = static_cast<int64_t>(M) * N;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -698,7 +699,7 @@ __global__ void k_gemv_reduce(const float* __restrict__ partial, int ksplit, int
     const int64_t n = i % N;
     float acc = 0.f;
     for (int s = 0; s < ksplit; ++s) acc += partial[(static_cast<int64_t>(s) * M + m) * Np + n];
-    y[m * ldy + n] = acc * col_scale[n];
+    y[m * ldy + n] = zt ? acc * col_scale[n] + zt[m] * zvec[n] : acc * col_scale[n];
   }
 }
 
@@ -855,11 +856,35 @@ void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __h
   LAUNCH_CHECK("k_xfrag_from_f32");
 }
 
+// zero-point token sums: one warp per row, fp16 rounding of the folded activation exactly as
+// the activation buffers hold it
+__global__ void k_zp_token_sums(const float* __restrict__ x, int64_t ldx, int64_t K, const float* __restrict__ row_scale,
+                                const float* __restrict__ zeta, float* __restrict__ zt) {
+  const int m = blockIdx.x;
+  float acc = 0.f;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+    acc += __half2float(__float2half_rn(x[m * ldx + k] * row_scale[k])) * zeta[k];
+  __shared__ float red[8];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];
+    zt[m] = t;
+  }
+}
+
+void zp_token_sums(const float* x, int64_t ldx, int M, const QWeightDev& w, float* zt, cudaStream_t st) {
+  k_zp_token_sums<<<M, 256, 0, st>>>(x, ldx, w.L.K, w.row_scale, w.zeta, zt);
+  LAUNCH_CHECK("k_zp_token_sums");
+}
+
 void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, float* y, int64_t ldy,
-                 cudaStream_t st) {
+                 cudaStream_t st, const float* zt) {
   const int64_t total = static_cast<int64_t>(M) * w.L.N;
   const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  k_gemv_reduce<<<grid, 256, 0, st>>>(partial, ksplit, M, w.L.N, w.L.Np, w.col_scale, y, ldy);
+  k_gemv_reduce<<<grid, 256, 0, st>>>(partial, ksplit, M, w.L.N, w.L.Np, w.col_scale, y, ldy, zt, w.zvec);
   LAUNCH_CHECK("k_gemv_reduce");
 }
 

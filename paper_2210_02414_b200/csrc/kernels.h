@@ -49,7 +49,15 @@ struct QWeightDev {
   float* row_scale = nullptr;    // [Kp] activation fold (kRow), 1 otherwise
   double* scales64 = nullptr;    // canonical FP64 scales of this (local) matrix
   int64_t nscales = 0;
+  // zeropoint scheme (quant.cpp:145-186, dequant :209-216): w = s_eff * (code + z) with
+  // s_eff = s (or 1 for constant groups, whose codes are 0 and value is z). The MMA still
+  // accumulates x . code; the zero points add a rank-1 term y[m][n] += zt[m] * zvec[n] with
+  // zt[m] = sum_k x'_k * zeta_k over the fp16 activations the MMA sees (zp_token_sums).
+  const float* zvec = nullptr;   // [Np]: s_eff_n * z_n (kColumn), s_eff * z (kWhole), s_max (kRow)
+  const float* zeta = nullptr;   // [Kp]: z_k (kRow), 1 (others); 0 beyond K
 };
+// zt[m] = sum_k half(x[m][k] * row_scale[k]) * zeta[k]   (the zero-point term of zeropoint weights)
+void zp_token_sums(const float* x, int64_t ldx, int M, const QWeightDev& w, float* zt, cudaStream_t st);
 
 struct GemvPlan {
   int ksplit = 1;
@@ -84,15 +92,16 @@ inline int xtile_tokens(int M) { return (M + kQmmTokens - 1) / kQmmTokens * kQmm
 GemvPlan plan_qmm(const QLayout& L, int M);
 // y (optional, ksplit == 1): write the scaled result y[M][ldy] directly instead of partials
 void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
-                float* y = nullptr, int64_t ldy = 0);
+                float* y = nullptr, int64_t ldy = 0, const float* zt = nullptr);
 void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st);
 long long*& qmm_trace_ptr();  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
 
 // x fp32 [M][K] (row stride ldx) -> x_frag fp16 with the kRow scale fold
 void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xfrag, cudaStream_t st);
 // y[m][n] (row stride ldy) = col_scale[n] * sum_s partial[s][m][n]
+// (zt: per-row zero-point sums for zeropoint weights, else null)
 void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, float* y, int64_t ldy,
-                 cudaStream_t st);
+                 cudaStream_t st, const float* zt = nullptr);
 
 // diagnostics: bind the timeline trace buffer of each translation unit (common.cuh)
 void trace_bind_gemv(unsigned long long* buf, unsigned long long cap);

@@ -112,6 +112,7 @@ struct QmmArgs {
   const __half* xt;   // activations, 128-token tiles (xtile_index)
   float* partial;     // [ksplit][M][Np], or the final y [M][ldo] when col_scale is set
   const float* col_scale;  // non-null (ksplit == 1): write y = acc * col_scale, columns < N
+  const float *zt, *zvec;  // optional zero-point rank-1 term y += zt[m] * zvec[n] (direct output)
   int64_t ldo, N;
   int64_t nrt16, nch, Np, Kp;
   int M, ksplit, ntt, nrt128;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
         const int64_t col = rt * 128 + row;
         const bool direct = a.col_scale != nullptr;  // final output, group scale applied here
         const float cs = direct && col < a.N ? a.col_scale[col] : 1.f;
+        const float zv = direct && a.zt && col < a.N ? a.zvec[col] : 0.f;
         const int64_t ld = direct ? a.ldo : a.Np;
         float* out = a.partial + (direct ? 0 : static_cast<int64_t>(s) * a.M * a.Np) + col;
         const bool keep = !direct || col < a.N;
@@ -326,7 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             const int64_t tok = tt * NTOK + c16 + m;
-            if (tok < a.M && keep) out[tok * ld] = __uint_as_float(v[m]) * cs;
+            if (tok < a.M && keep) out[tok * ld] = zv != 0.f ? __uint_as_float(v[m]) * cs + a.zt[tok] * zv
+                                                             : __uint_as_float(v[m]) * cs;
           }
         }
         tc_fence_before();
@@ -387,7 +390,7 @@ GemvPlan plan_qmm(const QLayout& L, int M) {
 }
 
 void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
-                float* y, int64_t ldy) {
+                float* y, int64_t ldy, const float* zt) {
   if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
   if (w.L.Np % 128 || w.L.Kp % 64) fail(GLM_DIMENSION, "qlinear", "layout not padded for the tcgen05 path");
   if (y && p.ksplit != 1) fail(GLM_CONTRACT, "qlinear", "direct output needs an unsplit K");
@@ -396,6 +399,8 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
   a.xt = xt;
   a.partial = y ? y : partial;
   a.col_scale = y ? w.col_scale : nullptr;
+  a.zt = y ? zt : nullptr;
+  a.zvec = w.zvec;
   a.ldo = ldy;
   a.N = w.L.N;
   a.nrt16 = w.L.nrt;

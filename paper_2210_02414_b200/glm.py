@@ -96,6 +96,7 @@ SIGNATURES = {
     "glm_model_set_quantized": (I32, [P, I32, I32, P, I64, P, I64]),
     "glm_model_get_config": (I32, [P, P]),
     "glm_model_load_quantized": (I32, [C.c_char_p, I32, I32, I32, I32, I32, P]),
+    "glm_qweight_create_ex": (I32, [P, P, P, I64, I64, I32, I32, I32, P]),
     "glm_tp_unique_id": (I32, [P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
@@ -221,8 +222,13 @@ class QLinear:
         h = C.c_void_p()
         payload = np.ascontiguousarray(q["payload"], np.int8)
         scales = np.ascontiguousarray(q["scales"], np.float64)
-        _check(lib().glm_qweight_create(_p(payload), _p(scales), q["rows"], q["cols"], q["bits"], AXIS[q["axis"]],
-                                        C.byref(h)))
+        if q.get("scheme", "absmax") == "zeropoint":
+            zp = np.ascontiguousarray(q["zero_points"], np.float64)
+            _check(lib().glm_qweight_create_ex(_p(payload), _p(scales), _p(zp), q["rows"], q["cols"], q["bits"],
+                                               SCHEME["zeropoint"], AXIS[q["axis"]], C.byref(h)))
+        else:
+            _check(lib().glm_qweight_create(_p(payload), _p(scales), q["rows"], q["cols"], q["bits"],
+                                            AXIS[q["axis"]], C.byref(h)))
         return cls(h, q["rows"], q["cols"], q["bits"], q["axis"])
 
     @classmethod

@@ -80,3 +80,24 @@ def test_qlinear_quantize_handle_equals_payload_handle():
     x = rng.normal(size=(4, 256))
     assert np.array_equal(a(x), b(x))
     assert np.array_equal(a.device_bytes(), b.device_bytes())
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("axis", ["row", "column", "whole"])
+def test_zeropoint_qlinear_matches_oracle(bits, axis):
+    """quantize_zeropoint payloads (quant.cpp:145-186) on the GPU: the MMA accumulates x.code
+    and the zero points enter as a rank-1 epilogue term; constant groups (quant.cpp:209-216)
+    included. Reference: the oracle's x . dequantize(q)."""
+    rng = np.random.default_rng(bits * 10 + len(axis))
+    K, N = 640, 384
+    w = rng.normal(0.01, 0.02, size=(K, N))
+    w[:, 5] = 0.037        # constant column
+    w[7, :] = -0.011       # constant row
+    q = O.quantize(w, bits, axis, scheme="zeropoint")
+    lin = glm.QLinear.from_payload(q)
+    deq = O.dequantize(q)
+    for M in (1, 5, 16, 37, 300):
+        x = rng.normal(0, 1, size=(M, K))
+        y = lin(x).astype(np.float64)
+        ref = x @ deq
+        assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
