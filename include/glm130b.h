@@ -192,6 +192,14 @@ glm_status glm_model_memory(const glm_model* m, glm_memory* out);
  * logits (host, optional) receives [n, vocab] fp32. */
 glm_status glm_model_prefill(glm_model* m, int seq, const int* tokens, const int* positions,
                              int n, int context_length, float* logits);
+/* Packed prefill (pack_samples, corruption.cpp:295-334): nseg samples concatenated row-wise
+ * (tokens/positions of sample i at rows [sum_{j<i} lengths[j], ...)) run as one batch through
+ * the linears; attention is per sample (segment isolation) with its own context length, and
+ * sample i fills the KV cache of sequence seqs[i] (distinct) from slot 0. logits (optional)
+ * receives [sum(lengths), vocab]. */
+glm_status glm_model_prefill_batch(glm_model* m, int nseg, const int* seqs, const int* lengths,
+                                   const int* context_lengths, const int* tokens, const int* positions,
+                                   float* logits);
 /* One decode step for sequences 0..batch-1: token b at position positions[b] attends to
  * its whole cache plus itself (decode rows are causal-suffix rows, corruption.cpp:349-362).
  * next_tokens (host, optional) = greedy argmax; logits (host, optional) [batch, vocab]. */

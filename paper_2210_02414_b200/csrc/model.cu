@@ -628,10 +628,28 @@ struct glm_model {
   }
 
   void prefill(int seq, const int* tokens, const int* positions, int n, int context_len, float* logits_out) {
+    prefill_batch(1, &seq, &n, &context_len, tokens, positions, logits_out);
+  }
+
+  // Packed prefill (pack_samples, corruption.cpp:295-334): `nseg` samples concatenated row-wise
+  // run through every linear / LayerNorm / GeGLU as one M = sum(n) batch; RoPE, the KV-cache
+  // write and attention stay per sample (segment isolation: each sample attends only to its
+  // own sequence's cache), each filling sequence seqs[i] from slot 0.
+  void prefill_batch(int nseg, const int* seqs, const int* lens, const int* ctx, const int* tokens,
+                     const int* positions, float* logits_out) {
     check_loaded();
-    if (seq < 0 || seq >= max_batch) fail(GLM_CONTRACT, "glmmodel", "sequence index outside max_batch");
-    if (n < 1 || n > max_ctx) fail(GLM_CONTRACT, "glmmodel", "prefill length must be in 1..max_ctx");
-    if (context_len < 0 || context_len > n) fail(GLM_CONTRACT, "glmmodel", "context_length must be in 0..n");
+    if (nseg < 1 || nseg > max_batch) fail(GLM_CONTRACT, "glmmodel", "segment count must be in 1..max_batch");
+    std::vector<int> row0(nseg + 1, 0);
+    std::vector<bool> used(max_batch, false);
+    for (int i = 0; i < nseg; ++i) {
+      if (seqs[i] < 0 || seqs[i] >= max_batch) fail(GLM_CONTRACT, "glmmodel", "sequence index outside max_batch");
+      if (used[seqs[i]]) fail(GLM_CONTRACT, "glmmodel", "a sequence appears twice in one packed prefill");
+      used[seqs[i]] = true;
+      if (lens[i] < 1 || lens[i] > max_ctx) fail(GLM_CONTRACT, "glmmodel", "prefill length must be in 1..max_ctx");
+      if (ctx[i] < 0 || ctx[i] > lens[i]) fail(GLM_CONTRACT, "glmmodel", "context_length must be in 0..n");
+      row0[i + 1] = row0[i] + lens[i];
+    }
+    const int n = row0[nseg];
     for (int i = 0; i < n; ++i) {
       if (tokens[i] < 0 || tokens[i] >= V)
         fail(GLM_CONTRACT, "glmmodel", "token id " + std::to_string(tokens[i]) + " overflows vocabulary " + std::to_string(V));
@@ -648,12 +666,16 @@ struct glm_model {
       Layer& ly = layers[l];
       Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
       linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
-      RopeStoreArgs rs{y_qkv.as<float>(), 3ll * dl, dl, n, Hl, dh, seq, max_ctx, 0, dpos.as<int>(), rope,
-                       q_rot.as<float>(), kcache(l), vcache(l)};
-      launch_rope_store(rs, st);
-      AttnPrefillArgs ap{q_rot.as<float>(), kcache(l), vcache(l), n, Hl, dh, seq, max_ctx, context_len,
-                         attn_out.as<float>(), dl};
-      launch_attn_prefill(ap, st);
+      for (int i = 0; i < nseg; ++i) {
+        const int r0 = row0[i], ni = lens[i];
+        float* qseg = q_rot.as<float>() + static_cast<int64_t>(r0) * dl;  // [heads][ni][dh] of this sample
+        RopeStoreArgs rs{y_qkv.as<float>() + static_cast<int64_t>(r0) * 3 * dl, 3ll * dl, dl, ni, Hl, dh, seqs[i],
+                         max_ctx, 0, dpos.as<int>() + r0, rope, qseg, kcache(l), vcache(l)};
+        launch_rope_store(rs, st);
+        AttnPrefillArgs ap{qseg, kcache(l), vcache(l), ni, Hl, dh, seqs[i], max_ctx, ctx[i],
+                           attn_out.as<float>() + static_cast<int64_t>(r0) * dl, dl};
+        launch_attn_prefill(ap, st);
+      }
       launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
       linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
       if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
@@ -695,12 +717,13 @@ struct glm_model {
       launch_argmax_finish(d_argmax, d_next_rows, n, st);
       CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(n) * V * 4, cudaMemcpyDeviceToHost, st));
     }
-    const int len = n;
-    CUDA_CHECK(cudaMemcpyAsync(d_len + seq, &len, 4, cudaMemcpyHostToDevice, st));
+    for (int i = 0; i < nseg; ++i)
+      CUDA_CHECK(cudaMemcpyAsync(d_len + seqs[i], &lens[i], 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
-    h_len[seq] = n;
+    for (int i = 0; i < nseg; ++i) h_len[seqs[i]] = lens[i];
     last_rows = n;
   }
+
 };
 
 // ======================================================================================
@@ -823,6 +846,14 @@ glm_status glm_model_memory(const glm_model* m, glm_memory* out) {
 glm_status glm_model_prefill(glm_model* m, int seq, const int* tokens, const int* positions, int n, int context_length,
                              float* logits) {
   return guarded([&] { checked(m)->prefill(seq, tokens, positions, n, context_length, logits); });
+}
+
+glm_status glm_model_prefill_batch(glm_model* m, int nseg, const int* seqs, const int* lengths,
+                                   const int* context_lengths, const int* tokens, const int* positions, float* logits) {
+  return guarded([&] {
+    if (!seqs || !lengths || !context_lengths || !tokens || !positions) fail(GLM_CONTRACT, "glmmodel", "null argument");
+    checked(m)->prefill_batch(nseg, seqs, lengths, context_lengths, tokens, positions, logits);
+  });
 }
 
 glm_status glm_model_decode_step(glm_model* m, int batch, const int* tokens, const int* positions, int* next_tokens,

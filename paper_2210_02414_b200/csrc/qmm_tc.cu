@@ -124,12 +124,28 @@ __device__ __forceinline__ void stamp(const QmmArgs& a, int ev, uint32_t q) {
 
 // item -> (128-feature tile, token tile, k split); token tiles innermost so the CTAs working
 // at the same time share a few weight row tiles (L2-resident), stages = 64-k chunks.
+// Token tiles are walked in groups of kTokGroup (2048 tokens = 50 MB of activations at
+// K = 12288) so that a group's activations stay L2-resident while every row tile passes
+// over them; a packed prefill of many samples would otherwise re-read them from HBM.
+constexpr int64_t kTokGroup = 16;
 __device__ __forceinline__ void decode_item(const QmmArgs& a, int64_t item, int64_t& rt, int64_t& tt, int& s,
                                             int64_t& c0, int64_t& c1) {
   s = static_cast<int>(item % a.ksplit);
-  const int64_t rest = item / a.ksplit;
-  tt = rest % a.ntt;
-  rt = rest / a.ntt;
+  int64_t rest = item / a.ksplit;
+  const int64_t full = a.ntt / kTokGroup;              // complete token groups
+  const int64_t per_full = static_cast<int64_t>(a.nrt128) * kTokGroup;
+  int64_t tg, tgn;
+  if (rest < full * per_full) {
+    tg = rest / per_full;
+    rest -= tg * per_full;
+    tgn = kTokGroup;
+  } else {
+    rest -= full * per_full;
+    tg = full;
+    tgn = a.ntt - full * kTokGroup;
+  }
+  tt = tg * kTokGroup + rest % tgn;
+  rt = rest / tgn;
   c0 = a.nch * s / a.ksplit;
   c1 = a.nch * (s + 1) / a.ksplit;
 }

@@ -97,6 +97,7 @@ SIGNATURES = {
     "glm_model_get_config": (I32, [P, P]),
     "glm_model_load_quantized": (I32, [C.c_char_p, I32, I32, I32, I32, I32, P]),
     "glm_qweight_create_ex": (I32, [P, P, P, I64, I64, I32, I32, I32, P]),
+    "glm_model_prefill_batch": (I32, [P, I32, P, P, P, P, P, P]),
     "glm_tp_unique_id": (I32, [P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
@@ -404,6 +405,19 @@ class Model:
         out = np.empty((n, self.cfg.vocab), np.float32) if logits else None
         _check(lib().glm_model_prefill(self.h, seq, _p(tokens), _p(positions), n,
                                        n if context_length is None else context_length, _p(out)))
+        return out
+
+    def prefill_batch(self, samples, logits=True):
+        """Packed prefill (pack_samples, corruption.cpp:295-334): samples = [(seq, tokens,
+        positions, context_length), ...]; one batch through the linears, per-sample attention."""
+        seqs = np.array([s[0] for s in samples], np.int32)
+        lens = np.array([len(s[1]) for s in samples], np.int32)
+        ctx = np.array([s[3] for s in samples], np.int32)
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(s[1], np.int32) for s in samples]))
+        poss = np.ascontiguousarray(np.concatenate([np.asarray(s[2], np.int32) for s in samples]))
+        out = np.zeros((int(lens.sum()), self.cfg.vocab), np.float32) if logits else None
+        _check(lib().glm_model_prefill_batch(self.h, len(samples), _p(seqs), _p(lens), _p(ctx), _p(toks), _p(poss),
+                                             _p(out)))
         return out
 
     def decode_step(self, tokens, positions, logits=True):

@@ -288,3 +288,23 @@ def test_unidirectional_forward_is_context_length_zero(int8_row):
     check_logits(lg, ref, zero)
     check_taps(pa, at)
     check_taps(pf, ft)
+
+
+def test_packed_prefill_isolates_samples_and_fills_their_caches():
+    """Packed prefill (pack_samples, corruption.cpp:295-334): three samples in one call, each
+    attending only to itself; logits per sample = oracle forward of that sample alone, and a
+    batched decode step afterwards continues every sequence from its own cache."""
+    p, m, _ = build(4, "column", max_batch=3)
+    samples = [O.gmask_sample(PREFIX[:40]), O.gmask_sample(PREFIX[7:30], [41, 42]), O.gmask_sample(PREFIX[3:60])]
+    refs = [oracle_rows(p, s) for s in samples]
+    m.reset()
+    lg = m.prefill_batch([(b, s["tokens"][:-1], s["positions"][:-1], s["context_length"])
+                          for b, s in enumerate(samples)]).astype(np.float64)
+    r = 0
+    for s, (ref, _, _, zero) in zip(samples, refs):
+        n = s["n"] - 1
+        check_logits(lg[r:r + n], ref[:n], zero[:n])
+        r += n
+    _, ld = m.decode_step([s["tokens"][-1] for s in samples], [s["positions"][-1] for s in samples])
+    for b, (s, (ref, _, _, zero)) in enumerate(zip(samples, refs)):
+        check_logits(ld[b:b + 1].astype(np.float64), ref[-1:], zero[-1:])

@@ -19,6 +19,7 @@ ap.add_argument("--seq", type=int, default=2048)
 ap.add_argument("--batch", type=int, default=4)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--bits", type=int, nargs="+", default=[4, 8])
+ap.add_argument("--separate", action="store_true", help="one prefill call per sample instead of one packed call")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 d, H, f = 12288, 96, 32768
@@ -35,8 +36,11 @@ for bits in a.bits:
         samples.append((toks, pos[:a.seq], C))
 
     def run():
-        for b, (toks, pos, C) in enumerate(samples):
-            m.prefill(toks, pos, C, seq=b, logits=False)
+        if a.separate:
+            for b, (toks, pos, C) in enumerate(samples):
+                m.prefill(toks, pos, C, seq=b, logits=False)
+        else:  # packed: one call, M = batch * seq rows through every linear
+            m.prefill_batch([(b, toks, pos, C) for b, (toks, pos, C) in enumerate(samples)], logits=False)
 
     run()
     torch.cuda.synchronize()
@@ -53,6 +57,7 @@ for bits in a.bits:
                       "seq": a.seq, "batch": a.batch, "ms": ms, "tokens_per_s": n / ms * 1e3,
                       "linear_tflop": lin_flop / 1e12, "attention_tflop": att_flop / 1e12,
                       "tflops": (lin_flop + att_flop) / (ms * 1e-3) / 1e12,
+                      "mode": "separate calls" if a.separate else "packed (one call)",
                       "timing": "host wall clock around synchronised prefill calls (includes host copies)"}),
           flush=True)
     del m
