@@ -142,10 +142,10 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) y[i] = make_float2(0.f, 0.f);
   if (!a.zero_sublayer) {
-    for (int s0 = 0; s0 < a.in.ksplit; s0 += 4) {
-      float2 v[4][kLnPairs];
+    for (int s0 = 0; s0 < a.in.ksplit; s0 += 8) {
+      float2 v[8][kLnPairs];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int i = 0; i < kLnPairs; ++i) {
           const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
@@ -155,7 +155,7 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
                         : make_float2(0.f, 0.f);
         }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int i = 0; i < kLnPairs; ++i) {
           y[i].x += v[u][i].x;
@@ -306,11 +306,13 @@ __global__ void k_geglu_act(ActArgs a) {
 // each), softmax is fp32, P.V has lanes own DH/32 features with 8 independent row loads in
 // flight, and the new key/value enter from shared memory. With several splits, the last
 // CTA of a (head, batch) merges them in split order (deterministic).
-constexpr int kAttnThreads = 256;
+constexpr int kAttnThreadsFew = 256;  // threads per CTA at batch <= 2 (few CTAs)
+constexpr int kAttnThreadsMany = 128;  // larger batches: more resident CTAs per SM
 constexpr int kSplitKeys = 256;
 
-template <int DH>
-__global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) {
+template <int DH, int kAttnThreads>
+__global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
+    k_attn_decode(AttnDecodeArgs a) {
   trace_point(30);
   constexpr int NW = kAttnThreads / 32;
   constexpr int FPL = DH / 32;          // features per lane in the PV phase
@@ -321,9 +323,12 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   __shared__ float opart[NW][DH];
   __shared__ int last;
   __shared__ __align__(8) uint64_t kvbar;
-  extern __shared__ __align__(128) __half kvs[];  // [2][kSplitKeys][DH]: this split's keys, values
+  __shared__ __align__(16) __half knew[DH];       // the new key / value (unstaged mode)
+  __shared__ __align__(16) __half vnew[DH];
+  extern __shared__ __align__(128) __half kvs[];  // [2][stage_keys][DH]: this split's keys, values
+  const bool staged = a.stage_keys > 0;
   __half* kst = kvs;
-  __half* vst = kvs + kSplitKeys * DH;
+  __half* vst = kvs + a.stage_keys * DH;
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cache length / position were written by earlier steps (complete before our predecessor ran)
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&kvbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (n_old > 0) {
+    if (staged && n_old > 0) {
       const uint32_t bytes = static_cast<uint32_t>(n_old) * DH * 2;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&kvbar)), "r"(2 * bytes)
                    : "memory");
@@ -374,13 +379,21 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 
   if (k0 < total) {
     const bool has_new = (len >= k0 && len < k1);
-    auto raw2 = [&](int64_t f) {  // split-K sum of columns (f, f+1), unscaled
+    auto raw2 = [&](int64_t f) {  // split-K sum of columns (f, f+1), unscaled; 8 loads in flight
       float2 acc = make_float2(0.f, 0.f);
-      for (int s = 0; s < a.qkv.ksplit; ++s) {
-        const float2 v = *reinterpret_cast<const float2*>(a.qkv.p + static_cast<int64_t>(s) * a.qkv.split_stride +
-                                                          b * a.qkv.ld + f);
-        acc.x += v.x;
-        acc.y += v.y;
+      for (int s0 = 0; s0 < a.qkv.ksplit; s0 += 8) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = s0 + u < a.qkv.ksplit
+                     ? *reinterpret_cast<const float2*>(a.qkv.p + static_cast<int64_t>(s0 + u) * a.qkv.split_stride +
+                                                        b * a.qkv.ld + f)
+                     : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+        }
       }
       return acc;
     };
@@ -403,11 +416,16 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
         const __half2 vh = __floats2half2_rn(va, vb);
         *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jj) = kh;
         *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * jj) = vh;
-        *reinterpret_cast<__half2*>(kst + (len - k0) * DH + 2 * jj) = kh;
-        *reinterpret_cast<__half2*>(vst + (len - k0) * DH + 2 * jj) = vh;
+        if (staged) {
+          *reinterpret_cast<__half2*>(kst + (len - k0) * DH + 2 * jj) = kh;
+          *reinterpret_cast<__half2*>(vst + (len - k0) * DH + 2 * jj) = vh;
+        } else {
+          *reinterpret_cast<__half2*>(knew + 2 * jj) = kh;
+          *reinterpret_cast<__half2*>(vnew + 2 * jj) = vh;
+        }
       }
     }
-    if (n_old > 0)
+    if (staged && n_old > 0)
       asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W_%=;\n}\n" ::"r"(
                        smem_addr(&kvbar))
                    : "memory");
@@ -434,7 +452,10 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         const int s = s0 + u * NW * KPW + kin;
-        kv[u] = s < k1 ? *reinterpret_cast<const uint4*>(kst + (s - k0) * DH + sub * 8) : make_uint4(0, 0, 0, 0);
+        const __half* kr = staged ? kst + (s - k0) * DH : (s < kold ? kc + static_cast<int64_t>(s) * DH : knew);
+        kv[u] = s < k1 ? (staged || s >= kold ? *reinterpret_cast<const uint4*>(kr + sub * 8)
+                                             : ld_nc(reinterpret_cast<const uint4*>(kr + sub * 8)))
+                       : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
@@ -479,7 +500,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_decode(AttnDecodeArgs a) 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * NW;
-        const __half* vr = vst + (s - k0) * DH + lane * FPL;
+        const __half* vr = (staged ? vst + (s - k0) * DH : (s < kold ? vc + static_cast<int64_t>(s) * DH : vnew)) +
+                           lane * FPL;
         if (s < k1) {
           if constexpr (FPL == 4) vv[u] = *reinterpret_cast<const uint2*>(vr);
           else vv[u] = make_uint2(*reinterpret_cast<const uint32_t*>(vr), 0u);
@@ -1049,19 +1071,30 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
 
 int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplitKeys; }
 
-void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st) {
+void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
+  AttnDecodeArgs a = in;
   const dim3 grid(a.heads, B, a.max_splits);
-  // keys + values of one split staged in shared memory
-  const size_t smem = 2ull * kSplitKeys * a.dh * sizeof(__half);
+  // Few sequences: each CTA bulk-copies its split's keys + values into shared memory ahead
+  // of the dependency wait (one HBM round trip). Many sequences: that shared memory would
+  // cap residency at one CTA per SM over B * heads CTAs, so rows are read from L2/HBM.
+  const int stage = B <= 2 ? std::min(kSplitKeys, (a.max_ctx + 15) / 16 * 16) : 0;
+  a.stage_keys = stage;
+  const size_t smem = 2ull * stage * a.dh * sizeof(__half);
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 128 * 2));
-    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 64 * 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<128, kAttnThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 128 * 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<64, kAttnThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 64 * 2));
     attr = true;
   }
-  if (a.dh == 128) launch_k(k_attn_decode<128>, grid, dim3(kAttnThreads), smem, st, a);
-  else if (a.dh == 64) launch_k(k_attn_decode<64>, grid, dim3(kAttnThreads), smem, st, a);
-  else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
+  if (stage) {
+    if (a.dh == 128) launch_k(k_attn_decode<128, kAttnThreadsFew>, grid, dim3(kAttnThreadsFew), smem, st, a);
+    else if (a.dh == 64) launch_k(k_attn_decode<64, kAttnThreadsFew>, grid, dim3(kAttnThreadsFew), smem, st, a);
+    else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
+  } else {
+    if (a.dh == 128) launch_k(k_attn_decode<128, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), 0, st, a);
+    else if (a.dh == 64) launch_k(k_attn_decode<64, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), 0, st, a);
+    else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
+  }
   LAUNCH_CHECK("k_attn_decode");
 }
 

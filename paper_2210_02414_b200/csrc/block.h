@@ -70,6 +70,7 @@ struct AttnDecodeArgs {
   int* counters;            // [B][heads], zero-initialised
   XOut xo;                  // x_frag of out_proj
   float* out;               // optional fp32 [B][d_local]
+  int stage_keys = 0;       // set by launch_attn_decode: keys per CTA staged in shared memory (0: read from L2/HBM)
 };
 
 struct RopeStoreArgs {

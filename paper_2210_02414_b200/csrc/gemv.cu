@@ -346,6 +346,7 @@ constexpr int kMkSliceBytes = 48 * 1024;  // one activation-slice buffer (all x 
 
 template <int BITS, int NT>
 __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx) {
+  trace_point(10);
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
   constexpr int U = kStageBytes / CHUNK;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -404,6 +405,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
     for (int q = 0; q < kMkStages; ++q) issue();
   pdl_wait();
   pdl_trigger();
+  trace_point(11);
   // activation slices: buffer b holds [nx][M][chunks of the slice][128 B]
   auto load_x = [&](int local, int item) {
     int c0, c1;
@@ -493,6 +495,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
     __syncthreads();  // every warp is done with activation buffer b
     if (threadIdx.x == 0 && item + 2 * static_cast<int>(gridDim.x) < nitems) load_x(local + 2, item + 2 * gridDim.x);
   }
+  trace_point(13);
 }
 
 // ---- single-token variant (batch-1 decode, the headline path) -----------------------------

@@ -52,7 +52,7 @@ w = np.where(kind == 1)[0]
 w = w[np.argsort(t[w])]
 inst = []
 for i in w:
-    if inst and inst[-1]["fam"] == fam[i] and t[i] - inst[-1]["wait_last"] < 3000:
+    if inst and inst[-1]["fam"] == fam[i] and t[i] - inst[-1]["wait_last"] < 20000:
         inst[-1]["wait_last"] = t[i]
         inst[-1]["n"] += 1
     else:
