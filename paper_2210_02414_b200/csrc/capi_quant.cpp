@@ -18,6 +18,17 @@ namespace glm {
 thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
 
+// Row count from which the quantized linear runs on the tcgen05 GEMM instead of the
+// decode GEMV (GLM_QMM_MIN_M, default 17: the GEMV covers M <= 16).
+int qmm_min_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("GLM_QMM_MIN_M");
+    const int x = e ? std::atoi(e) : 17;
+    return x < 2 ? 2 : (x > 17 ? 17 : x);
+  }();
+  return v;
+}
+
 bool sync_launch_debug() {
   static const bool on = std::getenv("GLM_SYNC_LAUNCH") != nullptr;
   return on;
@@ -88,7 +99,7 @@ void check_policy(int bits, int axis) {
 // the tcgen05 GEMM (128-token tiles) above; then the split-K reduce with the group scale.
 void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, cudaStream_t st) {
   const QWeightDev& w = q->w;
-  const bool gemv = M <= 16;
+  const bool gemv = M < qmm_min_rows();
   const GemvPlan p = gemv ? plan_gemv(w.L, static_cast<int>(M)) : plan_qmm(w.L, static_cast<int>(M));
   const int64_t rows = gemv ? M : xtile_tokens(static_cast<int>(M));
   DeviceBuffer xb(rows * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
@@ -395,7 +406,7 @@ glm_status glm_qlinear_bench(const glm_qweight* q, int64_t M, int iters, int flu
   return guarded([&] {
     if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
     const QWeightDev& w = q->w;
-    const bool gemv = M <= 16;
+    const bool gemv = M < qmm_min_rows();
     const GemvPlan p = gemv ? plan_gemv(w.L, static_cast<int>(M)) : plan_qmm(w.L, static_cast<int>(M));
     const int64_t rows = gemv ? M : xtile_tokens(static_cast<int>(M));
     DeviceBuffer xb(rows * w.L.Kp * 2), part(static_cast<int64_t>(p.ksplit) * M * w.L.Np * 4);
