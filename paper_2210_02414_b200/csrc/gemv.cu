@@ -344,16 +344,21 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_tma(GemvArgs a) {
 constexpr int kMkStages = 2;
 constexpr int kMkSliceBytes = 48 * 1024;  // one activation-slice buffer (all x vectors, all tokens)
 
-template <int BITS, int NT>
+// RT row tiles per warp (CTA-item = 16 * RT row tiles): with RT = 2 every activation
+// fragment read from shared memory feeds both tiles' MMAs, halving the activation traffic
+// that bounds INT4 at 9..16 tokens (16 warps re-read the same slice; ncu: ~0.7 shared
+// wavefronts per cycle per SM at RT = 1). A stage then holds U/2 chunks of each tile.
+template <int BITS, int NT, int RT>
 __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx) {
   trace_point(10);
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
-  constexpr int U = kStageBytes / CHUNK;
+  constexpr int U = kStageBytes / CHUNK / RT;  // chunks per tile per stage
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int nch = static_cast<int>(a.nch), ksplit = a.ksplit, M = a.M;
   const int nrt = static_cast<int>(a.nrt);
+  constexpr int kTiles = kTWarps * RT;  // row tiles per CTA-item
   uint8_t* ring = smem + static_cast<size_t>(warp) * kMkStages * kStageBytes;
   uint8_t* xbuf = smem + static_cast<size_t>(kTWarps) * kMkStages * kStageBytes;  // [2][kMkSliceBytes]
   uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * kMkSliceBytes);          // [2]
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
   uint64_t policy, keep;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-  const int ngroups = (nrt + kTWarps - 1) / kTWarps;
+  const int ngroups = (nrt + kTiles - 1) / kTiles;
   const int nitems = ngroups * ksplit;
   auto slice = [&](int s, int& c0, int& c1) {
     c0 = nch * s / ksplit;
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
   int pj = blockIdx.x, pc = 0, pc1 = 0, prt = -1, pslot = 0;
   auto pitem = [&]() {  // position the producer on item pj (skipping items where this warp idles)
     while (pj < nitems) {
-      prt = (pj / ksplit) * kTWarps + warp;
+      prt = (pj / ksplit) * kTiles + warp * RT;
       slice(pj % ksplit, pc, pc1);
       if (prt < nrt) return;
       pj += gridDim.x;
@@ -391,9 +396,12 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
   auto issue = [&]() {
     if (pj >= nitems) return;
     const int n = min(U, pc1 - pc);
-    const uint8_t* src = wbase + (static_cast<int64_t>(prt) * nch + pc) * CHUNK;
-    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(n * CHUNK));
-    bulk_g2s(ring + pslot * kStageBytes, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    const int ntile = (RT == 2 && prt + 1 < nrt) ? 2 : 1;
+    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(ntile * n * CHUNK));
+    for (int q = 0; q < ntile; ++q) {
+      const uint8_t* src = wbase + (static_cast<int64_t>(prt + q) * nch + pc) * CHUNK;
+      bulk_g2s(ring + pslot * kStageBytes + q * n * CHUNK, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    }
     pslot = pslot + 1 == kMkStages ? 0 : pslot + 1;
     pc += n;
     if (pc >= pc1) {
@@ -430,33 +438,34 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
   int local = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
     const int s = item % ksplit;
-    const int rt = (item / ksplit) * kTWarps + warp;
+    const int rt = (item / ksplit) * kTiles + warp * RT;
     int c0, c1;
     slice(s, c0, c1);
     const int nck = c1 - c0;
     const int b = local & 1;
     mbar_wait(xbar + b, (local >> 1) & 1);
     if (rt < nrt) {
+      // (RT = 2: the host only pairs tiles on one side of rt_split, which is even)
       const int v = rt < a.rt_split ? 0 : nx - 1;
+      const bool two = RT == 2 && rt + 1 < nrt;
       const uint8_t* xrow[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
         xrow[nt] = xbuf + b * kMkSliceBytes + ((v * M + min(nt * 8 + g, M - 1)) * nck) * 128 + t * 32;
-      float acc[4][NT][4];
+      float acc[RT][4][NT][4];
 #pragma unroll
-      for (int h = 0; h < 4; ++h)
+      for (int r = 0; r < RT; ++r)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int h = 0; h < 4; ++h)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[h][nt][i] = 0.f;
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[r][h][nt][i] = 0.f;
       for (int c = 0; c < nck; c += U) {
         const int n = min(U, nck - c);
         mbar_wait(bars + cslot, cpar);
         const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
         auto chunk = [&](int u) {
-          uint4 wv[BITS == 4 ? 1 : 2];
-          wv[0] = *reinterpret_cast<const uint4*>(st + u * CHUNK);
-          if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(st + u * CHUNK + 512);
           uint4 xv[NT][2];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
@@ -464,7 +473,15 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
             xv[nt][0] = xa[0];
             xv[nt][1] = xa[1];
           }
-          compute_chunk4<BITS, NT>(wv, xv, acc);
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            if (r == 1 && !two) break;
+            uint4 wv[BITS == 4 ? 1 : 2];
+            const uint8_t* sp = st + (r * n + u) * CHUNK;
+            wv[0] = *reinterpret_cast<const uint4*>(sp);
+            if constexpr (BITS == 8) wv[1] = *reinterpret_cast<const uint4*>(sp + 512);
+            compute_chunk4<BITS, NT>(wv, xv, acc[r]);
+          }
         };
         if (n == U) {
 #pragma unroll
@@ -481,16 +498,21 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
         }
         if (lane == 0) issue();
       }
-      float* out = a.partial + static_cast<int64_t>(s) * M * a.Np + static_cast<int64_t>(rt) * kTileN;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int r = 0; r < RT; ++r) {
+        if (r == 1 && !two) break;
+        float* out = a.partial + static_cast<int64_t>(s) * M * a.Np + static_cast<int64_t>(rt + r) * kTileN;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int m = nt * 8 + 2 * t + (i & 1);
-          const int row = g + 8 * (i >> 1);
-          if (m < M)
-            out[static_cast<int64_t>(m) * a.Np + row] = (acc[0][nt][i] + acc[1][nt][i]) + (acc[2][nt][i] + acc[3][nt][i]);
-        }
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int m = nt * 8 + 2 * t + (i & 1);
+            const int row = g + 8 * (i >> 1);
+            if (m < M)
+              out[static_cast<int64_t>(m) * a.Np + row] =
+                  (acc[r][0][nt][i] + acc[r][1][nt][i]) + (acc[r][2][nt][i] + acc[r][3][nt][i]);
+          }
+      }
     }
     __syncthreads();  // every warp is done with activation buffer b
     if (threadIdx.x == 0 && item + 2 * static_cast<int>(gridDim.x) < nitems) load_x(local + 2, item + 2 * gridDim.x);
@@ -717,15 +739,23 @@ int m1_warps() {
   return w;
 }
 
+// Row tiles per warp of the multi-token kernel (GLM_MK_RT overrides: 1 or 2).
+int mk_row_tiles(int bits, int M) {
+  static const int env = [] { const char* e = getenv("GLM_MK_RT"); return e ? atoi(e) : 0; }();
+  if (env == 1 || env == 2) return env;
+  return M > 8 ? 2 : 1;  // measured: +12% (INT4) / +13% (INT8) at 16 tokens, a loss at <= 8
+}
+
 GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
   GemvPlan p;
   if (M >= 2) {
     // multi-token kernel: CTA-items of 16 row tiles x one k-slice; the slice of all M
     // activation rows (nx vectors) must fit one shared-memory buffer
     p.warps = kTWarps;
+    p.rt_per_warp = mk_row_tiles(bits, M);
     const int64_t kmax = std::max<int64_t>(1, kMkSliceBytes / (static_cast<int64_t>(nx) * M * 128));
     const int64_t ks_min = (nch + kmax - 1) / kmax;
-    const int64_t ngroups = (nrt + kTWarps - 1) / kTWarps;
+    const int64_t ngroups = (nrt + kTWarps * p.rt_per_warp - 1) / (kTWarps * p.rt_per_warp);
     double best = -1.0;
     for (int64_t ks = ks_min; ks <= std::min<int64_t>(nch, ks_min + 24); ++ks) {
       const int64_t items = ngroups * ks;
@@ -770,25 +800,25 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   if (M >= 2) {
     const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
     const int64_t slice_max = (op.nch + p.ksplit - 1) / p.ksplit;
-    if (slice_max * 128 * M * nx > kMkSliceBytes || p.warps != kTWarps)
+    if (slice_max * 128 * M * nx > kMkSliceBytes || p.warps != kTWarps || (p.rt_per_warp == 2 && op.rt_split % 2))
       fail(GLM_CONTRACT, "qlinear", "GEMV plan does not match the multi-token kernel (plan for this M and x count)");
     const size_t smem1 = static_cast<size_t>(kTWarps) * kMkStages * kStageBytes + 2 * kMkSliceBytes +
                          (2 + kTWarps * kMkStages) * 8;
     static bool attr_mk = false;
     if (!attr_mk) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-      CUDA_CHECK(cudaFuncSetAttribute(k_gemv_mk<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+      for (auto k : {k_gemv_mk<4, 1, 1>, k_gemv_mk<4, 2, 1>, k_gemv_mk<8, 1, 1>, k_gemv_mk<8, 2, 1>, k_gemv_mk<4, 1, 2>,
+                     k_gemv_mk<4, 2, 2>, k_gemv_mk<8, 1, 2>, k_gemv_mk<8, 2, 2>})
+        CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
       attr_mk = true;
     }
     const dim3 gridm(p.grid), blockm(kTWarps * 32);
+    const bool two = p.rt_per_warp == 2;
     if (op.bits == 4) {
-      if (M <= 8) launch_k(k_gemv_mk<4, 1>, gridm, blockm, smem1, st, a, nx);
-      else launch_k(k_gemv_mk<4, 2>, gridm, blockm, smem1, st, a, nx);
+      if (M <= 8) launch_k(two ? k_gemv_mk<4, 1, 2> : k_gemv_mk<4, 1, 1>, gridm, blockm, smem1, st, a, nx);
+      else launch_k(two ? k_gemv_mk<4, 2, 2> : k_gemv_mk<4, 2, 1>, gridm, blockm, smem1, st, a, nx);
     } else {
-      if (M <= 8) launch_k(k_gemv_mk<8, 1>, gridm, blockm, smem1, st, a, nx);
-      else launch_k(k_gemv_mk<8, 2>, gridm, blockm, smem1, st, a, nx);
+      if (M <= 8) launch_k(two ? k_gemv_mk<8, 1, 2> : k_gemv_mk<8, 1, 1>, gridm, blockm, smem1, st, a, nx);
+      else launch_k(two ? k_gemv_mk<8, 2, 2> : k_gemv_mk<8, 2, 1>, gridm, blockm, smem1, st, a, nx);
     }
     LAUNCH_CHECK("k_gemv_mk");
     return;

@@ -63,7 +63,9 @@ struct GemvPlan {
   int ksplit = 1;
   int grid = 1;
   int warps = 16;  // warps per CTA the split-K balance was computed for
+  int rt_per_warp = 1;  // multi-token kernel: row tiles per warp (1 or 2)
 };
+int mk_row_tiles(int bits, int M);
 // Split-K plan for an M-row GEMV; the single-token INT4 kernel runs more warps per SM.
 GemvPlan plan_gemv(const QLayout& L, int M);
 // nx: activation vectors the launch reads (2 for a fused W1|V launch with distinct kRow folds)

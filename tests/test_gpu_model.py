@@ -242,6 +242,31 @@ def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
     check_logits(lg.astype(np.float64), ref, zero)
 
 
+@pytest.mark.parametrize("bits,axis", [(4, "row"), (8, "row"), (8, "column")])
+@pytest.mark.parametrize("batch", [9, 16])
+def test_batched_decode_two_row_tiles_per_warp(bits, axis, batch):
+    """9..16 tokens run the multi-token GEMV with two row tiles per warp (gemv.cu
+    k_gemv_mk<., 2, 2>), including the fused W1|V launch with distinct kRow folds: every
+    sequence of the batch matches its own batch-1 decode."""
+    cfg = glm.GLMConfig(num_layers=2, hidden=512, num_heads=4, vocab=300)
+    mb = glm.Model(cfg, bits=bits, axis=axis, max_batch=batch, max_ctx=64)
+    ms = glm.Model(cfg, bits=bits, axis=axis, max_batch=1, max_ctx=64)
+    mb.init_synthetic(11)
+    ms.init_synthetic(11)
+    rng = np.random.default_rng(batch + bits)
+    prefixes = [[int(v) for v in rng.integers(6, 290, size=int(rng.integers(5, 30)))] for _ in range(batch)]
+    for b, pre in enumerate(prefixes):
+        pos, C = glm.gmask_layout(len(pre), 0)
+        mb.prefill(pre + [2], pos[:C], C, seq=b, logits=False)
+    _, lb = mb.decode_step([3] * batch, [len(pre) for pre in prefixes])
+    for b, pre in enumerate(prefixes):
+        ms.reset()
+        pos, C = glm.gmask_layout(len(pre), 0)
+        ms.prefill(pre + [2], pos[:C], C, logits=False)
+        _, ls = ms.decode_step([3], [len(pre)])
+        assert np.abs(lb[b] - ls[0]).max() <= 1e-3 * np.abs(ls[0]).max(), b
+
+
 @pytest.mark.parametrize("batch", [2, 9, 16])
 def test_batched_decode_bf16_head_tensor_cores(batch):
     """Batched decode with the bf16 tied head (block.cu k_head_tc, h rounded to bf16): the
