@@ -19,7 +19,11 @@
 //   group 0     epilogue: tcgen05.ld of the accumulator tile into the split-K partial.
 //
 // Evidence: UTCHMMA / LDTM / STTM / UBLKCP in `cuobjdump -sass` of this object.
+#include <cuda.h>
+
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -32,14 +36,18 @@ namespace {
 constexpr int NTOK = kQmmTokens;  // 128 token columns per tile
 constexpr int kGroups = 4;
 constexpr int kTcWarps = 4 * kGroups;
-constexpr int kThreads = (kTcWarps + 2) * 32;
+constexpr int kThreads = (kTcWarps + 3) * 32;  // + activation producer, MMA issuer, weight producer
 constexpr int kPK = 64;                          // k per stage = one layout chunk
 constexpr int XB = kPK * NTOK * 2;               // activation bytes per stage (16 KB)
 constexpr int RX = 4;                            // activation ring
 constexpr int NA = 8;                            // 32-column A buffers (two per group)
 constexpr int NDB = 2;                           // accumulator tiles (epilogue overlaps next item)
 constexpr uint32_t D_COL = NA * 32;              // 256: accumulators at [256, 512)
-constexpr size_t kSmem = static_cast<size_t>(RX) * XB + 1024;
+constexpr int NW = 12;                           // weight-code ring (one 64-k chunk of 128 features per stage)
+template <int BITS>
+constexpr int wstage_bytes() { return BITS == 4 ? 4096 : 8192; }
+template <int BITS>
+constexpr size_t qmm_smem() { return static_cast<size_t>(RX) * XB + static_cast<size_t>(NW) * wstage_bytes<BITS>() + 1024 + 1024; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -65,6 +73,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// 128 features x one 64-k chunk of codes: the 8 row tiles' blocks (layout.cuh), gathered
+// by one tensor-map copy with the 64 B swizzle, so that the transcode threads' 16-byte reads
+// (lane g reads 16 B of each 64 B row g) hit 8 distinct bank groups.
+template <int BITS>
+__device__ __forceinline__ void tma_codes(void* dst, const CUtensorMap* map, int c, int rt16, uint64_t* bar) {
+  if constexpr (BITS == 4) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(0), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar))
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -155,15 +182,18 @@ template <int BITS>
 struct Codes {
   uint4 u[BITS == 4 ? 4 : 8];
 };
+// This thread's 64 B (INT8: 2 x 64 B) of a staged chunk: row tile i16 of the stage, row g,
+// 16-byte unit t stored at unit t ^ (g >> 1) of the 64 B row (64 B swizzle).
 template <int BITS>
-__device__ __forceinline__ void load_codes(const QmmArgs& a, int64_t rt16, int64_t c, int g, Codes<BITS>& cd) {
-  constexpr int CB = BITS == 4 ? 512 : 1024;
-  const uint4* base = reinterpret_cast<const uint4*>(a.w + (rt16 * a.nch + c) * CB + g * 64);
+__device__ __forceinline__ void smem_codes(const uint8_t* stage, int i16, int g, Codes<BITS>& cd) {
+  constexpr int TB = BITS == 4 ? 512 : 1024;
+  const uint8_t* row = stage + i16 * TB + g * 64;
+  const int sw = (g >> 1) & 3;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) cd.u[t] = __ldg(base + t);
+  for (int t = 0; t < 4; ++t) cd.u[t] = *reinterpret_cast<const uint4*>(row + ((t ^ sw) << 4));
   if constexpr (BITS == 8) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cd.u[4 + t] = __ldg(base + 32 + t);  // k-tiles 2,3 at +512 B
+    for (int t = 0; t < 4; ++t) cd.u[4 + t] = *reinterpret_cast<const uint4*>(row + 512 + ((t ^ sw) << 4));
   }
 }
 
@@ -202,10 +232,15 @@ __device__ __forceinline__ void transcode(const Codes<BITS>& cd, int h, uint32_t
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+__global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  constexpr int WB = wstage_bytes<BITS>();
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xring = smem;
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(RX) * XB);
+  uint8_t* wring = smem + static_cast<size_t>(RX) * XB;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(wring + static_cast<size_t>(NW) * WB);
+  uint64_t* wempty = wfull + NW;
+  uint64_t* xfull = wempty + NW;
   uint64_t* xempty = xfull + RX;
   uint64_t* a_full = xempty + RX;
   uint64_t* a_empty = a_full + NA;
@@ -221,6 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
     for (int i = 0; i < RX; ++i) {
       mbar_init(xfull + i, 1);
       mbar_init(xempty + i, 1);
+    }
+    for (int i = 0; i < NW; ++i) {
+      mbar_init(wfull + i, 1);
+      mbar_init(wempty + i, 4);  // the 4 warps of the transcode group that owns the stage
     }
     for (int i = 0; i < NA; ++i) {
       mbar_init(a_full + i, 4);
@@ -254,6 +293,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
           mbar_expect_tx(xfull + xs, XB);
           bulk_g2s(xring + xs * XB, a.xt + tt * a.Kp * NTOK + c * kPK * NTOK, XB, xfull + xs, pol);
           stamp(a, 5, q);
+        }
+      }
+    }
+  } else if (warp == kTcWarps + 2) {
+    // ---------------- TMA producer: weight codes, one 64-k chunk of 128 features per stage ------
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int64_t rt, tt, c0, c1;
+        int s;
+        decode_item(a, item, rt, tt, s, c0, c1);
+        for (int64_t c = c0; c < c1; ++c, ++q) {
+          const int ws = q % NW;
+          mbar_wait(wempty + ws, ((q / NW) & 1) ^ 1);
+          mbar_expect_tx(wfull + ws, WB);
+          tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 8),
+                          wfull + ws);
         }
       }
     }
@@ -301,18 +357,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
       int64_t rt, tt, c0, c1;
       int s;
       decode_item(a, item, rt, tt, s, c0, c1);
-      const int64_t rt16 = rt * 8 + i16;
-      // first owned stage of this item, then prefetch one owned stage ahead
+      // owned stages of this item: chunks with (global chunk index) % kGroups == group
       int64_t c = c0 + ((group - static_cast<int>(q % kGroups)) + kGroups) % kGroups;
       uint32_t qq = q + static_cast<uint32_t>(c - c0);
-      Codes<BITS> cur;
-      if (c < c1) load_codes<BITS>(a, rt16, c, g, cur);
       for (; c < c1; c += kGroups, qq += kGroups) {
-        Codes<BITS> nxt;
-        if (c + kGroups < c1) load_codes<BITS>(a, rt16, c + kGroups, g, nxt);
-        const int ab = qq % NA;
+        const int ws = qq % NW, ab = qq % NA;
+        mbar_wait(wfull + ws, (qq / NW) & 1);
+        Codes<BITS> cur;
+        smem_codes<BITS>(wring + static_cast<size_t>(ws) * WB, i16, g, cur);
         uint32_t r[32];
         transcode<BITS>(cur, h, r);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(wempty + ws);
         mbar_wait(a_empty + ab, ((qq / NA) & 1) ^ 1);
         tc_fence_after();
         tmem_st16(lane_base + ab * 32, r);
@@ -322,7 +378,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a) {
         __syncwarp();
         if (warp == 0 && lane == 0) stamp(a, 2, qq);
         if (lane == 0) mbar_arrive(a_full + ab);
-        cur = nxt;
       }
       q += static_cast<uint32_t>(c1 - c0);
       if (group == 0) {
@@ -382,6 +437,54 @@ long long*& qmm_trace_ptr() {
   return p;
 }
 
+// Tensor map of a linear's device-layout codes: [64 B row][8 rows g][(INT8: 2 halves)]
+// [nch chunks][nrt16 row tiles], box = one chunk of 8 row tiles, 64 B swizzle. The driver
+// entry point comes through the runtime (no libcuda link); maps are cached per buffer.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+CUtensorMap codes_tensor_map(const QWeightDev& w) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
+  static EncodeTiledFn encode = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(static_cast<const void*>(w.codes), w.L.nrt * 1000003 + w.L.nch * 17 + w.L.bits);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  CUtensorMap m;
+  const bool i8 = w.L.bits == 8;
+  const cuuint32_t rank = i8 ? 5 : 4;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  const cuuint64_t cb = static_cast<cuuint64_t>(w.L.chunk_bytes());
+  if (i8) {
+    const cuuint64_t d[5] = {64, 8, 2, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
+    const cuuint64_t sd[4] = {64, 512, 1024, static_cast<cuuint64_t>(w.L.nch) * cb};
+    const cuuint32_t bx[5] = {64, 8, 2, 1, 8};
+    for (int i = 0; i < 5; ++i) dims[i] = d[i], box[i] = bx[i];
+    for (int i = 0; i < 4; ++i) strides[i] = sd[i];
+  } else {
+    const cuuint64_t d[4] = {64, 8, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
+    const cuuint64_t sd[3] = {64, 512, static_cast<cuuint64_t>(w.L.nch) * cb};
+    const cuuint32_t bx[4] = {64, 8, 1, 8};
+    for (int i = 0; i < 4; ++i) dims[i] = d[i], box[i] = bx[i];
+    for (int i = 0; i < 3; ++i) strides[i] = sd[i];
+  }
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, w.codes, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  cache[key] = m;
+  return m;
+}
+
 GemvPlan plan_qmm(const QLayout& L, int M) {
   GemvPlan p;
   const int64_t ntt = (M + NTOK - 1) / NTOK, nrt128 = L.Np / 128;
@@ -438,12 +541,13 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
   static bool attr[2] = {false, false};
   const int bi = w.L.bits == 4 ? 0 : 1;
   if (!attr[bi]) {
-    if (bi == 0) CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
-    else CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
+    if (bi == 0) CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qmm_smem<4>())));
+    else CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qmm_smem<8>())));
     attr[bi] = true;
   }
-  if (bi == 0) k_qmm_tc<4><<<p.grid, kThreads, kSmem, st>>>(a);
-  else k_qmm_tc<8><<<p.grid, kThreads, kSmem, st>>>(a);
+  const CUtensorMap wmap = codes_tensor_map(w);
+  if (bi == 0) k_qmm_tc<4><<<p.grid, kThreads, qmm_smem<4>(), st>>>(a, wmap);
+  else k_qmm_tc<8><<<p.grid, kThreads, qmm_smem<8>(), st>>>(a, wmap);
   LAUNCH_CHECK("k_qmm_tc");
 }
 
