@@ -88,7 +88,7 @@ void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial
 
 // ---- qmm_tc.cu : tcgen05 quantized GEMM for prefill (M > 16 tokens) ----
 int qmm_min_rows();
-constexpr int kQmmTokens = 128;  // token columns per MMA tile (UMMA N)
+constexpr int kQmmTokens = kXTileTokens;  // token columns per MMA tile (UMMA N)
 inline int xtile_tokens(int M) { return (M + kQmmTokens - 1) / kQmmTokens * kQmmTokens; }
 // partial[s][m][n] (fp32, [ksplit][M][Np]) from activations xt in the tcgen05 B-operand
 // layout (layout.cuh xtile_index) holding NT = xtile_tokens(M) token rows.

@@ -109,14 +109,16 @@ __host__ __device__ inline int64_t xfrag_index(int64_t nch, int64_t m, int64_t k
   return ((m * nch + c) * 4 + t) * 16 + j * 4 + (kc >> 3) * 2 + (kc & 1);
 }
 
-// Half index of activation (m, k) in a tcgen05 B-operand buffer: 128-token tiles, each
-// tile [k/16][k-half][16 core-matrix rows of 8 tokens][8 tokens][8 k] (the K-major
-// no-swizzle canonical layout, LBO = 2048 B, SBO = 128 B), so a 64-k stage of a tile is
-// one contiguous 16 KB block for the bulk-copy engine.
+// Half index of activation (m, k) in a tcgen05 B-operand buffer: T-token tiles (T =
+// kXTileTokens, the GEMM's UMMA N), each tile [k/16][k-half][T/8 core-matrix rows of 8
+// tokens][8 tokens][8 k] (the K-major no-swizzle canonical layout, LBO = 16·T B, SBO =
+// 128 B), so a 64-k stage of a tile is one contiguous 128·T B block for the bulk-copy engine.
+constexpr int kXTileTokens = 256;
 __host__ __device__ inline int64_t xtile_index(int64_t Kp, int64_t m, int64_t k) {
-  const int64_t tile = m / 128;
-  const int mm = static_cast<int>(m % 128), kk = static_cast<int>(k % 16);
-  return tile * Kp * 128 + ((k / 16) * 2 + kk / 8) * 1024 + (mm / 8) * 64 + (mm % 8) * 8 + kk % 8;
+  constexpr int T = kXTileTokens;
+  const int64_t tile = m / T;
+  const int mm = static_cast<int>(m % T), kk = static_cast<int>(k % 16);
+  return tile * Kp * T + ((k / 16) * 2 + kk / 8) * (8 * T) + (mm / 8) * 64 + (mm % 8) * 8 + kk % 8;
 }
 
 }  // namespace glm

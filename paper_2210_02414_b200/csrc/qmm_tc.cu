@@ -33,15 +33,15 @@ namespace glm {
 
 namespace {
 
-constexpr int NTOK = kQmmTokens;  // 128 token columns per tile
+constexpr int NTOK = kQmmTokens;  // token columns per tile (UMMA N)
 constexpr int kGroups = 4;
 constexpr int kTcWarps = 4 * kGroups;
 constexpr int kThreads = (kTcWarps + 3) * 32;  // + activation producer, MMA issuer, weight producer
 constexpr int kPK = 64;                          // k per stage = one layout chunk
-constexpr int XB = kPK * NTOK * 2;               // activation bytes per stage (16 KB)
+constexpr int XB = kPK * NTOK * 2;               // activation bytes per stage (32 KB at N = 256)
 constexpr int RX = 4;                            // activation ring
 constexpr int NA = 8;                            // 32-column A buffers (two per group)
-constexpr int NDB = 2;                           // accumulator tiles (epilogue overlaps next item)
+constexpr int NDB = NTOK <= 128 ? 2 : 1;         // accumulator tiles (2: epilogue overlaps the next item)
 constexpr uint32_t D_COL = NA * 32;              // 256: accumulators at [256, 512)
 constexpr int NW = 12;                           // weight-code ring (one 64-k chunk of 128 features per stage)
 template <int BITS>
@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
         for (int64_t c = c0; c < c1; ++c, ++q) {
           const int xs = q % RX;
           mbar_wait(xempty + xs, ((q / RX) & 1) ^ 1);
+          stamp(a, 0, q);
           mbar_expect_tx(xfull + xs, XB);
           bulk_g2s(xring + xs * XB, a.xt + tt * a.Kp * NTOK + c * kPK * NTOK, XB, xfull + xs, pol);
           stamp(a, 5, q);
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
         tc_commit_elect(xempty + xs);
         tc_commit_elect(a_empty + ab);
         __syncwarp();
+        if (lane == 0) stamp(a, 4, q);
       }
       tc_commit_elect(d_full + db);
       __syncwarp();
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
       for (; c < c1; c += kGroups, qq += kGroups) {
         const int ws = qq % NW, ab = qq % NA;
         mbar_wait(wfull + ws, (qq / NW) & 1);
+        if (warp == 0 && lane == 0) stamp(a, 1, qq);
         Codes<BITS> cur;
         smem_codes<BITS>(wring + static_cast<size_t>(ws) * WB, i16, g, cur);
         uint32_t r[32];
