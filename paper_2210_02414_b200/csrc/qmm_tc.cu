@@ -1,22 +1,27 @@
 // qmm_tc.cu — W4A16 / W8A16 quantized GEMM for prefill on the 5th-generation tensor cores.
 //
 // Replaces `matmul(x, dequantize(q))` (quant.cpp:188-221 + tensor.cpp:135-155) when many
-// token rows share the weights (prefill, M > 16): a 128-feature x 128-token output tile per
-// CTA item, fp32 accumulators in TMEM, one persistent CTA per SM (all 512 TMEM columns).
+// token rows share the weights (prefill, M > 16): a 128-feature x 256-token output tile per
+// CTA item, fp32 accumulator in TMEM, one persistent CTA per SM (all 512 TMEM columns:
+// 8 x 32 A-operand columns + one 256-column accumulator).
 //
+//   warp 18     TMA producer (weights): one tensor-map copy per stage gathers the 8 row
+//               tiles' 512 B (INT8: 1 KB) blocks of one 64-k chunk, 64 B swizzle, into a
+//               12-stage ring;
 //   warps 0-15  transcode: 4 groups x 4 TMEM lane quarters; group g owns the 64-k stages with
-//               q % 4 == g. Each thread owns one output feature (TMEM lane): it loads the
-//               64 B of fragment-ordered codes that hold its feature (layout.cuh) straight
-//               from global memory (L2-resident across the token tiles of a row tile, the
-//               next stage prefetched in registers), regroups them into fp16 pairs
-//               (k, k+1) with LOP3/PRMT magic-number conversion and writes them to its TMEM
-//               lane with tcgen05.st (the MMA's A operand);
-//   warp 16     TMA producer: one cp.async.bulk per stage brings the 128-token x 64-k
-//               activation tile (16 KB, canonical K-major layout) into a 4-stage smem ring;
+//               q % 4 == g. Each thread owns one output feature (TMEM lane): it reads the
+//               64 B of fragment-ordered codes that hold its feature (layout.cuh) from the
+//               staged chunk, regroups them into fp16 pairs (k, k+1) with LOP3/PRMT
+//               magic-number conversion and writes them to its TMEM lane with tcgen05.st
+//               (the MMA's A operand); after an item, every group drains a quarter of the
+//               accumulator's token columns (epilogue: tcgen05.ld, scale, store);
+//   warp 16     TMA producer (activations): one cp.async.bulk per stage brings the 256-token
+//               x 64-k activation tile (32 KB, canonical K-major layout) into a 4-stage ring;
 //   warp 17     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, A = transcoded weights in TMEM,
-//               B = activations in smem, M = 128 features, N = 128 tokens, K = 16 per
-//               instruction; tcgen05.commit releases the smem slot / TMEM buffer;
-//   group 0     epilogue: tcgen05.ld of the accumulator tile into the split-K partial.
+//               B = activations in smem, M = 128 features, N = 256 tokens (a 128 x 128 MMA
+//               costs ~125 cycles of issue, so the wider N halves the instruction count per
+//               FLOP), K = 16 per instruction; tcgen05.commit releases the smem slot / TMEM
+//               buffer.
 //
 // Evidence: UTCHMMA / LDTM / STTM / UBLKCP in `cuobjdump -sass` of this object.
 #include <cuda.h>
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
     }
     for (int i = 0; i < NDB; ++i) {
       mbar_init(d_full + i, 1);
-      mbar_init(d_empty + i, 4);
+      mbar_init(d_empty + i, kTcWarps);  // every transcode warp drains a quarter of the tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -383,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
         if (lane == 0) mbar_arrive(a_full + ab);
       }
       q += static_cast<uint32_t>(c1 - c0);
-      if (group == 0) {
+      {  // epilogue: group g drains token columns [g, g + 1) * NTOK / kGroups of the tile
         const int db = it % NDB;
         mbar_wait(d_full + db, (it / NDB) & 1);
         tc_fence_after();
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
         float* out = a.partial + (direct ? 0 : static_cast<int64_t>(s) * a.M * a.Np) + col;
         const bool keep = !direct || col < a.N;
 #pragma unroll 1
-        for (int c16 = 0; c16 < NTOK; c16 += 16) {
+        for (int c16 = group * (NTOK / kGroups); c16 < (group + 1) * (NTOK / kGroups); c16 += 16) {
           uint32_t v[16];
           tmem_ld16(lane_base + D_COL + db * NTOK + c16, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
