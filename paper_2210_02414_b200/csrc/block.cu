@@ -716,13 +716,16 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
                : "memory");
 }
 
+// Occupancy: Q lives in shared memory only until its fragments are in registers, so it
+// shares the second V buffer (first filled for key block 1, after the Q fragments are
+// loaded) and three 4-warp CTAs fit per SM (registers capped at 170 per thread).
 template <int DH>
-__global__ void __launch_bounds__(kFaThreads) k_attn_prefill_tc(AttnPrefillArgs a) {
+__global__ void __launch_bounds__(kFaThreads, DH == 128 ? 3 : 4) k_attn_prefill_tc(AttnPrefillArgs a) {
   constexpr int LDS = DH + 8;  // padded row (halves): ldmatrix rows land in distinct banks
   extern __shared__ __align__(16) __half fsm[];
-  __half* Qs = fsm;                        // [64][LDS]
-  __half* Ks = Qs + kFaRows * LDS;         // [2][64][LDS]
+  __half* Ks = fsm;                        // [2][64][LDS]
   __half* Vs = Ks + 2 * kFaKeys * LDS;     // [2][64][LDS]
+  __half* Qs = Vs + kFaKeys * LDS;         // [64][LDS], aliases V buffer 1 (kFaRows == kFaKeys)
   const int head = blockIdx.y, i0 = blockIdx.x * kFaRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -745,6 +748,7 @@ __global__ void __launch_bounds__(kFaThreads) k_attn_prefill_tc(AttnPrefillArgs 
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  static_assert(kFaRows == kFaKeys, "Q aliases one V buffer");
   load_kv(0, 0);
   // Q (fp32, rotated) -> fp16, pre-scaled by log2(e) / sqrt(dh)
   const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(DH));
@@ -761,6 +765,7 @@ __global__ void __launch_bounds__(kFaThreads) k_attn_prefill_tc(AttnPrefillArgs 
   for (int kt = 0; kt < DH / 16; ++kt)
     ldsm_x4(qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3],
             Qs + (warp * 16 + (lane & 15)) * LDS + kt * 16 + (lane >> 4) * 8);
+  __syncthreads();  // every warp holds its Q fragments: V buffer 1 may be filled
   float o[DH / 8][4];
 #pragma unroll
   for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -1170,7 +1175,7 @@ void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
 void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st) {
   const dim3 grid((a.n + kFaRows - 1) / kFaRows, a.heads);
   auto go = [&](auto kernel, int dh) {
-    const size_t smem = static_cast<size_t>(kFaRows + 4 * kFaKeys) * (dh + 8) * sizeof(__half);
+    const size_t smem = static_cast<size_t>(4 * kFaKeys) * (dh + 8) * sizeof(__half);
     CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kernel<<<grid, kFaThreads, smem, st>>>(a);
   };
