@@ -74,6 +74,54 @@ __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restri
   }
 }
 
+// Prefill variant writing tcgen05 activation tiles (k_geglu_act_tiles warp mapping: 32
+// tokens x 8 features per warp).
+template <typename ET>
+__global__ void k_embed_tiles(const ET* __restrict__ E, int64_t d, const int* __restrict__ tokens, int M,
+                              float* __restrict__ h, XOut xo) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int T = kXTileTokens;
+  const int64_t groups = d / 8, subs = T / 32;
+  const int64_t warps = (M + T - 1) / T * groups * subs;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < warps;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t sub = w % subs, rest = w / subs;
+    const int64_t g = rest % groups, tile = rest / groups;
+    const int64_t m = tile * T + sub * 32 + lane;
+    if (m >= M) continue;
+    const int64_t n = g * 8, row = tokens[m];
+    float v[8];
+    if constexpr (sizeof(ET) == 4) {
+      const float4* p = reinterpret_cast<const float4*>(E + row * d + n);
+      const float4 a = p[0], b = p[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+      const uint4 q = *reinterpret_cast<const uint4*>(E + row * d + n);
+      const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wd[e]));
+        v[2 * e] = f.x;
+        v[2 * e + 1] = f.y;
+      }
+    }
+    float4* hp = reinterpret_cast<float4*>(h + m * d + n);
+    hp[0] = make_float4(v[0], v[1], v[2], v[3]);
+    hp[1] = make_float4(v[4], v[5], v[6], v[7]);
+    if (!xo.xf) continue;
+    uint32_t hx[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float s0 = xo.row_scale ? xo.row_scale[n + e] : 1.f, s1 = xo.row_scale ? xo.row_scale[n + e + 1] : 1.f;
+      const __half2 hv = __floats2half2_rn(v[e] * s0, v[e + 1] * s1);
+      hx[e / 2] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    *reinterpret_cast<uint4*>(xo.xf + xtile_index(xo.Kp, m, n)) = make_uint4(hx[0], hx[1], hx[2], hx[3]);
+  }
+}
+
 // ---- deepnorm_residual = LN(alpha * x + y) (model.cpp:125-131, tensor.cpp:256-274) -----
 // One thread-block CLUSTER of kLnCluster CTAs per row: each CTA owns a contiguous slice of
 // the row (pairs of features kept in registers), the mean / variance partial sums are
@@ -891,6 +939,35 @@ __global__ void k_rows_to_xfrag(const float* __restrict__ x, int64_t ld, int M, 
   }
 }
 
+// fp32 rows -> tcgen05 activation tiles with the warp mapping of k_geglu_act_tiles
+// (32 consecutive tokens x one 8-feature group per warp: 32 B reads, 512 B of contiguous
+// tile per warp store).
+__global__ void k_rows_to_xtile(const float* __restrict__ x, int64_t ld, int M, int64_t K, XOut xo) {
+  constexpr int T = kXTileTokens;
+  const int64_t groups = K / 8, subs = T / 32;
+  const int64_t warps = (M + T - 1) / T * groups * subs;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < warps;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t sub = w % subs, rest = w / subs;
+    const int64_t g = rest % groups, tile = rest / groups;
+    const int64_t m = tile * T + sub * 32 + lane;
+    if (m >= M) continue;
+    const int64_t n = g * 8;
+    const float4* p = reinterpret_cast<const float4*>(x + m * ld + n);
+    const float4 a = p[0], b = p[1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t h[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float s0 = xo.row_scale ? xo.row_scale[n + e] : 1.f, s1 = xo.row_scale ? xo.row_scale[n + e + 1] : 1.f;
+      const __half2 hv = __floats2half2_rn(v[e] * s0, v[e + 1] * s1);
+      h[e / 2] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    *reinterpret_cast<uint4*>(xo.xf + xtile_index(xo.Kp, m, n)) = make_uint4(h[0], h[1], h[2], h[3]);
+  }
+}
+
 // ---- tied output head logits = h E^T + greedy argmax (model.cpp:225) -----------------------
 // HBM-bound stream over the (unquantised, quant.cpp:289) embedding table: one warp per
 // vocab row, each lane keeps kHeadU independent 16-byte loads in flight, fp32 FMA against
@@ -1109,6 +1186,14 @@ int grid_for(int64_t n, int threads, int cap = 148 * 16) {
 
 void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
                   cudaStream_t st) {
+  if (xo.tile && d % 8 == 0) {
+    const int64_t warps = (M + kXTileTokens - 1) / kXTileTokens * (d / 8) * (kXTileTokens / 32);
+    const dim3 grid(grid_for(warps * 32, 256));
+    if (bf16) launch_k(k_embed_tiles<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
+    else launch_k(k_embed_tiles<float>, grid, dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
+    LAUNCH_CHECK("k_embed_tiles");
+    return;
+  }
   if (bf16) launch_k(k_embed<__nv_bfloat16>, dim3(M), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
   else launch_k(k_embed<float>, dim3(M), dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
   LAUNCH_CHECK("k_embed");
@@ -1186,6 +1271,12 @@ void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st) {
 }
 
 void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st) {
+  if (xo.tile && K % 8 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const int64_t warps = (M + kXTileTokens - 1) / kXTileTokens * (K / 8) * (kXTileTokens / 32);
+    k_rows_to_xtile<<<grid_for(warps * 32, 256), 256, 0, st>>>(x, ld, M, K, xo);
+    LAUNCH_CHECK("k_rows_to_xtile");
+    return;
+  }
   k_rows_to_xfrag<<<grid_for(static_cast<int64_t>(M) * (K / 2), 256), 256, 0, st>>>(x, ld, M, K, xo);
   LAUNCH_CHECK("k_rows_to_xfrag");
 }
