@@ -101,3 +101,21 @@ def test_zeropoint_qlinear_matches_oracle(bits, axis):
         y = lin(x).astype(np.float64)
         ref = x @ deq
         assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("K,N", [(4096, 1024), (1024, 4096)])
+def test_tcgen05_gemm_token_tile_boundaries(bits, K, N):
+    """M > 16 runs the tcgen05 GEMM (qmm_tc.cu) on 256-token tiles: partial tiles (17, 255),
+    an exact tile (256), a tile plus one row (257) and several tiles (600), with the planner's
+    split-K (partials + reduce) and unsplit (direct scaled output) variants across the shapes."""
+    rng = np.random.default_rng(bits + K)
+    w = rng.normal(0, 0.02, size=(K, N))
+    q = glm.quantize_absmax(w, bits, "column")
+    lin = glm.QLinear.from_payload(q)
+    deq = O.dequantize(q)
+    for M in (17, 255, 256, 257, 600):
+        x = rng.normal(0, 1, size=(M, K))
+        y = lin(x).astype(np.float64)
+        ref = x @ deq
+        assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
