@@ -398,8 +398,9 @@ __global__ void k_geglu_act_tiles(ActArgs a) {
 }
 
 // ---- decode attention (model.cpp:137-152 for the rows of the generation part) ----------
-// grid (heads, batch, splits); each CTA owns kSplitKeys consecutive keys of its sequence's
-// cache, so up to kSplitKeys cached tokens need no cross-CTA merge at all. Before the
+// grid (heads, batch, splits); each CTA owns split_keys (256, or 64 for caches longer than
+// 256 tokens) consecutive keys of its sequence's cache, so up to 256 cached tokens need no
+// cross-CTA merge at all. Before the
 // programmatic-dependency wait (the qkv GEMV is still running) the CTA prefetches its
 // cached K/V rows into L2; after it, q (and the new k, v) are reduced from the GEMV's
 // split-K partials and rotated (RoPE), scores use DH/8 lanes per key (one 16-byte load
@@ -408,7 +409,8 @@ __global__ void k_geglu_act_tiles(ActArgs a) {
 // CTA of a (head, batch) merges them in split order (deterministic).
 constexpr int kAttnThreadsFew = 256;  // threads per CTA at batch <= 2 (few CTAs)
 constexpr int kAttnThreadsMany = 128;  // larger batches: more resident CTAs per SM
-constexpr int kSplitKeys = 256;
+constexpr int kSplitKeys = 256;    // largest split (size of the score buffer)
+constexpr int kSplitKeysLong = 64;  // split of caches longer than kSplitKeys
 
 template <int DH, int kAttnThreads>
 __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
   // cache length / position were written by earlier steps (complete before our predecessor ran)
   const int len = a.cache_len[b];
   const int total = len + 1;
-  const int k0 = split * kSplitKeys, k1 = min(total, k0 + kSplitKeys);
+  const int k0 = split * a.split_keys, k1 = min(total, k0 + a.split_keys);
   const int kold = min(k1, len);  // cached keys of this split: [k0, kold)
   const int pos = a.positions[b];
   const float inv_sqrt = rsqrtf(static_cast<float>(DH));
@@ -461,6 +463,7 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
                    : "memory");
     }
   }
+  __syncthreads();  // the barrier is initialised before any thread waits on it
   // RoPE factors and the qkv column scales do not depend on the running GEMV either
   const int jt = threadIdx.x < DH / 2 ? threadIdx.x : threadIdx.x - DH / 2;
   float2 cs = make_float2(1.f, 0.f), sq = make_float2(1.f, 1.f), sk = sq, sv = sq;
@@ -673,24 +676,38 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
   if (!last) return;
   __threadfence();
   const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (DH + 2);
-  const int nsp = (total + kSplitKeys - 1) / kSplitKeys;
-  float gm = -FLT_MAX;
-  for (int s = 0; s < nsp; ++s) gm = fmaxf(gm, base[s * (DH + 2) + DH]);
-  float gl = 0.f;
-  for (int s = 0; s < nsp; ++s) gl += base[s * (DH + 2) + DH + 1] * __expf(base[s * (DH + 2) + DH] - gm);
-  const float inv = 1.f / gl;
+  const int nsp = (total + a.split_keys - 1) / a.split_keys;
+  // split weights exp(m_s - max) / sum_s l_s exp(m_s - max), one warp, splits in a fixed order
+  float* wsp = p;  // the score buffer is free now (nsp <= kSplitKeys)
+  if (warp == 0) {
+    float gm = -FLT_MAX;
+    for (int s = lane; s < nsp; s += 32) gm = fmaxf(gm, __ldcg(base + s * (DH + 2) + DH));
+    gm = warp_max(gm);
+    float gl = 0.f;
+    for (int s = lane; s < nsp; s += 32) {
+      const float w = __expf(__ldcg(base + s * (DH + 2) + DH) - gm);
+      wsp[s] = w;
+      gl += __ldcg(base + s * (DH + 2) + DH + 1) * w;
+    }
+    gl = warp_sum(gl);
+    const float inv = 1.f / gl;
+    for (int s = lane; s < nsp; s += 32) wsp[s] *= inv;
+  }
+  __syncthreads();
   for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kAttnThreads) {
     float o0 = 0.f, o1 = 0.f;
+#pragma unroll 8
     for (int s = 0; s < nsp; ++s) {
-      const float w = __expf(base[s * (DH + 2) + DH] - gm);
-      o0 += w * base[s * (DH + 2) + 2 * c2];
-      o1 += w * base[s * (DH + 2) + 2 * c2 + 1];
+      const float w = wsp[s];
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(base + s * (DH + 2) + 2 * c2));
+      o0 += w * v.x;
+      o1 += w * v.y;
     }
     const int64_t k = static_cast<int64_t>(head) * DH + 2 * c2;
-    store_xfrag_pair(a.xo, b, k, o0 * inv, o1 * inv);
+    store_xfrag_pair(a.xo, b, k, o0, o1);
     if (a.out) {
-      a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0 * inv;
-      a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0;
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1;
     }
   }
   trace_point(32);
@@ -1218,7 +1235,11 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
   LAUNCH_CHECK("k_geglu_act");
 }
 
-int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeys - 1) / kSplitKeys; }
+int attn_decode_split_keys(int max_ctx) { return max_ctx <= kSplitKeys ? kSplitKeys : kSplitKeysLong; }
+int attn_decode_splits(int max_ctx) {
+  const int sk = attn_decode_split_keys(max_ctx);
+  return (max_ctx + sk - 1) / sk;
+}
 
 void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   AttnDecodeArgs a = in;
@@ -1226,22 +1247,26 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   // Few sequences: each CTA bulk-copies its split's keys + values into shared memory ahead
   // of the dependency wait (one HBM round trip). Many sequences: that shared memory would
   // cap residency at one CTA per SM over B * heads CTAs, so rows are read from L2/HBM.
-  const int stage = B <= 2 ? std::min(kSplitKeys, (a.max_ctx + 15) / 16 * 16) : 0;
+  a.split_keys = attn_decode_split_keys(a.max_ctx);
+  if (a.max_splits != attn_decode_splits(a.max_ctx)) fail(GLM_CONTRACT, "glmmodel", "decode attention split count");
+  const int stage = B <= 2 ? std::min(a.split_keys, (a.max_ctx + 15) / 16 * 16) : 0;
   a.stage_keys = stage;
   const size_t smem = 2ull * stage * a.dh * sizeof(__half);
   static bool attr = false;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<128, kAttnThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 128 * 2));
     CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<64, kAttnThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeys * 64 * 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<128, kAttnThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeysLong * 128 * 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode<64, kAttnThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSplitKeysLong * 64 * 2));
     attr = true;
   }
-  if (stage) {
+  if (stage && a.split_keys == kSplitKeys) {
     if (a.dh == 128) launch_k(k_attn_decode<128, kAttnThreadsFew>, grid, dim3(kAttnThreadsFew), smem, st, a);
     else if (a.dh == 64) launch_k(k_attn_decode<64, kAttnThreadsFew>, grid, dim3(kAttnThreadsFew), smem, st, a);
     else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
-  } else {
-    if (a.dh == 128) launch_k(k_attn_decode<128, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), 0, st, a);
-    else if (a.dh == 64) launch_k(k_attn_decode<64, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), 0, st, a);
+  } else {  // many sequences, or 64-key splits of a long cache (staged at <= 2 sequences): 128-thread CTAs
+    if (a.dh == 128) launch_k(k_attn_decode<128, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), smem, st, a);
+    else if (a.dh == 64) launch_k(k_attn_decode<64, kAttnThreadsMany>, grid, dim3(kAttnThreadsMany), smem, st, a);
     else fail(GLM_DIMENSION, "glmmodel", "decode attention supports head_dim 64 or 128");
   }
   LAUNCH_CHECK("k_attn_decode");

@@ -71,6 +71,7 @@ struct AttnDecodeArgs {
   XOut xo;                  // x_frag of out_proj
   float* out;               // optional fp32 [B][d_local]
   int stage_keys = 0;       // set by launch_attn_decode: keys per CTA staged in shared memory (0: read from L2/HBM)
+  int split_keys = 256;     // set by launch_attn_decode: cached keys per CTA (attn_decode_split_keys)
 };
 
 struct RopeStoreArgs {
@@ -106,6 +107,9 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
                   cudaStream_t st);
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st);
 void launch_geglu_act(const ActArgs& a, cudaStream_t st);
+// keys per CTA of the decode attention: 256 up to a 256-token cache (no merge), else 64
+// (long caches: many small CTAs stream the cache concurrently, deterministic merge)
+int attn_decode_split_keys(int max_ctx);
 int attn_decode_splits(int max_ctx);
 void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st);
 void launch_advance(int* cache_len, int B, cudaStream_t st);

@@ -242,6 +242,36 @@ def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
     check_logits(lg.astype(np.float64), ref, zero)
 
 
+@pytest.mark.parametrize("batch", [1, 3])
+def test_decode_attention_long_cache_splits(batch):
+    """Caches longer than 256 tokens run the decode attention in 64-key splits (block.cu
+    attn_decode_split_keys) merged by the last CTA of each head in split order; batch 1 stages
+    the keys in shared memory, batch 3 reads them from L2/HBM. Teacher-forced decode rows at
+    ~330 cached tokens against the oracle, every layer's sublayer taps included."""
+    p, m, _ = build(4, "column", layers=2, hidden=256, heads=2, vocab=300, seed=13, max_batch=batch, max_ctx=400)
+    rng = np.random.default_rng(batch)
+    prefix = [int(v) for v in rng.integers(6, 290, size=327)]
+    gen = [int(v) for v in rng.integers(6, 290, size=3)]
+    sample = O.gmask_sample(prefix, gen)
+    ref, at, ft, zero = oracle_rows(p, sample)
+    C = sample["context_length"]
+    m.reset()
+    for b in range(batch):
+        m.prefill(sample["tokens"][:C], sample["positions"][:C], C, seq=b, logits=False)
+    m.enable_taps(True)
+    rows, ta, tf = [], [], []
+    for j in range(3):
+        _, lg = m.decode_step([sample["tokens"][C + j]] * batch, [sample["positions"][C + j]] * batch)
+        a, f = m.taps(batch)
+        rows.append(lg[batch - 1])
+        ta.append(a[:, batch - 1])
+        tf.append(f[:, batch - 1])
+    m.enable_taps(False)
+    check_logits(np.array(rows, np.float64), ref[C:C + 3], zero[C:C + 3])
+    check_taps(np.stack(ta, 1), at[:, C:C + 3])
+    check_taps(np.stack(tf, 1), ft[:, C:C + 3])
+
+
 @pytest.mark.parametrize("bits,axis", [(4, "row"), (8, "row"), (8, "column")])
 @pytest.mark.parametrize("batch", [9, 16])
 def test_batched_decode_two_row_tiles_per_warp(bits, axis, batch):
