@@ -630,8 +630,8 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
     for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
     __syncthreads();
     trace_point(35);
-    if (gridDim.z == 1) {
-      // single split: normalise and hand the row to out_proj directly
+    if (total <= a.split_keys) {
+      // single active split: normalise and hand the row to out_proj directly
       const float inv = 1.f / sum;
       for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kAttnThreads) {
         float o0 = 0.f, o1 = 0.f;
@@ -660,23 +660,22 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
       part[DH] = mx;
       part[DH + 1] = sum;
     }
-  } else if (threadIdx.x == 0) {
-    part[DH] = -FLT_MAX;
-    part[DH + 1] = 0.f;
+  } else {
+    return;  // beyond the cache: no keys, not counted (the merge takes the active splits)
   }
-  // ---- the last CTA of this (head, b) merges the splits in order ----
+  // ---- the last of the active splits of this (head, b) merges them in order ----
+  const int nsp = (total + a.split_keys - 1) / a.split_keys;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     int* ctr = a.counters + b * a.heads + head;
-    last = (atomicAdd(ctr, 1) == a.max_splits - 1);
+    last = (atomicAdd(ctr, 1) == nsp - 1);
     if (last) *ctr = 0;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (DH + 2);
-  const int nsp = (total + a.split_keys - 1) / a.split_keys;
   // split weights exp(m_s - max) / sum_s l_s exp(m_s - max), one warp, splits in a fixed order
   float* wsp = p;  // the score buffer is free now (nsp <= kSplitKeys)
   if (warp == 0) {
