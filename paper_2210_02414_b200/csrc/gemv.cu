@@ -530,7 +530,10 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk(GemvArgs a, int nx)
 constexpr int kM1MaxWarps = 24;
 constexpr int kM1DefaultWarps = 16;
 
-template <int BITS, int NST, int SB>
+// MT = 2 (two-token decode): the same kernel with both tokens' activation vectors resident;
+// lane (g, t) reads token min(g, MT - 1), so token columns 0 and 1 of the MMA are real and
+// the others duplicate token MT - 1 (discarded).
+template <int BITS, int NST, int SB, int MT = 1>
 __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int nx, int early) {
   trace_point(10);
   constexpr int CHUNK = BITS == 4 ? 512 : 1024;
@@ -540,9 +543,10 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   const int g = lane >> 2, t = lane & 3;
   const int nch = static_cast<int>(a.nch), ksplit = a.ksplit;
   const int xbytes = nch * 128;  // one token: Kp halves
+  const int vbytes = MT * xbytes;  // one activation vector set: [MT tokens][chunks][128 B]
   uint8_t* ring = smem + static_cast<size_t>(warp) * NST * SB;
   uint8_t* xs = smem + static_cast<size_t>(nw) * NST * SB;
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * xbytes);
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * vbytes);
   uint64_t* bars = xbar + 1 + warp * NST;
   if (lane == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
@@ -592,12 +596,12 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   if (threadIdx.x == 0) {
     // the activation vector(s): L2-resident (just written by the producer), kept there;
     // requested ahead of any weight stage not yet in flight
-    mbar_expect_tx(xbar, static_cast<uint32_t>(nx * xbytes));
+    mbar_expect_tx(xbar, static_cast<uint32_t>(nx * vbytes));
     for (int v = 0; v < nx; ++v) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2);
-      for (int o = 0; o < xbytes; o += 16384) {
-        const uint32_t nb = static_cast<uint32_t>(min(16384, xbytes - o));
-        bulk_g2s(xs + v * xbytes + o, src + o, nb, xbar, keep);
+      for (int o = 0; o < vbytes; o += 16384) {
+        const uint32_t nb = static_cast<uint32_t>(min(16384, vbytes - o));
+        bulk_g2s(xs + v * vbytes + o, src + o, nb, xbar, keep);
       }
     }
   }
@@ -607,18 +611,19 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
   // fragment of column 0 whatever g is), so the MMA computes 8 identical result columns and
   // only column 0 is stored: no zero-fill, no per-lane address selection, and the 8 lanes
   // reading one address are served by a single shared-memory broadcast.
-  const uint8_t* xs0 = xs + t * 32;
-  const uint8_t* xs1 = xs0 + (nx - 1) * xbytes;
+  const uint8_t* xs0 = xs + (MT == 1 ? 0 : min(g, MT - 1)) * xbytes + t * 32;
+  const uint8_t* xs1 = xs0 + (nx - 1) * vbytes;
   constexpr int cstride = 128;
   const int64_t rt_split = a.rt_split;
   mbar_wait(xbar, 0);
   // per-chunk sums of the fp16 activations as the MMA sees them (exact in fp32: 64 terms)
   float* xsum = reinterpret_cast<float*>(xbar + 1 + nw * NST);
   // 8 lanes per 128-byte chunk, one 16-byte load each, 3-step shuffle reduction
-  for (int i0 = 0; i0 < nx * nch; i0 += blockDim.x >> 3) {  // warp-uniform trip count
+  const int nxc = nx * MT * nch;  // chunk sums, [vector][token][chunk]
+  for (int i0 = 0; i0 < nxc; i0 += blockDim.x >> 3) {  // warp-uniform trip count
     const int i = i0 + (threadIdx.x >> 3);
-    const uint4 v = i < nx * nch ? reinterpret_cast<const uint4*>(xs + static_cast<int64_t>(i) * 128)[threadIdx.x & 7]
-                                 : make_uint4(0, 0, 0, 0);
+    const uint4 v = i < nxc ? reinterpret_cast<const uint4*>(xs + static_cast<int64_t>(i) * 128)[threadIdx.x & 7]
+                            : make_uint4(0, 0, 0, 0);
     const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
     float sum = 0.f;
 #pragma unroll
@@ -629,7 +634,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-    if ((threadIdx.x & 7) == 0 && i < nx * nch) xsum[i] = sum;
+    if ((threadIdx.x & 7) == 0 && i < nxc) xsum[i] = sum;
   }
   __syncthreads();
   trace_point(12);
@@ -675,6 +680,34 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
         ++cslot;
       }
       if (lane == 0) issue();
+    }
+    if constexpr (MT > 1) {
+      // token column n = 2t + e lives in accumulator elements e (row g) and 2 + e (row g + 8)
+      static_assert(BITS == 4, "multi-token m1 kernel is INT4 only");
+      const float* xsv = xsum + (rt < rt_split ? 0 : (nx - 1) * MT * nch);
+      float sxm[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        float v = 0.f;
+        for (int cc = c0 + lane; cc < c1; cc += 32) v += xsv[m * nch + cc];
+        sxm[m] = warp_sum(v);
+      }
+      float* outm = a.partial + static_cast<int64_t>(s) * MT * a.Np + static_cast<int64_t>(rt) * kTileN;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * t + e;
+        if (n < MT) {
+          float sxn = sxm[0];
+#pragma unroll
+          for (int m = 1; m < MT; ++m)
+            if (n == m) sxn = sxm[m];
+          const float lo = (acc[0][0][e] + acc[1][0][e]) + (acc[2][0][e] + acc[3][0][e]);
+          const float hi = (acc[0][0][2 + e] + acc[1][0][2 + e]) + (acc[2][0][2 + e] + acc[3][0][2 + e]);
+          outm[static_cast<int64_t>(n) * a.Np + g] = lo - 1032.f * sxn;
+          outm[static_cast<int64_t>(n) * a.Np + g + 8] = (hi - 1152.f * sxn) * 0.0625f;
+        }
+      }
+      continue;
     }
     float* out = a.partial + static_cast<int64_t>(s) * a.Np + static_cast<int64_t>(rt) * kTileN;
     float sx = 0.f;
@@ -746,9 +779,47 @@ int mk_row_tiles(int bits, int M) {
   return M > 8 ? 2 : 1;  // measured: +12% (INT4) / +13% (INT8) at 16 tokens, a loss at <= 8
 }
 
+namespace {
+// Shared-memory plan of the single-token kernel family (k_gemv_m1, MT = M tokens): ring
+// depth, stage bytes and warps next to the resident activation vectors.
+struct M1Shape {
+  int nst, sb, warps;
+  size_t smem;
+  bool ok;
+};
+constexpr size_t kM1SmemLimit = 227 * 1024 - 1024;  // leave room for the static shared memory
+constexpr int kM1MaxTokens = 2;
+
+M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
+  static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
+  static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
+  const size_t xb = static_cast<size_t>(nx) * M * nch * (128 + 4) + 8;
+  M1Shape m;
+  m.nst = m1s >= 3 ? 3 : 2;
+  m.sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
+  m.warps = plan_warps;  // the plan's warps if the rings fit next to x, else fewer
+  auto need = [&](int w, int n, int b) { return xb + static_cast<size_t>(w) * n * (b + 8); };
+  if (need(m.warps, m.nst, m.sb) > kM1SmemLimit) m.nst = 2;
+  while (m.sb > 4096 && need(m.warps, m.nst, m.sb) > kM1SmemLimit) m.sb -= 2048;
+  while (m.warps > 8 && need(m.warps, m.nst, m.sb) > kM1SmemLimit) --m.warps;
+  m.smem = need(m.warps, m.nst, m.sb);
+  m.ok = m.smem <= kM1SmemLimit && nch * 128 * M < (int64_t{1} << 30);
+  return m;
+}
+
+// The single-token kernel family takes INT4 at up to GLM_M1_TOKENS (default 2) tokens when
+// the activation vectors fit next to 12 or more warps' rings (else the multi-token kernel).
+bool use_m1(int64_t nch, int M, int bits, int nx) {
+  static const int maxm = [] { const char* e = getenv("GLM_M1_TOKENS"); const int v = e ? atoi(e) : kM1MaxTokens; return v < 1 ? 1 : (v > kM1MaxTokens ? kM1MaxTokens : v); }();
+  if (bits != 4 || M > maxm) return false;
+  const M1Shape m = m1_shape(nch, M, nx, m1_warps());
+  return m.ok && (M == 1 || m.warps >= 12);
+}
+}  // namespace
+
 GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
   GemvPlan p;
-  if (M >= 2) {
+  if (M >= 2 && !use_m1(nch, M, bits, nx)) {
     // multi-token kernel: CTA-items of 16 row tiles x one k-slice; the slice of all M
     // activation rows (nx vectors) must fit one shared-memory buffer
     p.warps = kTWarps;
@@ -770,7 +841,7 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
     p.grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
     return p;
   }
-  p.warps = (M == 1 && bits == 4) ? m1_warps() : kTWarps;
+  p.warps = use_m1(nch, M, bits, nx) ? m1_warps() : kTWarps;
   const int64_t total_warps = static_cast<int64_t>(kNumSMs) * p.warps;
   double best = -1.0;
   const int64_t max_split = nch < 32 ? nch : 32;
@@ -797,8 +868,9 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   GemvArgs a{static_cast<const uint4*>(op.codes), reinterpret_cast<const uint4*>(op.xf),
              reinterpret_cast<const uint4*>(op.xf2 ? op.xf2 : op.xf), op.xf2 ? op.rt_split : op.nrt, partial,
              op.nrt, op.nch, op.nrt * kTileN, M, p.ksplit};
-  if (M >= 2) {
-    const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
+  const int nx_op = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
+  if (M >= 2 && !use_m1(op.nch, M, op.bits, nx_op)) {
+    const int nx = nx_op;
     const int64_t slice_max = (op.nch + p.ksplit - 1) / p.ksplit;
     if (slice_max * 128 * M * nx > kMkSliceBytes || p.warps != kTWarps || (p.rt_per_warp == 2 && op.rt_split % 2))
       fail(GLM_CONTRACT, "qlinear", "GEMV plan does not match the multi-token kernel (plan for this M and x count)");
@@ -833,38 +905,31 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     attr = true;
   }
   const dim3 grid(p.grid), block(kTWarps * 32);
-  if (M == 1 && op.bits == 4) {
-    static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
-    static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
-    const int nx = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
-    const size_t xb = static_cast<size_t>(nx) * op.nch * (128 + 4) + 8;
-    const size_t limit = 227 * 1024 - 1024;  // leave room for the static shared memory
-    int nst = m1s >= 3 ? 3 : 2;
-    int sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
-    int m1w = p.warps;  // the plan's warps if the rings fit next to x, else fewer
-    auto need = [&](int w, int n, int b) { return xb + static_cast<size_t>(w) * n * (b + 8); };
-    if (need(m1w, nst, sb) > limit) nst = 2;
-    while (sb > 4096 && need(m1w, nst, sb) > limit) sb -= 2048;
-    while (m1w > 8 && need(m1w, nst, sb) > limit) --m1w;
-    const size_t sm1 = need(m1w, nst, sb);
-    const dim3 block1(m1w * 32);
-    if (sm1 <= limit && op.nch * 128 < (int64_t{1} << 30)) {
-      static bool attr1 = false;
-      if (!attr1) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 6144>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 2, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemv_m1<4, 3, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        attr1 = true;
-      }
-      static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
-      if (nst == 3) launch_k(k_gemv_m1<4, 3, 4096>, grid, block1, sm1, st, a, nx, early);
-      else if (sb == 8192) launch_k(k_gemv_m1<4, 2, 8192>, grid, block1, sm1, st, a, nx, early);
-      else if (sb == 6144) launch_k(k_gemv_m1<4, 2, 6144>, grid, block1, sm1, st, a, nx, early);
-      else launch_k(k_gemv_m1<4, 2, 4096>, grid, block1, sm1, st, a, nx, early);
-      LAUNCH_CHECK("k_gemv_m1");
-      return;
+  if (use_m1(op.nch, M, op.bits, nx_op)) {
+    const M1Shape m = m1_shape(op.nch, M, nx_op, p.warps);
+    static bool attr1 = false;
+    if (!attr1) {
+      for (auto k : {k_gemv_m1<4, 2, 4096, 1>, k_gemv_m1<4, 2, 6144, 1>, k_gemv_m1<4, 2, 8192, 1>, k_gemv_m1<4, 3, 4096, 1>,
+                     k_gemv_m1<4, 2, 4096, 2>, k_gemv_m1<4, 2, 6144, 2>})
+        CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kM1SmemLimit));
+      attr1 = true;
     }
+    static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
+    const dim3 block1(m.warps * 32);
+    if (M == 2) {
+      if (m.sb >= 6144) launch_k(k_gemv_m1<4, 2, 6144, 2>, grid, block1, m.smem, st, a, nx_op, early);
+      else launch_k(k_gemv_m1<4, 2, 4096, 2>, grid, block1, m.smem, st, a, nx_op, early);
+    } else if (m.nst == 3) {
+      launch_k(k_gemv_m1<4, 3, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
+    } else if (m.sb == 8192) {
+      launch_k(k_gemv_m1<4, 2, 8192, 1>, grid, block1, m.smem, st, a, nx_op, early);
+    } else if (m.sb == 6144) {
+      launch_k(k_gemv_m1<4, 2, 6144, 1>, grid, block1, m.smem, st, a, nx_op, early);
+    } else {
+      launch_k(k_gemv_m1<4, 2, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
+    }
+    LAUNCH_CHECK("k_gemv_m1");
+    return;
   }
   if (op.bits == 4) {
     if (M <= 8) launch_k(k_gemv_tma<4, 1>, grid, block, smem, st, a);

@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 def contract_tol(M, bits):
-    return 2e-4 if (M == 1 and bits == 4) else 2e-6
+    # INT4 at 1..2 tokens runs the offset-binary transcode (gemv.cu dq4_raw): ~5e-5 of max|y|
+    return 2e-4 if (M <= 2 and bits == 4) else 2e-6
 
 
 def kernel_contract(x, q):
@@ -48,7 +49,7 @@ def test_qlinear_matches_contract_and_oracle(bits, axis, K, N):
     w = rng.normal(0, 0.02, size=(K, N))
     q = glm.quantize_absmax(w, bits, axis)
     lin = glm.QLinear.from_payload(q)
-    for M in (1, 3, 8, 9, 16, 37):
+    for M in (1, 2, 3, 8, 9, 16, 37):
         x = rng.normal(0, 1, size=(M, K))
         y = lin(x).astype(np.float64)
         c = kernel_contract(x, q)
