@@ -1248,6 +1248,8 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   // cap residency at one CTA per SM over B * heads CTAs, so rows are read from L2/HBM.
   a.split_keys = attn_decode_split_keys(a.max_ctx);
   if (a.max_splits != attn_decode_splits(a.max_ctx)) fail(GLM_CONTRACT, "glmmodel", "decode attention split count");
+  if (a.max_splits > kSplitKeys)  // the merge keeps one weight per split in the score buffer
+    fail(GLM_DIMENSION, "glmmodel", "decode attention supports caches up to 16384 tokens");
   const int stage = B <= 2 ? std::min(a.split_keys, (a.max_ctx + 15) / 16 * 16) : 0;
   a.stage_keys = stage;
   const size_t smem = 2ull * stage * a.dh * sizeof(__half);

@@ -250,6 +250,7 @@ struct glm_model {
     d_len = alloc<int>(max_batch);
     d_next = alloc<int>(max_batch);
     attn_splits = attn_decode_splits(max_ctx);
+    if (attn_splits > 256) fail(GLM_DIMENSION, "glmmodel", "max_ctx above 16384 tokens is not supported by the decode attention");
     attn_part = alloc<float>(static_cast<int64_t>(max_batch) * Hl * attn_splits * (dh + 2));
     attn_ctr = alloc<int>(static_cast<int64_t>(max_batch) * Hl);
     CUDA_CHECK(cudaMallocHost(&h_tokens, max_batch * sizeof(int)));
