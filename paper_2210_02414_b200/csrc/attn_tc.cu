@@ -1,0 +1,403 @@
+// attn_tc.cu — prefill attention on the 5th-generation tensor cores (head_dim 128).
+//
+// softmax(q k^T / sqrt(dh) + gMASK) v for one [gMASK] sample (model.cpp:137-152; visibility
+// j < max(C, i + 1), corruption.cpp:338-367), flash schedule over 128-key blocks:
+//
+//   warp 5      MMA issuer: S_j = Q K_j^T into one of two TMEM score tiles (A = Q and B = K_j
+//               from shared memory, both K-major), then O += P_j V_j (A = P_j from TMEM,
+//               B = V_j from shared memory, MN-major), fp32 accumulators in TMEM;
+//   warp 4      producer: K_j and V_j of the sequence's fp16 cache rows into three shared-
+//               memory slots, one tensor-map TMA per tile whose box (8 halves x 128 keys x 16
+//               dh groups) lands directly in the no-swizzle core-matrix layout the MMA
+//               descriptors describe;
+//   warps 0-3   softmax, one query row per thread = one TMEM lane: the score row (128
+//               fp32) from TMEM, gMASK, online max / sum in fp32, P = 2^(s - m) as fp16 into
+//               TMEM, the O rescale in TMEM when the running max rises, and the final
+//               O / l store.
+//
+// TMEM columns: S tiles [0, 128) and [128, 256), O [256, 384), P [384, 448).
+#include <cuda.h>
+
+#include <cfloat>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "block.h"
+#include "common.cuh"
+
+namespace glm {
+
+namespace {
+
+constexpr int kUR = 128;   // query rows per CTA (UMMA M)
+constexpr int kUK = 128;   // keys per block (UMMA N of S, K of P.V)
+constexpr int kUD = 128;   // head dim (UMMA K of S, N of P.V)
+constexpr int kTileBytes = kUR * kUD * 2;  // 32 KB: Q, one K block, one V block
+constexpr int kUSlots = 3;      // K/V block slots (one TMA per tile)
+constexpr int kUThreads = 6 * 32;
+constexpr uint32_t kColS = 0, kColO = 256, kColP = 384;
+constexpr size_t kUSmem = (1ull + 2 * kUSlots) * kTileBytes + 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void ub_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void ub_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void ub_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(bar))
+      : "memory");
+}
+// D (TMEM) (+)= A (smem desc) * B (smem desc)
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D (TMEM) (+)= A (TMEM) * B (smem desc)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tst32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void twait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void twait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Shared-memory matrix descriptor, no swizzle: start >> 4, leading / stride byte offsets >> 4,
+// sm100 descriptor version bit 46.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// Canonical K-major no-swizzle layout of a 128-row x 128-k fp16 tile: core matrices of
+// 8 rows x 8 k (16 B rows); k-group stride 2048 B (LBO), 8-row-group stride 128 B (SBO).
+__device__ __forceinline__ uint32_t kmaj_off(int row, int k) { return (k >> 3) * 2048 + row * 16 + (k & 7) * 2; }
+// MN-major no-swizzle layout of V (K = keys, N = dh): 8 keys x 8 dh core matrices with dh
+// contiguous (16 B per key); dh-group stride 2048 B, 8-key-group stride 128 B. For this
+// MN-major operand the descriptor's leading offset is the K-direction (key-group) stride and
+// the stride offset the MN-direction (dh-group) stride: LBO = 128, SBO = 2048 (verified
+// against the oracle; the K-major convention of Q and K is the transpose).
+__device__ __forceinline__ uint32_t vmaj_off(int key, int d) { return (d >> 3) * 2048 + key * 16 + (d & 7) * 2; }
+
+__device__ __forceinline__ void tma_kv(void* dst, const CUtensorMap* map, int key0, int head, int seq, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+          su32(dst)),
+      "l"(map), "r"(0), "r"(key0), "r"(0), "r"(head), "r"(seq), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ub_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillArgs a, int v_lbo, int v_sbo,
+                                                                    const __grid_constant__ CUtensorMap kmap,
+                                                                    const __grid_constant__ CUtensorMap vmap) {
+  extern __shared__ __align__(1024) uint8_t usm_raw[];
+  uint8_t* usm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(usm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = usm;
+  uint8_t* Ks = usm + kTileBytes;                    // [kUSlots]
+  uint8_t* Vs = usm + (1 + kUSlots) * kTileBytes;    // [kUSlots]
+  __shared__ __align__(8) uint64_t kv_full[kUSlots], kv_empty[kUSlots], s_full[2], s_free[2], p_full, o_done;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, i0 = blockIdx.x * kUR;
+  const int n = a.n, C = a.context_len;
+  const __half* kc = a.kcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * kUD;
+  const __half* vc = a.vcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * kUD;
+  const int kend = min(n, max(C, i0 + kUR));  // keys visible to some row of this block
+  const int nblk = (kend + kUK - 1) / kUK;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < kUSlots; ++i) {
+      ub_init(kv_full + i, 1);
+      ub_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ub_init(s_full + i, 1);
+      ub_init(s_free + i, 4);
+    }
+    ub_init(&p_full, 4);
+    ub_init(&o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // Q (fp32, rotated) -> fp16 scaled by log2(e) / sqrt(dh), K-major core matrices
+  if (warp < 4) {
+    const int r = threadIdx.x;
+    const int i = i0 + r;
+    const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(kUD));
+    const float* qrow = a.q + (static_cast<int64_t>(head) * n + (i < n ? i : 0)) * kUD;
+#pragma unroll 4
+    for (int k = 0; k < kUD; k += 8) {
+      uint32_t h[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 v = i < n ? *reinterpret_cast<const float2*>(qrow + k + 2 * e) : make_float2(0.f, 0.f);
+        const __half2 hv = __floats2half2_rn(v.x * qs, v.y * qs);
+        h[e] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+      *reinterpret_cast<uint4*>(Qs + kmaj_off(r, k)) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = tmem_slot;
+
+  if (warp == 4) {
+    // ---------------- producer: K_j, V_j into slot j % kUSlots (keys >= n arrive as zeros) ----------------
+    if (lane == 0)
+      for (int j = 0; j < nblk; ++j) {
+        const int slot = j % kUSlots;
+        ub_wait(kv_empty + slot, ((j / kUSlots) & 1) ^ 1);
+        ub_expect_tx(kv_full + slot, 2 * kTileBytes);
+        tma_kv(Ks + slot * kTileBytes, &kmap, j * kUK, head, a.seq, kv_full + slot);
+        tma_kv(Vs + slot * kTileBytes, &vmap, j * kUK, head, a.seq, kv_full + slot);
+      }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer ----------------
+    // kind::f16: D f32 (bit 4), A/B f16, N >> 3 at bit 17, M >> 4 at bit 24; bit 16: B MN-major
+    const uint32_t idesc_s = (1u << 4) | (static_cast<uint32_t>(kUK >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
+    const uint32_t idesc_o = (1u << 4) | (1u << 16) | (static_cast<uint32_t>(kUD >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
+    const uint32_t q0 = su32(Qs);
+    auto issue_s = [&](int j) {
+      const int kvs = j % kUSlots, ss = j & 1;
+      ub_wait(kv_full + kvs, (j / kUSlots) & 1);
+      if (j >= 2) ub_wait(s_free + ss, ((j >> 1) - 1) & 1);
+      fence_after();
+      const uint32_t k0 = su32(Ks + kvs * kTileBytes);
+#pragma unroll
+      for (int ks = 0; ks < kUD / 16; ++ks)
+        mma_ss(tbase + kColS + ss * kUK, sdesc(q0 + ks * 4096, 2048, 128), sdesc(k0 + ks * 4096, 2048, 128), idesc_s,
+               ks > 0 ? 1u : 0u);
+      commit_elect(s_full + ss);
+      __syncwarp();
+    };
+    if (nblk > 0) issue_s(0);
+    for (int j = 0; j < nblk; ++j) {
+      if (j + 1 < nblk) issue_s(j + 1);
+      ub_wait(&p_full, j & 1);
+      fence_after();
+      const uint32_t v0 = su32(Vs + (j % kUSlots) * kTileBytes);
+#pragma unroll
+      for (int ks = 0; ks < kUK / 16; ++ks)
+        mma_ts(tbase + kColO, tbase + kColP + ks * 8, sdesc(v0 + ks * 256, v_lbo, v_sbo), idesc_o,
+               (j > 0 || ks > 0) ? 1u : 0u);
+      commit_elect(&o_done);
+      commit_elect(kv_empty + (j % kUSlots));
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    // ---------------- softmax: thread = query row = TMEM lane ----------------
+    const int r = threadIdx.x;
+    const int i = i0 + r;
+    const int lim = min(max(C, i + 1), n);  // keys j < lim are visible to row i
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int slot = j & 1;
+      ub_wait(s_full + slot, (j >> 1) & 1);
+      fence_after();
+      float sv[kUK];
+#pragma unroll
+      for (int c = 0; c < kUK; c += 32) {
+        uint32_t v[32];
+        tld32(lane_base + kColS + slot * kUK + c, v);
+        twait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(v[e]);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) ub_arrive(s_free + slot);
+      const int j0 = j * kUK;
+      float bm = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kUK; ++c) {
+        if (j0 + c >= lim) sv[c] = -INFINITY;
+        bm = fmaxf(bm, sv[c]);
+      }
+      const float mn = fmaxf(m, bm);
+      const float ms = mn == -INFINITY ? 0.f : mn;  // fully masked row so far: keep p = 0
+      const float corr = ex2(m - ms);
+      l *= corr;
+      uint32_t pw[kUK / 2];
+#pragma unroll
+      for (int c = 0; c < kUK; c += 2) {
+        const float p0 = ex2(sv[c] - ms), p1 = ex2(sv[c + 1] - ms);
+        l += p0 + p1;
+        const __half2 hv = __floats2half2_rn(p0, p1);
+        pw[c / 2] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+      // P and O are free once P.V of the previous block has completed
+      if (j > 0) {
+        ub_wait(&o_done, (j - 1) & 1);
+        fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < kUD; c += 32) {
+            uint32_t v[32];
+            tld32(lane_base + kColO + c, v);
+            twait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * corr);
+            tst32(lane_base + kColO + c, v);
+          }
+        }
+      }
+      tst32(lane_base + kColP, *reinterpret_cast<const uint32_t(*)[32]>(&pw[0]));
+      tst32(lane_base + kColP + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pw[32]));
+      twait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) ub_arrive(&p_full);
+      m = mn;
+    }
+    // ---- O / l ----
+    if (nblk > 0) {
+      ub_wait(&o_done, (nblk - 1) & 1);
+      fence_after();
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+    for (int c = 0; c < kUD; c += 32) {
+      uint32_t v[32];
+      if (nblk > 0) {
+        tld32(lane_base + kColO + c, v);
+        twait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0u;
+      }
+      if (i < n) {
+        float* orow = a.out + static_cast<int64_t>(i) * a.ldout + head * kUD + c;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(orow + e) = make_float4(__uint_as_float(v[e]) * inv, __uint_as_float(v[e + 1]) * inv,
+                                                             __uint_as_float(v[e + 2]) * inv, __uint_as_float(v[e + 3]) * inv);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+}  // namespace
+
+namespace {
+// Tensor map of one layer's K or V cache [batch][heads][max_ctx][128] fp16 as the 5-D view
+// (8 halves, key, dh group, head, sequence) with strides (256 B, 16 B, ...): a box of
+// (8, 128, 16, 1, 1) lands as [dh group][key][8 halves], the no-swizzle core-matrix layout.
+// Rows beyond the cache read as zeros. Maps are cached per (buffer, shape): a later model may
+// reuse an address with another shape.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+CUtensorMap kv_tensor_map(const __half* base, const AttnPrefillArgs& a) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, CUtensorMap> cache;  // (base, max_ctx, heads)
+  static EncodeTiledFn encode = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(static_cast<const void*>(base), a.max_ctx, a.heads);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(GLM_CUDA, "attention", "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  // the sequence count is not in the arguments; the map never reads beyond the sequence asked for
+  const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(a.max_ctx), 16, static_cast<cuuint64_t>(a.heads), 65536};
+  const cuuint64_t row = kUD * 2;
+  const cuuint64_t strides[4] = {row, 16, row * a.max_ctx, row * a.max_ctx * a.heads};
+  const cuuint32_t box[5] = {8, kUK, kUD / 8, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GLM_CUDA, "attention", "K/V tensor map rejected (" + std::to_string(static_cast<int>(r)) + ")");
+  cache[key] = m;
+  return m;
+}
+}  // namespace
+
+// The tcgen05 prefill attention takes head_dim 128 (GLM_ATTN_UMMA=0 selects the mma.sync
+// flash kernel); V descriptor offsets overridable for bring-up (GLM_ATTN_VLBO / _VSBO).
+bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st) {
+  static const int on = [] { const char* e = getenv("GLM_ATTN_UMMA"); return e ? atoi(e) : 1; }();
+  if (!on || a.dh != kUD) return false;
+  static const int vlbo = [] { const char* e = getenv("GLM_ATTN_VLBO"); return e ? atoi(e) : 128; }();
+  static const int vsbo = [] { const char* e = getenv("GLM_ATTN_VSBO"); return e ? atoi(e) : 2048; }();
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_attn_prefill_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kUSmem)));
+    attr = true;
+  }
+  const CUtensorMap km = kv_tensor_map(a.kcache, a), vm = kv_tensor_map(a.vcache, a);
+  const dim3 grid((a.n + kUR - 1) / kUR, a.heads);
+  k_attn_prefill_umma<<<grid, kUThreads, kUSmem, st>>>(a, vlbo, vsbo, km, vm);
+  LAUNCH_CHECK("k_attn_prefill_umma");
+  return true;
+}
+
+}  // namespace glm

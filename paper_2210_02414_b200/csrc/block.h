@@ -115,6 +115,8 @@ void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st);
 void launch_advance(int* cache_len, int B, cudaStream_t st);
 void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st);
 void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st);
+// tcgen05 prefill attention (attn_tc.cu): false if it does not take this call (head_dim != 128)
+bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st);
 void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st);
 void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st);
 void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st);
