@@ -7,9 +7,9 @@
 //               from shared memory, both K-major), then O += P_j V_j (A = P_j from TMEM,
 //               B = V_j from shared memory, MN-major), fp32 accumulators in TMEM;
 //   warp 4      producer: K_j and V_j of the sequence's fp16 cache rows into three shared-
-//               memory slots, one tensor-map TMA per tile whose box (8 halves x 128 keys x 16
-//               dh groups) lands directly in the no-swizzle core-matrix layout the MMA
-//               descriptors describe;
+//               memory slots, one tensor-map TMA per tile (box 64 dh x 128 keys x 2 dh
+//               halves, 128 B swizzle: the same bytes serve as the K-major B operand of
+//               Q K^T and, for V, as the MN-major B operand of P V);
 //   warps 0-3   softmax, one query row per thread = one TMEM lane: the score row (128
 //               fp32) from TMEM, gMASK, online max / sum in fp32, P = 2^(s - m) as fp16 into
 //               TMEM, the O rescale in TMEM when the running max rises, and the final
@@ -119,15 +119,19 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-// Canonical K-major no-swizzle layout of a 128-row x 128-k fp16 tile: core matrices of
-// 8 rows x 8 k (16 B rows); k-group stride 2048 B (LBO), 8-row-group stride 128 B (SBO).
-__device__ __forceinline__ uint32_t kmaj_off(int row, int k) { return (k >> 3) * 2048 + row * 16 + (k & 7) * 2; }
-// MN-major no-swizzle layout of V (K = keys, N = dh): 8 keys x 8 dh core matrices with dh
-// contiguous (16 B per key); dh-group stride 2048 B, 8-key-group stride 128 B. For this
-// MN-major operand the descriptor's leading offset is the K-direction (key-group) stride and
-// the stride offset the MN-direction (dh-group) stride: LBO = 128, SBO = 2048 (verified
-// against the oracle; the K-major convention of Q and K is the transpose).
-__device__ __forceinline__ uint32_t vmaj_off(int key, int d) { return (d >> 3) * 2048 + key * 16 + (d & 7) * 2; }
+// 128-byte-swizzled tiles (what a TMA box with a 128 B inner extent writes at full speed):
+// a 128-row x 128-element fp16 tile is two 16 KB halves [element/64][row][64 elements],
+// each 128 B row with its 16-byte chunks XOR-ed by row % 8. Descriptor layout type 2
+// (SWIZZLE_128B), 8-row stride (SBO) 1024 B; for the K-major Q and K the MMA's 16-element
+// K step moves 32 B inside a row, for the MN-major V the two 64-element N halves are 16 KB
+// apart (LBO) and a 16-key K step moves 2 KB.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return sdesc(addr, lbo, sbo) | (2ull << 61);
+}
+__device__ __forceinline__ uint32_t sw128_off(int row, int e) {
+  return (e >> 6) * 16384 + row * 128 + ((((e & 63) >> 3) ^ (row & 7)) << 4) + (e & 7) * 2;
+}
+
 
 __device__ __forceinline__ void tma_kv(void* dst, const CUtensorMap* map, int key0, int head, int seq, uint64_t* bar) {
   asm volatile(
@@ -135,7 +139,7 @@ __device__ __forceinline__ void tma_kv(void* dst, const CUtensorMap* map, int ke
           su32(dst)),
       "l"(map), "r"(0), "r"(key0), "r"(0), "r"(head), "r"(seq), "r"(su32(bar))
       : "memory");
-}
+}  // (box: 64 elements x 128 keys x 2 halves of dh, 128 B swizzle)
 __device__ __forceinline__ void ub_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
 }
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         const __half2 hv = __floats2half2_rn(v.x * qs, v.y * qs);
         h[e] = *reinterpret_cast<const uint32_t*>(&hv);
       }
-      *reinterpret_cast<uint4*>(Qs + kmaj_off(r, k)) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(Qs + sw128_off(r, k)) = make_uint4(h[0], h[1], h[2], h[3]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -222,8 +226,8 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       const uint32_t k0 = su32(Ks + kvs * kTileBytes);
 #pragma unroll
       for (int ks = 0; ks < kUD / 16; ++ks)
-        mma_ss(tbase + kColS + ss * kUK, sdesc(q0 + ks * 4096, 2048, 128), sdesc(k0 + ks * 4096, 2048, 128), idesc_s,
-               ks > 0 ? 1u : 0u);
+        mma_ss(tbase + kColS + ss * kUK, sdesc_sw128(q0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
+               sdesc_sw128(k0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
       commit_elect(s_full + ss);
       __syncwarp();
     };
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       const uint32_t v0 = su32(Vs + (j % kUSlots) * kTileBytes);
 #pragma unroll
       for (int ks = 0; ks < kUK / 16; ++ks)
-        mma_ts(tbase + kColO, tbase + kColP + ks * 8, sdesc(v0 + ks * 256, v_lbo, v_sbo), idesc_o,
+        mma_ts(tbase + kColO, tbase + kColP + ks * 8, sdesc_sw128(v0 + ks * 2048, v_lbo, v_sbo), idesc_o,
                (j > 0 || ks > 0) ? 1u : 0u);
       commit_elect(&o_done);
       commit_elect(kv_empty + (j % kUSlots));
@@ -252,25 +256,25 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       const int slot = j & 1;
       ub_wait(s_full + slot, (j >> 1) & 1);
       fence_after();
-      float sv[kUK];
+      uint32_t sr[4][32];  // the score row: four loads in flight, one wait
 #pragma unroll
-      for (int c = 0; c < kUK; c += 32) {
-        uint32_t v[32];
-        tld32(lane_base + kColS + slot * kUK + c, v);
-        twait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(v[e]);
-      }
+      for (int q = 0; q < 4; ++q) tld32(lane_base + kColS + slot * kUK + q * 32, sr[q]);
+      twait_ld();
       fence_before();
       __syncwarp();
       if (lane == 0) ub_arrive(s_free + slot);
+      float sv[kUK];
+#pragma unroll
+      for (int c = 0; c < kUK; ++c) sv[c] = __uint_as_float(sr[c >> 5][c & 31]);
       const int j0 = j * kUK;
+      if (!__all_sync(0xffffffffu, j0 + kUK <= lim)) {  // the block straddles some row's limit
+#pragma unroll
+        for (int c = 0; c < kUK; ++c)
+          if (j0 + c >= lim) sv[c] = -INFINITY;
+      }
       float bm = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kUK; ++c) {
-        if (j0 + c >= lim) sv[c] = -INFINITY;
-        bm = fmaxf(bm, sv[c]);
-      }
+      for (int c = 0; c < kUK; ++c) bm = fmaxf(bm, sv[c]);
       const float mn = fmaxf(m, bm);
       const float ms = mn == -INFINITY ? 0.f : mn;  // fully masked row so far: keep p = 0
       const float corr = ex2(m - ms);
@@ -289,13 +293,18 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         fence_after();
         if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll
-          for (int c = 0; c < kUD; c += 32) {
-            uint32_t v[32];
-            tld32(lane_base + kColO + c, v);
+          for (int h = 0; h < kUD; h += 64) {  // two halves: two loads in flight per wait
+            uint32_t v0[32], v1[32];
+            tld32(lane_base + kColO + h, v0);
+            tld32(lane_base + kColO + h + 32, v1);
             twait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * corr);
-            tst32(lane_base + kColO + c, v);
+            for (int e = 0; e < 32; ++e) {
+              v0[e] = __float_as_uint(__uint_as_float(v0[e]) * corr);
+              v1[e] = __float_as_uint(__uint_as_float(v1[e]) * corr);
+            }
+            tst32(lane_base + kColO + h, v0);
+            tst32(lane_base + kColO + h + 32, v1);
           }
         }
       }
@@ -344,8 +353,8 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
 
 namespace {
 // Tensor map of one layer's K or V cache [batch][heads][max_ctx][128] fp16 as the 5-D view
-// (8 halves, key, dh group, head, sequence) with strides (256 B, 16 B, ...): a box of
-// (8, 128, 16, 1, 1) lands as [dh group][key][8 halves], the no-swizzle core-matrix layout.
+// (64 halves, key, dh half, head, sequence) with strides (256 B, 128 B, ...): a box of
+// (64, 128, 2, 1, 1) with the 128 B swizzle lands as [dh half][key][64 halves] (sw128_off).
 // Rows beyond the cache read as zeros. Maps are cached per (buffer, shape): a later model may
 // reuse an address with another shape.
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -367,13 +376,13 @@ CUtensorMap kv_tensor_map(const __half* base, const AttnPrefillArgs& a) {
     encode = reinterpret_cast<EncodeTiledFn>(fn);
   }
   // the sequence count is not in the arguments; the map never reads beyond the sequence asked for
-  const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(a.max_ctx), 16, static_cast<cuuint64_t>(a.heads), 65536};
+  const cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(a.max_ctx), 2, static_cast<cuuint64_t>(a.heads), 65536};
   const cuuint64_t row = kUD * 2;
-  const cuuint64_t strides[4] = {row, 16, row * a.max_ctx, row * a.max_ctx * a.heads};
-  const cuuint32_t box[5] = {8, kUK, kUD / 8, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+  const cuuint64_t strides[4] = {row, 128, row * a.max_ctx, row * a.max_ctx * a.heads};
+  const cuuint32_t box[5] = {64, kUK, 2, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
   CUtensorMap m;
   const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(base), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(GLM_CUDA, "attention", "K/V tensor map rejected (" + std::to_string(static_cast<int>(r)) + ")");
   cache[key] = m;
@@ -382,12 +391,14 @@ CUtensorMap kv_tensor_map(const __half* base, const AttnPrefillArgs& a) {
 }  // namespace
 
 // The tcgen05 prefill attention takes head_dim 128 (GLM_ATTN_UMMA=0 selects the mma.sync
-// flash kernel); V descriptor offsets overridable for bring-up (GLM_ATTN_VLBO / _VSBO).
+// flash kernel); V descriptor offsets overridable for bring-up (GLM_ATTN_VLBO / _VSBO; the
+// defaults were verified against the oracle: the MN-major V takes the N-half distance as
+// LBO and the 8-key stride as SBO).
 bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st) {
   static const int on = [] { const char* e = getenv("GLM_ATTN_UMMA"); return e ? atoi(e) : 1; }();
   if (!on || a.dh != kUD) return false;
-  static const int vlbo = [] { const char* e = getenv("GLM_ATTN_VLBO"); return e ? atoi(e) : 128; }();
-  static const int vsbo = [] { const char* e = getenv("GLM_ATTN_VSBO"); return e ? atoi(e) : 2048; }();
+  static const int vlbo = [] { const char* e = getenv("GLM_ATTN_VLBO"); return e ? atoi(e) : 16384; }();
+  static const int vsbo = [] { const char* e = getenv("GLM_ATTN_VSBO"); return e ? atoi(e) : 1024; }();
   static bool attr = false;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(k_attn_prefill_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kUSmem)));
