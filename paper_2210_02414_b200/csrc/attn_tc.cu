@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
   uint8_t* Qs = usm;
   uint8_t* Ks = usm + kTileBytes;                    // [kUSlots]
   uint8_t* Vs = usm + (1 + kUSlots) * kTileBytes;    // [kUSlots]
-  __shared__ __align__(8) uint64_t kv_full[kUSlots], kv_empty[kUSlots], s_full[2], s_free[2], p_full, o_done;
+  __shared__ __align__(8) uint64_t kv_full[kUSlots], kv_empty[kUSlots], s_full[2], s_free[2], p_full, o_done, q_ready;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y, i0 = blockIdx.x * kUR;
@@ -176,31 +176,34 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
     }
     ub_init(&p_full, 4);
     ub_init(&o_done, 1);
+    ub_init(&q_ready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // Q (fp32, rotated) -> fp16 scaled by log2(e) / sqrt(dh), K-major core matrices
-  if (warp < 4) {
-    const int r = threadIdx.x;
-    const int i = i0 + r;
-    const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(kUD));
-    const float* qrow = a.q + (static_cast<int64_t>(head) * n + (i < n ? i : 0)) * kUD;
-#pragma unroll 4
-    for (int k = 0; k < kUD; k += 8) {
-      uint32_t h[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 v = i < n ? *reinterpret_cast<const float2*>(qrow + k + 2 * e) : make_float2(0.f, 0.f);
-        const __half2 hv = __floats2half2_rn(v.x * qs, v.y * qs);
-        h[e] = *reinterpret_cast<const uint32_t*>(&hv);
-      }
-      *reinterpret_cast<uint4*>(Qs + sw128_off(r, k)) = make_uint4(h[0], h[1], h[2], h[3]);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tbase = tmem_slot;
+  // Q (fp32, rotated) -> fp16 scaled by log2(e) / sqrt(dh), swizzled K-major tile; the K/V
+  // stream starts meanwhile, the first Q K^T waits for q_ready
+  if (warp < 4) {
+    const int r = threadIdx.x;
+    const int i = i0 + r;
+    const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(kUD));
+    const float4* qrow = reinterpret_cast<const float4*>(a.q + (static_cast<int64_t>(head) * n + (i < n ? i : 0)) * kUD);
+#pragma unroll
+    for (int k = 0; k < kUD; k += 8) {
+      const float4 v0 = i < n ? qrow[k / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v1 = i < n ? qrow[k / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const __half2 h0 = __floats2half2_rn(v0.x * qs, v0.y * qs), h1 = __floats2half2_rn(v0.z * qs, v0.w * qs);
+      const __half2 h2 = __floats2half2_rn(v1.x * qs, v1.y * qs), h3 = __floats2half2_rn(v1.z * qs, v1.w * qs);
+      *reinterpret_cast<uint4*>(Qs + sw128_off(r, k)) =
+          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) ub_arrive(&q_ready);
+  }
 
   if (warp == 4) {
     // ---------------- producer: K_j, V_j into slot j % kUSlots (keys >= n arrive as zeros) ----------------
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
     const uint32_t idesc_s = (1u << 4) | (static_cast<uint32_t>(kUK >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
     const uint32_t idesc_o = (1u << 4) | (1u << 16) | (static_cast<uint32_t>(kUD >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
     const uint32_t q0 = su32(Qs);
+    ub_wait(&q_ready, 0);
     auto issue_s = [&](int j) {
       const int kvs = j % kUSlots, ss = j & 1;
       ub_wait(kv_full + kvs, (j / kUSlots) & 1);
