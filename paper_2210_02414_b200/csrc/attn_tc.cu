@@ -276,21 +276,28 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         for (int c = 0; c < kUK; ++c)
           if (j0 + c >= lim) sv[c] = -INFINITY;
       }
-      float bm = -INFINITY;
+      float bm8[8];  // eight independent max chains, then a tree
 #pragma unroll
-      for (int c = 0; c < kUK; ++c) bm = fmaxf(bm, sv[c]);
+      for (int t = 0; t < 8; ++t) bm8[t] = sv[t];
+#pragma unroll
+      for (int c = 8; c < kUK; ++c) bm8[c & 7] = fmaxf(bm8[c & 7], sv[c]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bm8[t] = fmaxf(bm8[t], bm8[t + 4]);
+      const float bm = fmaxf(fmaxf(bm8[0], bm8[1]), fmaxf(bm8[2], bm8[3]));
       const float mn = fmaxf(m, bm);
       const float ms = mn == -INFINITY ? 0.f : mn;  // fully masked row so far: keep p = 0
       const float corr = ex2(m - ms);
       l *= corr;
       uint32_t pw[kUK / 2];
+      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // eight independent sum chains
 #pragma unroll
       for (int c = 0; c < kUK; c += 2) {
         const float p0 = ex2(sv[c] - ms), p1 = ex2(sv[c + 1] - ms);
-        l += p0 + p1;
+        ls[(c >> 1) & 7] += p0 + p1;
         const __half2 hv = __floats2half2_rn(p0, p1);
         pw[c / 2] = *reinterpret_cast<const uint32_t*>(&hv);
       }
+      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       // P and O are free once P.V of the previous block has completed
       if (j > 0) {
         ub_wait(&o_done, (j - 1) & 1);
