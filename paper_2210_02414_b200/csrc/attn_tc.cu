@@ -1,21 +1,24 @@
 // attn_tc.cu — prefill attention on the 5th-generation tensor cores (head_dim 128).
 //
 // softmax(q k^T / sqrt(dh) + gMASK) v for one [gMASK] sample (model.cpp:137-152; visibility
-// j < max(C, i + 1), corruption.cpp:338-367), flash schedule over 128-key blocks:
+// j < max(C, i + 1), corruption.cpp:338-367), flash schedule over 128-key blocks, two
+// 128-row query tiles per CTA so the tensor core works on one tile while the other's
+// softmax runs:
 //
-//   warp 5      MMA issuer: S_j = Q K_j^T into one of two TMEM score tiles (A = Q and B = K_j
-//               from shared memory, both K-major), then O += P_j V_j (A = P_j from TMEM,
-//               B = V_j from shared memory, MN-major), fp32 accumulators in TMEM;
-//   warp 4      producer: K_j and V_j of the sequence's fp16 cache rows into three shared-
+//   warp 9      MMA issuer: S_t(j) = Q_t K_j^T into tile t's TMEM score columns (A = Q_t and
+//               B = K_j from shared memory, K-major), then, once softmax t has written P_t(j)
+//               over the first half of those columns, O_t += P_t(j) V_j (A = P_t from TMEM,
+//               B = V_j from shared memory, MN-major) and at once S_t(j + 1);
+//   warp 8      producer: K_j and V_j of the sequence's fp16 cache rows into two shared-
 //               memory slots, one tensor-map TMA per tile (box 64 dh x 128 keys x 2 dh
 //               halves, 128 B swizzle: the same bytes serve as the K-major B operand of
 //               Q K^T and, for V, as the MN-major B operand of P V);
-//   warps 0-3   softmax, one query row per thread = one TMEM lane: the score row (128
-//               fp32) from TMEM, gMASK, online max / sum in fp32, P = 2^(s - m) as fp16 into
-//               TMEM, the O rescale in TMEM when the running max rises, and the final
-//               O / l store.
+//   warps 0-7   softmax, group t = warps 4t..4t+3, one query row per thread = one TMEM lane:
+//               the score row (fp32) from TMEM, gMASK, online max / sum in fp32, P = 2^(s - m)
+//               as fp16 back into TMEM, the O_t rescale in TMEM when a row's max rises, and
+//               the final O / l store.
 //
-// TMEM columns: S tiles [0, 128) and [128, 256), O [256, 384), P [384, 448).
+// TMEM columns: S_t / P_t [128 t, 128 t + 128), O_t [256 + 128 t, 384 + 128 t).
 #include <cuda.h>
 
 #include <cfloat>
@@ -36,10 +39,11 @@ constexpr int kUR = 128;   // query rows per CTA (UMMA M)
 constexpr int kUK = 128;   // keys per block (UMMA N of S, K of P.V)
 constexpr int kUD = 128;   // head dim (UMMA K of S, N of P.V)
 constexpr int kTileBytes = kUR * kUD * 2;  // 32 KB: Q, one K block, one V block
-constexpr int kUSlots = 3;      // K/V block slots (one TMA per tile)
-constexpr int kUThreads = 6 * 32;
-constexpr uint32_t kColS = 0, kColO = 256, kColP = 384;
-constexpr size_t kUSmem = (1ull + 2 * kUSlots) * kTileBytes + 1024;
+constexpr int kUTiles = 2;      // query tiles per CTA: one softmax group each, the tensor core alternates
+constexpr int kUSlots = 2;      // K/V block slots (one TMA per tile)
+constexpr int kUThreads = (4 * kUTiles + 2) * 32;
+constexpr uint32_t kColS = 0, kColO = 256;  // S_t / P_t at 128 t, O_t at 256 + 128 t
+constexpr size_t kUSmem = (static_cast<size_t>(kUTiles) + 2 * kUSlots) * kTileBytes + 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void ub_init(uint64_t* bar, uint32_t count) {
@@ -149,17 +153,16 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
                                                                     const __grid_constant__ CUtensorMap vmap) {
   extern __shared__ __align__(1024) uint8_t usm_raw[];
   uint8_t* usm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(usm_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Qs = usm;
-  uint8_t* Ks = usm + kTileBytes;                    // [kUSlots]
-  uint8_t* Vs = usm + (1 + kUSlots) * kTileBytes;    // [kUSlots]
-  __shared__ __align__(8) uint64_t kv_full[kUSlots], kv_empty[kUSlots], s_full[2], s_free[2], p_full, o_done, q_ready;
+  uint8_t* Qs = usm;                                          // [kUTiles]
+  uint8_t* Ks = usm + kUTiles * kTileBytes;                   // [kUSlots]
+  uint8_t* Vs = usm + (kUTiles + kUSlots) * kTileBytes;       // [kUSlots]
+  __shared__ __align__(8) uint64_t kv_full[kUSlots], kv_empty[kUSlots], s_full[kUTiles], p_full[kUTiles],
+      o_done[kUTiles], q_ready;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, i0 = blockIdx.x * kUR;
+  const int head = blockIdx.y, i0 = blockIdx.x * (kUTiles * kUR);
   const int n = a.n, C = a.context_len;
-  const __half* kc = a.kcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * kUD;
-  const __half* vc = a.vcache + ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx) * kUD;
-  const int kend = min(n, max(C, i0 + kUR));  // keys visible to some row of this block
+  const int kend = min(n, max(C, i0 + kUTiles * kUR));  // keys visible to some row of the CTA
   const int nblk = (kend + kUK - 1) / kUK;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)), "r"(512));
@@ -170,126 +173,77 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       ub_init(kv_full + i, 1);
       ub_init(kv_empty + i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      ub_init(s_full + i, 1);
-      ub_init(s_free + i, 4);
+    for (int t = 0; t < kUTiles; ++t) {
+      ub_init(s_full + t, 1);
+      ub_init(p_full + t, 4);
+      ub_init(o_done + t, 1);
     }
-    ub_init(&p_full, 4);
-    ub_init(&o_done, 1);
-    ub_init(&q_ready, 4);
+    ub_init(&q_ready, 4 * kUTiles);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tbase = tmem_slot;
-  // Q (fp32, rotated) -> fp16 scaled by log2(e) / sqrt(dh), swizzled K-major tile; the K/V
-  // stream starts meanwhile, the first Q K^T waits for q_ready
-  if (warp < 4) {
-    const int r = threadIdx.x;
-    const int i = i0 + r;
-    const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(kUD));
-    const float4* qrow = reinterpret_cast<const float4*>(a.q + (static_cast<int64_t>(head) * n + (i < n ? i : 0)) * kUD);
-#pragma unroll
-    for (int k = 0; k < kUD; k += 8) {
-      const float4 v0 = i < n ? qrow[k / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 v1 = i < n ? qrow[k / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const __half2 h0 = __floats2half2_rn(v0.x * qs, v0.y * qs), h1 = __floats2half2_rn(v0.z * qs, v0.w * qs);
-      const __half2 h2 = __floats2half2_rn(v1.x * qs, v1.y * qs), h3 = __floats2half2_rn(v1.z * qs, v1.w * qs);
-      *reinterpret_cast<uint4*>(Qs + sw128_off(r, k)) =
-          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
-                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) ub_arrive(&q_ready);
-  }
 
-  if (warp == 4) {
-    // ---------------- producer: K_j, V_j into slot j % kUSlots (keys >= n arrive as zeros) ----------------
-    if (lane == 0)
-      for (int j = 0; j < nblk; ++j) {
-        const int slot = j % kUSlots;
-        ub_wait(kv_empty + slot, ((j / kUSlots) & 1) ^ 1);
-        ub_expect_tx(kv_full + slot, 2 * kTileBytes);
-        tma_kv(Ks + slot * kTileBytes, &kmap, j * kUK, head, a.seq, kv_full + slot);
-        tma_kv(Vs + slot * kTileBytes, &vmap, j * kUK, head, a.seq, kv_full + slot);
+  if (warp < 4 * kUTiles) {
+    // ---------------- softmax group t (4 warps): one query row per thread = TMEM lane ----------------
+    const int t = warp >> 2, q = warp & 3;
+    const int r = q * 32 + lane;
+    const int i = i0 + t * kUR + r;
+    // Q row -> fp16 scaled by log2(e) / sqrt(dh) into the swizzled K-major tile of group t
+    {
+      const float qs = 1.4426950408889634f * rsqrtf(static_cast<float>(kUD));
+      const float4* qrow = reinterpret_cast<const float4*>(a.q + (static_cast<int64_t>(head) * n + (i < n ? i : 0)) * kUD);
+      uint8_t* Qt = Qs + t * kTileBytes;
+#pragma unroll
+      for (int k = 0; k < kUD; k += 8) {
+        const float4 v0 = i < n ? qrow[k / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v1 = i < n ? qrow[k / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const __half2 h0 = __floats2half2_rn(v0.x * qs, v0.y * qs), h1 = __floats2half2_rn(v0.z * qs, v0.w * qs);
+        const __half2 h2 = __floats2half2_rn(v1.x * qs, v1.y * qs), h3 = __floats2half2_rn(v1.z * qs, v1.w * qs);
+        *reinterpret_cast<uint4*>(Qt + sw128_off(r, k)) =
+            make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                       *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
       }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer ----------------
-    // kind::f16: D f32 (bit 4), A/B f16, N >> 3 at bit 17, M >> 4 at bit 24; bit 16: B MN-major
-    const uint32_t idesc_s = (1u << 4) | (static_cast<uint32_t>(kUK >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
-    const uint32_t idesc_o = (1u << 4) | (1u << 16) | (static_cast<uint32_t>(kUD >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
-    const uint32_t q0 = su32(Qs);
-    ub_wait(&q_ready, 0);
-    auto issue_s = [&](int j) {
-      const int kvs = j % kUSlots, ss = j & 1;
-      ub_wait(kv_full + kvs, (j / kUSlots) & 1);
-      if (j >= 2) ub_wait(s_free + ss, ((j >> 1) - 1) & 1);
-      fence_after();
-      const uint32_t k0 = su32(Ks + kvs * kTileBytes);
-#pragma unroll
-      for (int ks = 0; ks < kUD / 16; ++ks)
-        mma_ss(tbase + kColS + ss * kUK, sdesc_sw128(q0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
-               sdesc_sw128(k0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-      commit_elect(s_full + ss);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-    };
-    if (nblk > 0) issue_s(0);
-    for (int j = 0; j < nblk; ++j) {
-      if (j + 1 < nblk) issue_s(j + 1);
-      ub_wait(&p_full, j & 1);
-      fence_after();
-      const uint32_t v0 = su32(Vs + (j % kUSlots) * kTileBytes);
-#pragma unroll
-      for (int ks = 0; ks < kUK / 16; ++ks)
-        mma_ts(tbase + kColO, tbase + kColP + ks * 8, sdesc_sw128(v0 + ks * 2048, v_lbo, v_sbo), idesc_o,
-               (j > 0 || ks > 0) ? 1u : 0u);
-      commit_elect(&o_done);
-      commit_elect(kv_empty + (j % kUSlots));
-      __syncwarp();
+      if (lane == 0) ub_arrive(&q_ready);
     }
-  } else if (warp < 4) {
-    // ---------------- softmax: thread = query row = TMEM lane ----------------
-    const int r = threadIdx.x;
-    const int i = i0 + r;
     const int lim = min(max(C, i + 1), n);  // keys j < lim are visible to row i
-    const uint32_t lane_base = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t colS = kColS + t * kUK, colO = kColO + t * kUD;  // P_t overwrites S_t's first 64 columns
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
-      const int slot = j & 1;
-      ub_wait(s_full + slot, (j >> 1) & 1);
+      ub_wait(s_full + t, j & 1);  // S_t(j) complete => P.V_t(j - 1) complete as well (in order)
       fence_after();
-      uint32_t sr[4][32];  // the score row: four loads in flight, one wait
+      uint32_t sr[4][32];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tld32(lane_base + kColS + slot * kUK + q * 32, sr[q]);
+      for (int c = 0; c < 4; ++c) tld32(lane_base + colS + c * 32, sr[c]);
       twait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) ub_arrive(s_free + slot);
       float sv[kUK];
 #pragma unroll
       for (int c = 0; c < kUK; ++c) sv[c] = __uint_as_float(sr[c >> 5][c & 31]);
       const int j0 = j * kUK;
-      if (!__all_sync(0xffffffffu, j0 + kUK <= lim)) {  // the block straddles some row's limit
+      if (!__all_sync(0xffffffffu, j0 + kUK <= lim)) {
 #pragma unroll
         for (int c = 0; c < kUK; ++c)
           if (j0 + c >= lim) sv[c] = -INFINITY;
       }
-      float bm8[8];  // eight independent max chains, then a tree
+      float bm8[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) bm8[t] = sv[t];
+      for (int u = 0; u < 8; ++u) bm8[u] = sv[u];
 #pragma unroll
       for (int c = 8; c < kUK; ++c) bm8[c & 7] = fmaxf(bm8[c & 7], sv[c]);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) bm8[t] = fmaxf(bm8[t], bm8[t + 4]);
+      for (int u = 0; u < 4; ++u) bm8[u] = fmaxf(bm8[u], bm8[u + 4]);
       const float bm = fmaxf(fmaxf(bm8[0], bm8[1]), fmaxf(bm8[2], bm8[3]));
       const float mn = fmaxf(m, bm);
-      const float ms = mn == -INFINITY ? 0.f : mn;  // fully masked row so far: keep p = 0
+      const float ms = mn == -INFINITY ? 0.f : mn;  // row with nothing visible yet: p = 0
       const float corr = ex2(m - ms);
       l *= corr;
       uint32_t pw[kUK / 2];
-      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // eight independent sum chains
+      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < kUK; c += 2) {
         const float p0 = ex2(sv[c] - ms), p1 = ex2(sv[c + 1] - ms);
@@ -298,38 +252,33 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         pw[c / 2] = *reinterpret_cast<const uint32_t*>(&hv);
       }
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-      // P and O are free once P.V of the previous block has completed
-      if (j > 0) {
-        ub_wait(&o_done, (j - 1) & 1);
-        fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O_t rescale (P.V_t(j - 1) is complete)
 #pragma unroll
-          for (int h = 0; h < kUD; h += 64) {  // two halves: two loads in flight per wait
-            uint32_t v0[32], v1[32];
-            tld32(lane_base + kColO + h, v0);
-            tld32(lane_base + kColO + h + 32, v1);
-            twait_ld();
+        for (int h = 0; h < kUD; h += 64) {
+          uint32_t v0[32], v1[32];
+          tld32(lane_base + colO + h, v0);
+          tld32(lane_base + colO + h + 32, v1);
+          twait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              v0[e] = __float_as_uint(__uint_as_float(v0[e]) * corr);
-              v1[e] = __float_as_uint(__uint_as_float(v1[e]) * corr);
-            }
-            tst32(lane_base + kColO + h, v0);
-            tst32(lane_base + kColO + h + 32, v1);
+          for (int e = 0; e < 32; ++e) {
+            v0[e] = __float_as_uint(__uint_as_float(v0[e]) * corr);
+            v1[e] = __float_as_uint(__uint_as_float(v1[e]) * corr);
           }
+          tst32(lane_base + colO + h, v0);
+          tst32(lane_base + colO + h + 32, v1);
         }
       }
-      tst32(lane_base + kColP, *reinterpret_cast<const uint32_t(*)[32]>(&pw[0]));
-      tst32(lane_base + kColP + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pw[32]));
+      tst32(lane_base + colS, *reinterpret_cast<const uint32_t(*)[32]>(&pw[0]));
+      tst32(lane_base + colS + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pw[32]));
       twait_st();
       fence_before();
       __syncwarp();
-      if (lane == 0) ub_arrive(&p_full);
+      if (lane == 0) ub_arrive(p_full + t);
       m = mn;
     }
     // ---- O / l ----
     if (nblk > 0) {
-      ub_wait(&o_done, (nblk - 1) & 1);
+      ub_wait(o_done + t, (nblk - 1) & 1);
       fence_after();
     }
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -337,7 +286,7 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
     for (int c = 0; c < kUD; c += 32) {
       uint32_t v[32];
       if (nblk > 0) {
-        tld32(lane_base + kColO + c, v);
+        tld32(lane_base + colO + c, v);
         twait_ld();
       } else {
 #pragma unroll
@@ -349,6 +298,56 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         for (int e = 0; e < 32; e += 4)
           *reinterpret_cast<float4*>(orow + e) = make_float4(__uint_as_float(v[e]) * inv, __uint_as_float(v[e + 1]) * inv,
                                                              __uint_as_float(v[e + 2]) * inv, __uint_as_float(v[e + 3]) * inv);
+      }
+    }
+  } else if (warp == 4 * kUTiles) {
+    // ---------------- producer: K_j, V_j into slot j % kUSlots (keys past the cache arrive as zeros) ----------------
+    if (lane == 0)
+      for (int j = 0; j < nblk; ++j) {
+        const int slot = j % kUSlots;
+        ub_wait(kv_empty + slot, ((j / kUSlots) & 1) ^ 1);
+        ub_expect_tx(kv_full + slot, 2 * kTileBytes);
+        tma_kv(Ks + slot * kTileBytes, &kmap, j * kUK, head, a.seq, kv_full + slot);
+        tma_kv(Vs + slot * kTileBytes, &vmap, j * kUK, head, a.seq, kv_full + slot);
+      }
+  } else {
+    // ---------------- MMA issuer: S_A(j), S_B(j); then per tile P.V_t(j) and S_t(j + 1) ----------------
+    // kind::f16: D f32 (bit 4), A/B f16, N >> 3 at bit 17, M >> 4 at bit 24; bit 16: B MN-major
+    const uint32_t idesc_s = (1u << 4) | (static_cast<uint32_t>(kUK >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
+    const uint32_t idesc_o = (1u << 4) | (1u << 16) | (static_cast<uint32_t>(kUD >> 3) << 17) | (static_cast<uint32_t>(kUR >> 4) << 24);
+    ub_wait(&q_ready, 0);
+    auto issue_s = [&](int t, int j) {
+      const uint32_t qa = su32(Qs + t * kTileBytes), k0 = su32(Ks + (j % kUSlots) * kTileBytes);
+#pragma unroll
+      for (int ks = 0; ks < kUD / 16; ++ks)
+        mma_ss(tbase + kColS + t * kUK, sdesc_sw128(qa + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
+               sdesc_sw128(k0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+      commit_elect(s_full + t);
+    };
+    auto issue_pv = [&](int t, int j) {
+      const uint32_t v0 = su32(Vs + (j % kUSlots) * kTileBytes);
+#pragma unroll
+      for (int ks = 0; ks < kUK / 16; ++ks)
+        mma_ts(tbase + kColO + t * kUD, tbase + kColS + t * kUK + ks * 8, sdesc_sw128(v0 + ks * 2048, v_lbo, v_sbo),
+               idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+      commit_elect(o_done + t);
+    };
+    if (nblk > 0) {
+      ub_wait(kv_full, 0);
+      fence_after();
+      for (int t = 0; t < kUTiles; ++t) issue_s(t, 0);
+      __syncwarp();
+    }
+    for (int j = 0; j < nblk; ++j) {
+      const bool more = j + 1 < nblk;
+      if (more) ub_wait(kv_full + (j + 1) % kUSlots, ((j + 1) / kUSlots) & 1);
+      for (int t = 0; t < kUTiles; ++t) {
+        ub_wait(p_full + t, j & 1);
+        fence_after();
+        issue_pv(t, j);
+        if (t == kUTiles - 1) commit_elect(kv_empty + j % kUSlots);  // every MMA of block j issued
+        if (more) issue_s(t, j + 1);
+        __syncwarp();
       }
     }
   }
@@ -416,7 +415,7 @@ bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st) {
     attr = true;
   }
   const CUtensorMap km = kv_tensor_map(a.kcache, a), vm = kv_tensor_map(a.vcache, a);
-  const dim3 grid((a.n + kUR - 1) / kUR, a.heads);
+  const dim3 grid((a.n + kUTiles * kUR - 1) / (kUTiles * kUR), a.heads);
   k_attn_prefill_umma<<<grid, kUThreads, kUSmem, st>>>(a, vlbo, vsbo, km, vm);
   LAUNCH_CHECK("k_attn_prefill_umma");
   return true;
