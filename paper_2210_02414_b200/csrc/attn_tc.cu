@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
 #pragma unroll
       for (int u = 0; u < 4; ++u) bm8[u] = fmaxf(bm8[u], bm8[u + 4]);
       const float bm = fmaxf(fmaxf(bm8[0], bm8[1]), fmaxf(bm8[2], bm8[3]));
-      const float mn = fmaxf(m, bm);
+      // lazy max: the exponent reference moves only when a score exceeds it by more than
+      // 8 (P <= 2^8 stays exact enough in fp16, l and O accumulate in fp32), so O needs a
+      // rescale in TMEM only rarely after the first blocks
+      const float mn = bm > m + 8.f ? bm : m;
       const float ms = mn == -INFINITY ? 0.f : mn;  // row with nothing visible yet: p = 0
       const float corr = ex2(m - ms);
       l *= corr;
