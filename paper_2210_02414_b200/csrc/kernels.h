@@ -96,6 +96,11 @@ GemvPlan plan_qmm(const QLayout& L, int M);
 // y (optional, ksplit == 1): write the scaled result y[M][ldy] directly instead of partials
 void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
                 float* y = nullptr, int64_t ldy = 0, const float* zt = nullptr);
+// Fused W1|V GEMM + GeGLU (prefill): xo (W2's activation tiles, Kp = xo_Kp, kRow fold xo_rs
+// or null) = fp16(gelu(x.W1 * s1) * (x.V * s2)) for absmax W1 / V of one shape sharing x.
+bool qmm_geglu_supported(const QWeightDev& w1, const QWeightDev& v, int M);
+void qmm_geglu_launch(const QWeightDev& w1, const QWeightDev& v, const __half* xt, int M, __half* xo, int64_t xo_Kp,
+                      const float* xo_rs, cudaStream_t st);
 void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st);
 long long*& qmm_trace_ptr();  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
 

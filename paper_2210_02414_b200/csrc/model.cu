@@ -693,15 +693,20 @@ struct glm_model {
       ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
       ln.zero_sublayer = zero_sub;
       launch_deepnorm_ln(ln, n, st);
-      linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
-      linear_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), n, y_b.as<float>());
-      ActArgs act;
-      act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
-      act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
-      act.M = n;
-      act.f = fl;
-      act.xo = xout(xf_w2.as<__half>(), w2, nt);
-      launch_geglu_act(act, st);
+      if (axis != GLM_AXIS_ROW && qmm_geglu_supported(w1.w, v.w, n)) {  // W1|V GEMM with the GeGLU epilogue
+        const XOut xo = xout(xf_w2.as<__half>(), w2, nt);
+        qmm_geglu_launch(w1.w, v.w, xf_w1.as<__half>(), n, xo.xf, xo.Kp, xo.row_scale, st);
+      } else {
+        linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
+        linear_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), n, y_b.as<float>());
+        ActArgs act;
+        act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
+        act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
+        act.M = n;
+        act.f = fl;
+        act.xo = xout(xf_w2.as<__half>(), w2, nt);
+        launch_geglu_act(act, st);
+      }
       linear_rows(w2, xf_w2.as<__half>(), n, y_ffn.as<float>());
       if (tp_size > 1) comm->allreduce_sum(y_ffn.as<float>(), static_cast<int64_t>(n) * d, st);
       LnArgs ln2 = ln;

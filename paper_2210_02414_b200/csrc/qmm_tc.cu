@@ -48,11 +48,20 @@ constexpr int RX = 4;                            // activation ring
 constexpr int NA = 8;                            // 32-column A buffers (two per group)
 constexpr int NDB = NTOK <= 128 ? 2 : 1;         // accumulator tiles (2: epilogue overlaps the next item)
 constexpr uint32_t D_COL = NA * 32;              // 256: accumulators at [256, 512)
-constexpr int NW = 12;                           // weight-code ring (one 64-k chunk of 128 features per stage)
 template <int BITS>
 constexpr int wstage_bytes() { return BITS == 4 ? 4096 : 8192; }
-template <int BITS>
-constexpr size_t qmm_smem() { return static_cast<size_t>(RX) * XB + static_cast<size_t>(NW) * wstage_bytes<BITS>() + 1024 + 1024; }
+// weight-code ring (one 64-k chunk of 128 features per stage); the GeGLU-paired INT8 launch
+// gives 4 stages to the u/v exchange buffer
+template <int BITS, bool PAIR>
+constexpr int wring_stages() { return PAIR && BITS == 8 ? 8 : 12; }
+// GeGLU epilogue exchange: per group, the two v warps' 16-token x 32-feature fp32 slices, x2 buffers
+constexpr int kXchFloats = 16 * 32;
+constexpr int kXchBytes = kGroups * 2 * 2 * kXchFloats * 4;
+template <int BITS, bool PAIR>
+constexpr size_t qmm_smem() {
+  return static_cast<size_t>(RX) * XB + static_cast<size_t>(wring_stages<BITS, PAIR>()) * wstage_bytes<BITS>() +
+         (PAIR ? kXchBytes : 0) + 1024 + 1024;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -141,6 +150,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 struct QmmArgs {
   const uint8_t* w;   // fragment-ordered device layout (layout.cuh)
+  // GeGLU-paired launch (PAIR): an item is 64 features of W1 (TMEM lanes 0-63) and the same 64
+  // features of V (lanes 64-127); the epilogue writes gelu(x.W1 * s1) * (x.V * s2) straight into
+  // W2's activation tiles (tensor.cpp:313-318 fused after both matmuls)
+  const float* col_scale2;  // V's group scale
+  __half* xo;               // W2 activation tiles (xtile_index), Kp = xo_Kp
+  const float* xo_rs;       // W2's kRow fold, or null
+  int64_t xo_Kp;
   const __half* xt;   // activations, 128-token tiles (xtile_index)
   float* partial;     // [ksplit][M][Np], or the final y [M][ldo] when col_scale is set
   const float* col_scale;  // non-null (ksplit == 1): write y = acc * col_scale, columns < N
@@ -236,14 +252,17 @@ __device__ __forceinline__ void transcode(const Codes<BITS>& cd, int h, uint32_t
   }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_constant__ CUtensorMap wmap) {
+template <int BITS, bool PAIR>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_qmm_tc(QmmArgs a, const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap vmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr int WB = wstage_bytes<BITS>();
+  constexpr int NW = wring_stages<BITS, PAIR>();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xring = smem;
   uint8_t* wring = smem + static_cast<size_t>(RX) * XB;
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(wring + static_cast<size_t>(NW) * WB);
+  float* xch = reinterpret_cast<float*>(wring + static_cast<size_t>(NW) * WB);  // PAIR only
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(wring + static_cast<size_t>(NW) * WB + (PAIR ? kXchBytes : 0));
   uint64_t* wempty = wfull + NW;
   uint64_t* xfull = wempty + NW;
   uint64_t* xempty = xfull + RX;
@@ -314,8 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
           const int ws = q % NW;
           mbar_wait(wempty + ws, ((q / NW) & 1) ^ 1);
           mbar_expect_tx(wfull + ws, WB);
-          tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 8),
-                          wfull + ws);
+          if constexpr (PAIR) {  // 4 row tiles of W1, then the same 4 of V
+            tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 4),
+                            wfull + ws);
+            tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB + WB / 2, &vmap, static_cast<int>(c),
+                            static_cast<int>(rt * 4), wfull + ws);
+          } else {
+            tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 8),
+                            wfull + ws);
+          }
         }
       }
     }
@@ -388,7 +414,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_qmm_tc(QmmArgs a, const __grid_
         if (lane == 0) mbar_arrive(a_full + ab);
       }
       q += static_cast<uint32_t>(c1 - c0);
-      {  // epilogue: group g drains token columns [g, g + 1) * NTOK / kGroups of the tile
+      if constexpr (PAIR) {  // GeGLU epilogue: v warps (quarters 2, 3) hand x.V to the u warps
+        const int db = it % NDB;
+        mbar_wait(d_full + db, (it / NDB) & 1);
+        tc_fence_after();
+        const int64_t f = rt * 64 + (quarter & 1) * 32 + lane;  // feature of W1 / V / W2's k
+        const bool keep = f < a.N;
+        const float cs = keep ? (quarter < 2 ? a.col_scale[f] : a.col_scale2[f]) : 0.f;
+        const float rs = keep && a.xo_rs ? a.xo_rs[f] : 1.f;
+        float* xw = xch + (group * 2 + (quarter & 1)) * 2 * kXchFloats + lane;
+        const int64_t tile_base = tt * a.xo_Kp * NTOK + ((f % 16) / 8 + (f / 16) * 2) * (8 * NTOK) + f % 8;
+#pragma unroll 1
+        for (int c16 = group * (NTOK / kGroups), b = 0; c16 < (group + 1) * (NTOK / kGroups); c16 += 16, b ^= 1) {
+          uint32_t v[16];
+          tmem_ld16(lane_base + D_COL + db * NTOK + c16, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (quarter >= 2) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) xw[b * kXchFloats + m * 32] = __uint_as_float(v[m]) * cs;
+          }
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
+          if (quarter < 2 && keep) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+              const int mm = c16 + m;
+              if (tt * NTOK + mm < a.M) {
+                const float u = __uint_as_float(v[m]) * cs, vv = xw[b * kXchFloats + m * 32];
+                const float o = 0.5f * u * (1.f + erff(u * 0.70710678118654752440f)) * vv * rs;
+                a.xo[tile_base + (mm / 8) * 64 + (mm % 8) * 8] = __float2half_rn(o);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty + db);
+      } else {  // epilogue: group g drains token columns [g, g + 1) * NTOK / kGroups of the tile
         const int db = it % NDB;
         mbar_wait(d_full + db, (it / NDB) & 1);
         tc_fence_after();
@@ -451,12 +512,14 @@ long long*& qmm_trace_ptr() {
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-CUtensorMap codes_tensor_map(const QWeightDev& w) {
+// box_rt: row tiles per copy (8; 4 for the GeGLU-paired launch, which stages W1 and V halves).
+CUtensorMap codes_tensor_map(const QWeightDev& w, int box_rt = 8) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
   static EncodeTiledFn encode = nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_pair(static_cast<const void*>(w.codes), w.L.nrt * 1000003 + w.L.nch * 17 + w.L.bits);
+  const auto key = std::make_pair(static_cast<const void*>(w.codes),
+                                  (w.L.nrt * 1000003 + w.L.nch * 17 + w.L.bits) * 16 + box_rt);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   if (!encode) {
@@ -475,13 +538,13 @@ CUtensorMap codes_tensor_map(const QWeightDev& w) {
   if (i8) {
     const cuuint64_t d[5] = {64, 8, 2, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
     const cuuint64_t sd[4] = {64, 512, 1024, static_cast<cuuint64_t>(w.L.nch) * cb};
-    const cuuint32_t bx[5] = {64, 8, 2, 1, 8};
+    const cuuint32_t bx[5] = {64, 8, 2, 1, static_cast<cuuint32_t>(box_rt)};
     for (int i = 0; i < 5; ++i) dims[i] = d[i], box[i] = bx[i];
     for (int i = 0; i < 4; ++i) strides[i] = sd[i];
   } else {
     const cuuint64_t d[4] = {64, 8, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
     const cuuint64_t sd[3] = {64, 512, static_cast<cuuint64_t>(w.L.nch) * cb};
-    const cuuint32_t bx[4] = {64, 8, 1, 8};
+    const cuuint32_t bx[4] = {64, 8, 1, static_cast<cuuint32_t>(box_rt)};
     for (int i = 0; i < 4; ++i) dims[i] = d[i], box[i] = bx[i];
     for (int i = 0; i < 3; ++i) strides[i] = sd[i];
   }
@@ -491,6 +554,18 @@ CUtensorMap codes_tensor_map(const QWeightDev& w) {
   if (r != CUDA_SUCCESS) fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
   cache[key] = m;
   return m;
+}
+
+template <int BITS, bool PAIR>
+void launch_qmm(const QmmArgs& a, int grid, const CUtensorMap& wmap, const CUtensorMap& vmap, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<BITS, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(qmm_smem<BITS, PAIR>())));
+    attr = true;
+  }
+  k_qmm_tc<BITS, PAIR><<<grid, kThreads, qmm_smem<BITS, PAIR>(), st>>>(a, wmap, vmap);
+  LAUNCH_CHECK("k_qmm_tc");
 }
 
 GemvPlan plan_qmm(const QLayout& L, int M) {
@@ -521,7 +596,7 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
   if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
   if (w.L.Np % 128 || w.L.Kp % 64) fail(GLM_DIMENSION, "qlinear", "layout not padded for the tcgen05 path");
   if (y && p.ksplit != 1) fail(GLM_CONTRACT, "qlinear", "direct output needs an unsplit K");
-  QmmArgs a;
+  QmmArgs a{};
   a.w = static_cast<const uint8_t*>(w.codes);
   a.xt = xt;
   a.partial = y ? y : partial;
@@ -546,17 +621,46 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
     a.trace = trace_buf;
     qmm_trace_ptr() = trace_buf;
   }
-  static bool attr[2] = {false, false};
-  const int bi = w.L.bits == 4 ? 0 : 1;
-  if (!attr[bi]) {
-    if (bi == 0) CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qmm_smem<4>())));
-    else CUDA_CHECK(cudaFuncSetAttribute(k_qmm_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qmm_smem<8>())));
-    attr[bi] = true;
-  }
   const CUtensorMap wmap = codes_tensor_map(w);
-  if (bi == 0) k_qmm_tc<4><<<p.grid, kThreads, qmm_smem<4>(), st>>>(a, wmap);
-  else k_qmm_tc<8><<<p.grid, kThreads, qmm_smem<8>(), st>>>(a, wmap);
-  LAUNCH_CHECK("k_qmm_tc");
+  if (w.L.bits == 4) launch_qmm<4, false>(a, p.grid, wmap, wmap, st);
+  else launch_qmm<8, false>(a, p.grid, wmap, wmap, st);
+}
+
+bool qmm_geglu_supported(const QWeightDev& w1, const QWeightDev& v, int M) {
+  static const bool off = [] {
+    const char* e = getenv("GLM_QMM_GEGLU");
+    return e && e[0] == '0';
+  }();
+  return !off && M > 16 && w1.L.bits == v.L.bits && w1.L.K == v.L.K && w1.L.N == v.L.N && w1.L.Np == v.L.Np &&
+         w1.L.nch == v.L.nch && w1.zvec == nullptr && v.zvec == nullptr && w1.L.Np % 128 == 0 && w1.L.Kp % 64 == 0;
+}
+
+void qmm_geglu_launch(const QWeightDev& w1, const QWeightDev& v, const __half* xt, int M, __half* xo, int64_t xo_Kp,
+                      const float* xo_rs, cudaStream_t st) {
+  if (!qmm_geglu_supported(w1, v, M)) fail(GLM_CONTRACT, "qlinear", "W1 / V pair not eligible for the fused GeGLU GEMM");
+  QmmArgs a{};
+  a.w = static_cast<const uint8_t*>(w1.codes);
+  a.xt = xt;
+  a.col_scale = w1.col_scale;
+  a.col_scale2 = v.col_scale;
+  a.xo = xo;
+  a.xo_Kp = xo_Kp;
+  a.xo_rs = xo_rs;
+  a.N = w1.L.N;
+  a.nrt16 = w1.L.nrt;
+  a.nch = w1.L.nch;
+  a.Np = w1.L.Np;
+  a.Kp = w1.L.Kp;
+  a.M = M;
+  a.ksplit = 1;
+  a.ntt = (M + NTOK - 1) / NTOK;
+  a.nrt128 = static_cast<int>(w1.L.Np / 64);  // 64-feature blocks of the pair
+  a.trace = nullptr;
+  const int64_t items = static_cast<int64_t>(a.nrt128) * a.ntt;
+  const int grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
+  const CUtensorMap wmap = codes_tensor_map(w1, 4), vmap = codes_tensor_map(v, 4);
+  if (w1.L.bits == 4) launch_qmm<4, true>(a, grid, wmap, vmap, st);
+  else launch_qmm<8, true>(a, grid, wmap, vmap, st);
 }
 
 void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st) {

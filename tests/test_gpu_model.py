@@ -221,12 +221,12 @@ def test_contract_errors(int8_row):
     assert m.cached_length() == 10
 
 
-@pytest.mark.parametrize("prefix_len,gen", [(200, 0), (150, 60), (63, 2)])
+@pytest.mark.parametrize("prefix_len,gen", [(200, 0), (150, 60), (63, 2), (280, 24)])
 def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
     """Tensor-core flash prefill (block.cu k_attn_prefill_tc) at head_dim 128 over several
     64-key blocks: bidirectional prefix, causal generation rows, and a context length that
     straddles block boundaries (j < max(C, i + 1), corruption.cpp:338-367)."""
-    p, m, _ = build(4, "column", layers=2, hidden=256, heads=2, vocab=300, seed=9, max_ctx=320)
+    p, m, _ = build(4, "column", layers=2, hidden=256, heads=2, vocab=300, seed=9, max_ctx=320)  # (280, 24): two 256-token tiles through the fused W1|V + GeGLU GEMM
     rng = np.random.default_rng(prefix_len)
     prefix = [int(v) for v in rng.integers(6, 290, size=prefix_len)]
     gen_toks = [int(v) for v in rng.integers(6, 290, size=gen)]
