@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const int64_t f = rt * 64 + (quarter & 1) * 32 + lane;  // feature of W1 / V / W2's k
         const bool keep = f < a.N;
-        const float cs = keep ? (quarter < 2 ? a.col_scale[f] : a.col_scale2[f]) : 0.f;
+        const float cs = keep ? (quarter < 2 ? a.col_scale[f] : a.col_scale2[f]) : 0.f;  // v warps: V's scale
         const float rs = keep && a.xo_rs ? a.xo_rs[f] : 1.f;
         float* xw = xch + (group * 2 + (quarter & 1)) * 2 * kXchFloats + lane;
         const int64_t tile_base = tt * a.xo_Kp * NTOK + ((f % 16) / 8 + (f / 16) * 2) * (8 * NTOK) + f % 8;
@@ -429,19 +429,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t v[16];
           tmem_ld16(lane_base + D_COL + db * NTOK + c16, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (quarter >= 2) {
+          // the u warp computes tokens 0-7 of the chunk, its v partner tokens 8-15: each hands
+          // the other half of its operand over (v: tokens 0-7 at +0, u: tokens 8-15 at +256)
+          const bool is_u = quarter < 2;  // warp-uniform: both branches index v[] statically
+          float* xb = xw + b * kXchFloats;
+          float own[8];
+          if (is_u) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) xw[b * kXchFloats + m * 32] = __uint_as_float(v[m]) * cs;
+            for (int m = 0; m < 8; ++m) {
+              xb[256 + m * 32] = __uint_as_float(v[8 + m]) * cs;
+              own[m] = __uint_as_float(v[m]) * cs;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+              xb[m * 32] = __uint_as_float(v[m]) * cs;
+              own[m] = __uint_as_float(v[8 + m]) * cs;
+            }
           }
           asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
-          if (quarter < 2 && keep) {
+          const int m0 = c16 + (is_u ? 0 : 8);
+          const float* src = xb + (is_u ? 0 : 256);
+          if (keep) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-              const int mm = c16 + m;
-              if (tt * NTOK + mm < a.M) {
-                const float u = __uint_as_float(v[m]) * cs, vv = xw[b * kXchFloats + m * 32];
+            for (int m = 0; m < 8; ++m) {
+              if (tt * NTOK + m0 + m < a.M) {
+                const float other = src[m * 32];
+                const float u = is_u ? own[m] : other, vv = is_u ? other : own[m];
                 const float o = 0.5f * u * (1.f + erff(u * 0.70710678118654752440f)) * vv * rs;
-                a.xo[tile_base + (mm / 8) * 64 + (mm % 8) * 8] = __float2half_rn(o);
+                a.xo[tile_base + ((m0 + m) / 8) * 64 + ((m0 + m) % 8) * 8] = __float2half_rn(o);
               }
             }
           }

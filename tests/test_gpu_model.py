@@ -363,3 +363,38 @@ def test_packed_prefill_isolates_samples_and_fills_their_caches():
     _, ld = m.decode_step([s["tokens"][-1] for s in samples], [s["positions"][-1] for s in samples])
     for b, (s, (ref, _, _, zero)) in enumerate(zip(samples, refs)):
         check_logits(ld[b:b + 1].astype(np.float64), ref[-1:], zero[-1:])
+
+
+_FUSED_GEGLU_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+from oracle import pyoracle as O
+from paper_2210_02414_b200 import glm
+p = O.Params(2, 256, 2, vocab=300, seed=5)
+m = glm.Model(glm.GLMConfig(num_layers=2, hidden=256, num_heads=2, vocab=300), bits=int(sys.argv[1]),
+              axis="column", max_batch=1, max_ctx=320)
+m.load_reference_params(lambda layer, slot: p.tensor(0, O.EMBED) if slot == "embed" else p.tensor(layer, slot))
+rng = np.random.default_rng(3)
+toks = [int(v) for v in rng.integers(6, 290, size=300)]
+np.save(sys.argv[2], m.prefill(toks, list(range(300)), 300))
+"""
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_fused_geglu_gemm_equals_unfused(bits, tmp_path):
+    """The W1|V GEMM with the GeGLU epilogue (qmm_tc.cu, PAIR) computes the same fp32
+    products, scales and erf-GeLU as the two GEMMs + k_geglu_act_tiles it replaces, so the
+    prefill logits are bit-identical with it switched off (GLM_QMM_GEGLU=0)."""
+    import os
+    import subprocess
+    import sys
+
+    outs = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"logits_{flag}.npy"
+        env = dict(os.environ, GLM_QMM_GEGLU=flag)
+        r = subprocess.run([sys.executable, "-c", _FUSED_GEGLU_SCRIPT, str(bits), str(f)], env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
