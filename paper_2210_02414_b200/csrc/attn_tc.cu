@@ -295,7 +295,22 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0u;
       }
-      if (i < n) {
+      if (i < n && a.xo.xf) {  // fp16 activation tiles of the out-proj (16-byte runs of 8 features)
+        const int64_t m = a.xrow0 + i;
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          const int64_t k = static_cast<int64_t>(head) * kUD + c + e;
+          uint32_t hx[4];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const float s0 = a.xo.row_scale ? a.xo.row_scale[k + j] : 1.f;
+            const float s1 = a.xo.row_scale ? a.xo.row_scale[k + j + 1] : 1.f;
+            const __half2 hv = __floats2half2_rn(__uint_as_float(v[e + j]) * inv * s0, __uint_as_float(v[e + j + 1]) * inv * s1);
+            hx[j / 2] = *reinterpret_cast<const uint32_t*>(&hv);
+          }
+          *reinterpret_cast<uint4*>(a.xo.xf + xtile_index(a.xo.Kp, m, k)) = make_uint4(hx[0], hx[1], hx[2], hx[3]);
+        }
+      } else if (i < n) {
         float* orow = a.out + static_cast<int64_t>(i) * a.ldout + head * kUD + c;
 #pragma unroll
         for (int e = 0; e < 32; e += 4)
@@ -407,9 +422,13 @@ CUtensorMap kv_tensor_map(const __half* base, const AttnPrefillArgs& a) {
 // flash kernel); V descriptor offsets overridable for bring-up (GLM_ATTN_VLBO / _VSBO; the
 // defaults were verified against the oracle: the MN-major V takes the N-half distance as
 // LBO and the 8-key stride as SBO).
-bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st) {
+bool attn_prefill_umma_eligible(int dh) {
   static const int on = [] { const char* e = getenv("GLM_ATTN_UMMA"); return e ? atoi(e) : 1; }();
-  if (!on || a.dh != kUD) return false;
+  return on && dh == kUD;
+}
+
+bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st) {
+  if (!attn_prefill_umma_eligible(a.dh)) return false;
   static const int vlbo = [] { const char* e = getenv("GLM_ATTN_VLBO"); return e ? atoi(e) : 16384; }();
   static const int vsbo = [] { const char* e = getenv("GLM_ATTN_VSBO"); return e ? atoi(e) : 1024; }();
   static bool attr = false;

@@ -1285,6 +1285,7 @@ void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
 
 void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st) {
   if (launch_attn_prefill_umma(a, st)) return;
+  if (a.xo.xf) fail(GLM_CONTRACT, "glmmodel", "activation-tile attention output needs the tcgen05 kernel");
   const dim3 grid((a.n + kFaRows - 1) / kFaRows, a.heads);
   auto go = [&](auto kernel, int dh) {
     const size_t smem = static_cast<size_t>(4 * kFaKeys) * (dh + 8) * sizeof(__half);

@@ -90,6 +90,10 @@ struct AttnPrefillArgs {
   int n, heads, dh, seq, max_ctx, context_len;
   float* out;               // [n][ldout]
   int64_t ldout;
+  // tcgen05 kernel only (attn_prefill_umma_eligible): write O straight into the out-proj's
+  // activation tiles at token rows xrow0 + i instead of the fp32 rows
+  XOut xo{};
+  int xrow0 = 0;
 };
 
 struct HeadArgs {
@@ -117,6 +121,7 @@ void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st);
 void launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t st);
 // tcgen05 prefill attention (attn_tc.cu): false if it does not take this call (head_dim != 128)
 bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st);
+bool attn_prefill_umma_eligible(int dh);
 void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st);
 void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st);
 void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st);

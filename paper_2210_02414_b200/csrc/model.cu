@@ -658,6 +658,7 @@ struct glm_model {
     }
     ensure_prefill(n);
     const int nt = n > 16 ? 1 : 0;  // activation layout of this prefill: tcgen05 tiles or x_frag
+    const bool attn_tiles = nt && attn_prefill_umma_eligible(dh);  // attention writes out-proj tiles
     if (taps) ensure_taps(n);
     DeviceBuffer dtok(n * 4), dpos(n * 4);
     CUDA_CHECK(cudaMemcpyAsync(dtok.ptr, tokens, n * 4, cudaMemcpyHostToDevice, st));
@@ -675,9 +676,13 @@ struct glm_model {
         launch_rope_store(rs, st);
         AttnPrefillArgs ap{qseg, kcache(l), vcache(l), ni, Hl, dh, seqs[i], max_ctx, ctx[i],
                            attn_out.as<float>() + static_cast<int64_t>(r0) * dl, dl};
+        if (attn_tiles) {
+          ap.xo = xout(xf_out.as<__half>(), out, nt);
+          ap.xrow0 = r0;
+        }
         launch_attn_prefill(ap, st);
       }
-      launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
+      if (!attn_tiles) launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
       linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
       if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
       LnArgs ln;
