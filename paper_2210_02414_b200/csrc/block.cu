@@ -310,6 +310,95 @@ __global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
   }
 }
 
+// 8 features per thread (two float4 per operand, one 16-byte activation-tile store): the
+// same two passes with a quarter of the memory instructions (hidden % 8 == 0, aligned rows).
+__device__ __forceinline__ void store_x8(const XOut& xo, int m, int64_t n, const float (&o)[8]) {
+  if (!xo.xf) return;
+  if (!xo.tile) {
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) store_xfrag_pair(xo, m, n + e, o[e], o[e + 1]);
+    return;
+  }
+  uint32_t hx[4];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    const float s0 = xo.row_scale ? xo.row_scale[n + e] : 1.f, s1 = xo.row_scale ? xo.row_scale[n + e + 1] : 1.f;
+    const __half2 hv = __floats2half2_rn(o[e] * s0, o[e + 1] * s1);
+    hx[e / 2] = *reinterpret_cast<const uint32_t*>(&hv);
+  }
+  *reinterpret_cast<uint4*>(xo.xf + xtile_index(xo.Kp, m, n)) = make_uint4(hx[0], hx[1], hx[2], hx[3]);
+}
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kLnRowThreads, MINB) k_deepnorm_ln_rows8(LnArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float2 red[kLnRowThreads / 32];
+  const int m = blockIdx.x;
+  const int64_t nv = a.d / 8;
+  float* hrow = a.h + static_cast<int64_t>(m) * a.d;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int64_t p = threadIdx.x; p < nv; p += kLnRowThreads) {
+    const int64_t n = 8 * p;
+    float y[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (!a.zero_sublayer) {
+      for (int s = 0; s < a.in.ksplit; ++s) {
+        float v[8];
+        ld8(a.in.p + static_cast<int64_t>(s) * a.in.split_stride + m * a.in.ld + n, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] += v[e];
+      }
+      if (a.in.scale)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] *= a.in.scale[n + e];
+    }
+    if (a.tap) st8(a.tap + static_cast<int64_t>(m) * a.d + n, y);
+    float z[8];
+    ld8(hrow + n, z);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      z[e] = a.alpha * z[e] + y[e];
+      acc.x += z[e];
+      acc.y += z[e] * z[e];
+    }
+    st8(hrow + n, z);
+  }
+  acc.x = warp_sum(acc.x);
+  acc.y = warp_sum(acc.y);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = acc;
+  __syncthreads();
+  float2 tot = make_float2(0.f, 0.f);
+  for (int i = 0; i < kLnRowThreads / 32; ++i) {
+    tot.x += red[i].x;
+    tot.y += red[i].y;
+  }
+  const float inv_d = 1.f / static_cast<float>(a.d);
+  const float mean = tot.x * inv_d;
+  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);  // biased (tensor.cpp:267)
+  const float rstd = rsqrtf(var + a.eps);
+  for (int64_t p = threadIdx.x; p < nv; p += kLnRowThreads) {
+    const int64_t n = 8 * p;
+    float z[8], g[8], b[8];
+    ld8(hrow + n, z);
+    ld8(a.gain + n, g);
+    ld8(a.bias + n, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) z[e] = (z[e] - mean) * rstd * g[e] + b[e];
+    st8(hrow + n, z);
+    store_x8(a.x0, m, n, z);
+    store_x8(a.x1, m, n, z);
+  }
+}
+
 // ---- GeGLU activation: gelu(x W1) * (x V) (model.cpp:133-135, tensor.cpp:313-318) --------
 __device__ __forceinline__ float2 reduce_partial2(const SubIn& in, int m, int64_t n) {
   float2 acc = make_float2(0.f, 0.f);
@@ -1217,7 +1306,15 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
 
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   if (a.d > 2ll * kLnPairs * kLnThreads * kLnCluster || a.d % 2) fail(GLM_DIMENSION, "glmmodel", "hidden unsupported by LN kernel");
-  if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
+  const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool v8 = a.d % 8 == 0 && a.in.ld % 4 == 0 && a.in.split_stride % 4 == 0 && al(a.in.p) && al(a.h) &&
+                  al(a.gain) && al(a.bias) && al(a.tap);
+  static const bool rows8 = [] { const char* e = getenv("GLM_LN_ROWS8"); return !e || e[0] != '0'; }();
+  // 3 resident 512-thread CTAs per SM (40 registers): the row's two passes are latency-bound,
+  // so occupancy sets the bandwidth (ncu, 8192 x 12288: 1 CTA/SM 487/403 us, 2: 328, 3: 341/263,
+  // 4 spills: 440/361)
+  if (M > 16 && v8 && rows8) launch_k(k_deepnorm_ln_rows8<3>, dim3(M), dim3(kLnRowThreads), 0, st, a);
+  else if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
   LAUNCH_CHECK("k_deepnorm_ln");
 }
