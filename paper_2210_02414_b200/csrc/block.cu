@@ -833,6 +833,29 @@ __global__ void k_rope_store(RopeStoreArgs a) {
   }
 }
 
+// head_dim 128: one warp per (row, head), a lane owns 4 features (two rotation pairs) of q,
+// k and v (16-byte loads, 8-byte cache stores), 8 heads per 256-thread CTA.
+__global__ void k_rope_store128(RopeStoreArgs a) {
+  const int i = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (head >= a.heads) return;
+  const int pos = a.positions[i];
+  const float4 cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(pos) * 64)[lane];  // pairs 2l, 2l+1
+  const float* row = a.qkv + static_cast<int64_t>(i) * a.ldqkv + static_cast<int64_t>(head) * 128 + 4 * lane;
+  const float4 q = *reinterpret_cast<const float4*>(row);
+  const float4 k = *reinterpret_cast<const float4*>(row + a.d_local);
+  const float4 v = *reinterpret_cast<const float4*>(row + 2 * a.d_local);
+  *reinterpret_cast<float4*>(a.q + (static_cast<int64_t>(head) * a.n + i) * 128 + 4 * lane) =
+      make_float4(cs.x * q.x - cs.y * q.y, cs.y * q.x + cs.x * q.y, cs.z * q.z - cs.w * q.w, cs.w * q.z + cs.z * q.w);
+  const int64_t c_off = ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx + a.slot0 + i) * 128 + 4 * lane;
+  const __half2 k0 = __floats2half2_rn(cs.x * k.x - cs.y * k.y, cs.y * k.x + cs.x * k.y);
+  const __half2 k1 = __floats2half2_rn(cs.z * k.z - cs.w * k.w, cs.w * k.z + cs.z * k.w);
+  const __half2 v0 = __floats2half2_rn(v.x, v.y), v1 = __floats2half2_rn(v.z, v.w);
+  *reinterpret_cast<uint2*>(a.kcache + c_off) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&k0), *reinterpret_cast<const uint32_t*>(&k1));
+  *reinterpret_cast<uint2*>(a.vcache + c_off) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&v0), *reinterpret_cast<const uint32_t*>(&v1));
+}
+
 // Tensor-core flash attention for prefill (FA2 schedule on mma.sync.m16n8k16, fp16 in,
 // fp32 accumulate): a CTA owns 64 query rows of one head (16 per warp), streams 64-key
 // blocks of K and V through double-buffered shared memory (cp.async), keeps S = Q K^T,
@@ -1376,6 +1399,13 @@ void launch_advance(int* cache_len, int B, cudaStream_t st) {
 }
 
 void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
+  const bool al = a.ldqkv % 4 == 0 && a.d_local % 4 == 0 && (reinterpret_cast<uintptr_t>(a.qkv) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(a.rope) & 15) == 0;
+  if (a.dh == 128 && al) {
+    k_rope_store128<<<dim3(a.n, (a.heads + 7) / 8), 256, 0, st>>>(a);
+    LAUNCH_CHECK("k_rope_store128");
+    return;
+  }
   k_rope_store<<<dim3(a.n, a.heads), 64, 0, st>>>(a);
   LAUNCH_CHECK("k_rope_store");
 }
