@@ -148,6 +148,25 @@ __device__ __forceinline__ void ub_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
 }
 
+// sm_100 three-input max and packed fp32-pair add / subtract (FMNMX3, FADD2)
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float2 add2f(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 sub2f(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillArgs a, int v_lbo, int v_sbo,
                                                                     const __grid_constant__ CUtensorMap kmap,
                                                                     const __grid_constant__ CUtensorMap vmap) {
@@ -230,14 +249,17 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
         for (int c = 0; c < kUK; ++c)
           if (j0 + c >= lim) sv[c] = -INFINITY;
       }
+      // row max: 8 chains of three-input max (FMNMX3), half the instructions of fmaxf
       float bm8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) bm8[u] = sv[u];
 #pragma unroll
-      for (int c = 8; c < kUK; ++c) bm8[c & 7] = fmaxf(bm8[c & 7], sv[c]);
+      for (int c = 8; c + 16 <= kUK; c += 16)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) bm8[u] = fmaxf(bm8[u], bm8[u + 4]);
-      const float bm = fmaxf(fmaxf(bm8[0], bm8[1]), fmaxf(bm8[2], bm8[3]));
+        for (int u = 0; u < 8; ++u) bm8[u] = max3f(bm8[u], sv[c + u], sv[c + 8 + u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) bm8[u] = fmaxf(bm8[u], sv[kUK - 8 + u]);
+      const float bm = max3f(max3f(bm8[0], bm8[1], bm8[2]), max3f(bm8[3], bm8[4], bm8[5]), fmaxf(bm8[6], bm8[7]));
       // lazy max: the exponent reference moves only when a score exceeds it by more than
       // 8 (P <= 2^8 stays exact enough in fp16, l and O accumulate in fp32), so O needs a
       // rescale in TMEM only rarely after the first blocks
@@ -245,16 +267,21 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       const float ms = mn == -INFINITY ? 0.f : mn;  // row with nothing visible yet: p = 0
       const float corr = ex2(m - ms);
       l *= corr;
+      // exponent arguments and the row sum on packed fp32 pairs (FADD2): one instruction per
+      // two scores instead of two
       uint32_t pw[kUK / 2];
-      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 ms2 = make_float2(ms, ms);
 #pragma unroll
       for (int c = 0; c < kUK; c += 2) {
-        const float p0 = ex2(sv[c] - ms), p1 = ex2(sv[c + 1] - ms);
-        ls[(c >> 1) & 7] += p0 + p1;
+        const float2 x = sub2f(make_float2(sv[c], sv[c + 1]), ms2);
+        const float p0 = ex2(x.x), p1 = ex2(x.y);
+        ls[(c >> 1) & 3] = add2f(ls[(c >> 1) & 3], make_float2(p0, p1));
         const __half2 hv = __floats2half2_rn(p0, p1);
         pw[c / 2] = *reinterpret_cast<const uint32_t*>(&hv);
       }
-      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+      const float2 ls01 = add2f(ls[0], ls[1]), ls23 = add2f(ls[2], ls[3]), lsum = add2f(ls01, ls23);
+      l += lsum.x + lsum.y;
       if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O_t rescale (P.V_t(j - 1) is complete)
 #pragma unroll
         for (int h = 0; h < kUD; h += 64) {
