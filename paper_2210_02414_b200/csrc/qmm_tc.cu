@@ -92,18 +92,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // by one tensor-map copy with the 64 B swizzle, so that the transcode threads' 16-byte reads
 // (lane g reads 16 B of each 64 B row g) hit 8 distinct bank groups.
 template <int BITS>
-__device__ __forceinline__ void tma_codes(void* dst, const CUtensorMap* map, int c, int rt16, uint64_t* bar) {
+__device__ __forceinline__ void tma_codes(void* dst, const CUtensorMap* map, int c, int rt16, uint64_t* bar,
+                                          uint64_t pol) {
   if constexpr (BITS == 4) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(
             smem_u32(dst)),
-        "l"(map), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar))
+        "l"(map), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
   } else {
     asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(
             smem_u32(dst)),
-        "l"(map), "r"(0), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar))
+        "l"(map), "r"(0), "r"(0), "r"(0), "r"(c), "r"(rt16), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
   }
 }
@@ -164,6 +165,8 @@ struct QmmArgs {
   int64_t ldo, N;
   int64_t nrt16, nch, Np, Kp;
   int M, ksplit, ntt, nrt128;
+  int tokgroup;  // token tiles walked together (their activations stay L2-resident)
+  int wevict;    // weight copies with an L2 evict_first hint
   long long* trace;
 };
 __device__ __forceinline__ void stamp(const QmmArgs& a, int ev, uint32_t q) {
@@ -172,12 +175,12 @@ __device__ __forceinline__ void stamp(const QmmArgs& a, int ev, uint32_t q) {
 
 // item -> (128-feature tile, token tile, k split); token tiles innermost so the CTAs working
 // at the same time share a few weight row tiles (L2-resident), stages = 64-k chunks.
-// Token tiles are walked in groups of kTokGroup (2048 tokens = 50 MB of activations at
+// Token tiles are walked in groups of a.tokgroup (qmm_token_group: 4 x 256 tokens = 25 MB of activations at
 // K = 12288) so that a group's activations stay L2-resident while every row tile passes
 // over them; a packed prefill of many samples would otherwise re-read them from HBM.
-constexpr int64_t kTokGroup = 16;
 __device__ __forceinline__ void decode_item(const QmmArgs& a, int64_t item, int64_t& rt, int64_t& tt, int& s,
                                             int64_t& c0, int64_t& c1) {
+  const int64_t kTokGroup = a.tokgroup;
   s = static_cast<int>(item % a.ksplit);
   int64_t rest = item / a.ksplit;
   const int64_t full = a.ntt / kTokGroup;              // complete token groups
@@ -324,6 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kTcWarps + 2) {
     // ---------------- TMA producer: weight codes, one 64-k chunk of 128 features per stage ------
     if (lane == 0) {
+      // weights are re-read by the G token tiles of a group close together in time; evict_first
+      // (GLM_QMM_WEVICT=1) lets the group's activations keep their L2 lines instead
+      uint64_t pol;
+      if (a.wevict) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
       uint32_t q = 0;
       for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int64_t rt, tt, c0, c1;
@@ -335,12 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(wfull + ws, WB);
           if constexpr (PAIR) {  // 4 row tiles of W1, then the same 4 of V
             tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 4),
-                            wfull + ws);
+                            wfull + ws, pol);
             tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB + WB / 2, &vmap, static_cast<int>(c),
-                            static_cast<int>(rt * 4), wfull + ws);
+                            static_cast<int>(rt * 4), wfull + ws, pol);
           } else {
             tma_codes<BITS>(wring + static_cast<size_t>(ws) * WB, &wmap, static_cast<int>(c), static_cast<int>(rt * 8),
-                            wfull + ws);
+                            wfull + ws, pol);
           }
         }
       }
@@ -572,6 +580,23 @@ CUtensorMap codes_tensor_map(const QWeightDev& w, int box_rt = 8) {
   return m;
 }
 
+// Token tiles per group (GLM_QMM_TOKGROUP overrides). The SMs hold ~148 items at once, so a
+// group of G token tiles spans 148 / G row tiles per wave: activations are read once while the
+// group's G x 256 x K fp16 tiles stay in L2, weights once per group. Config 3 (8192 tokens,
+// ncu DRAM reads per block): G = 16 (100 MB of activations at K = 12288) thrashes L2 —
+// 6.8 + 2.3 + 11.9 + 6.3 GB, 23.8 ms; G = 4: 2.3 + 1.0 + 3.5 + 3.5 GB, 22.5 ms (lower DRAM
+// traffic also buys SM clock under the power cap: 1.44 -> 1.49 GHz in the qkv GEMM).
+int qmm_token_group(int64_t Kp) {
+  static const int g = [] { const char* e = getenv("GLM_QMM_TOKGROUP"); return e ? atoi(e) : 4; }();
+  (void)Kp;
+  return g < 1 ? 1 : g;
+}
+
+int qmm_weight_evict_first() {
+  static const int v = [] { const char* e = getenv("GLM_QMM_WEVICT"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 template <int BITS, bool PAIR>
 void launch_qmm(const QmmArgs& a, int grid, const CUtensorMap& wmap, const CUtensorMap& vmap, cudaStream_t st) {
   static bool attr = false;
@@ -629,6 +654,8 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
   a.ksplit = p.ksplit;
   a.ntt = (M + NTOK - 1) / NTOK;
   a.nrt128 = static_cast<int>(w.L.Np / 128);
+  a.tokgroup = qmm_token_group(w.L.Kp);
+  a.wevict = qmm_weight_evict_first();
   a.trace = nullptr;
   static long long* trace_buf = nullptr;
   if (getenv("GLM_QMM_TRACE")) {
@@ -671,6 +698,8 @@ void qmm_geglu_launch(const QWeightDev& w1, const QWeightDev& v, const __half* x
   a.ksplit = 1;
   a.ntt = (M + NTOK - 1) / NTOK;
   a.nrt128 = static_cast<int>(w1.L.Np / 64);  // 64-feature blocks of the pair
+  a.tokgroup = qmm_token_group(w1.L.Kp);
+  a.wevict = qmm_weight_evict_first();
   a.trace = nullptr;
   const int64_t items = static_cast<int64_t>(a.nrt128) * a.ntt;
   const int grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
