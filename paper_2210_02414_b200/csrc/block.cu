@@ -1316,7 +1316,7 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
                   cudaStream_t st) {
   if (xo.tile && d % 8 == 0) {
     const int64_t warps = (M + kXTileTokens - 1) / kXTileTokens * (d / 8) * (kXTileTokens / 32);
-    const dim3 grid(grid_for(warps * 32, 256));
+    const dim3 grid(grid_for(warps * 32, 256, 1 << 30));  // one pass per warp: the row-id -> row load chain is latency-bound
     if (bf16) launch_k(k_embed_tiles<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
     else launch_k(k_embed_tiles<float>, grid, dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
     LAUNCH_CHECK("k_embed_tiles");
