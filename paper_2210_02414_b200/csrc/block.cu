@@ -835,15 +835,23 @@ __global__ void k_rope_store(RopeStoreArgs a) {
 
 // head_dim 128: one warp per (row, head), a lane owns 4 features (two rotation pairs) of q,
 // k and v (16-byte loads, 8-byte cache stores), 8 heads per 256-thread CTA.
-__global__ void k_rope_store128(RopeStoreArgs a) {
+__device__ __forceinline__ float4 ld4f(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4f(const __half* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+template <typename T>
+__global__ void k_rope_store128(RopeStoreArgs a, const T* __restrict__ qkv) {
   const int i = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (head >= a.heads) return;
   const int pos = a.positions[i];
   const float4 cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(pos) * 64)[lane];  // pairs 2l, 2l+1
-  const float* row = a.qkv + static_cast<int64_t>(i) * a.ldqkv + static_cast<int64_t>(head) * 128 + 4 * lane;
-  const float4 q = *reinterpret_cast<const float4*>(row);
-  const float4 k = *reinterpret_cast<const float4*>(row + a.d_local);
-  const float4 v = *reinterpret_cast<const float4*>(row + 2 * a.d_local);
+  const T* row = qkv + static_cast<int64_t>(i) * a.ldqkv + static_cast<int64_t>(head) * 128 + 4 * lane;
+  const float4 q = ld4f(row);
+  const float4 k = ld4f(row + a.d_local);
+  const float4 v = ld4f(row + 2 * a.d_local);
   *reinterpret_cast<float4*>(a.q + (static_cast<int64_t>(head) * a.n + i) * 128 + 4 * lane) =
       make_float4(cs.x * q.x - cs.y * q.y, cs.y * q.x + cs.x * q.y, cs.z * q.z - cs.w * q.w, cs.w * q.z + cs.z * q.w);
   const int64_t c_off = ((static_cast<int64_t>(a.seq) * a.heads + head) * a.max_ctx + a.slot0 + i) * 128 + 4 * lane;
@@ -1401,8 +1409,15 @@ void launch_advance(int* cache_len, int B, cudaStream_t st) {
 void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st) {
   const bool al = a.ldqkv % 4 == 0 && a.d_local % 4 == 0 && (reinterpret_cast<uintptr_t>(a.qkv) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(a.rope) & 15) == 0;
+  if (a.qkv_h) {
+    if (a.dh != 128 || a.ldqkv % 4 || a.d_local % 4 || (reinterpret_cast<uintptr_t>(a.qkv_h) & 7))
+      fail(GLM_CONTRACT, "glmmodel", "fp16 qkv rows need head_dim 128 and 8-byte aligned rows");
+    k_rope_store128<__half><<<dim3(a.n, (a.heads + 7) / 8), 256, 0, st>>>(a, a.qkv_h);
+    LAUNCH_CHECK("k_rope_store128");
+    return;
+  }
   if (a.dh == 128 && al) {
-    k_rope_store128<<<dim3(a.n, (a.heads + 7) / 8), 256, 0, st>>>(a);
+    k_rope_store128<float><<<dim3(a.n, (a.heads + 7) / 8), 256, 0, st>>>(a, a.qkv);
     LAUNCH_CHECK("k_rope_store128");
     return;
   }

@@ -82,6 +82,7 @@ struct RopeStoreArgs {
   const float2* rope;
   float* q;                 // [heads][n][dh] rotated q
   __half *kcache, *vcache;
+  const __half* qkv_h = nullptr;  // fp16 rows instead of qkv (prefill GEMM output, head_dim 128)
 };
 
 struct AttnPrefillArgs {

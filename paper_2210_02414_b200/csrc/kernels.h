@@ -95,7 +95,7 @@ inline int xtile_tokens(int M) { return (M + kQmmTokens - 1) / kQmmTokens * kQmm
 GemvPlan plan_qmm(const QLayout& L, int M);
 // y (optional, ksplit == 1): write the scaled result y[M][ldy] directly instead of partials
 void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
-                float* y = nullptr, int64_t ldy = 0, const float* zt = nullptr);
+                float* y = nullptr, int64_t ldy = 0, const float* zt = nullptr, bool y_half = false);
 // Fused W1|V GEMM + GeGLU (prefill): xo (W2's activation tiles, Kp = xo_Kp, kRow fold xo_rs
 // or null) = fp16(gelu(x.W1 * s1) * (x.V * s2)) for absmax W1 / V of one shape sharing x.
 bool qmm_geglu_supported(const QWeightDev& w1, const QWeightDev& v, int M);

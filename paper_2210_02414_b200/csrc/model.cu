@@ -667,12 +667,23 @@ struct glm_model {
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
       Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
-      linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
+      // qkv rows in fp16 straight from the tcgen05 epilogue when RoPE / the KV cache are the only
+      // readers (head_dim 128, unsplit K): half the bytes written and re-read
+      bool qkv_half = false;
+      if (nt && dh == 128) {
+        const GemvPlan pq = plan_qmm(qkv.w.L, n);
+        if (pq.ksplit == 1) {
+          qmm_launch(qkv.w, xf_qkv.as<__half>(), n, partial.as<float>(), pq, st, y_qkv.as<float>(), qkv.w.L.N, nullptr, true);
+          qkv_half = true;
+        }
+      }
+      if (!qkv_half) linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
       for (int i = 0; i < nseg; ++i) {
         const int r0 = row0[i], ni = lens[i];
         float* qseg = q_rot.as<float>() + static_cast<int64_t>(r0) * dl;  // [heads][ni][dh] of this sample
         RopeStoreArgs rs{y_qkv.as<float>() + static_cast<int64_t>(r0) * 3 * dl, 3ll * dl, dl, ni, Hl, dh, seqs[i],
                          max_ctx, 0, dpos.as<int>() + r0, rope, qseg, kcache(l), vcache(l)};
+        if (qkv_half) rs.qkv_h = reinterpret_cast<const __half*>(y_qkv.as<float>()) + static_cast<int64_t>(r0) * 3 * dl;
         launch_rope_store(rs, st);
         AttnPrefillArgs ap{qseg, kcache(l), vcache(l), ni, Hl, dh, seqs[i], max_ctx, ctx[i],
                            attn_out.as<float>() + static_cast<int64_t>(r0) * dl, dl};

@@ -166,6 +166,7 @@ struct QmmArgs {
   int64_t nrt16, nch, Np, Kp;
   int M, ksplit, ntt, nrt128;
   int tokgroup;  // token tiles walked together (their activations stay L2-resident)
+  int out_half;  // direct output as fp16 (prefill qkv feeding RoPE / the KV cache)
   int wevict;    // weight copies with an L2 evict_first hint
   long long* trace;
 };
@@ -492,8 +493,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             const int64_t tok = tt * NTOK + c16 + m;
-            if (tok < a.M && keep) out[tok * ld] = zv != 0.f ? __uint_as_float(v[m]) * cs + a.zt[tok] * zv
-                                                             : __uint_as_float(v[m]) * cs;
+            if (tok < a.M && keep) {
+              const float y = zv != 0.f ? __uint_as_float(v[m]) * cs + a.zt[tok] * zv : __uint_as_float(v[m]) * cs;
+              if (a.out_half) reinterpret_cast<__half*>(a.partial)[tok * ld + col] = __float2half_rn(y);
+              else out[tok * ld] = y;
+            }
           }
         }
         tc_fence_before();
@@ -633,7 +637,8 @@ GemvPlan plan_qmm(const QLayout& L, int M) {
 }
 
 void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, const GemvPlan& p, cudaStream_t st,
-                float* y, int64_t ldy, const float* zt) {
+                float* y, int64_t ldy, const float* zt, bool y_half) {
+  if (y_half && !y) fail(GLM_CONTRACT, "qlinear", "fp16 output needs the direct (unsplit) mode");
   if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
   if (w.L.Np % 128 || w.L.Kp % 64) fail(GLM_DIMENSION, "qlinear", "layout not padded for the tcgen05 path");
   if (y && p.ksplit != 1) fail(GLM_CONTRACT, "qlinear", "direct output needs an unsplit K");
@@ -656,6 +661,7 @@ void qmm_launch(const QWeightDev& w, const __half* xt, int M, float* partial, co
   a.nrt128 = static_cast<int>(w.L.Np / 128);
   a.tokgroup = qmm_token_group(w.L.Kp);
   a.wevict = qmm_weight_evict_first();
+  a.out_half = y_half ? 1 : 0;
   a.trace = nullptr;
   static long long* trace_buf = nullptr;
   if (getenv("GLM_QMM_TRACE")) {
