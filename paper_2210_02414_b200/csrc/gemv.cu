@@ -733,6 +733,288 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_m1(GemvArgs a, int
 }
 
 
+// ---- integer-MMA single-token variant (INT4, 1..4 tokens: batch-1 decode, the headline) ----
+// The fp16 path above spends ~17 of the ~21 issue cycles a 256-weight HMMA may take at the
+// HBM rate on the transcode (4 LOP3 + IMAD.HI) and the HMMA dispatch, so it is bound by the
+// SM issue rate and the clock, not by HBM. This kernel feeds the codes to the tensor core as
+// integers: mma.sync m16n8k32 u8 x s8 -> s32 (IMMA.16832, 512 weights per instruction at
+// the HMMA instruction rate, tools/imma_probe.cu) with the weight bytes taken straight from
+// the fragment-ordered layout: each byte of a lane's word holds (row g, row g + 8) at one k,
+// so `w & 0x0F0F0F0F` is row g's A register (code + 8) and `w & 0xF0F0F0F0` row g + 8's
+// (16 (code + 8)), one LOP3 each and no shift: 8 LOP3 + 2 IMMA per 1024 weights.
+//
+// The activations become exact integers: per token vector, x_int = rint(x / s_x) with
+// s_x = max|x| / 32512 (16-bit fixed point; the fp16 input has 11 significant bits, so the
+// added error is <= max|x| / 65024 per element), split into balanced base-256 digits
+// x_int = 256 hi + lo (hi, lo signed bytes). MMA column 2m holds token m's hi digits and
+// column 2m + 1 its lo digits, so lane (g, t) ends with token t's two digit sums for rows g and
+// g + 8. Every product and sum is exact integer arithmetic (|acc| < 2^31 for K <= 32768);
+// the code offsets leave with the integer digit sums of the slice, and the only rounding left
+// is the final fp32 scale: results are bit-reproducible and independent of summation order.
+// The conversion runs once per CTA in place in shared memory after the activation bulk copy:
+// [v][m][chunk][t][32 B] of fp16 fragments -> [.. 16 B hi digits | 16 B lo digits] in the byte
+// order of the lane's weight words (k = 16 j + {2t, 2t + 8, 2t + 1, 2t + 9}).
+__device__ __forceinline__ void imma16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void compute_chunk_i4(const uint4& wv, const uint4& xv, int (&acc0)[4], int (&acc1)[4]) {
+  imma16832(acc0, wv.x & 0x0F0F0F0Fu, wv.x & 0xF0F0F0F0u, wv.y & 0x0F0F0F0Fu, wv.y & 0xF0F0F0F0u, xv.x, xv.y);
+  imma16832(acc1, wv.z & 0x0F0F0F0Fu, wv.z & 0xF0F0F0F0u, wv.w & 0x0F0F0F0Fu, wv.w & 0xF0F0F0F0u, xv.z, xv.w);
+}
+
+constexpr float kDigitQ = 32512.f;  // 127 * 256: keeps the balanced hi digit in [-127, 127]
+
+// One 16-k group of fragment-ordered fp16 activations (32 B, halves [j][2t, 2t+1, 2t+8, 2t+9])
+// -> 16 hi digits | 16 lo digits in weight-word byte order ([j][2t, 2t+8, 2t+1, 2t+9]); returns
+// the digit sums (hi, lo) of the group.
+__device__ __forceinline__ int2 digits_group(uint4* p, float inv_s) {
+  const uint4 h0 = p[0], h1 = p[1];
+  const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  uint32_t hi[4], lo[4];
+  int shi = 0, slo = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    // halves of k-tile j: q = 0: 2t, 1: 2t+1 (word 2j), 2: 2t+8, 3: 2t+9 (word 2j+1)
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j]));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j + 1]));
+    const float fq[4] = {f01.x, f23.x, f01.y, f23.y};  // byte order 2t, 2t+8, 2t+1, 2t+9
+    uint32_t bh = 0, bl = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int xi = __float2int_rn(fq[q] * inv_s);
+      const int l = ((xi + 128) & 255) - 128;
+      const int h = (xi - l) >> 8;
+      shi += h;
+      slo += l;
+      bh |= (static_cast<uint32_t>(h) & 255u) << (8 * q);
+      bl |= (static_cast<uint32_t>(l) & 255u) << (8 * q);
+    }
+    hi[j] = bh;
+    lo[j] = bl;
+  }
+  p[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  p[1] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  return make_int2(shi, slo);
+}
+
+template <int NST, int SB, int MT>
+__global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int nx, int early) {
+  trace_point(10);
+  constexpr int CHUNK = 512;
+  constexpr int U = SB / CHUNK;  // chunks per stage
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = static_cast<int>(a.nch), ksplit = a.ksplit;
+  const int xbytes = nch * 128;    // one token: Kp halves (fp16) = Kp digit pairs (int8 x 2)
+  const int vbytes = MT * xbytes;  // one activation vector set: [MT tokens][chunks][128 B]
+  uint8_t* ring = smem + static_cast<size_t>(warp) * NST * SB;
+  uint8_t* xs = smem + static_cast<size_t>(nw) * NST * SB;
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * vbytes);
+  uint64_t* bars = xbar + 1 + warp * NST;
+  int2* dsum = reinterpret_cast<int2*>(xbar + 1 + nw * NST);  // [v][m][chunk] digit sums
+  float* sx = reinterpret_cast<float*>(dsum + nx * MT * nch);   // [v * MT + m]: s_x
+  float* isx = sx + 8;                                           // [v * MT + m]: 1 / s_x
+  float* wmax = isx + 8;                                         // [warps][v * MT + m]
+  if (lane == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
+    if (warp == 0) mbar_init(xbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t policy, keep;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+
+  const int nitems = static_cast<int>(a.nrt) * ksplit;
+  const int wstride = static_cast<int>(gridDim.x) * nw;
+  const int first = static_cast<int>(blockIdx.x) * nw + warp;
+  auto decode = [&](int item, int& rt, int& s, int& c0, int& c1) {
+    rt = item / ksplit;
+    s = item - rt * ksplit;
+    c0 = nch * s / ksplit;
+    c1 = nch * (s + 1) / ksplit;
+  };
+  int pi = first, prt = 0, ps = 0, pc = 0, pc1 = 0, pslot = 0;
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  if (pi < nitems) decode(pi, prt, ps, pc, pc1);
+  auto issue = [&]() {
+    if (pi >= nitems) return;
+    const int n = min(U, pc1 - pc);
+    const uint8_t* src = wbase + (static_cast<int64_t>(prt) * nch + pc) * CHUNK;
+    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(n * CHUNK));
+    bulk_g2s(ring + pslot * SB, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    pslot = pslot + 1 == NST ? 0 : pslot + 1;
+    pc += n;
+    if (pc >= pc1) {
+      pi += wstride;
+      if (pi < nitems) decode(pi, prt, ps, pc, pc1);
+    }
+  };
+  if (lane == 0)
+    for (int s = 0; s < early && s < NST; ++s) issue();
+  pdl_wait();
+  pdl_trigger();
+  trace_point(11);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(xbar, static_cast<uint32_t>(nx * vbytes));
+    for (int v = 0; v < nx; ++v) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2);
+      for (int o = 0; o < vbytes; o += 16384) {
+        const uint32_t nb = static_cast<uint32_t>(min(16384, vbytes - o));
+        bulk_g2s(xs + v * vbytes + o, src + o, nb, xbar, keep);
+      }
+    }
+  }
+  if (lane == 0)
+    for (int s = early; s < NST; ++s) issue();
+  mbar_wait(xbar, 0);
+  // (1) max |x| per activation vector (v, m): 16-byte units, [vm][chunk][8 units]
+  const int nvm = nx * MT;
+  const int upv = nch * 8;
+  {
+    float mx[2 * MT];
+#pragma unroll
+    for (int i = 0; i < 2 * MT; ++i) mx[i] = 0.f;
+    for (int i = threadIdx.x; i < nvm * upv; i += blockDim.x) {
+      const uint4 v = reinterpret_cast<const uint4*>(xs)[i];
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+      __half2 m2 = __habs2(*reinterpret_cast<const __half2*>(&wd[0]));
+#pragma unroll
+      for (int e = 1; e < 4; ++e) m2 = __hmax2_nan(m2, __habs2(*reinterpret_cast<const __half2*>(&wd[e])));
+      const float2 f = __half22float2(m2);
+      float m = fmaxf(f.x, f.y);
+      if (f.x != f.x || f.y != f.y) m = __int_as_float(0x7fc00000);
+      const int vm = i / upv;
+#pragma unroll
+      for (int q = 0; q < 2 * MT; ++q)
+        if (q == vm) mx[q] = (m != m || mx[q] != mx[q]) ? __int_as_float(0x7fc00000) : fmaxf(mx[q], m);
+    }
+#pragma unroll
+    for (int q = 0; q < 2 * MT; ++q) {
+      float m = mx[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float r = __shfl_xor_sync(0xffffffffu, m, o);
+        m = (m != m || r != r) ? __int_as_float(0x7fc00000) : fmaxf(m, r);
+      }
+      if (lane == 0 && q < nvm) wmax[warp * 8 + q] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x < nvm) {
+      float m = 0.f;
+      for (int w = 0; w < nw; ++w) {
+        const float r = wmax[w * 8 + threadIdx.x];
+        m = (m != m || r != r) ? __int_as_float(0x7fc00000) : fmaxf(m, r);
+      }
+      // non-finite activations propagate as NaN results (the fp16 path would produce inf/NaN)
+      sx[threadIdx.x] = (m == 0.f) ? 0.f : (isfinite(m) ? m / kDigitQ : __int_as_float(0x7fc00000));
+      isx[threadIdx.x] = (m > 0.f && isfinite(m)) ? kDigitQ / m : 0.f;
+    }
+    __syncthreads();
+  }
+  // (2) in-place conversion to digits, 32-byte groups [vm][chunk][t]; chunk digit sums
+  {
+    const int ngroups = nvm * nch * 4;
+    for (int i0 = 0; i0 < ngroups; i0 += blockDim.x) {  // warp-uniform trip count
+      const int i = i0 + threadIdx.x;
+      int2 sm = make_int2(0, 0);
+      if (i < ngroups) sm = digits_group(reinterpret_cast<uint4*>(xs) + 2 * i, isx[i / (nch * 4)]);
+      sm.x += __shfl_xor_sync(0xffffffffu, sm.x, 1);
+      sm.y += __shfl_xor_sync(0xffffffffu, sm.y, 1);
+      sm.x += __shfl_xor_sync(0xffffffffu, sm.x, 2);
+      sm.y += __shfl_xor_sync(0xffffffffu, sm.y, 2);
+      if ((i & 3) == 0 && i < ngroups) dsum[i >> 2] = sm;
+    }
+    __syncthreads();
+  }
+  trace_point(12);
+
+  // B fragments: column g = digit (g & 1) of token min(g >> 1, MT - 1)
+  const uint8_t* xs0 = xs + min(g >> 1, MT - 1) * xbytes + t * 32 + (g & 1) * 16;
+  const uint8_t* xs1 = xs0 + (nx - 1) * vbytes;
+  const int64_t rt_split = a.rt_split;
+  int cslot = 0;
+  uint32_t cpar = 0;
+  for (int item = first; item < nitems; item += wstride) {
+    int rt, s, c0, c1;
+    decode(item, rt, s, c0, c1);
+    const int v = rt < rt_split ? 0 : nx - 1;
+    const uint8_t* xc = (v == 0 ? xs0 : xs1) + c0 * 128;
+    int acc[4][4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[h][i] = 0;
+    for (int c = c0; c < c1; c += U) {
+      const int n = min(U, c1 - c);
+      mbar_wait(bars + cslot, cpar);
+      const uint8_t* st = ring + cslot * SB + lane * 16;
+      if (n == U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint4 wv = *reinterpret_cast<const uint4*>(st + u * CHUNK);
+          const uint4 xv = *reinterpret_cast<const uint4*>(xc + u * 128);
+          compute_chunk_i4(wv, xv, acc[2 * (u & 1)], acc[2 * (u & 1) + 1]);
+        }
+      } else {
+        for (int u = 0; u < n; ++u) {
+          const uint4 wv = *reinterpret_cast<const uint4*>(st + u * CHUNK);
+          const uint4 xv = *reinterpret_cast<const uint4*>(xc + u * 128);
+          compute_chunk_i4(wv, xv, acc[0], acc[1]);
+        }
+      }
+      xc += U * 128;
+      __syncwarp();
+      if (cslot + 1 == NST) {
+        cslot = 0;
+        cpar ^= 1u;
+      } else {
+        ++cslot;
+      }
+      if (lane == 0) issue();
+    }
+    // digit sums of this slice per token (the code offsets: rows g carry code + 8, rows g + 8
+    // carry 16 (code + 8))
+    int shi = 0, slo = 0;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      int h = 0, l = 0;
+      for (int cc = c0 + lane; cc < c1; cc += 32) {
+        const int2 d = dsum[(v * MT + m) * nch + cc];
+        h += d.x;
+        l += d.y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        h += __shfl_xor_sync(0xffffffffu, h, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+      }
+      if (t == m) {
+        shi = h;
+        slo = l;
+      }
+    }
+    if (t < MT) {
+      const int c_hi = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]) - 8 * shi;
+      const int c_lo = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]) - 8 * slo;
+      const int u_hi = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]) - 128 * shi;
+      const int u_lo = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]) - 128 * slo;
+      const float s_x = sx[v * MT + t];
+      float* out = a.partial + (static_cast<int64_t>(s) * MT + t) * a.Np + static_cast<int64_t>(rt) * kTileN;
+      out[g] = fmaf(256.f, static_cast<float>(c_hi), static_cast<float>(c_lo)) * s_x;
+      out[g + 8] = fmaf(256.f, static_cast<float>(u_hi), static_cast<float>(u_lo)) * (0.0625f * s_x);
+    }
+  }
+  __syncthreads();
+  trace_point(13);
+}
+
 __global__ void k_xfrag_from_f32(const float* __restrict__ x, int64_t ldx, int M, int64_t K, int64_t Kp,
                                  int64_t nch, const float* __restrict__ row_scale, __half* __restrict__ xf) {
   // one thread per (m, even k) pair
@@ -790,10 +1072,19 @@ struct M1Shape {
 constexpr size_t kM1SmemLimit = 227 * 1024 - 1024;  // leave room for the static shared memory
 constexpr int kM1MaxTokens = 2;
 
+// INT4 single-token family on the integer MMA (k_gemv_i4) unless GLM_GEMV_IMMA=0 (fp16 HMMA
+// k_gemv_m1, the round-1 kernel, kept for A/B)
+bool gemv_imma() {
+  static const bool on = [] { const char* e = getenv("GLM_GEMV_IMMA"); return !e || e[0] != '0'; }();
+  return on;
+}
+
 M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
   static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
   static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
-  const size_t xb = static_cast<size_t>(nx) * M * nch * (128 + 4) + 8;
+  // activation vectors + per-chunk sums (fp32, or int2 digit sums + scales + per-warp maxima)
+  const size_t xb = gemv_imma() ? static_cast<size_t>(nx) * M * nch * (128 + 8) + 8 + 64 + kM1MaxWarps * 32
+                                : static_cast<size_t>(nx) * M * nch * (128 + 4) + 8;
   M1Shape m;
   m.nst = m1s >= 3 ? 3 : 2;
   m.sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
@@ -916,6 +1207,29 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     }
     static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
     const dim3 block1(m.warps * 32);
+    if (gemv_imma()) {
+      static bool attr2 = false;
+      if (!attr2) {
+        for (auto k : {k_gemv_i4<2, 4096, 1>, k_gemv_i4<2, 6144, 1>, k_gemv_i4<2, 8192, 1>, k_gemv_i4<3, 4096, 1>,
+                       k_gemv_i4<2, 4096, 2>, k_gemv_i4<2, 6144, 2>})
+          CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kM1SmemLimit));
+        attr2 = true;
+      }
+      if (M == 2) {
+        if (m.sb >= 6144) launch_k(k_gemv_i4<2, 6144, 2>, grid, block1, m.smem, st, a, nx_op, early);
+        else launch_k(k_gemv_i4<2, 4096, 2>, grid, block1, m.smem, st, a, nx_op, early);
+      } else if (m.nst == 3) {
+        launch_k(k_gemv_i4<3, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
+      } else if (m.sb == 8192) {
+        launch_k(k_gemv_i4<2, 8192, 1>, grid, block1, m.smem, st, a, nx_op, early);
+      } else if (m.sb == 6144) {
+        launch_k(k_gemv_i4<2, 6144, 1>, grid, block1, m.smem, st, a, nx_op, early);
+      } else {
+        launch_k(k_gemv_i4<2, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
+      }
+      LAUNCH_CHECK("k_gemv_i4");
+      return;
+    }
     if (M == 2) {
       if (m.sb >= 6144) launch_k(k_gemv_m1<4, 2, 6144, 2>, grid, block1, m.smem, st, a, nx_op, early);
       else launch_k(k_gemv_m1<4, 2, 4096, 2>, grid, block1, m.smem, st, a, nx_op, early);

@@ -3,9 +3,10 @@ y = x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155).
 
 Two bars: (1) exact-arithmetic check against a float64 evaluation of the kernel's own
 contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only fp32
-accumulation error remains: <= 2e-6 of max|y|, except the single-token INT4 GEMV, which
-accumulates offset-binary codes (1032 + code) and removes 1032 * sum(x) afterwards, so its
-fp32 accumulator carries the larger offset term: <= 2e-4 of max|y| (gemv.cu, dq4_raw);
+accumulation error remains: <= 2e-6 of max|y|. The single-token INT4 GEMV (1..2 tokens,
+gemv.cu k_gemv_i4) runs on the integer MMA: its contract re-quantizes each fp16 activation
+vector to 16-bit fixed point, x_int = rint(x * (32512 / max|x|)), and the products and sums
+are exact integers, so only the final fp32 scaling rounds: <= 2e-6 of max|y|;
 (2) the reference check against the oracle's float64 x . dequantize(q),
 max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
 import numpy as np
@@ -18,24 +19,46 @@ pytestmark = pytest.mark.gpu
 
 
 def contract_tol(M, bits):
-    # INT4 at 1..2 tokens runs the offset-binary transcode (gemv.cu dq4_raw): ~5e-5 of max|y|
-    return 2e-4 if (M <= 2 and bits == 4) else 2e-6
+    return 2e-6
 
 
-def kernel_contract(x, q):
+DIGIT_Q = np.float32(32512.0)  # gemv.cu kDigitQ
+
+
+def imma_activations(xh):
+    """The integer-MMA GEMV's view of fp16 activations (gemv.cu k_gemv_i4): per row,
+    x_int = rint(fp32(x) * fp32(32512 / max|x|)) and the scale s_x = max|x| / 32512."""
+    xh32 = xh.astype(np.float32)
+    out = np.zeros(xh.shape, np.float64)
+    for m in range(xh.shape[0]):
+        mx = np.float32(np.abs(xh32[m]).max())
+        if mx == 0:
+            continue
+        inv = np.float32(DIGIT_Q / mx)
+        xi = np.rint(xh32[m] * inv).astype(np.int64)
+        assert np.abs(xi).max() <= 32512
+        out[m] = xi.astype(np.float64) * np.float64(np.float32(mx / DIGIT_Q))
+    return out
+
+
+def kernel_contract(x, q, M=None):
     """float64 evaluation of what the kernel computes."""
     K, N = q["rows"], q["cols"]
+    M = x.shape[0] if M is None else M
     codes = O.codes_of(q).reshape(K, N).astype(np.float64)
     s = q["scales"]
     x32 = x.astype(np.float32)
+    imma = q["bits"] == 4 and M <= 2  # k_gemv_i4 (integer MMA)
     if q["axis"] == "row":
         S = s.max()
         fold = (s / S).astype(np.float32) if S > 0 else np.zeros(K, np.float32)
-        xh = (x32 * fold[None, :]).astype(np.float16).astype(np.float64)
-        return (xh @ codes) * np.float64(np.float32(S))
-    xh = x32.astype(np.float16).astype(np.float64)
+        xh = (x32 * fold[None, :]).astype(np.float16)
+        xv = imma_activations(xh) if imma else xh.astype(np.float64)
+        return (xv @ codes) * np.float64(np.float32(S))
+    xh = x32.astype(np.float16)
+    xv = imma_activations(xh) if imma else xh.astype(np.float64)
     cs = (s if q["axis"] == "column" else np.full(N, s[0])).astype(np.float32).astype(np.float64)
-    return (xh @ codes) * cs[None, :]
+    return (xv @ codes) * cs[None, :]
 
 
 SHAPES = [(64, 16), (512, 1536), (1368, 512), (512, 1368), (200, 90), (4096, 1024)]
