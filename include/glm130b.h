@@ -161,6 +161,16 @@ glm_status glm_model_get_config(const glm_model* m, glm_config* out);
  * glm_model_init_comm before loading weights. No-op at tp_size == 1. */
 glm_status glm_tp_unique_id(void* out128);
 glm_status glm_model_init_comm(glm_model* m, const void* unique_id);
+/* Test hook (single GPU): an in-process group of `size` rank-models (tp_rank 0..size-1 of
+ * tp_size = size, all on the current device), each driven by its own host thread. Its
+ * collectives are stream-ordered sum kernels behind a host barrier; the fused decode
+ * allreduce runs its push and sum phases as two launches split by that barrier, so the same
+ * sharded model code runs with no kernel waiting on another rank's kernel. Decode then runs
+ * without a CUDA graph. Every rank calls glm_model_init_comm_emulated concurrently. */
+typedef struct glm_tp_group glm_tp_group;
+glm_status glm_tp_emulated_group_create(int size, glm_tp_group** out);
+glm_status glm_tp_emulated_group_destroy(glm_tp_group* g);
+glm_status glm_model_init_comm_emulated(glm_model* m, glm_tp_group* g);
 /* Reference parameters (host doubles, model.hpp:41-65), quantized on the GPU with the
  * model's policy (quantize_model, quant.cpp:284-311). which: 0 qkv [d,3d], 1 out_proj
  * [d,d], 2 ffn_w1 [d,f], 3 ffn_v [d,f], 4 ffn_w2 [f,d], 5 ln1_gain, 6 ln1_bias,

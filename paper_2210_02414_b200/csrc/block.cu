@@ -158,6 +158,74 @@ __device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* sl
   return r;
 }
 
+// Tensor-parallel sum of this CTA's slice [2 p0, 2 p1) of row m (PeerArgs, block.h): push
+// the rank's partial into every rank's inbox, raise the slice flag, wait for the t flags of
+// this generation and sum the inbox slots in rank order (same bits on every rank). Returns
+// false after a push-only launch (mode 1). A flag that does not arrive within ~20 s sets the
+// error word (Collective::check_peer) instead of hanging the GPU.
+static_assert(kPeerSlices == kLnCluster, "one peer flag per LayerNorm cluster CTA");
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool peer_allreduce(const PeerArgs& P, int m, int crank, int64_t p0, int64_t p1,
+                                               float2 (&y)[kLnPairs]) {
+  __shared__ unsigned s_gen;
+  const unsigned* genp = P.gen + m * kPeerSlices + crank;
+  if (threadIdx.x == 0) s_gen = *genp + 1u;
+  __syncthreads();
+  const unsigned gen = s_gen;
+  const int par = static_cast<int>(gen & 1u);
+  const int64_t slot = static_cast<int64_t>(P.max_b) * P.d;  // one (parity, source rank) slot
+  if (P.mode & 1) {
+    for (int dst = 0; dst < P.size; ++dst) {
+      float* box = P.inbox[dst] + static_cast<int64_t>(par * P.size + P.rank) * slot + static_cast<int64_t>(m) * P.d;
+#pragma unroll
+      for (int i = 0; i < kLnPairs; ++i) {
+        const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+        if (p < p1) *reinterpret_cast<float2*>(box + 2 * p) = y[i];
+      }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < P.size)
+      st_release_sys(P.flags[threadIdx.x] + ((par * P.size + P.rank) * P.max_b + m) * kPeerSlices + crank, gen);
+  }
+  if (!(P.mode & 2)) return false;
+  if (threadIdx.x < P.size) {
+    const unsigned* f = P.flags[P.rank] + ((par * P.size + threadIdx.x) * P.max_b + m) * kPeerSlices + crank;
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(f) != gen) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 20000000000ull) {
+        atomicExch(P.err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const float* own = P.inbox[P.rank] + static_cast<int64_t>(par * P.size) * slot + static_cast<int64_t>(m) * P.d;
+#pragma unroll
+  for (int i = 0; i < kLnPairs; ++i) {
+    const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+    float2 acc = make_float2(0.f, 0.f);
+    if (p < p1)
+      for (int r = 0; r < P.size; ++r) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(own + r * slot + 2 * p));
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+    y[i] = acc;
+  }
+  if (threadIdx.x == 0) P.gen[m * kPeerSlices + crank] = gen;
+  return true;
+}
+
 __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
   trace_point(20);
   __shared__ float2 red[kLnThreads / 32];
@@ -211,6 +279,12 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
         }
     }
   }
+#pragma unroll
+  for (int i = 0; i < kLnPairs; ++i) {
+    y[i].x *= sc[i].x;
+    y[i].y *= sc[i].y;
+  }
+  if (a.peer.size > 1 && !peer_allreduce(a.peer, m, rank, p0, p1, y)) return;  // push-only launch
   float2 z[kLnPairs];
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -218,8 +292,6 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
     z[i] = make_float2(0.f, 0.f);
     if (p < p1) {
-      y[i].x *= sc[i].x;
-      y[i].y *= sc[i].y;
       z[i] = make_float2(a.alpha * hv[i].x + y[i].x, a.alpha * hv[i].y + y[i].y);
       if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + 2 * p) = y[i];
       acc.x += z[i].x + z[i].y;
@@ -415,18 +487,26 @@ __device__ __forceinline__ float2 reduce_partial2(const SubIn& in, int m, int64_
   return acc;
 }
 
+// scalar form for an odd feature count (e.g. ffn 1368 over 8 ranks = 171 per rank) or odd row
+// strides: feature n + 1 == f reads as 0 (the consumer's padded k)
+__device__ __forceinline__ float2 reduce_partial2_any(const SubIn& in, int m, int64_t n, int64_t f) {
+  return make_float2(reduce_partial(in, m, n), n + 1 < f ? reduce_partial(in, m, n + 1) : 0.f);
+}
+
+template <bool V2>
 __global__ void k_geglu_act(ActArgs a) {
   trace_point(40);
   pdl_wait();
   pdl_trigger();
   trace_point(41);
-  const int64_t half = a.f / 2;
+  const int64_t half = (a.f + 1) / 2;
   const int64_t pairs = static_cast<int64_t>(a.M) * half;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int m = static_cast<int>(i / half);
     const int64_t n = (i % half) * 2;
-    const float2 u = reduce_partial2(a.w1, m, n), v = reduce_partial2(a.v, m, n);
+    const float2 u = V2 ? reduce_partial2(a.w1, m, n) : reduce_partial2_any(a.w1, m, n, a.f);
+    const float2 v = V2 ? reduce_partial2(a.v, m, n) : reduce_partial2_any(a.v, m, n, a.f);
     const float o0 = 0.5f * u.x * (1.f + erff(u.x * kInvSqrt2)) * v.x;  // tensor.cpp:313-318
     const float o1 = 0.5f * u.y * (1.f + erff(u.y * kInvSqrt2)) * v.y;
     store_xfrag_pair(a.xo, m, n, o0, o1);
@@ -1344,6 +1424,7 @@ void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   // 3 resident 512-thread CTAs per SM (40 registers): the row's two passes are latency-bound,
   // so occupancy sets the bandwidth (ncu, 8192 x 12288: 1 CTA/SM 487/403 us, 2: 328, 3: 341/263,
   // 4 spills: 440/361)
+  if (a.peer.size > 1 && M > 16) fail(GLM_CONTRACT, "glmmodel", "fused tensor-parallel LayerNorm is a decode (<= 16 rows) kernel");
   if (M > 16 && v8 && rows8) launch_k(k_deepnorm_ln_rows8<3>, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
@@ -1358,7 +1439,13 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
     LAUNCH_CHECK("k_geglu_act_tiles");
     return;
   }
-  launch_k(k_geglu_act, dim3(grid_for(static_cast<int64_t>(a.M) * (a.f / 2), 128)), dim3(128), 0, st, a);
+  const auto al2 = [](const SubIn& in) {
+    return in.ld % 2 == 0 && in.split_stride % 2 == 0 && (reinterpret_cast<uintptr_t>(in.p) & 7) == 0 &&
+           (!in.scale || (reinterpret_cast<uintptr_t>(in.scale) & 7) == 0);
+  };
+  const bool v2 = a.f % 2 == 0 && al2(a.w1) && al2(a.v);
+  launch_k(v2 ? k_geglu_act<true> : k_geglu_act<false>, dim3(grid_for(static_cast<int64_t>(a.M) * ((a.f + 1) / 2), 128)),
+           dim3(128), 0, st, a);
   LAUNCH_CHECK("k_geglu_act");
 }
 

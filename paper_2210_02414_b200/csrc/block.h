@@ -40,6 +40,24 @@ __device__ __forceinline__ void store_xfrag_pair(const XOut& xo, int m, int64_t 
 }
 #endif
 
+// Fused decode allreduce of a row-parallel sublayer output (tensor parallelism, collective.h):
+// rank r pushes its [row m][CTA slice c] of the sublayer output into inbox[dst] slot
+// (gen & 1, r) of every rank dst, then raises flags[dst][(gen & 1, r, m, c)] = gen; each rank
+// sums the t slots of its own inbox in rank order once the t flags read gen, so every rank
+// computes bit-identical sums. gen counts the calls per (m, c) (own counters). mode: 1 push
+// only, 2 wait + sum only (the two halves of the emulated single-GPU group, separated by a
+// host barrier), 3 both (one launch per rank on real multi-GPU).
+constexpr int kMaxTp = 8;
+constexpr int kPeerSlices = 8;  // one flag per (row, LayerNorm cluster CTA)
+struct PeerArgs {
+  float* inbox[kMaxTp] = {};     // per destination rank: [2][size][max_b][d] fp32
+  unsigned* flags[kMaxTp] = {};  // per destination rank: [2][size][max_b][kPeerSlices]
+  unsigned* gen = nullptr;       // own: [max_b][kPeerSlices]
+  int* err = nullptr;            // own: set when a peer's flag does not arrive (timeout)
+  int rank = 0, size = 1, max_b = 0, mode = 3;
+  int64_t d = 0;
+};
+
 struct LnArgs {
   SubIn in;
   float* h;                 // [M][d] residual in / LN output out
@@ -49,6 +67,7 @@ struct LnArgs {
   XOut x0, x1;              // up to two consumers (ffn_w1 and ffn_v have distinct kRow scales)
   float* tap;               // optional [M][d] copy of the sublayer output
   int zero_sublayer;
+  PeerArgs peer{};          // size > 1: sum the sublayer output across tensor-parallel ranks
 };
 
 struct ActArgs {

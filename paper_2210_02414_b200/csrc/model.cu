@@ -135,7 +135,7 @@ struct glm_model {
   int64_t last_rows = 0;
 
   cudaStream_t st = nullptr;
-  std::map<std::tuple<int, bool, bool>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, bool, bool, bool>, cudaGraphExec_t> graphs;
   std::unique_ptr<Collective> comm;
 
   ~glm_model() {
@@ -143,6 +143,7 @@ struct glm_model {
     if (h_tokens) cudaFreeHost(h_tokens);
     if (h_positions) cudaFreeHost(h_positions);
     if (h_next) cudaFreeHost(h_next);
+    if (h_peer_err) cudaFreeHost(h_peer_err);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -259,8 +260,33 @@ struct glm_model {
     h_len.assign(max_batch, 0);
     ensure_rows(max_batch);
     ensure_partial(16);
-    if (tp_size > 1) comm = std::make_unique<Collective>();
+    if (tp_size > 1) {
+      comm = std::make_unique<Collective>();
+      // NCCL decode path: reduced sublayer rows [max_batch][d] (allocated here: never inside
+      // a captured decode step)
+      ar_buf.alloc(static_cast<int64_t>(max_batch) * d * 4);
+      CUDA_CHECK(cudaMallocHost(&h_peer_err, sizeof(int)));
+      *h_peer_err = 0;
+    }
     CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+
+  // Decode sublayer sums across ranks fused into the DeepNorm LayerNorm (collective.h) unless
+  // GLM_TP_FUSED=0 (reduce + ncclAllReduce + LayerNorm)
+  bool fused_ar() const {
+    static const bool on = [] { const char* e = getenv("GLM_TP_FUSED"); return !e || e[0] != '0'; }();
+    return on && comm && comm->peer_ready();
+  }
+  int* h_peer_err = nullptr;  // pinned copy of the fused collective's timeout word
+
+  void init_comm(const void* uid) {
+    comm->init(tp_rank, tp_size, uid);
+    comm->setup_peer(max_batch, d, st);
+  }
+  void init_comm_emulated(EmuGroup* g) {
+    comm->init_emulated(g, tp_rank);
+    if (comm->size() != tp_size) fail(GLM_CONTRACT, "glmmodel", "emulated group size differs from tp_size");
+    comm->setup_peer(max_batch, d, st);
   }
 
   GemvPlan fused_plans[17];
@@ -459,14 +485,39 @@ struct glm_model {
   SubIn row_parallel_out(const Linear& lin, const GemvPlan& p, int M) {
     SubIn in{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale};
     if (tp_size == 1) return in;
-    if (ar_buf.bytes < static_cast<int64_t>(M) * d * 4) ar_buf.alloc(static_cast<int64_t>(max_batch > M ? max_batch : M) * d * 4);
+    if (ar_buf.bytes < static_cast<int64_t>(M) * d * 4) fail(GLM_CONTRACT, "glmmodel", "decode batch above max_batch");
     gemv_reduce(partial.as<float>(), p.ksplit, M, lin.w, ar_buf.as<float>(), d, st);
     comm->allreduce_sum(ar_buf.as<float>(), static_cast<int64_t>(M) * d, st);
     return SubIn{ar_buf.as<float>(), 1, 0, d, nullptr};
   }
 
+  // DeepNorm LayerNorm after a row-parallel linear (out_proj, ffn_w2) in decode: at t > 1 the
+  // rank partials are summed inside the LayerNorm kernel (PeerArgs); returns our launches.
+  int ln_after_row_parallel(LnArgs ln, const Linear& lin, const GemvPlan& p, int M) {
+    if (tp_size > 1 && fused_ar()) {
+      ln.in = SubIn{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale};
+      ln.peer = comm->peer_args();
+      if (comm->emulated()) {  // push phase, group barrier, sum phase
+        ln.peer.mode = 1;
+        launch_deepnorm_ln(ln, M, st);
+        comm->barrier(st);
+        ln.peer.mode = 2;
+        launch_deepnorm_ln(ln, M, st);
+        return 2;
+      }
+      ln.peer.mode = 3;
+      launch_deepnorm_ln(ln, M, st);
+      return 1;
+    }
+    ln.in = row_parallel_out(lin, p, M);
+    launch_deepnorm_ln(ln, M, st);
+    return tp_size > 1 ? 2 : 1;
+  }
+
   // ---- decode step (enqueued; captured into a CUDA graph) --------------------------------
-  int enqueue_decode(int B) {
+  // with_logits: the caller reads the logits (at t > 1 that adds the vocab all-gather; the
+  // greedy token needs only the (value, index) max-reduction)
+  int enqueue_decode(int B, bool with_logits = true) {
     int launches = 0;
     const Layer& l0 = layers[0];
     launch_embed(E, head_bf16, d, d_tokens, B, h.as<float>(), xout(xf_qkv.as<__half>(), l0.lin[QKV]), st);
@@ -494,7 +545,6 @@ struct glm_model {
       launch_attn_decode(aa, B, st);
       gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
       LnArgs ln;
-      ln.in = row_parallel_out(out, out.plan(B), B);
       ln.h = h.as<float>();
       ln.gain = ly.ln1g;
       ln.bias = ly.ln1b;
@@ -505,7 +555,7 @@ struct glm_model {
       ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v) : XOut{};  // W1 and V share x unless kRow
       ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
       ln.zero_sublayer = zero_sub;
-      launch_deepnorm_ln(ln, B, st);
+      launches += ln_after_row_parallel(ln, out, out.plan(B), B);
       GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
                 axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
       gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
@@ -519,17 +569,16 @@ struct glm_model {
       launch_geglu_act(act, st);
       gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan(B), st);
       LnArgs ln2 = ln;
-      ln2.in = row_parallel_out(w2, w2.plan(B), B);
       ln2.gain = ly.ln2g;
       ln2.bias = ly.ln2b;
       const bool last = l + 1 == L;
       ln2.x0 = last ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]);
       ln2.x1 = XOut{};
       ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
-      launch_deepnorm_ln(ln2, B, st);
-      launches += 8 + (tp_size > 1 ? 4 : 0);
+      launches += ln_after_row_parallel(ln2, w2, w2.plan(B), B);
+      launches += 6;  // 4 GEMVs + attention + GeGLU activation
     }
-    launches += enqueue_head(B, logits.as<float>());
+    launches += enqueue_head(B, logits.as<float>(), with_logits);
     launch_argmax_finish(d_argmax, d_next, B, st);
     launch_advance(d_len, B, st);
     launch_k(k_feed, dim3(1), dim3(32), 0, st, d_next, d_tokens, d_positions, B);
@@ -537,7 +586,7 @@ struct glm_model {
     return launches + 3;
   }
 
-  int enqueue_head(int M, float* logit_out) {
+  int enqueue_head(int M, float* logit_out, bool gather = true) {
     HeadArgs ha;
     ha.E = E;
     ha.h = h.as<float>();
@@ -552,20 +601,21 @@ struct glm_model {
     launch_head(ha, head_bf16, st);
     if (tp_size > 1) {
       comm->allreduce_max_u64(d_argmax, M, st);
-      if (logit_out) comm->allgather_logits(logit_out, M, V, vocab_offset, vocab_local, st);
+      if (logit_out && gather) comm->allgather_logits(logit_out, M, V, vocab_offset, vocab_local, st);
     }
     return 1;
   }
 
-  cudaGraphExec_t graph_for(int B) {
-    auto key = std::make_tuple(B, taps, zero_sub);
+  cudaGraphExec_t graph_for(int B, bool with_logits = true) {
+    with_logits = with_logits || tp_size == 1;  // one graph at t = 1 (its logits cost nothing extra)
+    auto key = std::make_tuple(B, taps, zero_sub, with_logits);
     auto it = graphs.find(key);
     if (it != graphs.end()) return it->second;
     if (taps) ensure_taps(B);
     cudaGraph_t g;
     CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_decode(B);
+      enqueue_decode(B, with_logits);
     } catch (...) {
       cudaStreamEndCapture(st, &g);
       throw;
@@ -597,11 +647,15 @@ struct glm_model {
     CUDA_CHECK(cudaMemcpyAsync(d_tokens, h_tokens, B * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(d_positions, h_positions, B * sizeof(int), cudaMemcpyHostToDevice, st));
     static const bool eager = getenv("GLM_EAGER") != nullptr;  // debugging: no graph
-    if (eager) enqueue_decode(B);
-    else CUDA_CHECK(cudaGraphLaunch(graph_for(B), st));
+    // the emulated single-GPU rank group separates its phases on the host: no graph
+    if (eager || (comm && comm->emulated())) enqueue_decode(B, logits_out != nullptr);
+    else CUDA_CHECK(cudaGraphLaunch(graph_for(B, logits_out != nullptr), st));
     if (logits_out) CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(B) * V * 4, cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaMemcpyAsync(h_next, d_next, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (fused_ar()) CUDA_CHECK(cudaMemcpyAsync(h_peer_err, comm->peer_args().err, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
+    if (h_peer_err && *h_peer_err)
+      fail(GLM_NCCL, "collective", "a tensor-parallel peer did not deliver its decode partial (timeout)");
     for (int b = 0; b < B; ++b) {
       if (next_tokens) next_tokens[b] = h_next[b];
       h_len[b] += 1;
@@ -786,7 +840,27 @@ glm_status glm_model_init_comm(glm_model* m, const void* unique_id) {
   return guarded([&] {
     checked(m);
     if (m->tp_size == 1) return;
-    m->comm->init(m->tp_rank, m->tp_size, unique_id);
+    if (!unique_id) fail(GLM_CONTRACT, "glmmodel", "null unique id");
+    m->init_comm(unique_id);
+  });
+}
+
+glm_status glm_tp_emulated_group_create(int size, glm_tp_group** out) {
+  return guarded([&] {
+    if (!out) fail(GLM_CONTRACT, "collective", "null output");
+    *out = reinterpret_cast<glm_tp_group*>(emu_group_create(size));
+  });
+}
+
+glm_status glm_tp_emulated_group_destroy(glm_tp_group* g) {
+  return guarded([&] { emu_group_destroy(reinterpret_cast<EmuGroup*>(g)); });
+}
+
+glm_status glm_model_init_comm_emulated(glm_model* m, glm_tp_group* g) {
+  return guarded([&] {
+    checked(m);
+    if (m->tp_size == 1) return;
+    m->init_comm_emulated(reinterpret_cast<EmuGroup*>(g));
   });
 }
 
@@ -921,11 +995,12 @@ glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup
   return guarded([&] {
     checked(m);
     m->check_loaded();
+    if (m->comm && m->comm->emulated()) fail(GLM_CONTRACT, "glmmodel", "bench_decode needs a real communicator (graph replay)");
     if (batch < 1 || batch > m->max_batch) fail(GLM_CONTRACT, "glmmodel", "batch must be in 1..max_batch");
     for (int b = 0; b < batch; ++b)
       if (m->h_len[b] + warmup + steps > m->max_ctx) fail(GLM_CONTRACT, "glmmodel", "bench would overflow the KV cache");
     // counts our kernel launches of one step (capture-free dry count happens in graph_for)
-    cudaGraphExec_t ge = m->graph_for(batch);
+    cudaGraphExec_t ge = m->graph_for(batch, false);
     for (int i = 0; i < warmup; ++i) CUDA_CHECK(cudaGraphLaunch(ge, m->st));
     cudaEvent_t e0, e1;
     CUDA_CHECK(cudaEventCreate(&e0));
@@ -943,7 +1018,7 @@ glm_status glm_model_bench_decode(glm_model* m, int batch, int steps, int warmup
       // count kernel nodes of the step graph
       cudaGraph_t g;
       CUDA_CHECK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
-      m->enqueue_decode(batch);
+      m->enqueue_decode(batch, false);
       CUDA_CHECK(cudaStreamEndCapture(m->st, &g));
       size_t nn = 0;
       CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));

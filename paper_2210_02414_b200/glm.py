@@ -99,6 +99,9 @@ SIGNATURES = {
     "glm_qweight_create_ex": (I32, [P, P, P, I64, I64, I32, I32, I32, P]),
     "glm_model_prefill_batch": (I32, [P, I32, P, P, P, P, P, P]),
     "glm_tp_unique_id": (I32, [P]),
+    "glm_tp_emulated_group_create": (I32, [I32, C.POINTER(P)]),
+    "glm_tp_emulated_group_destroy": (I32, [P]),
+    "glm_model_init_comm_emulated": (I32, [P, P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
     "glm_model_set_tensor": (I32, [P, I32, I32, P]),
@@ -309,6 +312,45 @@ def tp_unique_id() -> bytes:
     return uid.tobytes()
 
 
+class EmulatedGroup:
+    """Single-GPU test group of tensor-parallel rank-models (glm_tp_emulated_group_create):
+    the same sharded model code, with collectives emulated by stream-ordered sums behind a
+    host barrier. Each rank must be driven from its own thread (see run_ranks)."""
+
+    def __init__(self, size):
+        h = C.c_void_p()
+        _check(lib().glm_tp_emulated_group_create(size, C.byref(h)))
+        self.h, self.size = h, size
+
+    def __del__(self):
+        if getattr(self, "h", None) and _LIB is not None:
+            _LIB.glm_tp_emulated_group_destroy(self.h)
+            self.h = None
+
+
+def run_ranks(fns):
+    """Run fns[r]() on one thread per rank (ctypes releases the GIL inside the library);
+    returns the results in rank order and re-raises the first failure."""
+    import threading
+    out, err = [None] * len(fns), [None] * len(fns)
+
+    def body(r):
+        try:
+            out[r] = fns[r]()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(len(fns))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
 class Model:
     """GLM model on the B200: quantized linears, fp32 residual stream, KV cache."""
 
@@ -354,6 +396,10 @@ class Model:
         payload = np.ascontiguousarray(payload, np.int8)
         scales = np.ascontiguousarray(scales, np.float64)
         _check(lib().glm_model_set_quantized(self.h, layer, which, _p(payload), payload.size, _p(scales), scales.size))
+
+    def init_comm_emulated(self, group: "EmulatedGroup"):
+        """Join a single-GPU emulated rank group (test hook; call from this rank's thread)."""
+        _check(lib().glm_model_init_comm_emulated(self.h, group.h))
 
     def init_comm(self, unique_id: bytes):
         """Join the tensor-parallel group (NCCL over NVLink); no-op at tp_size == 1."""

@@ -1,0 +1,152 @@
+"""Megatron tensor parallelism executed on one B200: t = 2/4/8 rank-models of
+the same sharded model code (model.cu, tp_size > 1) in one process, one host thread per
+rank, joined by the emulated group (collective.h). Prefill runs the NCCL-path code
+(allreduce after out_proj / ffn_w2, vocab-sharded head with the logits all-gather and the
+(value, index) argmax max-reduction); decode runs the fused push/sum allreduce inside the
+DeepNorm LayerNorm (block.cu peer_allreduce). Gates as test_gpu_model.py: per-layer
+sublayer taps and logits normalised by Delta_ref against the single-process CPU oracle
+(model.cpp:166-226), plus bit-identical logits on every rank."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2210_02414_b200 import glm
+
+pytestmark = pytest.mark.gpu
+PREFIX = [6 + (37 * i + 11) % 256 for i in range(126)]
+
+
+def check_logits(gpu, ref, zero):
+    err = np.abs(gpu - ref).max()
+    delta = np.abs(ref - zero).max()
+    assert err <= 1e-2 * delta, f"logit err {err:.3e} vs 1e-2*Delta_ref {1e-2 * delta:.3e}"
+    return err / delta
+
+
+def check_taps(gpu_taps, ref_taps):
+    for layer in range(ref_taps.shape[0]):
+        err = np.abs(gpu_taps[layer] - ref_taps[layer]).max()
+        assert err <= 1e-2 * np.abs(ref_taps[layer]).max(), (layer, err)
+
+
+def rank_models(p, t, bits, axis, cfg, max_batch=1, max_ctx=256):
+    group = glm.EmulatedGroup(t)
+    ms = [glm.Model(cfg, bits=bits, axis=axis, max_batch=max_batch, max_ctx=max_ctx, tp_rank=r, tp_size=t)
+          for r in range(t)]
+    glm.run_ranks([lambda m=m: m.init_comm_emulated(group) for m in ms])
+    for m in ms:
+        m.load_reference_params(lambda layer, slot: p.tensor(0, O.EMBED) if slot == "embed" else p.tensor(layer, slot))
+    return group, ms
+
+
+@pytest.mark.parametrize("t,bits,axis", [(2, 8, "row"), (4, 4, "column"), (8, 4, "row"), (8, 8, "column")])
+def test_tp_prefill_and_decode_match_oracle(t, bits, axis):
+    cfg = glm.GLMConfig(num_layers=4, hidden=512, num_heads=8, vocab=262)
+    p = O.Params(4, 512, 8, vocab=262, seed=1234)
+    group, ms = rank_models(p, t, bits, axis, cfg)
+    p.quantize(bits, axis)
+    gen = [40, 100, 200, 57, 9]
+    sample = O.gmask_sample(PREFIX[:70], gen)
+    ref, at, ft = p.forward(sample, taps=True)
+    zero = p.forward(sample, zero_sublayers=True)
+    C = sample["context_length"]
+    for m in ms:
+        m.enable_taps(True)
+
+    def prefill(m):
+        lg = m.prefill(sample["tokens"][:C], sample["positions"][:C], C)
+        return lg, m.taps(C)
+
+    outs = glm.run_ranks([lambda m=m: prefill(m) for m in ms])
+    for r in range(1, t):  # every rank holds the same residual stream and logits
+        assert np.array_equal(outs[r][0], outs[0][0])
+    check_logits(outs[0][0].astype(np.float64), ref[:C], zero[:C])
+    check_taps(outs[0][1][0], at[:, :C])
+    check_taps(outs[0][1][1], ft[:, :C])
+
+    rows = []
+    for j in range(len(gen) + 1):
+        tok, pos = [sample["tokens"][C + j]], [sample["positions"][C + j]]
+        res = glm.run_ranks([lambda m=m: (m.decode_step(tok, pos), m.taps(1)) for m in ms])
+        (nxt0, lg0), (ta, tf) = res[0]
+        for r in range(1, t):
+            assert np.array_equal(res[r][0][1], lg0) and int(res[r][0][0][0]) == int(nxt0[0])
+        assert int(nxt0[0]) == int(np.argmax(lg0[0]))  # vocab-sharded argmax == full argmax
+        check_taps(ta, at[:, C + j:C + j + 1])
+        check_taps(tf, ft[:, C + j:C + j + 1])
+        rows.append(lg0[0])
+    check_logits(np.array(rows, np.float64), ref[C:], zero[C:])
+    del ms, group
+
+
+def test_tp_batched_decode_matches_single_rank():
+    """Batch-3 decode at t = 4 (fused allreduce over 3 rows) equals the t = 1 model."""
+    cfg = glm.GLMConfig(num_layers=2, hidden=512, num_heads=8, vocab=300)
+    t, B = 4, 3
+    group = glm.EmulatedGroup(t)
+    ms = [glm.Model(cfg, bits=4, axis="column", max_batch=B, max_ctx=64, tp_rank=r, tp_size=t) for r in range(t)]
+    glm.run_ranks([lambda m=m: m.init_comm_emulated(group) for m in ms])
+    one = glm.Model(cfg, bits=4, axis="column", max_batch=B, max_ctx=64)
+    for m in ms + [one]:
+        m.init_synthetic(17)
+    rng = np.random.default_rng(5)
+    prefixes = [[int(v) for v in rng.integers(6, 290, size=int(rng.integers(5, 30)))] for _ in range(B)]
+    for b, pre in enumerate(prefixes):
+        pos, C = glm.gmask_layout(len(pre), 0)
+        glm.run_ranks([lambda m=m: m.prefill(pre + [2], pos[:C], C, seq=b, logits=False) for m in ms])
+        one.prefill(pre + [2], pos[:C], C, seq=b, logits=False)
+    toks, poss = [3] * B, [len(pre) for pre in prefixes]
+    for _ in range(3):
+        res = glm.run_ranks([lambda m=m: m.decode_step(toks, poss) for m in ms])
+        n1, l1 = one.decode_step(toks, poss)
+        assert np.abs(res[0][1] - l1).max() <= 1e-3 * np.abs(l1).max()
+        toks, poss = [int(v) for v in n1], [q + 1 for q in poss]
+
+
+def test_tp_shard_sizes_must_divide():
+    cfg = glm.GLMConfig(num_layers=1, hidden=512, num_heads=8, vocab=262)
+    with pytest.raises(glm.ContractError):
+        glm.Model(cfg, bits=4, axis="row", tp_rank=0, tp_size=3)
+
+
+_NCCL_PATH_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+from oracle import pyoracle as O
+from paper_2210_02414_b200 import glm
+cfg = glm.GLMConfig(num_layers=2, hidden=512, num_heads=8, vocab=262)
+p = O.Params(2, 512, 8, vocab=262, seed=21)
+t = 4
+group = glm.EmulatedGroup(t)
+ms = [glm.Model(cfg, bits=4, axis="column", max_ctx=64, tp_rank=r, tp_size=t) for r in range(t)]
+glm.run_ranks([lambda m=m: m.init_comm_emulated(group) for m in ms])
+for m in ms:
+    m.load_reference_params(lambda layer, slot: p.tensor(0, O.EMBED) if slot == "embed" else p.tensor(layer, slot))
+toks = [6 + (37 * i + 11) % 256 for i in range(20)] + [2]
+pos, C = glm.gmask_layout(20, 0)
+glm.run_ranks([lambda m=m: m.prefill(toks, pos[:C], C, logits=False) for m in ms])
+rows = []
+for j, tok in enumerate([3, 50, 60]):
+    rows.append(glm.run_ranks([lambda m=m: m.decode_step([tok], [20 + max(0, j - 1) + (1 if j else 0)]) for m in ms])[0][1][0])
+np.save(sys.argv[1], np.array(rows))
+"""
+
+
+def test_tp_decode_nccl_path_equals_fused_path(tmp_path):
+    """GLM_TP_FUSED=0 runs the decode sublayer sum as reduce + allreduce + LayerNorm (the NCCL
+    code path of model.cu row_parallel_out, here over the emulated group); it must agree with
+    the fused peer allreduce to fp32 rounding."""
+    import os
+    import subprocess
+    import sys
+
+    outs = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"rows_{flag}.npy"
+        env = dict(os.environ, GLM_TP_FUSED=flag)
+        r = subprocess.run([sys.executable, "-c", _NCCL_PATH_SCRIPT, str(f)], env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-5 * np.abs(outs[1]).max()
