@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 G = dict(num_layers=70, hidden=12288, num_heads=96, ffn_hidden=32768, vocab=150528)
 METRIC = "GLM-130B INT4 decode tokens/s (batch 1)"
 PROMPT = 127  # P = 127 + [gMASK] + [sop]
+SETTLE = 48   # extra untimed decode steps before the timed replays (clock settle)
 
 
 def peaks():
@@ -42,7 +43,10 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
+    """SM clock + throttle reasons DURING the timed region (B200_PROFILING.md clocks line):
+    NVML every 10 ms (nvidia_ml_py), nvidia-smi every 200 ms if NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
         self.samples, self.reasons, self.maxc = [], set(), None
@@ -50,7 +54,25 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.maxc = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        while not self._stop.is_set():
+            self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for n, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(n)
+            self._stop.wait(0.01)
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -82,6 +104,19 @@ class ClockSampler:
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and exit with their status; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------------------
@@ -192,12 +227,14 @@ def run_ours(args):
     from paper_2210_02414_b200 import glm
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch
     cfg = glm.GLMConfig(**G)
-    max_ctx = PROMPT + 2 + args.warmup + args.steps + args.e2e_steps + 8
+    max_ctx = PROMPT + 2 + args.warmup + SETTLE + args.steps + args.e2e_steps + 8
     t0 = time.time()
     m = glm.Model(cfg, bits=4, axis="column", max_batch=B, max_ctx=max_ctx, head_bf16=True, tp_rank=rank,
                   tp_size=world)
@@ -235,8 +272,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # clock settle: the timed replays start after >= SETTLE untimed steps on top of --warmup
+    # (the power-capped SM clock takes a few hundred ms to reach its steady state)
     with ClockSampler(local) as clk:
-        ms, gemv_ms, launches = m.bench_decode(B, args.steps, args.warmup)
+        ms, gemv_ms, launches = m.bench_decode(B, args.steps, args.warmup + SETTLE)
     torch.cuda.synchronize()
     if world > 1:
         mt = torch.tensor([ms, gemv_ms], device="cuda")
@@ -271,6 +310,9 @@ def run_ours(args):
                      "algorithmic_bytes_per_step": gb, "gemv_ms_per_step": gemv_ms,
                      "gemv_share_of_step": gemv_ms / ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650"},
+        # north_star's step-level metric: INT4 weight bytes per step / aggregate HBM bandwidth
+        "weight_roofline": {"frac": roofline_step_ms / ms, "ideal_ms_per_step": roofline_step_ms,
+                            "weight_bytes_per_rank": weights_per_rank, "peak_gbs": hbm},
         "clocks": clk.summary(),
         "init_seconds": init_s,
     }
@@ -295,6 +337,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
         run_ours(args)
 

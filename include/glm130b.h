@@ -215,6 +215,24 @@ glm_status glm_model_prefill_batch(glm_model* m, int nseg, const int* seqs, cons
  * next_tokens (host, optional) = greedy argmax; logits (host, optional) [batch, vocab]. */
 glm_status glm_model_decode_step(glm_model* m, int batch, const int* tokens,
                                  const int* positions, int* next_tokens, float* logits);
+/* One GLM block (model.cpp:198-224: qkv -> attention -> out_proj -> deepnorm_residual,
+ * then geglu -> deepnorm_residual; model.hpp:70-80) of `layer` on caller hidden states:
+ * x_io [n, hidden] fp32 DEVICE buffer holds the block input and receives its output;
+ * positions [n] int32 device (each in 0..max_ctx). The call is ordered after earlier work on
+ * `stream` (cudaStream_t, NULL = legacy stream) and later work on `stream` after it.
+ *   GLM_BLOCK_PREFILL: the n rows are one sample of sequence `seq`; they fill this layer's KV
+ *     cache of `seq` from slot 0; visibility j < max(context_length, i + 1).
+ *   GLM_BLOCK_DECODE: n = batch rows; row b appends one token to sequence b's cache of this
+ *     layer and attends over it.
+ * The block API tracks its own per-layer cache lengths (glm_model_reset clears them); it
+ * shares the KV storage with glm_model_prefill / decode_step, so drive a model through one
+ * API at a time. Taps (glm_model_enable_taps) record this layer's sublayer outputs. */
+typedef enum { GLM_BLOCK_PREFILL = 0, GLM_BLOCK_DECODE = 1 } glm_block_mode;
+glm_status glm_block_forward(glm_model* m, int layer, glm_block_mode mode, int seq, float* x_io,
+                             const int* positions, int n, int context_length, void* stream);
+/* Same with host buffers (positions validated on the host). */
+glm_status glm_block_forward_host(glm_model* m, int layer, glm_block_mode mode, int seq, float* x_io,
+                                  const int* positions, int n, int context_length);
 /* Sequence length currently cached for `seq`. */
 int glm_model_cached_length(const glm_model* m, int seq);
 glm_status glm_model_reset(glm_model* m);
@@ -225,6 +243,34 @@ glm_status glm_model_enable_taps(glm_model* m, int enable);
 glm_status glm_model_get_taps(const glm_model* m, float* attn, float* ffn);
 /* Test hook: force every sublayer output to zero (the "echo" chain of SURVEY §8c). */
 glm_status glm_model_zero_sublayers(glm_model* m, int enable);
+
+/* ---------------------------------------------------------------------------------
+ * Op-level block functions (model.hpp:70-80), fp32 in / out. The model's prefill / decode
+ * paths use fused kernels; these run the same arithmetic one op at a time.
+ * ------------------------------------------------------------------------------- */
+/* deepnorm_residual (model.cpp:125-131): out = LayerNorm(alpha * x + y) * gain + bias with
+ * the biased variance and eps (tensor.cpp:256-274); x, y, out [rows, d] (out may alias x),
+ * gain / bias [d]; d even. Device pointers, stream-ordered. */
+glm_status glm_deepnorm_residual(const float* x, const float* y, int64_t rows, int64_t d, double alpha,
+                                 const float* gain, const float* bias, double eps, float* out,
+                                 void* stream);
+glm_status glm_deepnorm_residual_host(const float* x, const float* y, int64_t rows, int64_t d,
+                                      double alpha, const float* gain, const float* bias, double eps,
+                                      float* out);
+/* geglu (model.cpp:133-135): y = (GeLU_erf(x.W1) * (x.V)).W2 with quantized W1, V [d, f] and
+ * W2 [f, n]; x [M, d], y [M, n]. */
+glm_status glm_geglu(const glm_qweight* w1, const glm_qweight* v, const glm_qweight* w2, const float* x,
+                     int64_t M, float* y, void* stream);
+glm_status glm_geglu_host(const glm_qweight* w1, const glm_qweight* v, const glm_qweight* w2,
+                          const float* x, int64_t M, float* y);
+/* attention (model.cpp:137-152), one head, default PrecisionPolicy: RoPE(q) RoPE(k)^T /
+ * sqrt(dh), entries with mask[i * n + j] == 0 -> -inf, wide softmax, weights . v. q, k, v,
+ * out [n, dh]; positions [n]; mask [n, n] (1 = visible). A row with no visible key ->
+ * GLM_POLICY (tensor.cpp:231-234). */
+glm_status glm_attention(const float* q, const float* k, const float* v, int64_t n, int64_t dh,
+                         const int* positions, const uint8_t* mask, float* out, void* stream);
+glm_status glm_attention_host(const float* q, const float* k, const float* v, int64_t n, int64_t dh,
+                              const int* positions, const uint8_t* mask, float* out);
 
 /* Decode benchmark: `steps` greedy decode steps for `batch` sequences, starting from the
  * current caches, on device-resident state via the captured CUDA graph. Times the steps

@@ -158,6 +158,7 @@ class QLinear {
   void run_device(const float* x, Index M, float* y, void* stream) const {
     check(glm_qlinear(h_.get(), x, M, y, stream));
   }
+  const glm_qweight* handle() const { return h_.get(); }
   QuantizedMatrix export_canonical(int bits, GroupAxis axis) const {
     QuantizedMatrix q;
     q.bits = bits;
@@ -177,6 +178,42 @@ class QLinear {
   Index rows_, cols_;
   std::unique_ptr<glm_qweight, Del> h_;
 };
+
+// ---- op-level block functions (model.hpp:70-80), host fp32 rows -------------------------
+// deepnorm_residual (model.cpp:125-131): LayerNorm(alpha * x + sublayer_output)
+inline std::vector<float> deepnorm_residual(const std::vector<float>& x, const std::vector<float>& sublayer_output,
+                                            Index rows, Index d, double alpha, const std::vector<float>& gain,
+                                            const std::vector<float>& bias, double eps = 1e-5) {
+  if (static_cast<Index>(x.size()) != rows * d || x.size() != sublayer_output.size())
+    throw DimensionError("[glmmodel] deepnorm_residual operands must share a shape");
+  if (static_cast<Index>(gain.size()) != d || static_cast<Index>(bias.size()) != d)
+    throw DimensionError("[tensorcore] layer_norm gain/bias must match last dimension");
+  std::vector<float> out(x.size());
+  check(glm_deepnorm_residual_host(x.data(), sublayer_output.data(), rows, d, alpha, gain.data(), bias.data(), eps,
+                                   out.data()));
+  return out;
+}
+
+// geglu (model.cpp:133-135): (GeLU(x W1) * x V) W2 with quantized weights
+inline std::vector<float> geglu(const std::vector<float>& x, Index M, const QLinear& w1, const QLinear& v,
+                                const QLinear& w2) {
+  if (static_cast<Index>(x.size()) != M * w1.rows()) throw DimensionError("[glmmodel] geglu x must be [M, d]");
+  std::vector<float> y(static_cast<size_t>(M * w2.cols()));
+  check(glm_geglu_host(w1.handle(), v.handle(), w2.handle(), x.data(), M, y.data()));
+  return y;
+}
+
+// attention (model.cpp:137-152): one head; mask row-major [n, n], nonzero = visible
+inline std::vector<float> attention(const std::vector<float>& q, const std::vector<float>& k,
+                                    const std::vector<float>& v, Index n, Index dh, const std::vector<int>& positions,
+                                    const std::vector<std::uint8_t>& mask) {
+  if (static_cast<Index>(q.size()) != n * dh || k.size() != q.size() || v.size() != q.size() ||
+      static_cast<Index>(positions.size()) != n || static_cast<Index>(mask.size()) != n * n)
+    throw DimensionError("[tensorcore] attention operands must be [n, dh] with [n] positions and an [n, n] mask");
+  std::vector<float> out(q.size());
+  check(glm_attention_host(q.data(), k.data(), v.data(), n, dh, positions.data(), mask.data(), out.data()));
+  return out;
+}
 
 // GLMConfig (model.hpp:15-31); zeros select the reference defaults.
 struct GLMConfig {
@@ -245,6 +282,21 @@ class QuantizedModel {
     return next;
   }
   void reset() { check(glm_model_reset(m_.get())); }
+  // One GLM block (model.cpp:198-224) of `layer` on host hidden states x [n, hidden], in place.
+  void block_forward(int layer, glm_block_mode mode, int seq, std::vector<float>& x, const std::vector<int>& positions,
+                     int context_length) {
+    const int n = static_cast<int>(positions.size());
+    if (static_cast<Index>(x.size()) != static_cast<Index>(n) * cfg_.hidden)
+      throw DimensionError("[glmmodel] block input must be [n, hidden]");
+    check(glm_block_forward_host(m_.get(), layer, mode, seq, x.data(), positions.data(), n, context_length));
+  }
+  void enable_taps(bool on) { check(glm_model_enable_taps(m_.get(), on ? 1 : 0)); }
+  // per-layer sublayer outputs of the last call: [layers, rows, hidden] each
+  void taps(int rows, std::vector<float>& attn, std::vector<float>& ffn) const {
+    attn.resize(static_cast<size_t>(cfg_.num_layers) * rows * cfg_.hidden);
+    ffn.resize(attn.size());
+    check(glm_model_get_taps(m_.get(), attn.data(), ffn.data()));
+  }
 
  private:
   explicit QuantizedModel(glm_model* m) : m_(m) {

@@ -10,4 +10,5 @@ from .glm import (  # noqa: F401
     GLMError, ContractError, DimensionError, FormatError, PolicyError, CudaError,
     lib, LIB_PATH, group_count, payload_bytes, quantize_absmax, quantize_zeropoint, quantize_weight,
     dequantize, pack_int4, unpack_int4, QLinear, Model, GLMConfig, gmask_layout,
+    deepnorm_residual, geglu, attention, EmulatedGroup, run_ranks,
 )

@@ -97,6 +97,11 @@ void check_policy(int bits, int axis) {
 
 // y = x . dequantize(q) for any M >= 1 (device pointers): the decode GEMV for M <= 16 rows,
 // the tcgen05 GEMM (128-token tiles) above; then the split-K reduce with the group scale.
+const QWeightDev& qweight_dev(const glm_qweight* q) {
+  if (!q) fail(GLM_CONTRACT, "qlinear", "null weight handle");
+  return q->w;
+}
+
 void qlinear_device(const glm_qweight* q, const float* x, int64_t M, float* y, cudaStream_t st) {
   const QWeightDev& w = q->w;
   const bool gemv = M < qmm_min_rows();

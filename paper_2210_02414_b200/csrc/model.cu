@@ -144,6 +144,8 @@ struct glm_model {
     if (h_positions) cudaFreeHost(h_positions);
     if (h_next) cudaFreeHost(h_next);
     if (h_peer_err) cudaFreeHost(h_peer_err);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -522,68 +524,74 @@ struct glm_model {
     const Layer& l0 = layers[0];
     launch_embed(E, head_bf16, d, d_tokens, B, h.as<float>(), xout(xf_qkv.as<__half>(), l0.lin[QKV]), st);
     ++launches;
-    for (int l = 0; l < L; ++l) {
-      Layer& ly = layers[l];
-      Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
-      gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan(B), st);
-      AttnDecodeArgs aa;
-      aa.qkv = SubIn{partial.as<float>(), qkv.plan(B).ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
-      aa.d_local = dl;
-      aa.heads = Hl;
-      aa.dh = dh;
-      aa.max_ctx = max_ctx;
-      aa.max_splits = attn_splits;
-      aa.positions = d_positions;
-      aa.cache_len = d_len;
-      aa.rope = rope;
-      aa.kcache = kcache(l);
-      aa.vcache = vcache(l);
-      aa.part = attn_part;
-      aa.counters = attn_ctr;
-      aa.xo = xout(xf_out.as<__half>(), out);
-      aa.out = nullptr;
-      launch_attn_decode(aa, B, st);
-      gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
-      LnArgs ln;
-      ln.h = h.as<float>();
-      ln.gain = ly.ln1g;
-      ln.bias = ly.ln1b;
-      ln.alpha = static_cast<float>(alpha);
-      ln.eps = static_cast<float>(eps);
-      ln.d = d;
-      ln.x0 = xout(xf_w1.as<__half>(), w1);
-      ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v) : XOut{};  // W1 and V share x unless kRow
-      ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
-      ln.zero_sublayer = zero_sub;
-      launches += ln_after_row_parallel(ln, out, out.plan(B), B);
-      GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
-                axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
-      gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
-      ActArgs act;
-      const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
-      act.w1 = SubIn{partial.as<float>(), fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
-      act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
-      act.M = B;
-      act.f = fl;
-      act.xo = xout(xf_w2.as<__half>(), w2);
-      launch_geglu_act(act, st);
-      gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan(B), st);
-      LnArgs ln2 = ln;
-      ln2.gain = ly.ln2g;
-      ln2.bias = ly.ln2b;
-      const bool last = l + 1 == L;
-      ln2.x0 = last ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]);
-      ln2.x1 = XOut{};
-      ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
-      launches += ln_after_row_parallel(ln2, w2, w2.plan(B), B);
-      launches += 6;  // 4 GEMVs + attention + GeGLU activation
-    }
+    for (int l = 0; l < L; ++l) launches += decode_layer(l, B, d_positions, d_len, l + 1 < L);
     launches += enqueue_head(B, logits.as<float>(), with_logits);
     launch_argmax_finish(d_argmax, d_next, B, st);
     launch_advance(d_len, B, st);
     launch_k(k_feed, dim3(1), dim3(32), 0, st, d_next, d_tokens, d_positions, B);
     LAUNCH_CHECK("k_feed");
     return launches + 3;
+  }
+
+  // One decode block (model.cpp:198-224) for B rows: input x = h (fp32 residual, [B][d]) and
+  // its fp16 copy in xf_qkv (layer l's QKV activation layout); output h (and, when next_x, the
+  // next layer's QKV activations). Row b appends one token at slot cache_len[b] of layer l's
+  // KV cache of sequence b (the caller advances cache_len).
+  int decode_layer(int l, int B, const int* positions, const int* cache_len, bool next_x) {
+    int launches = 0;
+    Layer& ly = layers[l];
+    Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
+    gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan(B), st);
+    AttnDecodeArgs aa;
+    aa.qkv = SubIn{partial.as<float>(), qkv.plan(B).ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
+    aa.d_local = dl;
+    aa.heads = Hl;
+    aa.dh = dh;
+    aa.max_ctx = max_ctx;
+    aa.max_splits = attn_splits;
+    aa.positions = positions;
+    aa.cache_len = cache_len;
+    aa.rope = rope;
+    aa.kcache = kcache(l);
+    aa.vcache = vcache(l);
+    aa.part = attn_part;
+    aa.counters = attn_ctr;
+    aa.xo = xout(xf_out.as<__half>(), out);
+    aa.out = nullptr;
+    launch_attn_decode(aa, B, st);
+    gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
+    LnArgs ln;
+    ln.h = h.as<float>();
+    ln.gain = ly.ln1g;
+    ln.bias = ly.ln1b;
+    ln.alpha = static_cast<float>(alpha);
+    ln.eps = static_cast<float>(eps);
+    ln.d = d;
+    ln.x0 = xout(xf_w1.as<__half>(), w1);
+    ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v) : XOut{};  // W1 and V share x unless kRow
+    ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
+    ln.zero_sublayer = zero_sub;
+    launches += ln_after_row_parallel(ln, out, out.plan(B), B);
+    GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
+              axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
+    gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
+    ActArgs act;
+    const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
+    act.w1 = SubIn{partial.as<float>(), fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
+    act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
+    act.M = B;
+    act.f = fl;
+    act.xo = xout(xf_w2.as<__half>(), w2);
+    launch_geglu_act(act, st);
+    gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan(B), st);
+    LnArgs ln2 = ln;
+    ln2.gain = ly.ln2g;
+    ln2.bias = ly.ln2b;
+    ln2.x0 = next_x ? xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]) : XOut{};
+    ln2.x1 = XOut{};
+    ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
+    launches += ln_after_row_parallel(ln2, w2, w2.plan(B), B);
+    return launches + 6;  // + 4 GEMVs, attention, GeGLU activation
   }
 
   int enqueue_head(int M, float* logit_out, bool gather = true) {
@@ -682,6 +690,141 @@ struct glm_model {
     gemv_reduce(partial.as<float>(), p.ksplit, static_cast<int>(M), lin.w, y, lin.w.L.N, st);
   }
 
+  // One prefill block (model.cpp:198-224) over the n packed rows: input h (fp32) + its fp16
+  // copy in xf_qkv (layer l's QKV layout: tcgen05 tiles when n > 16), output h (+ the next
+  // layer's QKV activations when next_x); segment i (rows row0[i].., sequence seqs[i]) fills
+  // layer l's KV cache of its sequence from slot 0 and attends only to itself.
+  void prefill_layer(int l, int n, int nseg, const int* seqs, const int* lens, const int* ctx, const int* row0,
+                     const int* dpos, bool next_x) {
+    const int nt = n > 16 ? 1 : 0;  // activation layout of this prefill: tcgen05 tiles or x_frag
+    const bool attn_tiles = nt && attn_prefill_umma_eligible(dh);  // attention writes out-proj tiles
+    Layer& ly = layers[l];
+    Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
+    // qkv rows in fp16 straight from the tcgen05 epilogue when RoPE / the KV cache are the only
+    // readers (head_dim 128, unsplit K): half the bytes written and re-read
+    bool qkv_half = false;
+    if (nt && dh == 128) {
+      const GemvPlan pq = plan_qmm(qkv.w.L, n);
+      if (pq.ksplit == 1) {
+        qmm_launch(qkv.w, xf_qkv.as<__half>(), n, partial.as<float>(), pq, st, y_qkv.as<float>(), qkv.w.L.N, nullptr, true);
+        qkv_half = true;
+      }
+    }
+    if (!qkv_half) linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
+    for (int i = 0; i < nseg; ++i) {
+      const int r0 = row0[i], ni = lens[i];
+      float* qseg = q_rot.as<float>() + static_cast<int64_t>(r0) * dl;  // [heads][ni][dh] of this sample
+      RopeStoreArgs rs{y_qkv.as<float>() + static_cast<int64_t>(r0) * 3 * dl, 3ll * dl, dl, ni, Hl, dh, seqs[i],
+                       max_ctx, 0, dpos + r0, rope, qseg, kcache(l), vcache(l)};
+      if (qkv_half) rs.qkv_h = reinterpret_cast<const __half*>(y_qkv.as<float>()) + static_cast<int64_t>(r0) * 3 * dl;
+      launch_rope_store(rs, st);
+      AttnPrefillArgs ap{qseg, kcache(l), vcache(l), ni, Hl, dh, seqs[i], max_ctx, ctx[i],
+                         attn_out.as<float>() + static_cast<int64_t>(r0) * dl, dl};
+      if (attn_tiles) {
+        ap.xo = xout(xf_out.as<__half>(), out, nt);
+        ap.xrow0 = r0;
+      }
+      launch_attn_prefill(ap, st);
+    }
+    if (!attn_tiles) launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
+    linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
+    if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
+    LnArgs ln;
+    ln.in = SubIn{y_out.as<float>(), 1, 0, d, nullptr};
+    ln.h = h.as<float>();
+    ln.gain = ly.ln1g;
+    ln.bias = ly.ln1b;
+    ln.alpha = static_cast<float>(alpha);
+    ln.eps = static_cast<float>(eps);
+    ln.d = d;
+    ln.x0 = xout(xf_w1.as<__half>(), w1, nt);
+    ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v, nt) : XOut{};  // W1 and V share x unless kRow
+    ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
+    ln.zero_sublayer = zero_sub;
+    launch_deepnorm_ln(ln, n, st);
+    if (axis != GLM_AXIS_ROW && qmm_geglu_supported(w1.w, v.w, n)) {  // W1|V GEMM with the GeGLU epilogue
+      const XOut xo = xout(xf_w2.as<__half>(), w2, nt);
+      qmm_geglu_launch(w1.w, v.w, xf_w1.as<__half>(), n, xo.xf, xo.Kp, xo.row_scale, st);
+    } else {
+      linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
+      linear_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), n, y_b.as<float>());
+      ActArgs act;
+      act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
+      act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
+      act.M = n;
+      act.f = fl;
+      act.xo = xout(xf_w2.as<__half>(), w2, nt);
+      launch_geglu_act(act, st);
+    }
+    linear_rows(w2, xf_w2.as<__half>(), n, y_ffn.as<float>());
+    if (tp_size > 1) comm->allreduce_sum(y_ffn.as<float>(), static_cast<int64_t>(n) * d, st);
+    LnArgs ln2 = ln;
+    ln2.in = SubIn{y_ffn.as<float>(), 1, 0, d, nullptr};
+    ln2.gain = ly.ln2g;
+    ln2.bias = ly.ln2b;
+    ln2.x0 = next_x ? xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV], nt) : XOut{};
+    ln2.x1 = XOut{};
+    ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
+    launch_deepnorm_ln(ln2, n, st);
+  }
+
+  // ---- block-level API (glm_block_forward): one layer on caller hidden states ------------
+  // The KV cache is the model's; the block API keeps its own per-layer cache lengths
+  // (blk_len[layer][seq]) so a caller can drive the layers one at a time.
+  std::vector<int> h_blen;  // [L][max_batch]
+  DeviceBuffer d_blen_buf;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+
+  void block_forward(int l, int mode, int seq, float* x, const int* dpos, const int* hpos, int n, int ctx,
+                     cudaStream_t user) {
+    check_loaded();
+    if (l < 0 || l >= L) fail(GLM_CONTRACT, "glmmodel", "layer index out of range");
+    if (mode != GLM_BLOCK_PREFILL && mode != GLM_BLOCK_DECODE) fail(GLM_CONTRACT, "glmmodel", "unknown block mode");
+    if (h_blen.empty()) {
+      h_blen.assign(static_cast<size_t>(L) * max_batch, 0);
+      d_blen_buf.alloc(static_cast<int64_t>(L) * max_batch * 4);
+      CUDA_CHECK(cudaMemsetAsync(d_blen_buf.ptr, 0, d_blen_buf.bytes, st));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    }
+    int* blen = d_blen_buf.as<int>() + static_cast<int64_t>(l) * max_batch;
+    int* hl = h_blen.data() + static_cast<size_t>(l) * max_batch;
+    if (mode == GLM_BLOCK_PREFILL) {
+      if (seq < 0 || seq >= max_batch) fail(GLM_CONTRACT, "glmmodel", "sequence index outside max_batch");
+      if (n < 1 || n > max_ctx) fail(GLM_CONTRACT, "glmmodel", "prefill length must be in 1..max_ctx");
+      if (ctx < 0 || ctx > n) fail(GLM_CONTRACT, "glmmodel", "context_length must be in 0..n");
+    } else {
+      if (n < 1 || n > max_batch) fail(GLM_CONTRACT, "glmmodel", "decode rows must be in 1..max_batch");
+      for (int b = 0; b < n; ++b)
+        if (hl[b] + 1 > max_ctx) fail(GLM_CONTRACT, "glmmodel", "KV cache of sequence " + std::to_string(b) + " is full");
+    }
+    if (hpos)
+      for (int i = 0; i < n; ++i)
+        if (hpos[i] < 0 || hpos[i] > max_ctx) fail(GLM_CONTRACT, "glmmodel", "position outside the RoPE table");
+    if (mode == GLM_BLOCK_PREFILL) ensure_prefill(n);
+    if (taps) ensure_taps(n);
+    CUDA_CHECK(cudaEventRecord(ev_in, user));
+    CUDA_CHECK(cudaStreamWaitEvent(st, ev_in, 0));
+    const int nt = (mode == GLM_BLOCK_PREFILL && n > 16) ? 1 : 0;
+    CUDA_CHECK(cudaMemcpyAsync(h.ptr, x, static_cast<int64_t>(n) * d * 4, cudaMemcpyDeviceToDevice, st));
+    launch_rows_to_xfrag(h.as<float>(), d, n, d, xout(xf_qkv.as<__half>(), layers[l].lin[QKV], nt), st);
+    if (mode == GLM_BLOCK_PREFILL) {
+      const int row0[2] = {0, n};
+      prefill_layer(l, n, 1, &seq, &n, &ctx, row0, dpos, false);
+      CUDA_CHECK(cudaMemcpyAsync(blen + seq, &n, 4, cudaMemcpyHostToDevice, st));
+    } else {
+      decode_layer(l, n, dpos, blen, false);
+      launch_advance(blen, n, st);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(x, h.ptr, static_cast<int64_t>(n) * d * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaEventRecord(ev_out, st));
+    CUDA_CHECK(cudaStreamWaitEvent(user, ev_out, 0));
+    if (mode == GLM_BLOCK_PREFILL) hl[seq] = n;
+    else
+      for (int b = 0; b < n; ++b) hl[b] += 1;
+    last_rows = n;
+  }
+
   void prefill(int seq, const int* tokens, const int* positions, int n, int context_len, float* logits_out) {
     prefill_batch(1, &seq, &n, &context_len, tokens, positions, logits_out);
   }
@@ -712,82 +855,12 @@ struct glm_model {
     }
     ensure_prefill(n);
     const int nt = n > 16 ? 1 : 0;  // activation layout of this prefill: tcgen05 tiles or x_frag
-    const bool attn_tiles = nt && attn_prefill_umma_eligible(dh);  // attention writes out-proj tiles
     if (taps) ensure_taps(n);
     DeviceBuffer dtok(n * 4), dpos(n * 4);
     CUDA_CHECK(cudaMemcpyAsync(dtok.ptr, tokens, n * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(dpos.ptr, positions, n * 4, cudaMemcpyHostToDevice, st));
     launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV], nt), st);
-    for (int l = 0; l < L; ++l) {
-      Layer& ly = layers[l];
-      Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
-      // qkv rows in fp16 straight from the tcgen05 epilogue when RoPE / the KV cache are the only
-      // readers (head_dim 128, unsplit K): half the bytes written and re-read
-      bool qkv_half = false;
-      if (nt && dh == 128) {
-        const GemvPlan pq = plan_qmm(qkv.w.L, n);
-        if (pq.ksplit == 1) {
-          qmm_launch(qkv.w, xf_qkv.as<__half>(), n, partial.as<float>(), pq, st, y_qkv.as<float>(), qkv.w.L.N, nullptr, true);
-          qkv_half = true;
-        }
-      }
-      if (!qkv_half) linear_rows(qkv, xf_qkv.as<__half>(), n, y_qkv.as<float>());
-      for (int i = 0; i < nseg; ++i) {
-        const int r0 = row0[i], ni = lens[i];
-        float* qseg = q_rot.as<float>() + static_cast<int64_t>(r0) * dl;  // [heads][ni][dh] of this sample
-        RopeStoreArgs rs{y_qkv.as<float>() + static_cast<int64_t>(r0) * 3 * dl, 3ll * dl, dl, ni, Hl, dh, seqs[i],
-                         max_ctx, 0, dpos.as<int>() + r0, rope, qseg, kcache(l), vcache(l)};
-        if (qkv_half) rs.qkv_h = reinterpret_cast<const __half*>(y_qkv.as<float>()) + static_cast<int64_t>(r0) * 3 * dl;
-        launch_rope_store(rs, st);
-        AttnPrefillArgs ap{qseg, kcache(l), vcache(l), ni, Hl, dh, seqs[i], max_ctx, ctx[i],
-                           attn_out.as<float>() + static_cast<int64_t>(r0) * dl, dl};
-        if (attn_tiles) {
-          ap.xo = xout(xf_out.as<__half>(), out, nt);
-          ap.xrow0 = r0;
-        }
-        launch_attn_prefill(ap, st);
-      }
-      if (!attn_tiles) launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
-      linear_rows(out, xf_out.as<__half>(), n, y_out.as<float>());
-      if (tp_size > 1) comm->allreduce_sum(y_out.as<float>(), static_cast<int64_t>(n) * d, st);
-      LnArgs ln;
-      ln.in = SubIn{y_out.as<float>(), 1, 0, d, nullptr};
-      ln.h = h.as<float>();
-      ln.gain = ly.ln1g;
-      ln.bias = ly.ln1b;
-      ln.alpha = static_cast<float>(alpha);
-      ln.eps = static_cast<float>(eps);
-      ln.d = d;
-      ln.x0 = xout(xf_w1.as<__half>(), w1, nt);
-      ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v, nt) : XOut{};  // W1 and V share x unless kRow
-      ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
-      ln.zero_sublayer = zero_sub;
-      launch_deepnorm_ln(ln, n, st);
-      if (axis != GLM_AXIS_ROW && qmm_geglu_supported(w1.w, v.w, n)) {  // W1|V GEMM with the GeGLU epilogue
-        const XOut xo = xout(xf_w2.as<__half>(), w2, nt);
-        qmm_geglu_launch(w1.w, v.w, xf_w1.as<__half>(), n, xo.xf, xo.Kp, xo.row_scale, st);
-      } else {
-        linear_rows(w1, xf_w1.as<__half>(), n, y_a.as<float>());
-        linear_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), n, y_b.as<float>());
-        ActArgs act;
-        act.w1 = SubIn{y_a.as<float>(), 1, 0, fl, nullptr};
-        act.v = SubIn{y_b.as<float>(), 1, 0, fl, nullptr};
-        act.M = n;
-        act.f = fl;
-        act.xo = xout(xf_w2.as<__half>(), w2, nt);
-        launch_geglu_act(act, st);
-      }
-      linear_rows(w2, xf_w2.as<__half>(), n, y_ffn.as<float>());
-      if (tp_size > 1) comm->allreduce_sum(y_ffn.as<float>(), static_cast<int64_t>(n) * d, st);
-      LnArgs ln2 = ln;
-      ln2.in = SubIn{y_ffn.as<float>(), 1, 0, d, nullptr};
-      ln2.gain = ly.ln2g;
-      ln2.bias = ly.ln2b;
-      ln2.x0 = l + 1 == L ? XOut{} : xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV], nt);
-      ln2.x1 = XOut{};
-      ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
-      launch_deepnorm_ln(ln2, n, st);
-    }
+    for (int l = 0; l < L; ++l) prefill_layer(l, n, nseg, seqs, lens, ctx, row0.data(), dpos.as<int>(), l + 1 < L);
     if (logits_out) {
       enqueue_head(n, logits.as<float>());
       launch_argmax_finish(d_argmax, d_next_rows, n, st);
@@ -967,6 +1040,32 @@ glm_status glm_model_reset(glm_model* m) {
     checked(m);
     std::fill(m->h_len.begin(), m->h_len.end(), 0);
     CUDA_CHECK(cudaMemsetAsync(m->d_len, 0, m->max_batch * sizeof(int), m->st));
+    std::fill(m->h_blen.begin(), m->h_blen.end(), 0);
+    if (m->d_blen_buf.bytes) CUDA_CHECK(cudaMemsetAsync(m->d_blen_buf.ptr, 0, m->d_blen_buf.bytes, m->st));
+    CUDA_CHECK(cudaStreamSynchronize(m->st));
+  });
+}
+
+glm_status glm_block_forward(glm_model* m, int layer, glm_block_mode mode, int seq, float* x_io, const int* positions,
+                             int n, int context_length, void* stream) {
+  return guarded([&] {
+    if (!x_io || !positions) fail(GLM_CONTRACT, "glmmodel", "null argument");
+    checked(m)->block_forward(layer, mode, seq, x_io, positions, nullptr, n, context_length,
+                              static_cast<cudaStream_t>(stream));
+  });
+}
+
+glm_status glm_block_forward_host(glm_model* m, int layer, glm_block_mode mode, int seq, float* x_io,
+                                  const int* positions, int n, int context_length) {
+  return guarded([&] {
+    if (!x_io || !positions) fail(GLM_CONTRACT, "glmmodel", "null argument");
+    checked(m);
+    if (n < 1 || n > std::max(m->max_ctx, m->max_batch)) fail(GLM_CONTRACT, "glmmodel", "row count out of range");
+    DeviceBuffer dx(static_cast<int64_t>(n) * m->d * 4), dp(static_cast<int64_t>(n) * 4);
+    CUDA_CHECK(cudaMemcpy(dx.ptr, x_io, dx.bytes, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(dp.ptr, positions, dp.bytes, cudaMemcpyHostToDevice));
+    m->block_forward(layer, mode, seq, dx.as<float>(), dp.as<int>(), positions, n, context_length, m->st);
+    CUDA_CHECK(cudaMemcpyAsync(x_io, dx.ptr, dx.bytes, cudaMemcpyDeviceToHost, m->st));
     CUDA_CHECK(cudaStreamSynchronize(m->st));
   });
 }

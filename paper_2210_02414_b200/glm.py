@@ -115,6 +115,14 @@ SIGNATURES = {
     "glm_model_enable_taps": (I32, [P, I32]),
     "glm_model_get_taps": (I32, [P, P, P]),
     "glm_model_zero_sublayers": (I32, [P, I32]),
+    "glm_block_forward": (I32, [P, I32, I32, I32, P, P, I32, I32, P]),
+    "glm_block_forward_host": (I32, [P, I32, I32, I32, P, P, I32, I32]),
+    "glm_deepnorm_residual": (I32, [P, P, I64, I64, D, P, P, D, P, P]),
+    "glm_deepnorm_residual_host": (I32, [P, P, I64, I64, D, P, P, D, P]),
+    "glm_geglu": (I32, [P, P, P, P, I64, P, P]),
+    "glm_geglu_host": (I32, [P, P, P, P, I64, P]),
+    "glm_attention": (I32, [P, P, P, I64, I64, P, P, P, P]),
+    "glm_attention_host": (I32, [P, P, P, I64, I64, P, P, P]),
     "glm_model_bench_decode": (I32, [P, I32, I32, I32, C.POINTER(D), C.POINTER(D), C.POINTER(I32)]),
 }
 
@@ -212,6 +220,40 @@ def unpack_int4(packed, count):
     packed = np.ascontiguousarray(packed, np.int8)
     out = np.zeros(max(count, 0), np.int8)
     _check(lib().glm_unpack_int4(_p(packed), len(packed), count, _p(out)))
+    return out
+
+
+def deepnorm_residual(x, y, alpha, gain, bias, eps=1e-5):
+    """deepnorm_residual (model.hpp:70-71, model.cpp:125-131) on the GPU: LN(alpha x + y)."""
+    x = np.ascontiguousarray(np.atleast_2d(x), np.float32)
+    y = np.ascontiguousarray(np.atleast_2d(y), np.float32)
+    if x.shape != y.shape:
+        raise DimensionError("[glmmodel] deepnorm_residual operands must share a shape")
+    g = np.ascontiguousarray(gain, np.float32)
+    b = np.ascontiguousarray(bias, np.float32)
+    out = np.empty_like(x)
+    _check(lib().glm_deepnorm_residual_host(_p(x), _p(y), x.shape[0], x.shape[1], alpha, _p(g), _p(b), eps, _p(out)))
+    return out
+
+
+def geglu(x, w1, v, w2):
+    """geglu (model.hpp:74, model.cpp:133-135) with quantized W1, V, W2 (QLinear handles)."""
+    x = np.ascontiguousarray(np.atleast_2d(x), np.float32)
+    y = np.empty((x.shape[0], w2.cols), np.float32)
+    _check(lib().glm_geglu_host(w1.h, v.h, w2.h, _p(x), x.shape[0], _p(y)))
+    return y
+
+
+def attention(q, k, v, positions, mask):
+    """Single-head attention (model.hpp:78-80, model.cpp:137-152) with a boolean mask."""
+    q = np.ascontiguousarray(q, np.float32)
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    pos = np.ascontiguousarray(positions, np.int32)
+    mk = np.ascontiguousarray(mask, np.uint8)
+    n, dh = q.shape
+    out = np.empty((n, dh), np.float32)
+    _check(lib().glm_attention_host(_p(q), _p(k), _p(v), n, dh, _p(pos), _p(mk), _p(out)))
     return out
 
 
@@ -474,6 +516,18 @@ class Model:
         out = np.empty((b, self.cfg.vocab), np.float32) if logits else None
         _check(lib().glm_model_decode_step(self.h, b, _p(tokens), _p(positions), _p(nxt), _p(out)))
         return nxt, out
+
+    def block_forward(self, layer, x, positions, mode="prefill", seq=0, context_length=None):
+        """glm_block_forward_host: one GLM block (model.cpp:198-224) of `layer` on hidden
+        states x [n, hidden]; prefill fills the layer's KV cache of `seq`, decode appends row b
+        to sequence b. Returns the block output."""
+        x = np.ascontiguousarray(np.atleast_2d(x), np.float32).copy()
+        pos = np.ascontiguousarray(np.atleast_1d(positions), np.int32)
+        n = x.shape[0]
+        ctx = n if context_length is None else context_length
+        _check(lib().glm_block_forward_host(self.h, layer, {"prefill": 0, "decode": 1}[mode], seq, _p(x), _p(pos), n,
+                                            ctx))
+        return x
 
     def cached_length(self, seq=0):
         return lib().glm_model_cached_length(self.h, seq)

@@ -85,8 +85,24 @@ def build_cpp_test():
     return out
 
 
+def build_cpp_block_test():
+    """Compile tests/cpp/test_block_capi.cpp: the product through glm130b.hpp, checked against
+    the CPU oracle (oracle/liboracle.so, test infrastructure) linked into the test binary."""
+    out = os.path.join(ROOT, "build", "test_block_capi")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    libdir = os.path.dirname(glm.LIB_PATH)
+    odir = os.path.join(ROOT, "oracle")
+    if not os.path.exists(os.path.join(odir, "liboracle.so")):
+        subprocess.run(["make", "-s", "-C", odir], check=True)
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_block_capi.cpp"), "-L" + libdir, "-lglm130b",
+                    "-L" + odir, "-loracle", "-Wl,-rpath," + libdir + ":" + odir, "-o", out], check=True)
+    return out
+
+
 def test_cpp_wrapper_compiles_and_links():
     assert os.path.exists(build_cpp_test())
+    assert os.path.exists(build_cpp_block_test())
 
 
 @pytest.mark.skipif(_has_gpu(), reason="a GPU is present; the no-GPU failure mode is not observable")
