@@ -577,6 +577,42 @@ void or_gen_matrix(uint64_t seed, uint32_t tensor_id, int64_t rows, int64_t cols
     }
 }
 
+void or_gen_rows(uint64_t seed, uint32_t tensor_id, int64_t row0, int64_t nrows, int64_t cols, float sigma_lo,
+                 float sigma_hi, int64_t split_col, double* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < nrows; ++r)
+    for (int64_t c = 0; c < cols; ++c) {
+      const uint64_t flat = static_cast<uint64_t>((row0 + r) * cols + c);
+      out[r * cols + c] = bf16_to_double(gen_bf16(seed, tensor_id, flat, c < split_col ? sigma_lo : sigma_hi));
+    }
+}
+
+int or_dequantize_cols(const int8_t* payload, const double* scales, int64_t rows, int64_t cols, int bits, int axis,
+                       const int64_t* sel, int64_t nsel, double* out) {
+  // dequantize (quant.cpp:188-221, absmax: W[r][c] = s_g * code, codes unpacked as
+  // unpack_int4 does, quant.cpp:242-255) for the selected columns only: out [rows, nsel]
+  return guarded([&] {
+    check_bits(bits);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t j = 0; j < nsel; ++j) {
+        const int64_t c = sel[j];
+        if (c < 0 || c >= cols) continue;
+        const int64_t flat = r * cols + c;
+        int code;
+        if (bits == 8) {
+          code = payload[flat];
+        } else {
+          const uint8_t byte = static_cast<uint8_t>(payload[flat / 2]);
+          code = (flat % 2 == 0) ? (byte & 0x0f) : (byte >> 4);
+          if (code >= 8) code -= 16;
+        }
+        const double sc = axis == OR_AXIS_ROW ? scales[r] : axis == OR_AXIS_COLUMN ? scales[c] : scales[0];
+        out[r * nsel + j] = sc * static_cast<double>(code);
+      }
+  });
+}
+
 or_params* or_params_init_philox(const or_config* cfg, uint64_t seed) {
   // Same stds as model.cpp:69-104, values from the counter-based generator.
   or_params* p = nullptr;

@@ -97,6 +97,12 @@ uint16_t or_philox_bf16(uint64_t seed, uint32_t tensor_id, uint64_t flat, float 
 double or_bf16_to_double(uint16_t b);
 void or_gen_matrix(uint64_t seed, uint32_t tensor_id, int64_t rows, int64_t cols,
                    float sigma_lo, float sigma_hi, int64_t split_col, double* out);
+/* rows [row0, row0 + nrows) of or_gen_matrix's matrix (chunked generation of large tables) */
+void or_gen_rows(uint64_t seed, uint32_t tensor_id, int64_t row0, int64_t nrows, int64_t cols,
+                 float sigma_lo, float sigma_hi, int64_t split_col, double* out);
+/* dequantize (quant.cpp:188-221, absmax) restricted to the columns sel[0..nsel): out [rows, nsel] */
+int or_dequantize_cols(const int8_t* payload, const double* scales, int64_t rows, int64_t cols, int bits,
+                       int axis, const int64_t* sel, int64_t nsel, double* out);
 /* quantized-linear oracle: y[M,N] = x[M,K] . dequantize(q) (quant.cpp:188-221 then
  * tensor.cpp:135-155), restricted to output columns cols[0..ncols) */
 int or_qlinear_cols(const double* x, int64_t M, int64_t K, int64_t N, const int8_t* payload,

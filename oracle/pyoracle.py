@@ -85,6 +85,8 @@ def lib():
         L.or_fnv1a64.argtypes = [p, i64, C.c_uint64]
         L.or_fnv1a64.restype = C.c_uint64
         L.or_qlinear_cols.argtypes = [p, i64, i64, i64, p, p, i32, i32, p, i64, p]
+        L.or_gen_rows.argtypes = [C.c_uint64, C.c_uint32, i64, i64, i64, C.c_float, C.c_float, i64, p]
+        L.or_dequantize_cols.argtypes = [p, p, i64, i64, i32, i32, p, i64, p]
         _LIB = L
     return _LIB
 
@@ -308,6 +310,58 @@ def gen_matrix(seed, tensor_id, rows, cols, sigma_lo, sigma_hi=None, split_col=N
     split_col = cols if split_col is None else split_col
     lib().or_gen_matrix(seed, tensor_id, rows, cols, sigma_lo, sigma_hi, split_col, _ptr(out))
     return out
+
+
+def gen_rows(seed, tensor_id, row0, nrows, cols, sigma_lo, sigma_hi=None, split_col=None):
+    """Rows [row0, row0 + nrows) of gen_matrix(seed, tensor_id, ., cols, ...)."""
+    out = np.empty((nrows, cols), np.float64)
+    sigma_hi = sigma_lo if sigma_hi is None else sigma_hi
+    split_col = cols if split_col is None else split_col
+    lib().or_gen_rows(seed, tensor_id, row0, nrows, cols, sigma_lo, sigma_hi, split_col, _ptr(out))
+    return out
+
+
+def dequantize_cols(q, cols):
+    """dequantize(q) (quant.cpp:188-221, absmax) restricted to output columns `cols`: [rows, len(cols)]."""
+    cols = np.ascontiguousarray(cols, np.int64)
+    out = np.empty((q["rows"], len(cols)), np.float64)
+    _check(lib().or_dequantize_cols(_ptr(np.ascontiguousarray(q["payload"])), _ptr(np.ascontiguousarray(q["scales"])),
+                                    q["rows"], q["cols"], q["bits"], AXIS[q["axis"]], _ptr(cols), len(cols), _ptr(out)))
+    return out
+
+
+def block_forward(x, W, ln, positions, mask, num_heads, alpha, eps=1e-5):
+    """One GLM block (model.cpp:198-224) in float64 on hidden states x [n, d]: W = dense
+    (dequantized) [in, out] matrices indexed QKV / OUT / W1 / V / W2; ln = (g1, b1, g2, b2);
+    mask [n, n] bool. Per head (model.cpp:141-152): RoPE(q), RoPE(k) (tensor.cpp:335-394,
+    or_rope_rotate), scores / sqrt(dh), invisible -> -inf, wide softmax (tensor.cpp:221-254),
+    P . v; then out_proj, deepnorm_residual (model.cpp:125-131), geglu (model.cpp:133-135),
+    deepnorm_residual. Returns (out, attention sublayer output, GeGLU sublayer output)."""
+    x = np.ascontiguousarray(x, np.float64)
+    n, d = x.shape
+    dh = d // num_heads
+    qkv = x @ W[QKV]
+    pos_all = np.tile(np.asarray(positions, np.int32), num_heads)
+
+    def heads(a):  # [n, d] -> [H * n, dh] (head-major rows)
+        return np.ascontiguousarray(a.reshape(n, num_heads, dh).transpose(1, 0, 2).reshape(num_heads * n, dh))
+
+    rq = rope_rotate(heads(qkv[:, :d]), pos_all).reshape(num_heads, n, dh)
+    rk = rope_rotate(heads(qkv[:, d:2 * d]), pos_all).reshape(num_heads, n, dh)
+    vh = heads(qkv[:, 2 * d:]).reshape(num_heads, n, dh)
+    sc = np.einsum("hid,hjd->hij", rq, rk) / np.sqrt(dh)
+    sc[:, ~np.asarray(mask, bool)] = -np.inf
+    if np.isneginf(sc.max(axis=2)).any():
+        raise OracleError(4, "[tensorcore] softmax row is entirely -inf; no distribution is defined")
+    sc = np.exp(sc - sc.max(axis=2, keepdims=True))
+    sc /= sc.sum(axis=2, keepdims=True)
+    att = np.einsum("hij,hjd->hid", sc, vh).transpose(1, 0, 2).reshape(n, d)
+    attn = att @ W[OUT]
+    g1, b1, g2, b2 = ln
+    h = layer_norm(alpha * x + attn, g1, b1, eps)
+    ff = (gelu(h @ W[W1]) * (h @ W[V])) @ W[W2]
+    out = layer_norm(alpha * h + ff, g2, b2, eps)
+    return out, attn, ff
 
 
 def qlinear_cols(x, q, cols):

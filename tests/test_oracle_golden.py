@@ -203,3 +203,40 @@ def test_philox_generator_is_deterministic_and_normal():
     # values are bf16-representable
     f = w.astype(np.float32).view(np.uint32)
     assert (f & 0xFFFF == 0).all()
+
+
+def test_numpy_block_oracle_equals_or_forward_taps():
+    """pyoracle.block_forward (the G-shape block oracle, model.cpp:198-224 restated over the
+    oracle's ops + numpy GEMMs) chained from the embedding rows reproduces or_forward's
+    per-layer sublayer taps and final logits (tiny config, INT4 kColumn weights)."""
+    import numpy as np
+    from oracle import pyoracle as O
+
+    p = O.Params(2, 256, 4, vocab=262, seed=5)
+    p.quantize(4, "column")
+    sample = O.gmask_sample([6 + (37 * i + 11) % 256 for i in range(30)], [40, 41])
+    ref, at, ft = p.forward(sample, taps=True)
+    n = sample["n"]
+    mask = O.build_mask(sample)
+    x = p.tensor(0, O.EMBED)[sample["tokens"]]
+    ones, zeros = np.ones(256), np.zeros(256)
+    alpha = np.sqrt(4.0)
+    for layer in range(2):
+        W = {w: p.tensor(layer, w) for w in range(5)}
+        x, attn, ff = O.block_forward(x, W, (ones, zeros, ones, zeros), sample["positions"], mask, 4, alpha)
+        assert np.abs(attn - at[layer]).max() <= 1e-12 * np.abs(at[layer]).max()
+        assert np.abs(ff - ft[layer]).max() <= 1e-12 * np.abs(ft[layer]).max()
+    logits = x @ p.tensor(0, O.EMBED).T
+    assert np.abs(logits - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert n == ref.shape[0]
+
+
+def test_oracle_chunked_generation_and_column_dequantize():
+    import numpy as np
+    from oracle import pyoracle as O
+
+    a = O.gen_matrix(3, 5, 10, 7, 0.1)
+    assert np.array_equal(a[4:7], O.gen_rows(3, 5, 4, 3, 7, 0.1))
+    for bits, axis in ((4, "column"), (8, "row"), (4, "whole")):
+        q = O.quantize(np.random.default_rng(bits).normal(size=(33, 21)), bits, axis)
+        assert np.array_equal(O.dequantize_cols(q, [0, 5, 20]), O.dequantize(q)[:, [0, 5, 20]])
