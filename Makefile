@@ -13,7 +13,7 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS     := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.cpp.o,$(CPP_SRCS))
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h)
 
-all: $(OUT) oracle
+all: $(OUT) oracle ref
 
 $(OBJDIR)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -29,8 +29,13 @@ $(OUT): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# the reference's own sources as oracle/_ref (test infrastructure; skipped without /root/reference)
+ref: oracle
+	oracle/build_ref.sh
+
 clean:
 	rm -rf build $(OUT)
 	$(MAKE) -s -C oracle clean
+	rm -rf oracle/_ref
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle ref

@@ -13,9 +13,11 @@ Timed regions (CUDA events on the model's stream, max over ranks):
   roofline: the W4A16 GEMV launches of one step replayed alone, algorithmic bytes
            (codes + fp32 scales + fp16 activations + fp32 partials) / their event time
 
-`--impl reference` times the reference's CPU path (oracle port of x . dequantize(q), the
-reference's forward() arithmetic, quant.cpp:188-221 + tensor.cpp:135-155) on one GLM-130B
-layer per step with all host threads and extrapolates to 70 layers + head.
+`--impl reference` times the reference's own CPU path: oracle/_ref, the reference's unmodified
+sources built with the test-infrastructure stand-ins (oracle/build_ref.sh; the Eigen product on
+OpenBLAS dgemm with all host threads): one decode token through one GLM-130B-shaped layer per
+step, extrapolated to 70 layers + the tied head (the oracle port when _ref is not built).
+The same measurement, bounded to a few steps, is the `cpu_baseline` of the B200 line.
 """
 import argparse
 import json
@@ -150,7 +152,51 @@ def cpu_layer_step(mats, x):
     return O.qlinear_full(g, mats[4]), np.abs(qkv).max()
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(steps, warmup):
+    """The reference's CPU path timed on this host: oracle/_ref (the reference's own sources,
+    oracle/build_ref.sh) when built, else the oracle port."""
+    try:
+        from oracle import pyref as R
+        if R.available():
+            return cpu_baseline_reference(R, steps, warmup)
+    except Exception as e:  # noqa: BLE001 - reported in the sample text of the port baseline
+        print(f"bench.py: reference CPU baseline unavailable ({e}); timing the oracle port", file=sys.stderr)
+    return cpu_baseline_port(steps, warmup)
+
+
+def cpu_baseline_reference(R, steps, warmup):
+    threads = os.cpu_count() or 1
+    head_rows = 16384
+    layer_s, setup_s, head_slice_s = R.bench_layer_decode(seed=2210, bits=4, axis="column", ctx=PROMPT + 3,
+                                                          warmup=warmup, steps=steps, threads=threads,
+                                                          head_vocab=head_rows)
+    head_s = head_slice_s * G["vocab"] / head_rows
+    token_s = G["num_layers"] * layer_s + head_s
+    return {
+        "value": 1.0 / token_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
+        "sample": (f"the reference's own sources (oracle/_ref: tensor/quant/model.cpp unmodified, Eigen stand-in "
+                   f"product on OpenBLAS dgemm with {threads} threads, {cpu_model()}): one decode token through one "
+                   f"GLM-130B-shaped layer per step (INT4 kColumn weights through quantize_absmax + dequantize, "
+                   f"matmul / attention over {PROMPT + 3} rows / deepnorm_residual / geglu, model.cpp:198-224), "
+                   f"mean of {steps} after {warmup} warm-up = {layer_s:.3f} s/layer; x70 layers + the tied head "
+                   f"matmul(h, transpose(E)) timed on {head_rows} of {G['vocab']} rows ({head_slice_s:.2f} s) and scaled "
+                   f"linearly; setup {setup_s:.0f} s; no KV cache exists in the reference, the harness reuses the "
+                   f"earlier rows' q/k/v"),
+        "seconds_per_token": token_s,
+    }
+
+
+def cpu_baseline_port(steps, warmup):
     import numpy as np
     t0 = time.time()
     mats = cpu_layer_setup()
@@ -171,7 +217,7 @@ def cpu_baseline(steps, warmup):
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {
         "value": 1.0 / token_s, "unit": "tokens/s", "cores": threads, "kind": "port",
-        "sample": (f"one GLM-130B layer decode (5 INT4 per-output-channel linears, x . dequantize(q) in f64, "
+        "sample": (f"oracle port ({cpu_model()}): one GLM-130B layer decode (5 INT4 per-output-channel linears, x . dequantize(q) in f64, "
                    f"oracle port of quant.cpp:188-221 + tensor.cpp:135-155) per step, median of {steps} after "
                    f"{warmup} warm-up; extrapolated x70 layers + head by MACs; {layer_s:.2f} s/layer; "
                    f"setup {setup_s:.0f} s (gen+quantize one layer)"),
@@ -187,7 +233,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_token"] * 1000.0,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "GLM-130B INT4 decode, batch 1 (CPU reference path, extrapolated from one layer)",
+            "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode, batch 1 (the reference's CPU path; one layer "
+                                   "per step, extrapolated x70 + head)",
                        "model": "GLM-130B-shaped (70L, d 12288, 96 heads, ffn 32768, vocab 150528)",
                        "global_batch": 1, "seq_len": PROMPT + 2, "parallelism": "cpu"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -317,6 +364,7 @@ def run_ours(args):
         "init_seconds": init_s,
     }
     if not args.no_cpu_baseline and world == 1:
+        del m  # the CPU baseline needs ~40 GB of host memory; the model's device state is done
         cb = cpu_baseline(max(1, min(3, args.steps)), 1)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
