@@ -131,30 +131,79 @@ constexpr int kLnCluster = 8;
 constexpr int kLnThreads = 384;
 constexpr int kLnPairs = 4;  // pairs per thread: d <= 2 * 4 * 384 * 8 = 24576
 
-// Cluster-wide sum of (a, b): each CTA pushes its partial into slot[rank] of every CTA of
-// the cluster (distributed shared memory stores), one cluster barrier (release/acquire),
-// then every CTA sums its local slots in rank order: identical on every CTA and every run.
-__device__ __forceinline__ float2 cluster_sum2(float2 v, float2* red, float2* slots) {
+// Row statistics (mean, biased variance; tensor.cpp:264-267) without the E[z^2] - mean^2
+// cancellation: every partial is (count, mean, M2 = sum of squared deviations from its own
+// mean) and partials merge with Chan et al.'s pairwise update, so a row whose mean is large
+// against its spread (loaded checkpoints with LN biases) keeps full fp32 precision. All merges
+// run in a fixed order: identical results on every CTA, rank and run.
+struct RowStat {
+  float n, mean, m2;
+};
+__device__ __forceinline__ RowStat stat_merge(RowStat a, RowStat b) {
+  const float n = a.n + b.n;
+  if (b.n == 0.f) return a;
+  if (a.n == 0.f) return b;
+  const float d = b.mean - a.mean, f = b.n / n;
+  return RowStat{n, fmaf(d, f, a.mean), a.m2 + b.m2 + d * d * a.n * f};
+}
+// A thread's own values accumulate as shifted sums about the first value it sees (K): within
+// a row |z - K| is a few standard deviations, so S2 - S1^2 / n loses only a few bits; the
+// per-thread partials then merge exactly (stat_merge).
+struct ShiftedSums {
+  float k = 0.f, s1 = 0.f, s2 = 0.f, n = 0.f;
+  __device__ __forceinline__ void add(float v) {
+    if (n == 0.f) k = v;
+    const float t = v - k;
+    s1 += t;
+    s2 = fmaf(t, t, s2);
+    n += 1.f;
+  }
+  __device__ __forceinline__ RowStat stat() const {
+    if (n == 0.f) return RowStat{0.f, 0.f, 0.f};
+    return RowStat{n, k + s1 / n, fmaxf(s2 - s1 * s1 / n, 0.f)};
+  }
+};
+__device__ __forceinline__ RowStat warp_stat(RowStat a) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    RowStat b{__shfl_xor_sync(0xffffffffu, a.n, o), __shfl_xor_sync(0xffffffffu, a.mean, o),
+              __shfl_xor_sync(0xffffffffu, a.m2, o)};
+    // merge in lane order so both partners compute the same bits
+    a = (threadIdx.x & o) ? stat_merge(b, a) : stat_merge(a, b);
+  }
+  return a;
+}
+// CTA-wide statistics (NT threads), fixed merge order; `red` holds NT / 32 entries
+template <int NT>
+__device__ __forceinline__ RowStat block_stat(RowStat a, RowStat* red) {
+  a = warp_stat(a);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = a;
+  __syncthreads();
+  RowStat t = red[0];
+  for (int i = 1; i < NT / 32; ++i) t = stat_merge(t, red[i]);
+  return t;
+}
+
+// Cluster-wide statistics: each CTA pushes its partial into slot[rank] of every CTA of the
+// cluster (distributed shared memory stores), one cluster barrier (release/acquire), then
+// every CTA merges its local slots in rank order: identical on every CTA and every run.
+__device__ __forceinline__ RowStat cluster_stat(RowStat v, RowStat* red, RowStat* slots) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  v.x = warp_sum(v.x);
-  v.y = warp_sum(v.y);
+  v = warp_stat(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
   if (w == 0) {
-    float2 t = l < kLnThreads / 32 ? red[l] : make_float2(0.f, 0.f);
-    t.x = warp_sum(t.x);
-    t.y = warp_sum(t.y);
+    RowStat t = red[0];
+    for (int i = 1; i < kLnThreads / 32; ++i) t = stat_merge(t, red[i]);
     const unsigned rank = cluster.block_rank();
     if (l < kLnCluster) *cluster.map_shared_rank(slots + rank, l) = t;
   }
   cluster.sync();
-  float2 r = make_float2(0.f, 0.f);
-  for (int i = 0; i < kLnCluster; ++i) {
-    r.x += slots[i].x;
-    r.y += slots[i].y;
-  }
+  RowStat r = slots[0];
+  for (int i = 1; i < kLnCluster; ++i) r = stat_merge(r, slots[i]);
   return r;
 }
 
@@ -228,8 +277,8 @@ __device__ __forceinline__ bool peer_allreduce(const PeerArgs& P, int m, int cra
 
 __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
   trace_point(20);
-  __shared__ float2 red[kLnThreads / 32];
-  __shared__ float2 slots[kLnCluster];
+  __shared__ RowStat red[kLnThreads / 32];
+  __shared__ RowStat slots[kLnCluster];
   namespace cg = cooperative_groups;
   const int rank = static_cast<int>(cg::this_cluster().block_rank());
   const int m = blockIdx.x / kLnCluster;
@@ -286,7 +335,7 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
   }
   if (a.peer.size > 1 && !peer_allreduce(a.peer, m, rank, p0, p1, y)) return;  // push-only launch
   float2 z[kLnPairs];
-  float2 acc = make_float2(0.f, 0.f);
+  ShiftedSums st;
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
@@ -294,17 +343,16 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
     if (p < p1) {
       z[i] = make_float2(a.alpha * hv[i].x + y[i].x, a.alpha * hv[i].y + y[i].y);
       if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + 2 * p) = y[i];
-      acc.x += z[i].x + z[i].y;
-      acc.y += z[i].x * z[i].x + z[i].y * z[i].y;
+      st.add(z[i].x);
+      st.add(z[i].y);
     }
   }
-  // one cluster reduction of (sum, sum of squares); biased variance (tensor.cpp:267)
+  // one cluster reduction of (count, mean, M2); biased variance (tensor.cpp:267)
   trace_point(23);
-  const float2 tot = cluster_sum2(acc, red, slots);
+  const RowStat tot = cluster_stat(st.stat(), red, slots);
   trace_point(24);
-  const float inv_d = 1.f / static_cast<float>(a.d);
-  const float mean = tot.x * inv_d;
-  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);
+  const float mean = tot.mean;
+  const float var = tot.m2 / static_cast<float>(a.d);
   const float rstd = rsqrtf(var + a.eps);
 #pragma unroll
   for (int i = 0; i < kLnPairs; ++i) {
@@ -328,11 +376,11 @@ constexpr int kLnRowThreads = 512;
 __global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float2 red[kLnRowThreads / 32];
+  __shared__ RowStat red[kLnRowThreads / 32];
   const int m = blockIdx.x;
   const int64_t npairs = a.d / 2;
   float* hrow = a.h + static_cast<int64_t>(m) * a.d;
-  float2 acc = make_float2(0.f, 0.f);
+  ShiftedSums acc;
   // pass 1: z = alpha h + y (kept in h), statistics
   for (int64_t p = threadIdx.x; p < npairs; p += kLnRowThreads) {
     const int64_t n = 2 * p;
@@ -353,22 +401,12 @@ __global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
     const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
     const float2 z = make_float2(a.alpha * hv.x + y.x, a.alpha * hv.y + y.y);
     *reinterpret_cast<float2*>(hrow + n) = z;
-    acc.x += z.x + z.y;
-    acc.y += z.x * z.x + z.y * z.y;
+    acc.add(z.x);
+    acc.add(z.y);
   }
-  acc.x = warp_sum(acc.x);
-  acc.y = warp_sum(acc.y);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = acc;
-  __syncthreads();
-  float2 tot = make_float2(0.f, 0.f);
-  for (int i = 0; i < kLnRowThreads / 32; ++i) {
-    tot.x += red[i].x;
-    tot.y += red[i].y;
-  }
-  const float inv_d = 1.f / static_cast<float>(a.d);
-  const float mean = tot.x * inv_d;
-  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);  // biased (tensor.cpp:267)
+  const RowStat tot = block_stat<kLnRowThreads>(acc.stat(), red);
+  const float mean = tot.mean;
+  const float var = tot.m2 / static_cast<float>(a.d);  // biased (tensor.cpp:267)
   const float rstd = rsqrtf(var + a.eps);
   // pass 2 (same thread -> same pairs, so z is read back from where this thread wrote it)
   for (int64_t p = threadIdx.x; p < npairs; p += kLnRowThreads) {
@@ -413,11 +451,11 @@ template <int MINB>
 __global__ void __launch_bounds__(kLnRowThreads, MINB) k_deepnorm_ln_rows8(LnArgs a) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float2 red[kLnRowThreads / 32];
+  __shared__ RowStat red[kLnRowThreads / 32];
   const int m = blockIdx.x;
   const int64_t nv = a.d / 8;
   float* hrow = a.h + static_cast<int64_t>(m) * a.d;
-  float2 acc = make_float2(0.f, 0.f);
+  ShiftedSums acc;
   for (int64_t p = threadIdx.x; p < nv; p += kLnRowThreads) {
     const int64_t n = 8 * p;
     float y[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -436,26 +474,14 @@ __global__ void __launch_bounds__(kLnRowThreads, MINB) k_deepnorm_ln_rows8(LnArg
     float z[8];
     ld8(hrow + n, z);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      z[e] = a.alpha * z[e] + y[e];
-      acc.x += z[e];
-      acc.y += z[e] * z[e];
-    }
+    for (int e = 0; e < 8; ++e) z[e] = a.alpha * z[e] + y[e];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc.add(z[e]);
     st8(hrow + n, z);
   }
-  acc.x = warp_sum(acc.x);
-  acc.y = warp_sum(acc.y);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = acc;
-  __syncthreads();
-  float2 tot = make_float2(0.f, 0.f);
-  for (int i = 0; i < kLnRowThreads / 32; ++i) {
-    tot.x += red[i].x;
-    tot.y += red[i].y;
-  }
-  const float inv_d = 1.f / static_cast<float>(a.d);
-  const float mean = tot.x * inv_d;
-  const float var = fmaxf(tot.y * inv_d - mean * mean, 0.f);  // biased (tensor.cpp:267)
+  const RowStat tot = block_stat<kLnRowThreads>(acc.stat(), red);
+  const float mean = tot.mean;
+  const float var = tot.m2 / static_cast<float>(a.d);  // biased (tensor.cpp:267)
   const float rstd = rsqrtf(var + a.eps);
   for (int64_t p = threadIdx.x; p < nv; p += kLnRowThreads) {
     const int64_t n = 8 * p;
