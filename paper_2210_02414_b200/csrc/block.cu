@@ -1220,7 +1220,8 @@ constexpr int kHeadRowsPerGroup = 4;
 constexpr int kHeadU = 6;
 
 __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
-  uint32_t u = __float_as_uint(v);
+  // NaN of either sign maps to the top key so a non-finite row always shows up in its winner
+  uint32_t u = (v != v) ? 0x7FFFFFFFu : __float_as_uint(v);
   u = (u >> 31) ? ~u : (u | 0x80000000u);
   return (static_cast<unsigned long long>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(idx));
 }
@@ -1409,12 +1410,20 @@ __global__ void k_rows_to_bf16(const float* __restrict__ x, __nv_bfloat16* __res
     *reinterpret_cast<__nv_bfloat162*>(y + i) = __floats2bfloat162_rn(x[i], x[i + 1]);
 }
 
-__global__ void k_argmax_finish(unsigned long long* __restrict__ keys, int* __restrict__ tokens, int M) {
+// The winning key also guards the fp16 activation path: NaN keys sort above every number and
+// +inf above every finite value, so a row whose activations left the fp16 range (inf -> NaN
+// through the LayerNorm) always has a non-finite winner; it raises *status (model.cu reports
+// GLM_POLICY) instead of returning a token picked from garbage.
+__global__ void k_argmax_finish(unsigned long long* __restrict__ keys, int* __restrict__ tokens, int M, int* status) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m < M) {
-    tokens[m] = static_cast<int>(~static_cast<uint32_t>(keys[m] & 0xFFFFFFFFull));
+    const unsigned long long k = keys[m];
+    tokens[m] = static_cast<int>(~static_cast<uint32_t>(k & 0xFFFFFFFFull));
+    const uint32_t u = static_cast<uint32_t>(k >> 32);
+    const float v = __uint_as_float((u >> 31) ? (u & 0x7FFFFFFFu) : ~u);
+    if (status && !finite_f32(v)) atomicOr(status, 1);
     keys[m] = 0ull;
   }
 }
@@ -1593,8 +1602,8 @@ void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
   LAUNCH_CHECK("k_head");
 }
 
-void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st) {
-  launch_k(k_argmax_finish, dim3(grid_for(M, 32)), dim3(32), 0, st, keys, tokens, M);
+void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st, int* status) {
+  launch_k(k_argmax_finish, dim3(grid_for(M, 32)), dim3(32), 0, st, keys, tokens, M, status);
   LAUNCH_CHECK("k_argmax_finish");
 }
 

@@ -144,6 +144,7 @@ bool launch_attn_prefill_umma(const AttnPrefillArgs& a, cudaStream_t st);
 bool attn_prefill_umma_eligible(int dh);
 void launch_rows_to_xfrag(const float* x, int64_t ld, int M, int64_t K, const XOut& xo, cudaStream_t st);
 void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st);
-void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st);
+// status (optional): set to 1 when a row's winning logit is not finite
+void launch_argmax_finish(unsigned long long* keys, int* tokens, int M, cudaStream_t st, int* status = nullptr);
 
 }  // namespace glm

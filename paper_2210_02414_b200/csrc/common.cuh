@@ -156,6 +156,10 @@ __device__ __forceinline__ void trace_point(unsigned tag) {
     CUDA_CHECK(cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap)));                          \
   }
 
+// IEEE finiteness from the exponent bits (NaN and +-inf have an all-ones exponent): explicit
+// so no compiler assumption about NaN can turn a check into |x| != inf.
+__device__ __forceinline__ bool finite_f32(float x) { return ((__float_as_uint(x) >> 23) & 0xFFu) != 0xFFu; }
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -771,35 +771,44 @@ constexpr float kDigitQ = 32512.f;  // 127 * 256: keeps the balanced hi digit in
 
 // One 16-k group of fragment-ordered fp16 activations (32 B, halves [j][2t, 2t+1, 2t+8, 2t+9])
 // -> 16 hi digits | 16 lo digits in weight-word byte order ([j][2t, 2t+8, 2t+1, 2t+9]); returns
-// the digit sums (hi, lo) of the group.
-__device__ __forceinline__ int2 digits_group(uint4* p, float inv_s) {
+// the sum of the group's x_int. x_int = rint(fp32(x) * inv_s) via the 1.5 * 2^23 magic add
+// (|x_int| <= 32512 < 2^22, so the add rounds to the nearest even integer exactly as rint);
+// u = x_int + 128 then holds lo + 128 in its low byte and hi in the next (two's complement), so
+// two PRMT levels gather the 4 lo / 4 hi bytes of a word and one LOP flips lo's sign bit.
+__device__ __forceinline__ int digits_group(uint4* p, float inv_s) {
   const uint4 h0 = p[0], h1 = p[1];
   const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  constexpr float kMagic = 12582912.f;              // 1.5 * 2^23
+  constexpr int kBias = 0x4B400000 - 128;           // magic bits, less the +128 offset
   uint32_t hi[4], lo[4];
-  int shi = 0, slo = 0;
+  int sum = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    // halves of k-tile j: q = 0: 2t, 1: 2t+1 (word 2j), 2: 2t+8, 3: 2t+9 (word 2j+1)
     const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j]));
     const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j + 1]));
     const float fq[4] = {f01.x, f23.x, f01.y, f23.y};  // byte order 2t, 2t+8, 2t+1, 2t+9
-    uint32_t bh = 0, bl = 0;
+    uint32_t u[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int xi = __float2int_rn(fq[q] * inv_s);
-      const int l = ((xi + 128) & 255) - 128;
-      const int h = (xi - l) >> 8;
-      shi += h;
-      slo += l;
-      bh |= (static_cast<uint32_t>(h) & 255u) << (8 * q);
-      bl |= (static_cast<uint32_t>(l) & 255u) << (8 * q);
+      u[q] = static_cast<uint32_t>(__float_as_int(__fadd_rn(__fmul_rn(fq[q], inv_s), kMagic)) - kBias);
+      sum += static_cast<int>(u[q]);
     }
-    hi[j] = bh;
-    lo[j] = bl;
+    const uint32_t t01 = __byte_perm(u[0], u[1], 0x5410), t23 = __byte_perm(u[2], u[3], 0x5410);
+    lo[j] = __byte_perm(t01, t23, 0x6420) ^ 0x80808080u;
+    hi[j] = __byte_perm(t01, t23, 0x7531);
   }
   p[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   p[1] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  return make_int2(shi, slo);
+  return sum - 16 * 128;
+}
+
+// Row results of one item from the integer accumulators: rows g carry (code + 8), rows g + 8
+// carry 16 (code + 8), both against digits x_int = 256 hi + lo; S = sum of x_int over the item's
+// k-range removes the code offset exactly (int64: 256 * acc can exceed int32)
+__device__ __forceinline__ float2 i4_rows(int c_hi, int c_lo, int u_hi, int u_lo, int S, float s_x) {
+  const long long r0 = 256ll * c_hi + c_lo - 8ll * S;
+  const long long r1 = 256ll * u_hi + u_lo - 128ll * S;
+  return make_float2(static_cast<float>(r0) * s_x, static_cast<float>(r1) * (0.0625f * s_x));
 }
 
 template <int NST, int SB, int MT>
@@ -817,7 +826,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
   uint8_t* xs = smem + static_cast<size_t>(nw) * NST * SB;
   uint64_t* xbar = reinterpret_cast<uint64_t*>(xs + nx * vbytes);
   uint64_t* bars = xbar + 1 + warp * NST;
-  int2* dsum = reinterpret_cast<int2*>(xbar + 1 + nw * NST);  // [v][m][chunk] digit sums
+  int* dsum = reinterpret_cast<int*>(xbar + 1 + nw * NST);      // [v][m][chunk] sums of x_int
   float* sx = reinterpret_cast<float*>(dsum + nx * MT * nch);   // [v * MT + m]: s_x
   float* isx = sx + 8;                                           // [v * MT + m]: 1 / s_x
   float* wmax = isx + 8;                                         // [warps][v * MT + m]
@@ -913,8 +922,8 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
         m = (m != m || r != r) ? __int_as_float(0x7fc00000) : fmaxf(m, r);
       }
       // non-finite activations propagate as NaN results (the fp16 path would produce inf/NaN)
-      sx[threadIdx.x] = (m == 0.f) ? 0.f : (isfinite(m) ? m / kDigitQ : __int_as_float(0x7fc00000));
-      isx[threadIdx.x] = (m > 0.f && isfinite(m)) ? kDigitQ / m : 0.f;
+      sx[threadIdx.x] = (m == 0.f) ? 0.f : (finite_f32(m) ? m / kDigitQ : __int_as_float(0x7fc00000));
+      isx[threadIdx.x] = (m > 0.f && finite_f32(m)) ? kDigitQ / m : 0.f;
     }
     __syncthreads();
   }
@@ -923,12 +932,10 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
     const int ngroups = nvm * nch * 4;
     for (int i0 = 0; i0 < ngroups; i0 += blockDim.x) {  // warp-uniform trip count
       const int i = i0 + threadIdx.x;
-      int2 sm = make_int2(0, 0);
+      int sm = 0;
       if (i < ngroups) sm = digits_group(reinterpret_cast<uint4*>(xs) + 2 * i, isx[i / (nch * 4)]);
-      sm.x += __shfl_xor_sync(0xffffffffu, sm.x, 1);
-      sm.y += __shfl_xor_sync(0xffffffffu, sm.y, 1);
-      sm.x += __shfl_xor_sync(0xffffffffu, sm.x, 2);
-      sm.y += __shfl_xor_sync(0xffffffffu, sm.y, 2);
+      sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+      sm += __shfl_xor_sync(0xffffffffu, sm, 2);
       if ((i & 3) == 0 && i < ngroups) dsum[i >> 2] = sm;
     }
     __syncthreads();
@@ -979,39 +986,247 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
       }
       if (lane == 0) issue();
     }
-    // digit sums of this slice per token (the code offsets: rows g carry code + 8, rows g + 8
-    // carry 16 (code + 8))
-    int shi = 0, slo = 0;
+    // sum of x_int over this slice per token (removes the code offsets)
+    int S = 0;
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-      int h = 0, l = 0;
-      for (int cc = c0 + lane; cc < c1; cc += 32) {
-        const int2 d = dsum[(v * MT + m) * nch + cc];
-        h += d.x;
-        l += d.y;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        h += __shfl_xor_sync(0xffffffffu, h, o);
-        l += __shfl_xor_sync(0xffffffffu, l, o);
-      }
-      if (t == m) {
-        shi = h;
-        slo = l;
-      }
+      int h = 0;
+      for (int cc = c0 + lane; cc < c1; cc += 32) h += dsum[(v * MT + m) * nch + cc];
+      h = __reduce_add_sync(0xffffffffu, h);
+      if (t == m) S = h;
     }
     if (t < MT) {
-      const int c_hi = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]) - 8 * shi;
-      const int c_lo = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]) - 8 * slo;
-      const int u_hi = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]) - 128 * shi;
-      const int u_lo = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]) - 128 * slo;
-      const float s_x = sx[v * MT + t];
+      const float2 y = i4_rows((acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]),
+                               (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]),
+                               (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]),
+                               (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]), S, sx[v * MT + t]);
       float* out = a.partial + (static_cast<int64_t>(s) * MT + t) * a.Np + static_cast<int64_t>(rt) * kTileN;
-      out[g] = fmaf(256.f, static_cast<float>(c_hi), static_cast<float>(c_lo)) * s_x;
-      out[g + 8] = fmaf(256.f, static_cast<float>(u_hi), static_cast<float>(u_lo)) * (0.0625f * s_x);
+      out[g] = y.x;
+      out[g + 8] = y.y;
     }
   }
   __syncthreads();
+  trace_point(13);
+}
+
+// ---- integer-MMA multi-token variant (INT4, 3..16 tokens: batched decode) -----------------
+// The CTA-item structure of k_gemv_mk (16 * RT row tiles x one k-slice, the slice of all M
+// activation rows bulk-copied into a double-buffered shared buffer) with the integer MMA of
+// k_gemv_i4: after each slice lands, the CTA turns it in place into digit pairs with one scale
+// per (vector, token, slice) — the max over the slice, so every k-slice partial carries its own
+// scale — and the slice's digit sums. A code fragment (8 LOP3 per 1024 weights) then feeds
+// NQ = ceil(M / 4) IMMA column groups of 4 tokens (column 2j + e: token 4q + j, digit e).
+template <int NQ, int RT>
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int nx) {
+  trace_point(10);
+  constexpr int CHUNK = 512;
+  constexpr int U = kStageBytes / CHUNK / RT;  // chunks per tile per stage
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = static_cast<int>(a.nch), ksplit = a.ksplit, M = a.M;
+  const int nrt = static_cast<int>(a.nrt);
+  constexpr int kTiles = kTWarps * RT;
+  uint8_t* ring = smem + static_cast<size_t>(warp) * kMkStages * kStageBytes;
+  uint8_t* xbuf = smem + static_cast<size_t>(kTWarps) * kMkStages * kStageBytes;  // [2][kMkSliceBytes]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * kMkSliceBytes);          // [2]
+  uint64_t* bars = xbar + 2 + warp * kMkStages;
+  float* sxs = reinterpret_cast<float*>(xbar + 2 + kTWarps * kMkStages);          // [32] slice scale per (v, m)
+  float* isx = sxs + 32;                                                           // [32] 1 / scale
+  int* dsum = reinterpret_cast<int*>(isx + 32);                                    // [32] slice sums of x_int
+  if (lane == 0) {
+    for (int q = 0; q < kMkStages; ++q) mbar_init(bars + q, 1);
+    if (warp == 0) {
+      mbar_init(xbar, 1);
+      mbar_init(xbar + 1, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t policy, keep;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const int ngroups = (nrt + kTiles - 1) / kTiles;
+  const int nitems = ngroups * ksplit;
+  auto slice = [&](int s, int& c0, int& c1) {
+    c0 = nch * s / ksplit;
+    c1 = nch * (s + 1) / ksplit;
+  };
+  int pj = blockIdx.x, pc = 0, pc1 = 0, prt = -1, pslot = 0;
+  auto pitem = [&]() {
+    while (pj < nitems) {
+      prt = (pj / ksplit) * kTiles + warp * RT;
+      slice(pj % ksplit, pc, pc1);
+      if (prt < nrt) return;
+      pj += gridDim.x;
+    }
+  };
+  pitem();
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  auto issue = [&]() {
+    if (pj >= nitems) return;
+    const int n = min(U, pc1 - pc);
+    const int ntile = (RT == 2 && prt + 1 < nrt) ? 2 : 1;
+    mbar_expect_tx(bars + pslot, static_cast<uint32_t>(ntile * n * CHUNK));
+    for (int q = 0; q < ntile; ++q) {
+      const uint8_t* src = wbase + (static_cast<int64_t>(prt + q) * nch + pc) * CHUNK;
+      bulk_g2s(ring + pslot * kStageBytes + q * n * CHUNK, src, static_cast<uint32_t>(n * CHUNK), bars + pslot, policy);
+    }
+    pslot = pslot + 1 == kMkStages ? 0 : pslot + 1;
+    pc += n;
+    if (pc >= pc1) {
+      pj += gridDim.x;
+      pitem();
+    }
+  };
+  if (lane == 0)
+    for (int q = 0; q < kMkStages; ++q) issue();
+  pdl_wait();
+  pdl_trigger();
+  trace_point(11);
+  auto load_x = [&](int local, int item) {
+    int c0, c1;
+    slice(item % ksplit, c0, c1);
+    const int nck = c1 - c0;
+    const int b = local & 1;
+    mbar_expect_tx(xbar + b, static_cast<uint32_t>(nx * M * nck * 128));
+    for (int v = 0; v < nx; ++v)
+      for (int m = 0; m < M; ++m) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2) +
+                             (static_cast<int64_t>(m) * nch + c0) * 128;
+        bulk_g2s(xbuf + b * kMkSliceBytes + ((v * M + m) * nck) * 128, src, static_cast<uint32_t>(nck * 128), xbar + b,
+                 keep);
+      }
+  };
+  if (threadIdx.x == 0) {
+    if (static_cast<int>(blockIdx.x) < nitems) load_x(0, blockIdx.x);
+    if (static_cast<int>(blockIdx.x + gridDim.x) < nitems) load_x(1, blockIdx.x + gridDim.x);
+  }
+  const int nvm = nx * M;
+  int cslot = 0;
+  uint32_t cpar = 0;
+  int local = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
+    const int s = item % ksplit;
+    const int rt = (item / ksplit) * kTiles + warp * RT;
+    int c0, c1;
+    slice(s, c0, c1);
+    const int nck = c1 - c0;
+    const int b = local & 1;
+    uint8_t* xb = xbuf + b * kMkSliceBytes;
+    mbar_wait(xbar + b, (local >> 1) & 1);
+    // (1) slice max per activation vector (v, m): one warp per vector
+    for (int vm = warp; vm < nvm; vm += kTWarps) {
+      const uint4* row = reinterpret_cast<const uint4*>(xb + static_cast<size_t>(vm) * nck * 128);
+      float mx = 0.f;
+      bool nan = false;
+      for (int i = lane; i < nck * 8; i += 32) {
+        const uint4 q = row[i];
+        const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(__habs2(*reinterpret_cast<const __half2*>(&wd[e])));
+          nan = nan || f.x != f.x || f.y != f.y;
+          mx = fmaxf(mx, fmaxf(f.x, f.y));
+        }
+      }
+      mx = warp_max(mx);
+      nan = __any_sync(0xffffffffu, nan);
+      if (lane == 0) {
+        const bool bad = nan || !finite_f32(mx);
+        sxs[vm] = bad ? __int_as_float(0x7fc00000) : mx / kDigitQ;
+        isx[vm] = (mx > 0.f && !bad) ? kDigitQ / mx : 0.f;
+        dsum[vm] = 0;
+      }
+    }
+    __syncthreads();
+    // (2) in place: fp16 fragments -> digit pairs; digit sums per vector over the slice
+    {
+      const int ng = nvm * nck * 4;
+      for (int i0 = 0; i0 < ng; i0 += kTWarps * 32) {
+        const int i = i0 + threadIdx.x;
+        const int vm = i < ng ? i / (nck * 4) : 0;
+        int sm = 0;
+        if (i < ng) sm = digits_group(reinterpret_cast<uint4*>(xb) + 2 * i, isx[vm]);
+        // groups of one vector reduce through shared atomics (integer: order-independent)
+        if (i < ng && sm) atomicAdd(&dsum[vm], sm);
+      }
+    }
+    __syncthreads();
+    if (rt < nrt) {
+      const int v = rt < a.rt_split ? 0 : nx - 1;
+      const bool two = RT == 2 && rt + 1 < nrt;
+      const uint8_t* xrow[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        xrow[q] = xb + ((v * M + min(4 * q + (g >> 1), M - 1)) * nck) * 128 + t * 32 + (g & 1) * 16;
+      int acc[RT][NQ][2][4];
+#pragma unroll
+      for (int r = 0; r < RT; ++r)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[r][q][h][i] = 0;
+      for (int c = 0; c < nck; c += U) {
+        const int n = min(U, nck - c);
+        mbar_wait(bars + cslot, cpar);
+        const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
+        auto chunk = [&](int u) {
+          uint4 xv[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) xv[q] = *reinterpret_cast<const uint4*>(xrow[q] + (c + u) * 128);
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            if (r == 1 && !two) break;
+            const uint4 wv = *reinterpret_cast<const uint4*>(st + (r * n + u) * CHUNK);
+            const uint32_t a0 = wv.x & 0x0F0F0F0Fu, a1 = wv.x & 0xF0F0F0F0u, a2 = wv.y & 0x0F0F0F0Fu,
+                           a3 = wv.y & 0xF0F0F0F0u;
+            const uint32_t a4 = wv.z & 0x0F0F0F0Fu, a5 = wv.z & 0xF0F0F0F0u, a6 = wv.w & 0x0F0F0F0Fu,
+                           a7 = wv.w & 0xF0F0F0F0u;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              imma16832(acc[r][q][0], a0, a1, a2, a3, xv[q].x, xv[q].y);
+              imma16832(acc[r][q][1], a4, a5, a6, a7, xv[q].z, xv[q].w);
+            }
+          }
+        };
+        if (n == U) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) chunk(u);
+        } else {
+          for (int u = 0; u < n; ++u) chunk(u);
+        }
+        __syncwarp();
+        if (cslot + 1 == kMkStages) {
+          cslot = 0;
+          cpar ^= 1u;
+        } else {
+          ++cslot;
+        }
+        if (lane == 0) issue();
+      }
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        if (r == 1 && !two) break;
+        float* out = a.partial + static_cast<int64_t>(s) * M * a.Np + static_cast<int64_t>(rt + r) * kTileN;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int m = 4 * q + t;
+          if (m < M) {
+            const float2 y = i4_rows(acc[r][q][0][0] + acc[r][q][1][0], acc[r][q][0][1] + acc[r][q][1][1],
+                                     acc[r][q][0][2] + acc[r][q][1][2], acc[r][q][0][3] + acc[r][q][1][3],
+                                     dsum[v * M + m], sxs[v * M + m]);
+            out[static_cast<int64_t>(m) * a.Np + g] = y.x;
+            out[static_cast<int64_t>(m) * a.Np + g + 8] = y.y;
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with activation buffer b (and the slice scales)
+    if (threadIdx.x == 0 && item + 2 * static_cast<int>(gridDim.x) < nitems) load_x(local + 2, item + 2 * gridDim.x);
+  }
   trace_point(13);
 }
 
@@ -1083,7 +1298,7 @@ M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
   static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
   static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
   // activation vectors + per-chunk sums (fp32, or int2 digit sums + scales + per-warp maxima)
-  const size_t xb = gemv_imma() ? static_cast<size_t>(nx) * M * nch * (128 + 8) + 8 + 64 + kM1MaxWarps * 32
+  const size_t xb = gemv_imma() ? static_cast<size_t>(nx) * M * nch * (128 + 4) + 8 + 64 + kM1MaxWarps * 32
                                 : static_cast<size_t>(nx) * M * nch * (128 + 4) + 8;
   M1Shape m;
   m.nst = m1s >= 3 ? 3 : 2;
@@ -1176,6 +1391,23 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     }
     const dim3 gridm(p.grid), blockm(kTWarps * 32);
     const bool two = p.rt_per_warp == 2;
+    if (op.bits == 4 && gemv_imma() && M * nx <= 32) {
+      const size_t smem2 = smem1 + 32 * 4 * 2 + 32 * 8;
+      static bool attr_i4 = false;
+      if (!attr_i4) {
+        for (auto k : {k_gemv_mk_i4<1, 1>, k_gemv_mk_i4<2, 1>, k_gemv_mk_i4<3, 1>, k_gemv_mk_i4<4, 1>,
+                       k_gemv_mk_i4<1, 2>, k_gemv_mk_i4<2, 2>, k_gemv_mk_i4<3, 2>, k_gemv_mk_i4<4, 2>})
+          CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        attr_i4 = true;
+      }
+      const int nq = (M + 3) / 4;
+      void (*k)(GemvArgs, int) = nullptr;
+      if (two) k = nq == 1 ? k_gemv_mk_i4<1, 2> : nq == 2 ? k_gemv_mk_i4<2, 2> : nq == 3 ? k_gemv_mk_i4<3, 2> : k_gemv_mk_i4<4, 2>;
+      else k = nq == 1 ? k_gemv_mk_i4<1, 1> : nq == 2 ? k_gemv_mk_i4<2, 1> : nq == 3 ? k_gemv_mk_i4<3, 1> : k_gemv_mk_i4<4, 1>;
+      launch_k(k, gridm, blockm, smem2, st, a, nx);
+      LAUNCH_CHECK("k_gemv_mk_i4");
+      return;
+    }
     if (op.bits == 4) {
       if (M <= 8) launch_k(two ? k_gemv_mk<4, 1, 2> : k_gemv_mk<4, 1, 1>, gridm, blockm, smem1, st, a, nx);
       else launch_k(two ? k_gemv_mk<4, 2, 2> : k_gemv_mk<4, 2, 1>, gridm, blockm, smem1, st, a, nx);

@@ -116,6 +116,8 @@ struct glm_model {
   // decode state
   int *d_tokens = nullptr, *d_positions = nullptr, *d_len = nullptr, *d_next = nullptr;
   int *h_tokens = nullptr, *h_positions = nullptr, *h_next = nullptr;  // pinned
+  int* d_status = nullptr;  // non-finite winning logit (k_argmax_finish)
+  int* h_status = nullptr;  // pinned copy
   unsigned long long* d_argmax = nullptr;
   float* attn_part = nullptr;
   int* attn_ctr = nullptr;
@@ -144,6 +146,7 @@ struct glm_model {
     if (h_positions) cudaFreeHost(h_positions);
     if (h_next) cudaFreeHost(h_next);
     if (h_peer_err) cudaFreeHost(h_peer_err);
+    if (h_status) cudaFreeHost(h_status);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (st) cudaStreamDestroy(st);
@@ -252,6 +255,9 @@ struct glm_model {
     d_positions = alloc<int>(max_batch);
     d_len = alloc<int>(max_batch);
     d_next = alloc<int>(max_batch);
+    d_status = alloc<int>(1);
+    CUDA_CHECK(cudaMallocHost(&h_status, sizeof(int)));
+    *h_status = 0;
     attn_splits = attn_decode_splits(max_ctx);
     if (attn_splits > 256) fail(GLM_DIMENSION, "glmmodel", "max_ctx above 16384 tokens is not supported by the decode attention");
     attn_part = alloc<float>(static_cast<int64_t>(max_batch) * Hl * attn_splits * (dh + 2));
@@ -526,7 +532,7 @@ struct glm_model {
     ++launches;
     for (int l = 0; l < L; ++l) launches += decode_layer(l, B, d_positions, d_len, l + 1 < L);
     launches += enqueue_head(B, logits.as<float>(), with_logits);
-    launch_argmax_finish(d_argmax, d_next, B, st);
+    launch_argmax_finish(d_argmax, d_next, B, st, d_status);
     launch_advance(d_len, B, st);
     launch_k(k_feed, dim3(1), dim3(32), 0, st, d_next, d_tokens, d_positions, B);
     LAUNCH_CHECK("k_feed");
@@ -661,9 +667,11 @@ struct glm_model {
     if (logits_out) CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(B) * V * 4, cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaMemcpyAsync(h_next, d_next, B * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (fused_ar()) CUDA_CHECK(cudaMemcpyAsync(h_peer_err, comm->peer_args().err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_peer_err && *h_peer_err)
       fail(GLM_NCCL, "collective", "a tensor-parallel peer did not deliver its decode partial (timeout)");
+    check_status();
     for (int b = 0; b < B; ++b) {
       if (next_tokens) next_tokens[b] = h_next[b];
       h_len[b] += 1;
@@ -863,14 +871,28 @@ struct glm_model {
     for (int l = 0; l < L; ++l) prefill_layer(l, n, nseg, seqs, lens, ctx, row0.data(), dpos.as<int>(), l + 1 < L);
     if (logits_out) {
       enqueue_head(n, logits.as<float>());
-      launch_argmax_finish(d_argmax, d_next_rows, n, st);
+      launch_argmax_finish(d_argmax, d_next_rows, n, st, d_status);
       CUDA_CHECK(cudaMemcpyAsync(logits_out, logits.ptr, static_cast<int64_t>(n) * V * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaMemcpyAsync(h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
     }
     for (int i = 0; i < nseg; ++i)
       CUDA_CHECK(cudaMemcpyAsync(d_len + seqs[i], &lens[i], 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     for (int i = 0; i < nseg; ++i) h_len[seqs[i]] = lens[i];
     last_rows = n;
+    if (logits_out) check_status();
+  }
+
+  // a non-finite winning logit (k_argmax_finish): an fp16 activation overflowed (|x| > 65504,
+  // e.g. a loaded checkpoint outside the range random init stays in) or the weights are not finite
+  void check_status() {
+    if (!*h_status) return;
+    *h_status = 0;
+    CUDA_CHECK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    fail(GLM_POLICY, "glmmodel",
+         "non-finite logits: an activation left the fp16 range of the quantized linears (|x| > 65504) or the "
+         "parameters are not finite");
   }
 
 };

@@ -59,7 +59,7 @@ __global__ void k_group_minmax(const T* __restrict__ w, int64_t rows, int64_t co
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double x = load_as_double(w, i);
-    if (!isfinite(x)) {
+    if (((__double_as_longlong(x) >> 52) & 0x7FF) == 0x7FF) {  // NaN or +-inf (quant.cpp:61-65)
       atomicOr(nonfinite, 1);
       continue;
     }

@@ -398,3 +398,24 @@ def test_fused_geglu_gemm_equals_unfused(bits, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_fp16_activation_overflow_raises_policy_error():
+    """Activations outside the fp16 range of the quantized linears (a loaded checkpoint with a
+    LayerNorm bias of 1e9) must not yield a token: the non-finite winning logit raises
+    PolicyError (block.cu k_argmax_finish) in prefill and in decode, and the model recovers
+    once the parameters are sane again."""
+    p = O.Params(2, 256, 4, vocab=262, seed=3)
+    m = glm.Model(glm.GLMConfig(num_layers=2, hidden=256, num_heads=4, vocab=262), bits=8, axis="row", max_ctx=64)
+    m.load_reference_params(lambda layer, slot: p.tensor(0, O.EMBED) if slot == "embed" else p.tensor(layer, slot))
+    m.set_tensor(0, m.LN1B, np.full(256, 1e9))
+    with pytest.raises(glm.PolicyError):
+        m.prefill(PREFIX[:20], list(range(20)))
+    m.reset()
+    m.prefill(PREFIX[:20], list(range(20)), logits=False)
+    with pytest.raises(glm.PolicyError):
+        m.decode_step([3], [20])
+    m.set_tensor(0, m.LN1B, np.zeros(256))
+    m.reset()
+    lg = m.prefill(PREFIX[:20], list(range(20)))
+    assert np.isfinite(lg).all()

@@ -19,7 +19,10 @@ pytestmark = pytest.mark.gpu
 
 
 def contract_tol(M, bits):
-    return 2e-6
+    # INT4 at 3..16 tokens (k_gemv_mk_i4) re-quantizes the fp16 activations to 16-bit fixed point
+    # per (token, k-slice) with the slice's own max, a split the contract below does not model
+    # (it uses fp16 activations there): the difference is <= 2^-16 of max|x| per element
+    return 1e-4 if (bits == 4 and 3 <= M <= 16) else 2e-6
 
 
 DIGIT_Q = np.float32(32512.0)  # gemv.cu kDigitQ
