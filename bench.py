@@ -341,7 +341,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "w4a16 (int4 weights, fp16 activations, fp32 accumulate/residual)", "data": "synthetic",
+        "dtype": "w4a16 (int4 weights; fp16 activations as 16-bit fixed-point digits on the integer MMA, exact int32 "
+                 "accumulation; fp32 residual / LayerNorm)", "data": "synthetic",
         "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode (BASELINE configs[3])",
                    "model": "GLM-130B shape: 70 layers, hidden 12288, 96 heads, ffn 32768 (GeGLU), vocab 150528, "
                             "random-init (counter-based, model.cpp:69-104 stds)",
@@ -353,7 +354,7 @@ def run_ours(args):
                 "steps": args.e2e_steps},
         "gpu_launches": launches * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": gemv_traffic(), "kernel": "k_gemv_m1<4,2> (W4A16 GEMV, 280 launches/step)",
+                     "traffic": gemv_traffic(), "kernel": "k_gemv_i4 (W4A16 GEMV on the integer MMA, 280 launches/step)",
                      "algorithmic_bytes_per_step": gb, "gemv_ms_per_step": gemv_ms,
                      "gemv_share_of_step": gemv_ms / ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650"},

@@ -1260,13 +1260,19 @@ __global__ void k_gemv_reduce(const float* __restrict__ partial, int ksplit, int
 
 }  // namespace
 
-int m1_warps() {
-  static const int w = [] {
-    const char* e = getenv("GLM_M1_WARPS");
-    const int v = e ? atoi(e) : kM1DefaultWarps;
-    return v < 4 ? 4 : (v > kM1MaxWarps ? kM1MaxWarps : v);
-  }();
-  return w;
+// INT4 decode GEMVs on the integer MMA (k_gemv_i4, k_gemv_mk_i4) unless GLM_GEMV_IMMA=0 (fp16 HMMA
+// k_gemv_m1, the round-1 kernel, kept for A/B)
+bool gemv_imma() {
+  static const bool on = [] { const char* e = getenv("GLM_GEMV_IMMA"); return !e || e[0] != '0'; }();
+  return on;
+}
+// warps per CTA of the single-token kernel family (GLM_M1_WARPS overrides): the integer-MMA
+// kernel at one token runs 8 (tools/r2_m1_sweep2.sh: 8 x 2 x 8 KB beat 4..16 warps and
+// 4..16 KB stages 2..4 deep on one box), the fp16 kernels 16
+int m1_warps(int M) {
+  static const int env = [] { const char* e = getenv("GLM_M1_WARPS"); return e ? atoi(e) : 0; }();
+  const int v = env ? env : (gemv_imma() && M == 1 ? 8 : kM1DefaultWarps);
+  return v < 4 ? 4 : (v > kM1MaxWarps ? kM1MaxWarps : v);
 }
 
 // Row tiles per warp of the multi-token kernel (GLM_MK_RT overrides: 1 or 2).
@@ -1287,24 +1293,39 @@ struct M1Shape {
 constexpr size_t kM1SmemLimit = 227 * 1024 - 1024;  // leave room for the static shared memory
 constexpr int kM1MaxTokens = 2;
 
-// INT4 single-token family on the integer MMA (k_gemv_i4) unless GLM_GEMV_IMMA=0 (fp16 HMMA
-// k_gemv_m1, the round-1 kernel, kept for A/B)
-bool gemv_imma() {
-  static const bool on = [] { const char* e = getenv("GLM_GEMV_IMMA"); return !e || e[0] != '0'; }();
-  return on;
-}
 
 M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
   static const int m1s = [] { const char* e = getenv("GLM_M1_STAGES"); return e ? atoi(e) : 2; }();
-  static const int m1sb = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 6144; }();
+  static const int m1sb_env = [] { const char* e = getenv("GLM_M1_STAGE_KB"); return e ? atoi(e) * 1024 : 0; }();
+  const int m1sb = m1sb_env ? m1sb_env : (gemv_imma() && M == 1 ? 8192 : 6144);
   // activation vectors + per-chunk sums (fp32, or int2 digit sums + scales + per-warp maxima)
   const size_t xb = gemv_imma() ? static_cast<size_t>(nx) * M * nch * (128 + 4) + 8 + 64 + kM1MaxWarps * 32
                                 : static_cast<size_t>(nx) * M * nch * (128 + 4) + 8;
   M1Shape m;
-  m.nst = m1s >= 3 ? 3 : 2;
-  m.sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
   m.warps = plan_warps;  // the plan's warps if the rings fit next to x, else fewer
   auto need = [&](int w, int n, int b) { return xb + static_cast<size_t>(w) * n * (b + 8); };
+  if (gemv_imma() && M == 1) {
+    // integer-MMA kernel: stages of 4..16 KB, 2..4 deep (k_gemv_i4 instantiations); shrink the
+    // stage, then the depth, then the warps until the rings fit next to the activations
+    static const int sbs[5] = {4096, 6144, 8192, 12288, 16384};
+    int si = 0;
+    for (int i = 0; i < 5; ++i)
+      if (m1sb >= sbs[i]) si = i;
+    m.nst = m1s < 2 ? 2 : (m1s > 4 ? 4 : m1s);
+    for (;;) {
+      m.sb = sbs[si];
+      if (need(m.warps, m.nst, m.sb) <= kM1SmemLimit) break;
+      if (si > 0) --si;
+      else if (m.nst > 2) --m.nst;
+      else if (m.warps > 4) --m.warps;
+      else break;
+    }
+    m.smem = need(m.warps, m.nst, m.sb);
+    m.ok = m.smem <= kM1SmemLimit;
+    return m;
+  }
+  m.nst = m1s >= 3 ? 3 : 2;
+  m.sb = m1sb >= 8192 ? 8192 : (m1sb >= 6144 ? 6144 : 4096);  // larger stages amortise per-stage work
   if (need(m.warps, m.nst, m.sb) > kM1SmemLimit) m.nst = 2;
   while (m.sb > 4096 && need(m.warps, m.nst, m.sb) > kM1SmemLimit) m.sb -= 2048;
   while (m.warps > 8 && need(m.warps, m.nst, m.sb) > kM1SmemLimit) --m.warps;
@@ -1318,7 +1339,7 @@ M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
 bool use_m1(int64_t nch, int M, int bits, int nx) {
   static const int maxm = [] { const char* e = getenv("GLM_M1_TOKENS"); const int v = e ? atoi(e) : kM1MaxTokens; return v < 1 ? 1 : (v > kM1MaxTokens ? kM1MaxTokens : v); }();
   if (bits != 4 || M > maxm) return false;
-  const M1Shape m = m1_shape(nch, M, nx, m1_warps());
+  const M1Shape m = m1_shape(nch, M, nx, m1_warps(M));
   return m.ok && (M == 1 || m.warps >= 12);
 }
 }  // namespace
@@ -1347,7 +1368,7 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
     p.grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
     return p;
   }
-  p.warps = use_m1(nch, M, bits, nx) ? m1_warps() : kTWarps;
+  p.warps = use_m1(nch, M, bits, nx) ? m1_warps(M) : kTWarps;
   const int64_t total_warps = static_cast<int64_t>(kNumSMs) * p.warps;
   double best = -1.0;
   const int64_t max_split = nch < 32 ? nch : 32;
@@ -1440,24 +1461,29 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     static const int early = [] { const char* e = getenv("GLM_PREFETCH"); return e ? atoi(e) : 2; }();
     const dim3 block1(m.warps * 32);
     if (gemv_imma()) {
+      using K1 = void (*)(GemvArgs, int, int);
+      // [stages - 2][stage size 4 / 6 / 8 / 12 / 16 KB]
+      static const K1 table[3][5] = {
+          {k_gemv_i4<2, 4096, 1>, k_gemv_i4<2, 6144, 1>, k_gemv_i4<2, 8192, 1>, k_gemv_i4<2, 12288, 1>,
+           k_gemv_i4<2, 16384, 1>},
+          {k_gemv_i4<3, 4096, 1>, k_gemv_i4<3, 6144, 1>, k_gemv_i4<3, 8192, 1>, k_gemv_i4<3, 12288, 1>,
+           k_gemv_i4<3, 16384, 1>},
+          {k_gemv_i4<4, 4096, 1>, k_gemv_i4<4, 6144, 1>, k_gemv_i4<4, 8192, 1>, k_gemv_i4<4, 12288, 1>,
+           k_gemv_i4<4, 16384, 1>}};
       static bool attr2 = false;
       if (!attr2) {
-        for (auto k : {k_gemv_i4<2, 4096, 1>, k_gemv_i4<2, 6144, 1>, k_gemv_i4<2, 8192, 1>, k_gemv_i4<3, 4096, 1>,
-                       k_gemv_i4<2, 4096, 2>, k_gemv_i4<2, 6144, 2>})
+        for (auto& row : table)
+          for (K1 k : row) CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kM1SmemLimit));
+        for (auto k : {k_gemv_i4<2, 4096, 2>, k_gemv_i4<2, 6144, 2>})
           CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kM1SmemLimit));
         attr2 = true;
       }
       if (M == 2) {
         if (m.sb >= 6144) launch_k(k_gemv_i4<2, 6144, 2>, grid, block1, m.smem, st, a, nx_op, early);
         else launch_k(k_gemv_i4<2, 4096, 2>, grid, block1, m.smem, st, a, nx_op, early);
-      } else if (m.nst == 3) {
-        launch_k(k_gemv_i4<3, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
-      } else if (m.sb == 8192) {
-        launch_k(k_gemv_i4<2, 8192, 1>, grid, block1, m.smem, st, a, nx_op, early);
-      } else if (m.sb == 6144) {
-        launch_k(k_gemv_i4<2, 6144, 1>, grid, block1, m.smem, st, a, nx_op, early);
       } else {
-        launch_k(k_gemv_i4<2, 4096, 1>, grid, block1, m.smem, st, a, nx_op, early);
+        const int si = m.sb == 4096 ? 0 : m.sb == 6144 ? 1 : m.sb == 8192 ? 2 : m.sb == 12288 ? 3 : 4;
+        launch_k(table[m.nst - 2][si], grid, block1, m.smem, st, a, nx_op, early);
       }
       LAUNCH_CHECK("k_gemv_i4");
       return;
