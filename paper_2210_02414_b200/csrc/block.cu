@@ -1484,23 +1484,32 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
   LAUNCH_CHECK("k_geglu_act");
 }
 
-int attn_decode_split_keys(int max_ctx) { return max_ctx <= kSplitKeys ? kSplitKeys : kSplitKeysLong; }
-int attn_decode_splits(int max_ctx) {
-  const int sk = attn_decode_split_keys(max_ctx);
-  return (max_ctx + sk - 1) / sk;
+// keys per CTA: 256 (no merge) up to a 256-token cache for one or two sequences (staged) and
+// for more than 8 (read from L2 / HBM: 96 x B CTAs already fill the SMs); 64-key splits, each
+// staged by one bulk copy issued before the dependency wait, for 3..8 sequences and for longer
+// caches (batch sweep, same box: B = 4 251 -> 280, B = 8 429 -> 454 tok/s; B = 16 662 -> 643, so
+// not there). GLM_ATTN_SPLIT64=0 keeps the 256-key unstaged CTAs at 3..8 sequences.
+int attn_decode_split_keys(int max_ctx, int B) {
+  static const bool many64 = [] { const char* e = getenv("GLM_ATTN_SPLIT64"); return !e || e[0] != '0'; }();
+  if (max_ctx > kSplitKeys) return kSplitKeysLong;
+  return (B > 2 && B <= 8 && many64) ? kSplitKeysLong : kSplitKeys;
 }
+int attn_decode_split_keys(int max_ctx) { return attn_decode_split_keys(max_ctx, 1); }
+// capacity of the split partial buffer: 64-key splits of the longest cache
+int attn_decode_splits(int max_ctx) { return (max_ctx + kSplitKeysLong - 1) / kSplitKeysLong; }
 
 void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   AttnDecodeArgs a = in;
-  const dim3 grid(a.heads, B, a.max_splits);
-  // Few sequences: each CTA bulk-copies its split's keys + values into shared memory ahead
-  // of the dependency wait (one HBM round trip). Many sequences: that shared memory would
-  // cap residency at one CTA per SM over B * heads CTAs, so rows are read from L2/HBM.
-  a.split_keys = attn_decode_split_keys(a.max_ctx);
+  // Each CTA bulk-copies its split's cached keys + values into shared memory ahead of the
+  // dependency wait (one HBM round trip, overlapping the qkv GEMV): 256-key CTAs for one or
+  // two sequences, 64-key CTAs (32 KB of staging, several per SM) otherwise.
+  a.split_keys = attn_decode_split_keys(a.max_ctx, B);
   if (a.max_splits != attn_decode_splits(a.max_ctx)) fail(GLM_CONTRACT, "glmmodel", "decode attention split count");
   if (a.max_splits > kSplitKeys)  // the merge keeps one weight per split in the score buffer
     fail(GLM_DIMENSION, "glmmodel", "decode attention supports caches up to 16384 tokens");
-  const int stage = B <= 2 ? std::min(a.split_keys, (a.max_ctx + 15) / 16 * 16) : 0;
+  const dim3 grid(a.heads, B, (a.max_ctx + a.split_keys - 1) / a.split_keys);
+  const bool many_unstaged = B > 2 && a.split_keys == kSplitKeys;  // GLM_ATTN_SPLIT64=0
+  const int stage = many_unstaged ? 0 : std::min(a.split_keys, (a.max_ctx + 15) / 16 * 16);
   a.stage_keys = stage;
   const size_t smem = 2ull * stage * a.dh * sizeof(__half);
   static bool attr = false;

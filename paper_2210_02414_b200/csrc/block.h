@@ -134,7 +134,8 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st);
 // keys per CTA of the decode attention: 256 up to a 256-token cache (no merge), else 64
 // (long caches: many small CTAs stream the cache concurrently, deterministic merge)
 int attn_decode_split_keys(int max_ctx);
-int attn_decode_splits(int max_ctx);
+int attn_decode_split_keys(int max_ctx, int batch);
+int attn_decode_splits(int max_ctx);  // capacity of the split partial buffer
 void launch_attn_decode(const AttnDecodeArgs& a, int B, cudaStream_t st);
 void launch_advance(int* cache_len, int B, cudaStream_t st);
 void launch_rope_store(const RopeStoreArgs& a, cudaStream_t st);
