@@ -176,6 +176,8 @@ glm_status glm_model_init_comm_emulated(glm_model* m, glm_tp_group* g);
  * [d,d], 2 ffn_w1 [d,f], 3 ffn_v [d,f], 4 ffn_w2 [f,d], 5 ln1_gain, 6 ln1_bias,
  * 7 ln2_gain, 8 ln2_bias; embedding [vocab, d] via glm_model_set_embedding. */
 glm_status glm_model_set_embedding(glm_model* m, const double* embedding);
+/* Rows [row0, row0 + nrows) of the embedding (host doubles [nrows, hidden]): streaming loaders. */
+glm_status glm_model_set_embedding_rows(glm_model* m, int64_t row0, int64_t nrows, const double* values);
 glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double* values);
 /* A quantized linear given as the reference's canonical QuantizedMatrix (quant.hpp:26-42:
  * payload bytes + FP64 scales of the FULL [K, N] matrix, the model's bits/axis, absmax);

@@ -97,6 +97,20 @@ void check_policy(int bits, int axis) {
 
 // y = x . dequantize(q) for any M >= 1 (device pointers): the decode GEMV for M <= 16 rows,
 // the tcgen05 GEMM (128-token tiles) above; then the split-K reduce with the group scale.
+void validate_absmax_payload(const int8_t* payload, int64_t payload_bytes, int64_t n, int bits) {
+  if (bits == 4) {
+    for (int64_t i = 0; i < payload_bytes; ++i) {
+      const uint8_t b = static_cast<uint8_t>(payload[i]);
+      if ((b & 0x0F) == 0x08 || (b & 0xF0) == 0x80) fail(GLM_CONTRACT, "quantlab", "INT4 code -8 outside [-7, 7]");
+    }
+    if (n % 2 && payload_bytes > 0 && (static_cast<uint8_t>(payload[payload_bytes - 1]) >> 4) != 0)
+      fail(GLM_FORMAT, "quantlab", "odd INT4 payload must pad its last nibble with 0");
+  } else {
+    for (int64_t i = 0; i < payload_bytes; ++i)
+      if (payload[i] == -128) fail(GLM_CONTRACT, "quantlab", "INT8 code -128 outside [-127, 127]");
+  }
+}
+
 const QWeightDev& qweight_dev(const glm_qweight* q) {
   if (!q) fail(GLM_CONTRACT, "qlinear", "null weight handle");
   return q->w;
@@ -231,14 +245,9 @@ glm_status glm_qweight_create(const int8_t* payload, const double* scales, int64
     DeviceBuffer dp(pb), ds(g * 8);
     CUDA_CHECK(cudaMemcpy(dp.ptr, payload, pb, cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(ds.ptr, scales, g * 8, cudaMemcpyHostToDevice));
-    if (bits == 4) {  // validate nibbles: -8 is not a legal absmax code (quant.cpp:225)
-      std::vector<int8_t> codes(rows * cols);
-      DeviceBuffer dc(rows * cols);
-      unpack_int4_device(dp.as<int8_t>(), rows * cols, dc.as<int8_t>(), nullptr);
-      CUDA_CHECK(cudaMemcpy(codes.data(), dc.ptr, codes.size(), cudaMemcpyDeviceToHost));
-      for (int8_t c : codes)
-        if (c < -7) fail(GLM_CONTRACT, "quantlab", "INT4 code -8 outside [-7, 7]");
-    }
+    validate_absmax_payload(payload, pb, rows * cols, bits);
+    for (int64_t i = 0; i < g; ++i)
+      if (!std::isfinite(scales[i]) || scales[i] < 0.0) fail(GLM_FORMAT, "quantlab", "scales must be finite and >= 0");
     auto q = make_qweight(dp.as<int8_t>(), ds.as<double>(), rows, cols, bits, axis, nullptr);
     CUDA_CHECK(cudaDeviceSynchronize());
     *out = q.release();

@@ -10,8 +10,9 @@
 //   layer<L>.<m>.codes.glmt i8  [payload bytes]   m in qkv, out_proj, ffn_w1, ffn_v, ffn_w2
 //   layer<L>.<m>.scales.glmt f64 [groups]
 //   layer<L>.ln{1,2}_{gain,bias}.glmt f64 [hidden]
-// Every file is parsed and validated before any device work, so format errors surface as
-// GLM_FORMAT (FormatError) even without a GPU.
+// Every header, shape and file size is validated before any device work, so format errors
+// surface as GLM_FORMAT (FormatError) even without a GPU; payloads then stream one matrix at a
+// time (the embedding in 256 MB row chunks), so host memory stays at one matrix, not the model.
 #include <cctype>
 #include <cmath>
 #include <cstdint>
@@ -25,6 +26,7 @@
 
 #include "common.cuh"
 #include "glm130b.h"
+#include "kernels.h"
 
 namespace glm {
 namespace {
@@ -42,6 +44,74 @@ struct Glmt {
     return n;
   }
 };
+
+// Header of a GLMT file and the byte offset of its payload; the file size is checked against
+// the payload the header announces (a truncated file fails before any payload is read).
+struct GlmtHeader {
+  int dtype = 0;
+  std::vector<uint64_t> dims;
+  std::streamoff data = 0;
+  uint64_t count() const {
+    uint64_t n = 1;
+    for (uint64_t d : dims) n *= d;
+    return n;
+  }
+  size_t elem() const { return dtype == 0 ? 8 : dtype == 1 ? 4 : 1; }
+};
+
+GlmtHeader read_glmt_header(const std::string& path) {
+  std::ifstream in(path, std::ios::binary | std::ios::ate);
+  if (!in) fail(GLM_FORMAT, "tensor_io", "cannot open " + path);
+  const std::streamoff size = in.tellg();
+  in.seekg(0);
+  auto bytes = [&](void* dst, size_t n) {
+    in.read(static_cast<char*>(dst), static_cast<std::streamsize>(n));
+    if (static_cast<size_t>(in.gcount()) != n) fail(GLM_FORMAT, "tensor_io", "truncated file " + path);
+  };
+  char magic[4];
+  bytes(magic, 4);
+  if (std::memcmp(magic, "GLMT", 4) != 0) fail(GLM_FORMAT, "tensor_io", "bad magic in " + path);
+  uint8_t version = 0, dtype = 0;
+  bytes(&version, 1);
+  if (version != 1) fail(GLM_FORMAT, "tensor_io", "unsupported version " + std::to_string(version));
+  bytes(&dtype, 1);
+  if (dtype > 2) fail(GLM_FORMAT, "tensor_io", "unknown dtype " + std::to_string(dtype));
+  uint8_t b[8];
+  bytes(b, 4);
+  uint32_t rank = 0;
+  for (int i = 3; i >= 0; --i) rank = (rank << 8) | b[i];
+  if (rank > 64) fail(GLM_FORMAT, "tensor_io", "implausible rank " + std::to_string(rank));
+  GlmtHeader h;
+  h.dtype = dtype;
+  h.dims.resize(rank);
+  for (uint32_t r = 0; r < rank; ++r) {
+    bytes(b, 8);
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+    h.dims[r] = v;
+  }
+  h.data = in.tellg();
+  if (static_cast<uint64_t>(size - h.data) < h.count() * h.elem()) fail(GLM_FORMAT, "tensor_io", "truncated file " + path);
+  return h;
+}
+
+// rows [row0, row0 + nrows) of an f64 / f32 GLMT matrix with `cols` columns, as doubles
+void read_glmt_rows(const std::string& path, const GlmtHeader& h, uint64_t row0, uint64_t nrows, uint64_t cols,
+                    std::vector<double>& out) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(GLM_FORMAT, "tensor_io", "cannot open " + path);
+  out.resize(nrows * cols);
+  in.seekg(h.data + static_cast<std::streamoff>(row0 * cols * h.elem()));
+  if (h.dtype == 0) {
+    in.read(reinterpret_cast<char*>(out.data()), static_cast<std::streamsize>(nrows * cols * 8));
+    if (static_cast<uint64_t>(in.gcount()) != nrows * cols * 8) fail(GLM_FORMAT, "tensor_io", "truncated file " + path);
+  } else {
+    std::vector<float> f(nrows * cols);
+    in.read(reinterpret_cast<char*>(f.data()), static_cast<std::streamsize>(f.size() * 4));
+    if (static_cast<uint64_t>(in.gcount()) != f.size() * 4) fail(GLM_FORMAT, "tensor_io", "truncated file " + path);
+    out.assign(f.begin(), f.end());
+  }
+}
 
 Glmt read_glmt(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
@@ -275,15 +345,16 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
     std::map<std::string, const Json*> by_name;
     for (const Json& e : man.at("matrices").arr) by_name[e.at("name").as_str()] = &e;
 
-    // read and validate every tensor before touching the device
+    // pass 1: every header, shape and file size, before any payload is read or device work
+    // starts (GLM_FORMAT on malformed input without a GPU)
     const int64_t d = cfg.hidden, f = cfg.ffn_hidden, L = cfg.num_layers;
     const int64_t shapes[5][2] = {{d, 3 * d}, {d, d}, {d, f}, {d, f}, {f, d}};
     const char* names[5] = {"qkv", "out_proj", "ffn_w1", "ffn_v", "ffn_w2"};
     const char* vecs[4] = {"ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias"};
-    Glmt emb = read_glmt(root + "/embedding.glmt");
-    if (emb.dtype != 0 || emb.count() != static_cast<uint64_t>(cfg.vocab) * d)
+    const std::string emb_path = root + "/embedding.glmt";
+    const GlmtHeader emb = read_glmt_header(emb_path);
+    if (emb.dtype == 2 || emb.count() != static_cast<uint64_t>(cfg.vocab) * d)
       fail(GLM_FORMAT, "quantlab", "embedding.glmt must be f64 [vocab, hidden]");
-    std::vector<Glmt> codes, scales, lnv;
     for (int64_t l = 0; l < L; ++l) {
       const std::string p = root + "/layer" + std::to_string(l) + ".";
       for (int w = 0; w < 5; ++w) {
@@ -296,23 +367,26 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
           fail(GLM_FORMAT, "quantlab", nm + " does not follow the manifest policy");
         if (e.at("rows").as_int() != shapes[w][0] || e.at("cols").as_int() != shapes[w][1])
           fail(GLM_FORMAT, "quantlab", nm + " has the wrong shape for the configured model");
-        codes.push_back(read_glmt(p + names[w] + ".codes.glmt"));
-        scales.push_back(read_glmt(p + names[w] + ".scales.glmt"));
+        const GlmtHeader c = read_glmt_header(p + names[w] + ".codes.glmt");
+        const GlmtHeader sc = read_glmt_header(p + names[w] + ".scales.glmt");
         const int64_t n = shapes[w][0] * shapes[w][1];
         const int64_t pb = bits == 4 ? (n + 1) / 2 : n;
         const int64_t ng = axis == GLM_AXIS_ROW ? shapes[w][0] : axis == GLM_AXIS_COLUMN ? shapes[w][1] : 1;
-        if (codes.back().dtype != 2 || static_cast<int64_t>(codes.back().count()) != pb)
+        if (c.dtype != 2 || static_cast<int64_t>(c.count()) != pb)
           fail(GLM_FORMAT, "quantlab", nm + ".codes.glmt payload length does not match");
-        if (scales.back().dtype != 0 || static_cast<int64_t>(scales.back().count()) != ng)
+        if (sc.dtype != 0 || static_cast<int64_t>(sc.count()) != ng)
           fail(GLM_FORMAT, "quantlab", nm + ".scales.glmt group count does not match");
       }
       for (int v = 0; v < 4; ++v) {
-        lnv.push_back(read_glmt(p + vecs[v] + ".glmt"));
-        if (lnv.back().dtype != 0 || static_cast<int64_t>(lnv.back().count()) != d)
+        const GlmtHeader h = read_glmt_header(p + vecs[v] + ".glmt");
+        if (h.dtype == 2 || static_cast<int64_t>(h.count()) != d)
           fail(GLM_FORMAT, "quantlab", std::string("layer LN vector ") + vecs[v] + " must be f64 [hidden]");
       }
     }
 
+    // pass 2: stream. One matrix of host memory at a time (GLM-130B: <= 403 MB of INT8 codes);
+    // the model keeps only this rank's shard on the device; codes and scales are validated
+    // like glm_qweight_create (INT4 -8 / INT8 -128 are not absmax codes, scales finite >= 0).
     glm_model* m = nullptr;
     glm_status s = glm_model_create(&cfg, bits, static_cast<glm_axis>(axis), max_batch, max_ctx, head_bf16, tp_rank,
                                     tp_size, &m);
@@ -321,15 +395,28 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
     auto check = [&](glm_status st) {
       if (st != GLM_OK) fail(st, "glmmodel", glm_last_error());
     };
-    check(glm_model_set_embedding(m, emb.f64.data()));
+    {
+      std::vector<double> rows;
+      const uint64_t chunk = std::max<uint64_t>(1, (uint64_t{256} << 20) / (8 * static_cast<uint64_t>(d)));
+      for (uint64_t r0 = 0; r0 < static_cast<uint64_t>(cfg.vocab); r0 += chunk) {
+        const uint64_t nr = std::min<uint64_t>(chunk, cfg.vocab - r0);
+        read_glmt_rows(emb_path, emb, r0, nr, d, rows);
+        check(glm_model_set_embedding_rows(m, static_cast<int64_t>(r0), static_cast<int64_t>(nr), rows.data()));
+      }
+    }
     for (int64_t l = 0; l < L; ++l) {
+      const std::string p = root + "/layer" + std::to_string(l) + ".";
       for (int w = 0; w < 5; ++w) {
-        const Glmt& c = codes[l * 5 + w];
-        const Glmt& sc = scales[l * 5 + w];
+        const Glmt c = read_glmt(p + names[w] + ".codes.glmt");
+        const Glmt sc = read_glmt(p + names[w] + ".scales.glmt");
+        validate_absmax_payload(c.i8.data(), static_cast<int64_t>(c.i8.size()), shapes[w][0] * shapes[w][1], bits);
         check(glm_model_set_quantized(m, static_cast<int>(l), w, c.i8.data(), static_cast<int64_t>(c.i8.size()),
                                       sc.f64.data(), static_cast<int64_t>(sc.f64.size())));
       }
-      for (int v = 0; v < 4; ++v) check(glm_model_set_tensor(m, static_cast<int>(l), 5 + v, lnv[l * 4 + v].f64.data()));
+      for (int v = 0; v < 4; ++v) {
+        const Glmt t = read_glmt(p + vecs[v] + ".glmt");
+        check(glm_model_set_tensor(m, static_cast<int>(l), 5 + v, t.f64.data()));
+      }
     }
     *out = guard.release();
   });

@@ -27,6 +27,9 @@ void unrepack_device(const void* dev, const QLayout& L, int8_t* payload, cudaStr
 void runtime_scales_device(const double* scales, int64_t nscales, const QLayout& L, int axis,
                            float* col_scale, float* row_scale, cudaStream_t st);
 double host_unkey(unsigned long long k);
+// Host check of a canonical absmax payload (n codes): INT4 nibble -8 / INT8 -128 are outside
+// the absmax code range (quant.cpp:19-31) -> GLM_CONTRACT; an odd INT4 count must pad with 0.
+void validate_absmax_payload(const int8_t* payload, int64_t payload_bytes, int64_t n, int bits);
 
 // Megatron shard of a [K, N] linear: local column j maps to full column
 // (j / col_per_rank_block) * col_block + col_offset + (j % col_per_rank_block);

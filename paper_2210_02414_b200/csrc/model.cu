@@ -418,6 +418,7 @@ struct glm_model {
     const int64_t ng = axis == GLM_AXIS_ROW ? K : axis == GLM_AXIS_COLUMN ? N : 1;
     if (payload_bytes != pb) fail(GLM_FORMAT, "quantlab", "payload length does not match the linear's shape and bits");
     if (nscales != ng) fail(GLM_FORMAT, "quantlab", "scale count does not match the model's group axis");
+    validate_absmax_payload(payload, pb, n, bits);
     for (int64_t g = 0; g < ng; ++g)
       if (!std::isfinite(scales[g]) || scales[g] < 0.0) fail(GLM_FORMAT, "quantlab", "scales must be finite and >= 0");
     DeviceBuffer dp(pb), ds(ng * 8);
@@ -428,14 +429,21 @@ struct glm_model {
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
 
-  void set_embedding(const double* e) {
-    const int64_t n = static_cast<int64_t>(V) * d;
-    DeviceBuffer de(n * 8);
-    CUDA_CHECK(cudaMemcpyAsync(de.ptr, e, n * 8, cudaMemcpyHostToDevice, st));
-    if (head_bf16) k_f64_to_bf16<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<__nv_bfloat16*>(E), n);
-    else k_f64_to_f32<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<float*>(E), n);
-    LAUNCH_CHECK("embedding upload");
-    CUDA_CHECK(cudaStreamSynchronize(st));
+  void set_embedding(const double* e) { set_embedding_rows(0, V, e); }
+
+  // rows [row0, row0 + nrows) of the tied table (streaming loaders: no full f64 copy on host or device)
+  void set_embedding_rows(int64_t row0, int64_t nrows, const double* e) {
+    if (row0 < 0 || nrows < 0 || row0 + nrows > V) fail(GLM_CONTRACT, "glmmodel", "embedding rows outside the vocabulary");
+    const int64_t chunk_rows = std::max<int64_t>(1, (int64_t{256} << 20) / (8 * static_cast<int64_t>(d)));
+    DeviceBuffer de(std::min(nrows, chunk_rows) * d * 8);
+    for (int64_t r = 0; r < nrows; r += chunk_rows) {
+      const int64_t nr = std::min(chunk_rows, nrows - r), n = nr * d, off = (row0 + r) * d;
+      CUDA_CHECK(cudaMemcpyAsync(de.ptr, e + r * d, n * 8, cudaMemcpyHostToDevice, st));
+      if (head_bf16) k_f64_to_bf16<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<__nv_bfloat16*>(E) + off, n);
+      else k_f64_to_f32<<<grid_of(n), 256, 0, st>>>(de.as<double>(), static_cast<float*>(E) + off, n);
+      LAUNCH_CHECK("embedding upload");
+      CUDA_CHECK(cudaStreamSynchronize(st));
+    }
   }
 
   void set_vector(int l, int which, const double* v) {
@@ -965,6 +973,13 @@ glm_status glm_model_destroy(glm_model* m) {
 
 glm_status glm_model_set_embedding(glm_model* m, const double* e) {
   return guarded([&] { checked(m)->set_embedding(e); });
+}
+
+glm_status glm_model_set_embedding_rows(glm_model* m, int64_t row0, int64_t nrows, const double* values) {
+  return guarded([&] {
+    if (!values && nrows > 0) fail(GLM_CONTRACT, "glmmodel", "null argument");
+    checked(m)->set_embedding_rows(row0, nrows, values);
+  });
 }
 
 glm_status glm_model_set_tensor(glm_model* m, int layer, int which, const double* values) {

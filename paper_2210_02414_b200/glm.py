@@ -104,6 +104,7 @@ SIGNATURES = {
     "glm_model_init_comm_emulated": (I32, [P, P]),
     "glm_model_init_comm": (I32, [P, P]),
     "glm_model_set_embedding": (I32, [P, P]),
+    "glm_model_set_embedding_rows": (I32, [P, I64, I64, P]),
     "glm_model_set_tensor": (I32, [P, I32, I32, P]),
     "glm_model_init_synthetic": (I32, [P, C.c_uint64]),
     "glm_model_export_linear": (I32, [P, I32, I32, P, P]),

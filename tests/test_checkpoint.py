@@ -130,3 +130,16 @@ def test_cpp_wrapper_loads_the_checkpoint(ckpt):
     _, path, _ = ckpt
     r = subprocess.run([build_cpp_test(), "--checkpoint", path], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "0 failed" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,byte", [(4, 0x08), (4, 0x80), (8, 0x80)])
+def test_codes_outside_the_absmax_range_are_rejected(tmp_path, bits, byte):
+    """The streaming loader validates every payload like glm_qweight_create: an INT4 nibble of
+    -8 or an INT8 code of -128 cannot come out of quantize_absmax (quant.cpp:19-31)."""
+    p = O.Params(1, 128, 2, vocab=64, seed=3)
+    write_checkpoint(str(tmp_path), p, bits, "column")
+    header = 4 + 2 + 4 + 8  # rank-1 GLMT header
+    corrupt(str(tmp_path), "layer0.ffn_w1.codes.glmt", header + 5, bytes([byte]))
+    with pytest.raises(glm.ContractError):
+        glm.Model.load_quantized(str(tmp_path))
