@@ -243,6 +243,11 @@ glm_status glm_model_reset(glm_model* m);
  * residual), [layers, rows, hidden] fp32, rows = n (prefill) or batch (decode). */
 glm_status glm_model_enable_taps(glm_model* m, int enable);
 glm_status glm_model_get_taps(const glm_model* m, float* attn, float* ffn);
+/* PrecisionPolicy (tensor.hpp:18-29) of later prefill / decode / block calls: half_storage != 0 is
+ * Storage::kHalfEmulated — the embedding rows, every DeepNorm output, the attention and GeGLU
+ * sublayer outputs, and the attention scores divided by softmax_prescale are rounded to binary16
+ * where forward() calls storage_round (model.cpp:148, 197, 213-223); 0 is kWide (the default). */
+glm_status glm_model_set_precision(glm_model* m, int half_storage, double softmax_prescale);
 /* Test hook: force every sublayer output to zero (the "echo" chain of SURVEY §8c). */
 glm_status glm_model_zero_sublayers(glm_model* m, int enable);
 

@@ -291,6 +291,10 @@ class QuantizedModel {
     check(glm_block_forward_host(m_.get(), layer, mode, seq, x.data(), positions.data(), n, context_length));
   }
   void enable_taps(bool on) { check(glm_model_enable_taps(m_.get(), on ? 1 : 0)); }
+  // PrecisionPolicy (tensor.hpp:18-29): Storage::kHalfEmulated and softmax_prescale
+  void set_precision(bool half_storage, double softmax_prescale = 1.0) {
+    check(glm_model_set_precision(m_.get(), half_storage ? 1 : 0, softmax_prescale));
+  }
   // per-layer sublayer outputs of the last call: [layers, rows, hidden] each
   void taps(int rows, std::vector<float>& attn, std::vector<float>& ffn) const {
     attn.resize(static_cast<size_t>(cfg_.num_layers) * rows * cfg_.hidden);

@@ -325,19 +325,41 @@ void build_mask(const or_sample* s, uint8_t* mask) {  // corruption.cpp:338-367
   }
 }
 
+double half_round(double x) {  // tensor.cpp:97-121
+  if (std::isnan(x)) return x;
+  const double sign = std::signbit(x) ? -1.0 : 1.0;
+  const double a = std::fabs(x);
+  if (a == 0.0 || std::isinf(x)) return x;
+  if (a >= 65520.0) return sign * std::numeric_limits<double>::infinity();
+  if (a <= 0x1p-25) return sign * 0.0;
+  double quantum;
+  if (a < 0x1p-14) {
+    quantum = 0x1p-24;
+  } else {
+    int e = 0;
+    std::frexp(a, &e);
+    quantum = std::ldexp(1.0, e - 11);
+  }
+  return sign * std::nearbyint(a / quantum) * quantum;
+}
+
+// half > 0: PrecisionPolicy kHalfEmulated with softmax_prescale `prescale` (tensor.hpp:18-29)
 void attention(const double* q, const double* k, const double* v, int64_t n, int64_t dh,
-               const int* pos, const uint8_t* mask, double* out) {
-  // model.cpp:137-152: RoPE(q), RoPE(k), scores / sqrt(dh), -inf fill, softmax, P.V
+               const int* pos, const uint8_t* mask, double* out, int half = 0, double prescale = 1.0) {
+  // model.cpp:137-152: RoPE(q), RoPE(k), scores / (sqrt(dh) * prescale), storage_round,
+  // -inf fill, softmax (multiplies the prescale back, tensor.cpp:229), P.V
   std::vector<double> rq(static_cast<size_t>(n * dh)), rk(static_cast<size_t>(n * dh));
   rope(q, n, dh, pos, rq.data());
   rope(k, n, dh, pos, rk.data());
   std::vector<double> sc(static_cast<size_t>(n * n)), p(static_cast<size_t>(n * n));
-  const double inv = 1.0 / (std::sqrt(static_cast<double>(dh)) * 1.0);
+  const double inv = 1.0 / (std::sqrt(static_cast<double>(dh)) * (half ? prescale : 1.0));
   for (int64_t i = 0; i < n; ++i)
     for (int64_t j = 0; j < n; ++j) {
       double acc = 0.0;
       for (int64_t c = 0; c < dh; ++c) acc += rq[i * dh + c] * rk[j * dh + c];
-      sc[i * n + j] = mask[i * n + j] ? acc * inv : -std::numeric_limits<double>::infinity();
+      double s = acc * inv;
+      if (half) s = half_round(s) * prescale;
+      sc[i * n + j] = mask[i * n + j] ? s : -std::numeric_limits<double>::infinity();
     }
   softmax(sc.data(), n, n, p.data());
   matmul(p.data(), v, out, n, n, dh);
@@ -690,9 +712,22 @@ int or_params_qpayload(const or_params* p, int layer, int which, const int8_t** 
   });
 }
 
+int or_forward_policy(const or_params* p, const or_sample* s, int half, double prescale, double* logits,
+                      double* attn_taps, double* ffn_taps, int zero_sublayers);
+
 int or_forward(const or_params* p, const or_sample* s, double* logits, double* attn_taps,
                double* ffn_taps, int zero_sublayers) {
-  // model.cpp:166-226
+  return or_forward_policy(p, s, 0, 1.0, logits, attn_taps, ffn_taps, zero_sublayers);
+}
+
+int or_forward_policy(const or_params* p, const or_sample* s, int half, double prescale, double* logits,
+                      double* attn_taps, double* ffn_taps, int zero_sublayers) {
+  // model.cpp:166-226; half: storage_round points of PrecisionPolicy kHalfEmulated
+  // (model.cpp:148, 197, 213-216, 220-223)
+  auto sround = [&](std::vector<double>& v) {
+    if (half)
+      for (double& x : v) x = half_round(x);
+  };
   return guarded([&] {
     const or_config& cfg = p->cfg;
     const int64_t n = s->n, d = p->d, f = p->f, dh = d / cfg.num_heads;
@@ -707,6 +742,7 @@ int or_forward(const or_params* p, const or_sample* s, double* logits, double* a
     std::vector<double> h(static_cast<size_t>(n * d));
     for (int64_t i = 0; i < n; ++i)  // embedding_rows (tensor.cpp:396-412)
       std::memcpy(&h[i * d], &p->embedding[static_cast<size_t>(s->tokens[i]) * d], d * 8);
+    sround(h);
     std::vector<double> qkv(static_cast<size_t>(n * 3 * d)), heads(static_cast<size_t>(n * d)),
         attn(static_cast<size_t>(n * d)), z(static_cast<size_t>(n * d)),
         a(static_cast<size_t>(n * f)), b(static_cast<size_t>(n * f)), ff(static_cast<size_t>(n * d));
@@ -720,15 +756,17 @@ int or_forward(const or_params* p, const or_sample* s, double* logits, double* a
             kh[i * dh + c] = qkv[i * 3 * d + d + hd * dh + c];
             vh[i * dh + c] = qkv[i * 3 * d + 2 * d + hd * dh + c];
           }
-        attention(qh.data(), kh.data(), vh.data(), n, dh, s->positions, mask.data(), oh.data());
+        attention(qh.data(), kh.data(), vh.data(), n, dh, s->positions, mask.data(), oh.data(), half, prescale);
         for (int64_t i = 0; i < n; ++i)
           for (int64_t c = 0; c < dh; ++c) heads[i * d + hd * dh + c] = oh[i * dh + c];
       }
       matmul(heads.data(), p->lin[OR_OUT][l].data(), attn.data(), n, d, d);
       if (zero_sublayers) std::fill(attn.begin(), attn.end(), 0.0);
+      sround(attn);
       if (attn_taps) std::memcpy(attn_taps + static_cast<int64_t>(l) * n * d, attn.data(), n * d * 8);
       for (int64_t i = 0; i < n * d; ++i) z[i] = alpha * h[i] + attn[i];  // model.cpp:125-131
       layernorm(z.data(), n, d, p->ln1g[l].data(), p->ln1b[l].data(), cfg.layernorm_eps, h.data());
+      sround(h);
       // geglu (model.cpp:133-135)
       matmul(h.data(), p->lin[OR_W1][l].data(), a.data(), n, d, f);
       matmul(h.data(), p->lin[OR_V][l].data(), b.data(), n, d, f);
@@ -736,9 +774,11 @@ int or_forward(const or_params* p, const or_sample* s, double* logits, double* a
       for (int64_t i = 0; i < n * f; ++i) a[i] *= b[i];
       matmul(a.data(), p->lin[OR_W2][l].data(), ff.data(), n, f, d);
       if (zero_sublayers) std::fill(ff.begin(), ff.end(), 0.0);
+      sround(ff);
       if (ffn_taps) std::memcpy(ffn_taps + static_cast<int64_t>(l) * n * d, ff.data(), n * d * 8);
       for (int64_t i = 0; i < n * d; ++i) z[i] = alpha * h[i] + ff[i];
       layernorm(z.data(), n, d, p->ln2g[l].data(), p->ln2b[l].data(), cfg.layernorm_eps, h.data());
+      sround(h);
     }
     // tied head: logits = h . E^T (model.cpp:225)
     const int64_t V = cfg.vocab;
@@ -776,23 +816,8 @@ int or_build_mask(const or_sample* s, uint8_t* mask) {
   return guarded([&] { build_mask(s, mask); });
 }
 
-double or_half_round(double x) {  // tensor.cpp:97-121
-  if (std::isnan(x)) return x;
-  const double sign = std::signbit(x) ? -1.0 : 1.0;
-  const double a = std::fabs(x);
-  if (a == 0.0 || std::isinf(x)) return x;
-  if (a >= 65520.0) return sign * std::numeric_limits<double>::infinity();
-  if (a <= 0x1p-25) return sign * 0.0;
-  double quantum;
-  if (a < 0x1p-14) {
-    quantum = 0x1p-24;
-  } else {
-    int e = 0;
-    std::frexp(a, &e);
-    quantum = std::ldexp(1.0, e - 11);
-  }
-  return sign * std::nearbyint(a / quantum) * quantum;
-}
+double or_half_round(double x) { return half_round(x); }
+
 
 int or_qlinear_cols(const double* x, int64_t M, int64_t K, int64_t N, const int8_t* payload,
                     const double* scales, int bits, int axis, const int64_t* cols, int64_t ncols,

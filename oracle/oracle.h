@@ -80,6 +80,10 @@ int or_params_qpayload(const or_params* p, int layer, int which, const int8_t** 
  * outputs to 0 (the "echo" chain used for the Delta_ref normalisation). */
 int or_forward(const or_params* p, const or_sample* s, double* logits, double* attn_taps,
                double* ffn_taps, int zero_sublayers);
+/* Same under PrecisionPolicy (tensor.hpp:18-29): half != 0 = kHalfEmulated storage, scores
+ * stored as binary16(score / prescale) and multiplied back inside the softmax. */
+int or_forward_policy(const or_params* p, const or_sample* s, int half, double prescale, double* logits,
+                      double* attn_taps, double* ffn_taps, int zero_sublayers);
 
 /* ---- ops (tensor.cpp) ---- */
 void or_rope_rotate(const double* x, int64_t rows, int64_t d, const int* positions, double* out);

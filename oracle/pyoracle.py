@@ -85,6 +85,7 @@ def lib():
         L.or_fnv1a64.argtypes = [p, i64, C.c_uint64]
         L.or_fnv1a64.restype = C.c_uint64
         L.or_qlinear_cols.argtypes = [p, i64, i64, i64, p, p, i32, i32, p, i64, p]
+        L.or_forward_policy.argtypes = [p, C.POINTER(Sample), i32, d, p, p, p, i32]
         L.or_gen_rows.argtypes = [C.c_uint64, C.c_uint32, i64, i64, i64, C.c_float, C.c_float, i64, p]
         L.or_dequantize_cols.argtypes = [p, p, i64, i64, i32, i32, p, i64, p]
         _LIB = L
@@ -204,14 +205,15 @@ class Params:
         return (np.ctypeslib.as_array(pl, shape=(nb.value,)).copy(),
                 np.ctypeslib.as_array(sc, shape=(ns.value,)).copy())
 
-    def forward(self, sample, taps=False, zero_sublayers=False):
+    def forward(self, sample, taps=False, zero_sublayers=False, half=False, prescale=1.0):
+        """forward (model.cpp:166-226); half / prescale: PrecisionPolicy kHalfEmulated."""
         n = sample["n"]
         logits = np.empty((n, self.vocab), np.float64)
         at = np.empty((self.num_layers, n, self.hidden)) if taps else None
         ft = np.empty((self.num_layers, n, self.hidden)) if taps else None
         s, keep = make_sample(sample)
-        _check(lib().or_forward(self.h, C.byref(s), _ptr(logits), _ptr(at), _ptr(ft),
-                                int(zero_sublayers)))
+        _check(lib().or_forward_policy(self.h, C.byref(s), int(half), float(prescale), _ptr(logits), _ptr(at),
+                                       _ptr(ft), int(zero_sublayers)))
         del keep
         return (logits, at, ft) if taps else logits
 

@@ -44,7 +44,7 @@ def lib(blas_threads=None):
         p, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
         L.ref_last_error.restype = C.c_char_p
         L.ref_use_blas.argtypes = [C.c_char_p, i32]
-        L.ref_forward.argtypes = [i32, i32, i32, i32, u64, i32, i32, p, p, i32, i32, i32, p]
+        L.ref_forward.argtypes = [i32, i32, i32, i32, u64, i32, i32, p, p, i32, i32, i32, i32, C.c_double, p]
         L.ref_quantize_hashes.argtypes = [i32, i32, i32, i32, u64, i32, i32, p, p, p, p]
         L.ref_bench_layer_decode.argtypes = [u64, i32, i32, i32, i32, i32, i32, i64, p, p, p]
         bp = blas_path()
@@ -63,15 +63,17 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def forward(layers, hidden, heads, vocab, seed, bits, axis, tokens, positions, context_length, unidirectional=False):
+def forward(layers, hidden, heads, vocab, seed, bits, axis, tokens, positions, context_length, unidirectional=False,
+            half=False, prescale=1.0):
     """forward(dequantize_model(quantize_model(init_parameters(cfg, Rng(seed)), policy)), gMASK sample)
-    (model.cpp:166-226 on quant.cpp:284-342); bits 0 = unquantized. Logits [n, vocab]."""
+    (model.cpp:166-226 on quant.cpp:284-342); bits 0 = unquantized; half: PrecisionPolicy
+    kHalfEmulated with softmax_prescale. Logits [n, vocab]."""
     L = lib()
     t = np.ascontiguousarray(tokens, np.int32)
     pos = np.ascontiguousarray(positions, np.int32)
     out = np.empty((len(t), vocab), np.float64)
     _check(L, L.ref_forward(layers, hidden, heads, vocab, seed, bits, AXIS[axis], _ptr(t), _ptr(pos), len(t),
-                            context_length, int(unidirectional), _ptr(out)))
+                            context_length, int(unidirectional), int(half), float(prescale), _ptr(out)))
     return out
 
 

@@ -153,9 +153,10 @@ int ref_use_blas(const char* path, int threads) {
 
 // forward(dequantize_model(quantize_model(init_parameters(cfg, Rng(seed)), {bits, absmax, axis})),
 // gmask sample) — the reference's quantized forward (test_quant.cpp:250-272); logits [n, vocab].
-// bits 0: unquantized forward(init_parameters(...)).
+// bits 0: unquantized forward(init_parameters(...)); half: PrecisionPolicy kHalfEmulated.
 int ref_forward(int layers, int hidden, int heads, int vocab, uint64_t seed, int bits, int axis, const int* tokens,
-                const int* positions, int n, int context_length, int unidirectional, double* logits) {
+                const int* positions, int n, int context_length, int unidirectional, int half, double prescale,
+                double* logits) {
   return guarded([&] {
     GLMConfig cfg = tiny_cfg(layers, hidden, heads, vocab);
     Rng rng(seed);
@@ -166,6 +167,10 @@ int ref_forward(int layers, int hidden, int heads, int vocab, uint64_t seed, int
     CorruptedSample s = gmask_sample(tokens, positions, n, context_length);
     ForwardOptions opts;
     if (unidirectional) opts.variant_override = AttentionVariant::kUnidirectional;
+    if (half) {  // PrecisionPolicy (tensor.hpp:18-29)
+      opts.policy.storage = PrecisionPolicy::Storage::kHalfEmulated;
+      opts.policy.softmax_prescale = prescale;
+    }
     const Tensor out = forward(q, s, opts);
     std::memcpy(logits, out.values().data(), sizeof(double) * static_cast<size_t>(n) * vocab);
   });

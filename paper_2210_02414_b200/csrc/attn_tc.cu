@@ -243,6 +243,11 @@ __global__ void __launch_bounds__(kUThreads, 1) k_attn_prefill_umma(AttnPrefillA
       float sv[kUK];
 #pragma unroll
       for (int c = 0; c < kUK; ++c) sv[c] = __uint_as_float(sr[c >> 5][c & 31]);
+      if (a.prescale > 0.f) {  // half-emulated storage: fp16(score / prescale), log2 units here
+        const float to = 0.6931471805599453f / a.prescale, back = a.prescale * 1.4426950408889634f;
+#pragma unroll
+        for (int c = 0; c < kUK; ++c) sv[c] = half_round(sv[c] * to) * back;
+      }
       const int j0 = j * kUK;
       if (!__all_sync(0xffffffffu, j0 + kUK <= lim)) {
 #pragma unroll

@@ -54,7 +54,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // ---- embedding_rows (tensor.cpp:396-412) ---------------------------------------------
 template <typename ET>
 __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restrict__ tokens, int M,
-                        float* __restrict__ h, XOut xo) {
+                        float* __restrict__ h, XOut xo, int half_store) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x;
@@ -68,6 +68,10 @@ __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restri
       v0 = __bfloat162float(E[row * d + k]);
       v1 = __bfloat162float(E[row * d + k + 1]);
     }
+    if (half_store) {
+      v0 = half_round(v0);
+      v1 = half_round(v1);
+    }
     h[m * d + k] = v0;
     h[m * d + k + 1] = v1;
     store_xfrag_pair(xo, m, k, v0, v1);
@@ -78,7 +82,7 @@ __global__ void k_embed(const ET* __restrict__ E, int64_t d, const int* __restri
 // tokens x 8 features per warp).
 template <typename ET>
 __global__ void k_embed_tiles(const ET* __restrict__ E, int64_t d, const int* __restrict__ tokens, int M,
-                              float* __restrict__ h, XOut xo) {
+                              float* __restrict__ h, XOut xo, int half_store) {
   pdl_wait();
   pdl_trigger();
   constexpr int T = kXTileTokens;
@@ -107,6 +111,9 @@ __global__ void k_embed_tiles(const ET* __restrict__ E, int64_t d, const int* __
         v[2 * e + 1] = f.y;
       }
     }
+    if (half_store)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = half_round(v[e]);
     float4* hp = reinterpret_cast<float4*>(h + m * d + n);
     hp[0] = make_float4(v[0], v[1], v[2], v[3]);
     hp[1] = make_float4(v[4], v[5], v[6], v[7]);
@@ -334,6 +341,9 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
     y[i].y *= sc[i].y;
   }
   if (a.peer.size > 1 && !peer_allreduce(a.peer, m, rank, p0, p1, y)) return;  // push-only launch
+  if (a.half_store)
+#pragma unroll
+    for (int i = 0; i < kLnPairs; ++i) y[i] = make_float2(half_round(y[i].x), half_round(y[i].y));
   float2 z[kLnPairs];
   ShiftedSums st;
 #pragma unroll
@@ -359,8 +369,12 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
     const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
     if (p < p1) {
       const int64_t n = 2 * p;
-      const float o0 = (z[i].x - mean) * rstd * gn[i].x + bs[i].x;
-      const float o1 = (z[i].y - mean) * rstd * gn[i].y + bs[i].y;
+      float o0 = (z[i].x - mean) * rstd * gn[i].x + bs[i].x;
+      float o1 = (z[i].y - mean) * rstd * gn[i].y + bs[i].y;
+      if (a.half_store) {
+        o0 = half_round(o0);
+        o1 = half_round(o1);
+      }
       *reinterpret_cast<float2*>(a.h + static_cast<int64_t>(m) * a.d + n) = make_float2(o0, o1);
       store_xfrag_pair(a.x0, m, n, o0, o1);
       store_xfrag_pair(a.x1, m, n, o0, o1);
@@ -396,6 +410,7 @@ __global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
         y.x *= a.in.scale[n];
         y.y *= a.in.scale[n + 1];
       }
+      if (a.half_store) y = make_float2(half_round(y.x), half_round(y.y));
     }
     if (a.tap) *reinterpret_cast<float2*>(a.tap + static_cast<int64_t>(m) * a.d + n) = y;
     const float2 hv = *reinterpret_cast<const float2*>(hrow + n);
@@ -412,8 +427,12 @@ __global__ void __launch_bounds__(kLnRowThreads) k_deepnorm_ln_rows(LnArgs a) {
   for (int64_t p = threadIdx.x; p < npairs; p += kLnRowThreads) {
     const int64_t n = 2 * p;
     const float2 z = *reinterpret_cast<const float2*>(hrow + n);
-    const float o0 = (z.x - mean) * rstd * a.gain[n] + a.bias[n];
-    const float o1 = (z.y - mean) * rstd * a.gain[n + 1] + a.bias[n + 1];
+    float o0 = (z.x - mean) * rstd * a.gain[n] + a.bias[n];
+    float o1 = (z.y - mean) * rstd * a.gain[n + 1] + a.bias[n + 1];
+    if (a.half_store) {
+      o0 = half_round(o0);
+      o1 = half_round(o1);
+    }
     *reinterpret_cast<float2*>(hrow + n) = make_float2(o0, o1);
     store_xfrag_pair(a.x0, m, n, o0, o1);
     store_xfrag_pair(a.x1, m, n, o0, o1);
@@ -469,6 +488,9 @@ __global__ void __launch_bounds__(kLnRowThreads, MINB) k_deepnorm_ln_rows8(LnArg
       if (a.in.scale)
 #pragma unroll
         for (int e = 0; e < 8; ++e) y[e] *= a.in.scale[n + e];
+      if (a.half_store)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = half_round(y[e]);
     }
     if (a.tap) st8(a.tap + static_cast<int64_t>(m) * a.d + n, y);
     float z[8];
@@ -491,6 +513,9 @@ __global__ void __launch_bounds__(kLnRowThreads, MINB) k_deepnorm_ln_rows8(LnArg
     ld8(a.bias + n, b);
 #pragma unroll
     for (int e = 0; e < 8; ++e) z[e] = (z[e] - mean) * rstd * g[e] + b[e];
+    if (a.half_store)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) z[e] = half_round(z[e]);
     st8(hrow + n, z);
     store_x8(a.x0, m, n, z);
     store_x8(a.x1, m, n, z);
@@ -761,6 +786,8 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
         float acc = dot8(kv[u]);
 #pragma unroll
         for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        // half-emulated storage: scores held as fp16(score / prescale), softmax multiplies back
+        if (a.prescale > 0.f) acc = half_round(acc / a.prescale) * a.prescale;
         if (sub == 0 && s < k1) p[s - k0] = acc;
       }
     }
@@ -1087,6 +1114,14 @@ __global__ void __launch_bounds__(kFaThreads, DH == 128 ? 3 : 4) k_attn_prefill_
         mma_f16(sc[2 * np], qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3], b0, b1);
         mma_f16(sc[2 * np + 1], qa[kt][0], qa[kt][1], qa[kt][2], qa[kt][3], b2, b3);
       }
+    }
+    // half-emulated storage: scores (log2 units here) held as fp16(score / prescale)
+    if (a.prescale > 0.f) {
+      const float to = 0.6931471805599453f / a.prescale, back = a.prescale * 1.4426950408889634f;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[nt][e] = half_round(sc[nt][e] * to) * back;
     }
     // ---- gMASK visibility on blocks that straddle it ----
     const int j0 = blk * kFaKeys;
@@ -1436,17 +1471,18 @@ int grid_for(int64_t n, int threads, int cap = 148 * 16) {
 }  // namespace
 
 void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool half_store) {
+  const int hs = half_store ? 1 : 0;
   if (xo.tile && d % 8 == 0) {
     const int64_t warps = (M + kXTileTokens - 1) / kXTileTokens * (d / 8) * (kXTileTokens / 32);
     const dim3 grid(grid_for(warps * 32, 256, 1 << 30));  // one pass per warp: the row-id -> row load chain is latency-bound
-    if (bf16) launch_k(k_embed_tiles<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
-    else launch_k(k_embed_tiles<float>, grid, dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
+    if (bf16) launch_k(k_embed_tiles<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo, hs);
+    else launch_k(k_embed_tiles<float>, grid, dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo, hs);
     LAUNCH_CHECK("k_embed_tiles");
     return;
   }
-  if (bf16) launch_k(k_embed<__nv_bfloat16>, dim3(M), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo);
-  else launch_k(k_embed<float>, dim3(M), dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo);
+  if (bf16) launch_k(k_embed<__nv_bfloat16>, dim3(M), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(E), d, tokens, M, h, xo, hs);
+  else launch_k(k_embed<float>, dim3(M), dim3(256), 0, st, static_cast<const float*>(E), d, tokens, M, h, xo, hs);
   LAUNCH_CHECK("k_embed");
 }
 

@@ -68,6 +68,7 @@ struct LnArgs {
   float* tap;               // optional [M][d] copy of the sublayer output
   int zero_sublayer;
   PeerArgs peer{};          // size > 1: sum the sublayer output across tensor-parallel ranks
+  int half_store = 0;       // PrecisionPolicy kHalfEmulated: round the sublayer output and h to fp16 (model.cpp:213-223)
 };
 
 struct ActArgs {
@@ -89,6 +90,7 @@ struct AttnDecodeArgs {
   int* counters;            // [B][heads], zero-initialised
   XOut xo;                  // x_frag of out_proj
   float* out;               // optional fp32 [B][d_local]
+  float prescale = 0.f;     // > 0: PrecisionPolicy kHalfEmulated, scores stored as fp16(score / prescale) (model.cpp:143-148)
   int stage_keys = 0;       // set by launch_attn_decode: keys per CTA staged in shared memory (0: read from L2/HBM)
   int split_keys = 256;     // set by launch_attn_decode: cached keys per CTA (attn_decode_split_keys)
 };
@@ -114,6 +116,7 @@ struct AttnPrefillArgs {
   // activation tiles at token rows xrow0 + i instead of the fp32 rows
   XOut xo{};
   int xrow0 = 0;
+  float prescale = 0.f;     // > 0: PrecisionPolicy kHalfEmulated (see AttnDecodeArgs)
 };
 
 struct HeadArgs {
@@ -127,8 +130,9 @@ struct HeadArgs {
   __nv_bfloat16* hb = nullptr;  // [M][d] scratch: bf16 copy of h for the tensor-core head
 };
 
+// half_store: round h to fp16 (PrecisionPolicy kHalfEmulated, model.cpp:197)
 void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M, float* h, const XOut& xo,
-                  cudaStream_t st);
+                  cudaStream_t st, bool half_store = false);
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st);
 void launch_geglu_act(const ActArgs& a, cudaStream_t st);
 // keys per CTA of the decode attention: 256 up to a 256-token cache (no merge), else 64

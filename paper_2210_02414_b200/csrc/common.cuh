@@ -160,6 +160,10 @@ __device__ __forceinline__ void trace_point(unsigned tag) {
 // so no compiler assumption about NaN can turn a check into |x| != inf.
 __device__ __forceinline__ bool finite_f32(float x) { return ((__float_as_uint(x) >> 23) & 0xFFu) != 0xFFu; }
 
+// binary16 storage emulation of the reference's PrecisionPolicy (half_round_value,
+// tensor.cpp:97-121): round to nearest even fp16, >= 65520 -> +-inf, below 2^-25 -> 0
+__device__ __forceinline__ float half_round(float x) { return __half2float(__float2half_rn(x)); }
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

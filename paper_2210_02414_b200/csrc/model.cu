@@ -134,6 +134,10 @@ struct glm_model {
   int64_t taps_rows = 0;
 
   bool taps = false, zero_sub = false;
+  // PrecisionPolicy (tensor.hpp:18-29): kHalfEmulated storage rounds h, the sublayer outputs and
+  // the attention scores (/ prescale) to binary16 at the reference's storage_round points
+  bool half_store = false;
+  float prescale = 1.f;
   int64_t last_rows = 0;
 
   cudaStream_t st = nullptr;
@@ -536,7 +540,7 @@ struct glm_model {
   int enqueue_decode(int B, bool with_logits = true) {
     int launches = 0;
     const Layer& l0 = layers[0];
-    launch_embed(E, head_bf16, d, d_tokens, B, h.as<float>(), xout(xf_qkv.as<__half>(), l0.lin[QKV]), st);
+    launch_embed(E, head_bf16, d, d_tokens, B, h.as<float>(), xout(xf_qkv.as<__half>(), l0.lin[QKV]), st, half_store);
     ++launches;
     for (int l = 0; l < L; ++l) launches += decode_layer(l, B, d_positions, d_len, l + 1 < L);
     launches += enqueue_head(B, logits.as<float>(), with_logits);
@@ -572,6 +576,7 @@ struct glm_model {
     aa.counters = attn_ctr;
     aa.xo = xout(xf_out.as<__half>(), out);
     aa.out = nullptr;
+    aa.prescale = half_store ? prescale : 0.f;
     launch_attn_decode(aa, B, st);
     gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
     LnArgs ln;
@@ -585,6 +590,7 @@ struct glm_model {
     ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v) : XOut{};  // W1 and V share x unless kRow
     ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
     ln.zero_sublayer = zero_sub;
+    ln.half_store = half_store ? 1 : 0;
     launches += ln_after_row_parallel(ln, out, out.plan(B), B);
     GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
               axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
@@ -740,6 +746,7 @@ struct glm_model {
         ap.xo = xout(xf_out.as<__half>(), out, nt);
         ap.xrow0 = r0;
       }
+      ap.prescale = half_store ? prescale : 0.f;
       launch_attn_prefill(ap, st);
     }
     if (!attn_tiles) launch_rows_to_xfrag(attn_out.as<float>(), dl, n, dl, xout(xf_out.as<__half>(), out, nt), st);
@@ -757,6 +764,7 @@ struct glm_model {
     ln.x1 = axis == GLM_AXIS_ROW ? xout(xf_v.as<__half>(), v, nt) : XOut{};  // W1 and V share x unless kRow
     ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * n * d : nullptr;
     ln.zero_sublayer = zero_sub;
+    ln.half_store = half_store ? 1 : 0;
     launch_deepnorm_ln(ln, n, st);
     if (axis != GLM_AXIS_ROW && qmm_geglu_supported(w1.w, v.w, n)) {  // W1|V GEMM with the GeGLU epilogue
       const XOut xo = xout(xf_w2.as<__half>(), w2, nt);
@@ -875,7 +883,8 @@ struct glm_model {
     DeviceBuffer dtok(n * 4), dpos(n * 4);
     CUDA_CHECK(cudaMemcpyAsync(dtok.ptr, tokens, n * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(dpos.ptr, positions, n * 4, cudaMemcpyHostToDevice, st));
-    launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV], nt), st);
+    launch_embed(E, head_bf16, d, dtok.as<int>(), n, h.as<float>(), xout(xf_qkv.as<__half>(), layers[0].lin[QKV], nt), st,
+                 half_store);
     for (int l = 0; l < L; ++l) prefill_layer(l, n, nseg, seqs, lens, ctx, row0.data(), dpos.as<int>(), l + 1 < L);
     if (logits_out) {
       enqueue_head(n, logits.as<float>());
@@ -1119,6 +1128,17 @@ glm_status glm_model_get_taps(const glm_model* m, float* attn, float* ffn) {
     const int64_t bytes = static_cast<int64_t>(m->L) * m->last_rows * m->d * 4;
     CUDA_CHECK(cudaMemcpy(attn, m->taps_attn.ptr, bytes, cudaMemcpyDeviceToHost));
     CUDA_CHECK(cudaMemcpy(ffn, m->taps_ffn.ptr, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+glm_status glm_model_set_precision(glm_model* m, int half_storage, double softmax_prescale) {
+  return guarded([&] {
+    checked(m);
+    if (!(softmax_prescale > 0.0) || !std::isfinite(softmax_prescale))
+      fail(GLM_CONTRACT, "tensorcore", "softmax_prescale must be a positive finite number");
+    m->drop_graphs();  // captured steps hold the old policy in their kernel arguments
+    m->half_store = half_storage != 0;
+    m->prescale = static_cast<float>(softmax_prescale);
   });
 }
 

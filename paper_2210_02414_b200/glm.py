@@ -116,6 +116,7 @@ SIGNATURES = {
     "glm_model_enable_taps": (I32, [P, I32]),
     "glm_model_get_taps": (I32, [P, P, P]),
     "glm_model_zero_sublayers": (I32, [P, I32]),
+    "glm_model_set_precision": (I32, [P, I32, D]),
     "glm_block_forward": (I32, [P, I32, I32, I32, P, P, I32, I32, P]),
     "glm_block_forward_host": (I32, [P, I32, I32, I32, P, P, I32, I32]),
     "glm_deepnorm_residual": (I32, [P, P, I64, I64, D, P, P, D, P, P]),
@@ -544,6 +545,11 @@ class Model:
         f = np.empty_like(a)
         _check(lib().glm_model_get_taps(self.h, _p(a), _p(f)))
         return a, f
+
+    def set_precision(self, half_storage=False, softmax_prescale=1.0):
+        """PrecisionPolicy (tensor.hpp:18-29): binary16 storage emulation at the reference's
+        storage_round points, attention scores stored / softmax_prescale."""
+        _check(lib().glm_model_set_precision(self.h, int(half_storage), float(softmax_prescale)))
 
     def zero_sublayers(self, on=True):
         _check(lib().glm_model_zero_sublayers(self.h, int(on)))

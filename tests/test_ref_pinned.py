@@ -69,3 +69,18 @@ def test_reference_forward_equals_oracle(bits, axis, uni):
     assert np.abs(ref - ora).max() <= 1e-10 * np.abs(ref).max()
     if bits == 8 and not uni:
         np.testing.assert_allclose(ref[-1, :4], GOLD["tiny_forward_int8_row"]["last_row_logits_0_3"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("prescale", [1.0, 8.0])
+def test_reference_half_storage_forward_equals_oracle(prescale):
+    """PrecisionPolicy kHalfEmulated (tensor.hpp:18-29; storage_round at model.cpp:148, 197,
+    213-223): the reference's forward with binary16 storage == the oracle's restatement."""
+    sample = O.gmask_sample(PREFIX[:60], [40, 41])
+    ref = R.forward(4, 512, 8, 262, 1234, 8, "row", sample["tokens"], sample["positions"], sample["context_length"],
+                    half=True, prescale=prescale)
+    p = O.Params(4, 512, 8, vocab=262, seed=1234)
+    p.quantize(8, "row")
+    ora = p.forward(sample, half=True, prescale=prescale)
+    assert np.abs(ref - ora).max() <= 1e-10 * np.abs(ref).max()
+    wide = p.forward(sample)
+    assert np.abs(ora - wide).max() > 1e-6  # the policy changes the result
