@@ -1279,7 +1279,10 @@ int m1_warps(int M) {
 int mk_row_tiles(int bits, int M) {
   static const int env = [] { const char* e = getenv("GLM_MK_RT"); return e ? atoi(e) : 0; }();
   if (env == 1 || env == 2) return env;
-  return M > 8 ? 2 : 1;  // measured: +12% (INT4) / +13% (INT8) at 16 tokens, a loss at <= 8
+  // measured: fp16 kernels +12% (INT4) / +13% (INT8) at 16 tokens, a loss at <= 8; the integer-MMA
+  // kernel gains from 8 tokens on (qkv shape, tools/r2_mk_probe.py: M = 8 47.3 -> 43.0 us)
+  if (bits == 4 && gemv_imma()) return M >= 6 ? 2 : 1;
+  return M > 8 ? 2 : 1;
 }
 
 namespace {
