@@ -195,6 +195,7 @@ __device__ __forceinline__ RowStat block_stat(RowStat a, RowStat* red) {
 // Cluster-wide statistics: each CTA pushes its partial into slot[rank] of every CTA of the
 // cluster (distributed shared memory stores), one cluster barrier (release/acquire), then
 // every CTA merges its local slots in rank order: identical on every CTA and every run.
+template <int CL>
 __device__ __forceinline__ RowStat cluster_stat(RowStat v, RowStat* red, RowStat* slots) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -206,11 +207,11 @@ __device__ __forceinline__ RowStat cluster_stat(RowStat v, RowStat* red, RowStat
     RowStat t = red[0];
     for (int i = 1; i < kLnThreads / 32; ++i) t = stat_merge(t, red[i]);
     const unsigned rank = cluster.block_rank();
-    if (l < kLnCluster) *cluster.map_shared_rank(slots + rank, l) = t;
+    if (l < CL) *cluster.map_shared_rank(slots + rank, l) = t;
   }
   cluster.sync();
   RowStat r = slots[0];
-  for (int i = 1; i < kLnCluster; ++i) r = stat_merge(r, slots[i]);
+  for (int i = 1; i < CL; ++i) r = stat_merge(r, slots[i]);
   return r;
 }
 
@@ -219,7 +220,7 @@ __device__ __forceinline__ RowStat cluster_stat(RowStat v, RowStat* red, RowStat
 // this generation and sum the inbox slots in rank order (same bits on every rank). Returns
 // false after a push-only launch (mode 1). A flag that does not arrive within ~20 s sets the
 // error word (Collective::check_peer) instead of hanging the GPU.
-static_assert(kPeerSlices == kLnCluster, "one peer flag per LayerNorm cluster CTA");
+static_assert(kPeerSlices >= kLnCluster, "one peer flag per LayerNorm cluster CTA");
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -282,15 +283,18 @@ __device__ __forceinline__ bool peer_allreduce(const PeerArgs& P, int m, int cra
   return true;
 }
 
-__global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
+// CL CTAs per row: 8 (up to 8 rows: 15 clusters of 8 are co-resident on the 148 SMs) or 4
+// (9..16 rows: 16 clusters of 8 would run in two waves, ncu at 16 rows 18-21 us per launch)
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
   trace_point(20);
   __shared__ RowStat red[kLnThreads / 32];
-  __shared__ RowStat slots[kLnCluster];
+  __shared__ RowStat slots[CL];
   namespace cg = cooperative_groups;
   const int rank = static_cast<int>(cg::this_cluster().block_rank());
-  const int m = blockIdx.x / kLnCluster;
+  const int m = blockIdx.x / CL;
   const int64_t npairs = a.d / 2;
-  const int64_t per = (npairs + kLnCluster - 1) / kLnCluster;
+  const int64_t per = (npairs + CL - 1) / CL;
   const int64_t p0 = rank * per, p1 = min(npairs, p0 + per);
   // everything that does not depend on the predecessor GEMV (LN parameters, the scale
   // vector, the residual written two kernels ago) is fetched before waiting on it
@@ -359,7 +363,7 @@ __global__ void __cluster_dims__(kLnCluster, 1, 1) __launch_bounds__(kLnThreads)
   }
   // one cluster reduction of (count, mean, M2); biased variance (tensor.cpp:267)
   trace_point(23);
-  const RowStat tot = cluster_stat(st.stat(), red, slots);
+  const RowStat tot = cluster_stat<CL>(st.stat(), red, slots);
   trace_point(24);
   const float mean = tot.mean;
   const float var = tot.m2 / static_cast<float>(a.d);
@@ -1488,6 +1492,8 @@ void launch_embed(const void* E, bool bf16, int64_t d, const int* tokens, int M,
 
 void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   if (a.d > 2ll * kLnPairs * kLnThreads * kLnCluster || a.d % 2) fail(GLM_DIMENSION, "glmmodel", "hidden unsupported by LN kernel");
+  // (the fused tensor-parallel sum keeps 8: its inbox slices and generation flags are per 8-CTA slice)
+  const bool cl4 = M > 8 && a.peer.size <= 1 && a.d <= 2ll * kLnPairs * kLnThreads * 4;
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool v8 = a.d % 8 == 0 && a.in.ld % 4 == 0 && a.in.split_stride % 4 == 0 && al(a.in.p) && al(a.h) &&
                   al(a.gain) && al(a.bias) && al(a.tap);
@@ -1498,7 +1504,8 @@ void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   if (a.peer.size > 1 && M > 16) fail(GLM_CONTRACT, "glmmodel", "fused tensor-parallel LayerNorm is a decode (<= 16 rows) kernel");
   if (M > 16 && v8 && rows8) launch_k(k_deepnorm_ln_rows8<3>, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
-  else launch_k(k_deepnorm_ln, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
+  else if (cl4) launch_k(k_deepnorm_ln<4>, dim3(M * 4), dim3(kLnThreads), 0, st, a);
+  else launch_k(k_deepnorm_ln<kLnCluster>, dim3(M * kLnCluster), dim3(kLnThreads), 0, st, a);
   LAUNCH_CHECK("k_deepnorm_ln");
 }
 

@@ -1010,14 +1010,18 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
 }
 
 // ---- integer-MMA multi-token variant (INT4, 3..16 tokens: batched decode) -----------------
-// The CTA-item structure of k_gemv_mk (16 * RT row tiles x one k-slice, the slice of all M
-// activation rows bulk-copied into a double-buffered shared buffer) with the integer MMA of
-// k_gemv_i4: after each slice lands, the CTA turns it in place into digit pairs with one scale
-// per (vector, token, slice) — the max over the slice, so every k-slice partial carries its own
-// scale — and the slice's digit sums. A code fragment (8 LOP3 per 1024 weights) then feeds
-// NQ = ceil(M / 4) IMMA column groups of 4 tokens (column 2j + e: token 4q + j, digit e).
+// A CTA owns a contiguous range of `per` items of the slice-major list (item = slice * ngroups +
+// row-tile group; a group is 16 * RT row tiles, one per warp and RT): consecutive items share
+// their k-slice, so the slice of all M activation rows is bulk-copied into ONE resident 96 KB
+// buffer and converted to digit pairs (one scale per (vector, token, slice): the slice's max,
+// so every split-K partial carries its own scale) only when the slice changes — once or twice
+// per CTA instead of once per item, and twice the slice of a double-buffered design, which
+// halves the split-K partials the LayerNorm / GeGLU kernels reduce. A code fragment (8 LOP3)
+// feeds NQ = ceil(M / 4) IMMA column groups of 4 tokens (column 2j + e: token 4q + j, digit e).
+constexpr int kMkXBytes = 2 * kMkSliceBytes;  // the resident activation slice (single buffer)
+
 template <int NQ, int RT>
-__global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int nx) {
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int nx, int per) {
   trace_point(10);
   constexpr int CHUNK = 512;
   constexpr int U = kStageBytes / CHUNK / RT;  // chunks per tile per stage
@@ -1028,18 +1032,15 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
   const int nrt = static_cast<int>(a.nrt);
   constexpr int kTiles = kTWarps * RT;
   uint8_t* ring = smem + static_cast<size_t>(warp) * kMkStages * kStageBytes;
-  uint8_t* xbuf = smem + static_cast<size_t>(kTWarps) * kMkStages * kStageBytes;  // [2][kMkSliceBytes]
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * kMkSliceBytes);          // [2]
-  uint64_t* bars = xbar + 2 + warp * kMkStages;
-  float* sxs = reinterpret_cast<float*>(xbar + 2 + kTWarps * kMkStages);          // [32] slice scale per (v, m)
-  float* isx = sxs + 32;                                                           // [32] 1 / scale
-  int* dsum = reinterpret_cast<int*>(isx + 32);                                    // [32] slice sums of x_int
+  uint8_t* xb = smem + static_cast<size_t>(kTWarps) * kMkStages * kStageBytes;  // [nx][M][nck][128]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xb + kMkXBytes);
+  uint64_t* bars = xbar + 1 + warp * kMkStages;
+  float* sxs = reinterpret_cast<float*>(xbar + 1 + kTWarps * kMkStages);  // [32] slice scale per (v, m)
+  float* isx = sxs + 32;                                                  // [32] 1 / scale
+  int* dsum = reinterpret_cast<int*>(isx + 32);                           // [32] slice sums of x_int
   if (lane == 0) {
     for (int q = 0; q < kMkStages; ++q) mbar_init(bars + q, 1);
-    if (warp == 0) {
-      mbar_init(xbar, 1);
-      mbar_init(xbar + 1, 1);
-    }
+    if (warp == 0) mbar_init(xbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1048,23 +1049,25 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   const int ngroups = (nrt + kTiles - 1) / kTiles;
   const int nitems = ngroups * ksplit;
+  const int i0 = blockIdx.x * per, i1 = min(nitems, i0 + per);
   auto slice = [&](int s, int& c0, int& c1) {
     c0 = nch * s / ksplit;
     c1 = nch * (s + 1) / ksplit;
   };
-  int pj = blockIdx.x, pc = 0, pc1 = 0, prt = -1, pslot = 0;
-  auto pitem = [&]() {
-    while (pj < nitems) {
-      prt = (pj / ksplit) * kTiles + warp * RT;
-      slice(pj % ksplit, pc, pc1);
+  // weight producer (lane 0 of each warp) walks this CTA's items in consumption order
+  int pj = i0, pc = 0, pc1 = 0, prt = -1, pslot = 0;
+  auto pitem = [&]() {  // position the producer on item pj (skipping items where this warp idles)
+    while (pj < i1) {
+      prt = (pj % ngroups) * kTiles + warp * RT;
+      slice(pj / ngroups, pc, pc1);
       if (prt < nrt) return;
-      pj += gridDim.x;
+      ++pj;
     }
   };
   pitem();
   const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
   auto issue = [&]() {
-    if (pj >= nitems) return;
+    if (pj >= i1) return;
     const int n = min(U, pc1 - pc);
     const int ntile = (RT == 2 && prt + 1 < nrt) ? 2 : 1;
     mbar_expect_tx(bars + pslot, static_cast<uint32_t>(ntile * n * CHUNK));
@@ -1075,7 +1078,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
     pslot = pslot + 1 == kMkStages ? 0 : pslot + 1;
     pc += n;
     if (pc >= pc1) {
-      pj += gridDim.x;
+      ++pj;
       pitem();
     }
   };
@@ -1084,75 +1087,65 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
   pdl_wait();
   pdl_trigger();
   trace_point(11);
-  auto load_x = [&](int local, int item) {
-    int c0, c1;
-    slice(item % ksplit, c0, c1);
-    const int nck = c1 - c0;
-    const int b = local & 1;
-    mbar_expect_tx(xbar + b, static_cast<uint32_t>(nx * M * nck * 128));
-    for (int v = 0; v < nx; ++v)
-      for (int m = 0; m < M; ++m) {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2) +
-                             (static_cast<int64_t>(m) * nch + c0) * 128;
-        bulk_g2s(xbuf + b * kMkSliceBytes + ((v * M + m) * nck) * 128, src, static_cast<uint32_t>(nck * 128), xbar + b,
-                 keep);
-      }
-  };
-  if (threadIdx.x == 0) {
-    if (static_cast<int>(blockIdx.x) < nitems) load_x(0, blockIdx.x);
-    if (static_cast<int>(blockIdx.x + gridDim.x) < nitems) load_x(1, blockIdx.x + gridDim.x);
-  }
   const int nvm = nx * M;
   int cslot = 0;
-  uint32_t cpar = 0;
-  int local = 0;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
-    const int s = item % ksplit;
-    const int rt = (item / ksplit) * kTiles + warp * RT;
+  uint32_t cpar = 0, xpar = 0;
+  int cur = -1;  // k-slice resident in xb
+  for (int item = i0; item < i1; ++item) {
+    const int s = item / ngroups;
+    const int rt = (item % ngroups) * kTiles + warp * RT;
     int c0, c1;
     slice(s, c0, c1);
     const int nck = c1 - c0;
-    const int b = local & 1;
-    uint8_t* xb = xbuf + b * kMkSliceBytes;
-    mbar_wait(xbar + b, (local >> 1) & 1);
-    // (1) slice max per activation vector (v, m): one warp per vector
-    for (int vm = warp; vm < nvm; vm += kTWarps) {
-      const uint4* row = reinterpret_cast<const uint4*>(xb + static_cast<size_t>(vm) * nck * 128);
-      float mx = 0.f;
-      bool nan = false;
-      for (int i = lane; i < nck * 8; i += 32) {
-        const uint4 q = row[i];
-        const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+    if (s != cur) {
+      // (0) the slice of all nx * M activation rows into the resident buffer
+      __syncthreads();  // every warp is done with the previous slice
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(xbar, static_cast<uint32_t>(nvm * nck * 128));
+        for (int v = 0; v < nx; ++v)
+          for (int m = 0; m < M; ++m) {
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(v == 0 ? a.xf : a.xf2) +
+                                 (static_cast<int64_t>(m) * nch + c0) * 128;
+            bulk_g2s(xb + ((v * M + m) * nck) * 128, src, static_cast<uint32_t>(nck * 128), xbar, keep);
+          }
+      }
+      mbar_wait(xbar, xpar);
+      xpar ^= 1u;
+      // (1) slice max per activation vector (v, m): one warp per vector
+      for (int vm = warp; vm < nvm; vm += kTWarps) {
+        const uint4* row = reinterpret_cast<const uint4*>(xb + static_cast<size_t>(vm) * nck * 128);
+        float mx = 0.f;
+        bool nan = false;
+        for (int i = lane; i < nck * 8; i += 32) {
+          const uint4 q = row[i];
+          const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __half22float2(__habs2(*reinterpret_cast<const __half2*>(&wd[e])));
-          nan = nan || f.x != f.x || f.y != f.y;
-          mx = fmaxf(mx, fmaxf(f.x, f.y));
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(__habs2(*reinterpret_cast<const __half2*>(&wd[e])));
+            nan = nan || f.x != f.x || f.y != f.y;
+            mx = fmaxf(mx, fmaxf(f.x, f.y));
+          }
+        }
+        mx = warp_max(mx);
+        nan = __any_sync(0xffffffffu, nan);
+        if (lane == 0) {
+          const bool bad = nan || !finite_f32(mx);
+          sxs[vm] = bad ? __int_as_float(0x7fc00000) : mx / kDigitQ;
+          isx[vm] = (mx > 0.f && !bad) ? kDigitQ / mx : 0.f;
+          dsum[vm] = 0;
         }
       }
-      mx = warp_max(mx);
-      nan = __any_sync(0xffffffffu, nan);
-      if (lane == 0) {
-        const bool bad = nan || !finite_f32(mx);
-        sxs[vm] = bad ? __int_as_float(0x7fc00000) : mx / kDigitQ;
-        isx[vm] = (mx > 0.f && !bad) ? kDigitQ / mx : 0.f;
-        dsum[vm] = 0;
-      }
-    }
-    __syncthreads();
-    // (2) in place: fp16 fragments -> digit pairs; digit sums per vector over the slice
-    {
+      __syncthreads();
+      // (2) in place: fp16 fragments -> digit pairs; sums of x_int per vector over the slice
       const int ng = nvm * nck * 4;
-      for (int i0 = 0; i0 < ng; i0 += kTWarps * 32) {
-        const int i = i0 + threadIdx.x;
-        const int vm = i < ng ? i / (nck * 4) : 0;
-        int sm = 0;
-        if (i < ng) sm = digits_group(reinterpret_cast<uint4*>(xb) + 2 * i, isx[vm]);
-        // groups of one vector reduce through shared atomics (integer: order-independent)
-        if (i < ng && sm) atomicAdd(&dsum[vm], sm);
+      for (int i = threadIdx.x; i < ng; i += kTWarps * 32) {
+        const int vm = i / (nck * 4);
+        const int sm = digits_group(reinterpret_cast<uint4*>(xb) + 2 * i, isx[vm]);
+        if (sm) atomicAdd(&dsum[vm], sm);  // integer: order-independent
       }
+      __syncthreads();
+      cur = s;
     }
-    __syncthreads();
     if (rt < nrt) {
       const int v = rt < a.rt_split ? 0 : nx - 1;
       const bool two = RT == 2 && rt + 1 < nrt;
@@ -1224,8 +1217,6 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
         }
       }
     }
-    __syncthreads();  // every warp is done with activation buffer b (and the slice scales)
-    if (threadIdx.x == 0 && item + 2 * static_cast<int>(gridDim.x) < nitems) load_x(local + 2, item + 2 * gridDim.x);
   }
   trace_point(13);
 }
@@ -1349,6 +1340,29 @@ bool use_m1(int64_t nch, int M, int bits, int nx) {
 
 GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
   GemvPlan p;
+  if (M >= 2 && !use_m1(nch, M, bits, nx) && bits == 4 && gemv_imma() && nx * M <= 32) {
+    // integer-MMA multi-token kernel: slice-major items, contiguous ranges of `per` items per
+    // CTA, one resident activation slice (kMkXBytes) per CTA
+    p.warps = kTWarps;
+    p.rt_per_warp = mk_row_tiles(bits, M);
+    const int64_t kmax = std::max<int64_t>(1, kMkXBytes / (static_cast<int64_t>(nx) * M * 128));
+    const int64_t ks_min = (nch + kmax - 1) / kmax;
+    const int64_t ngroups = (nrt + kTWarps * p.rt_per_warp - 1) / (kTWarps * p.rt_per_warp);
+    double best = -1.0;
+    for (int64_t ks = ks_min; ks <= std::min<int64_t>(nch, ks_min + 24); ++ks) {
+      const int64_t items = ngroups * ks;
+      const int64_t per = (items + kNumSMs - 1) / kNumSMs;
+      const double eff = static_cast<double>(items) / static_cast<double>(per * kNumSMs) - 0.004 * static_cast<double>(ks);
+      if (eff > best + 1e-9) {
+        best = eff;
+        p.ksplit = static_cast<int>(ks);
+        p.per = static_cast<int>(per);
+      }
+    }
+    const int64_t items = ngroups * p.ksplit;
+    p.grid = static_cast<int>((items + p.per - 1) / p.per);
+    return p;
+  }
   if (M >= 2 && !use_m1(nch, M, bits, nx)) {
     // multi-token kernel: CTA-items of 16 row tiles x one k-slice; the slice of all M
     // activation rows (nx vectors) must fit one shared-memory buffer
@@ -1402,7 +1416,9 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
   if (M >= 2 && !use_m1(op.nch, M, op.bits, nx_op)) {
     const int nx = nx_op;
     const int64_t slice_max = (op.nch + p.ksplit - 1) / p.ksplit;
-    if (slice_max * 128 * M * nx > kMkSliceBytes || p.warps != kTWarps || (p.rt_per_warp == 2 && op.rt_split % 2))
+    const bool i4 = op.bits == 4 && gemv_imma() && M * nx <= 32;
+    if (slice_max * 128 * M * nx > (i4 ? kMkXBytes : kMkSliceBytes) || p.warps != kTWarps ||
+        (p.rt_per_warp == 2 && op.rt_split % 2))
       fail(GLM_CONTRACT, "qlinear", "GEMV plan does not match the multi-token kernel (plan for this M and x count)");
     const size_t smem1 = static_cast<size_t>(kTWarps) * kMkStages * kStageBytes + 2 * kMkSliceBytes +
                          (2 + kTWarps * kMkStages) * 8;
@@ -1416,7 +1432,9 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
     const dim3 gridm(p.grid), blockm(kTWarps * 32);
     const bool two = p.rt_per_warp == 2;
     if (op.bits == 4 && gemv_imma() && M * nx <= 32) {
-      const size_t smem2 = smem1 + 32 * 4 * 2 + 32 * 8;
+      const size_t smem2 = static_cast<size_t>(kTWarps) * kMkStages * kStageBytes + kMkXBytes +
+                           (1 + kTWarps * kMkStages) * 8 + 32 * 4 * 3;
+      if (p.per < 1) fail(GLM_CONTRACT, "qlinear", "GEMV plan does not match the integer-MMA multi-token kernel");
       static bool attr_i4 = false;
       if (!attr_i4) {
         for (auto k : {k_gemv_mk_i4<1, 1>, k_gemv_mk_i4<2, 1>, k_gemv_mk_i4<3, 1>, k_gemv_mk_i4<4, 1>,
@@ -1425,10 +1443,10 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
         attr_i4 = true;
       }
       const int nq = (M + 3) / 4;
-      void (*k)(GemvArgs, int) = nullptr;
+      void (*k)(GemvArgs, int, int) = nullptr;
       if (two) k = nq == 1 ? k_gemv_mk_i4<1, 2> : nq == 2 ? k_gemv_mk_i4<2, 2> : nq == 3 ? k_gemv_mk_i4<3, 2> : k_gemv_mk_i4<4, 2>;
       else k = nq == 1 ? k_gemv_mk_i4<1, 1> : nq == 2 ? k_gemv_mk_i4<2, 1> : nq == 3 ? k_gemv_mk_i4<3, 1> : k_gemv_mk_i4<4, 1>;
-      launch_k(k, gridm, blockm, smem2, st, a, nx);
+      launch_k(k, gridm, blockm, smem2, st, a, nx, p.per);
       LAUNCH_CHECK("k_gemv_mk_i4");
       return;
     }

@@ -67,6 +67,7 @@ struct GemvPlan {
   int grid = 1;
   int warps = 16;  // warps per CTA the split-K balance was computed for
   int rt_per_warp = 1;  // multi-token kernel: row tiles per warp (1 or 2)
+  int per = 0;          // integer-MMA multi-token kernel: items per CTA (slice-major ranges)
 };
 int mk_row_tiles(int bits, int M);
 // Split-K plan for an M-row GEMV; the single-token INT4 kernel runs more warps per SM.
