@@ -1648,7 +1648,10 @@ void launch_head(const HeadArgs& a, bool bf16, cudaStream_t st) {
     return;
   }
   const int per_sm = static_cast<int>(std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
-  const int grid = kNumSMs * (per_sm < 1 ? 1 : per_sm);
+  // one vocabulary row per warp: no more CTAs than rows (each CTA stages h in shared memory,
+  // so idle CTAs of a small vocabulary would only add L2 traffic)
+  const int64_t need = (a.vocab_local + kHeadThreads / 32 - 1) / (kHeadThreads / 32);
+  const int grid = static_cast<int>(std::min<int64_t>(need, kNumSMs * (per_sm < 1 ? 1 : per_sm)));
   if (bf16) launch_k(k_head<__nv_bfloat16>, dim3(grid), dim3(kHeadThreads), smem, st, a);
   else launch_k(k_head<float>, dim3(grid), dim3(kHeadThreads), smem, st, a);
   LAUNCH_CHECK("k_head");

@@ -1258,11 +1258,12 @@ bool gemv_imma() {
   return on;
 }
 // warps per CTA of the single-token kernel family (GLM_M1_WARPS overrides): the integer-MMA
-// kernel at one token runs 8 (tools/r2_m1_sweep2.sh: 8 x 2 x 8 KB beat 4..16 warps and
-// 4..16 KB stages 2..4 deep on one box), the fp16 kernels 16
+// kernel runs 8 (tools/r2_m1_sweep2.sh: 8 x 2 x 8 KB beat 4..16 warps and 4..16 KB stages 2..4
+// deep at one token; tools/r2_b2_ab.sh: 8 warps 147-148 vs 16 warps 145-146 tok/s at two), the
+// fp16 kernels 16
 int m1_warps(int M) {
   static const int env = [] { const char* e = getenv("GLM_M1_WARPS"); return e ? atoi(e) : 0; }();
-  const int v = env ? env : (gemv_imma() && M == 1 ? 8 : kM1DefaultWarps);
+  const int v = env ? env : (gemv_imma() && M <= 2 ? 8 : kM1DefaultWarps);
   return v < 4 ? 4 : (v > kM1MaxWarps ? kM1MaxWarps : v);
 }
 
