@@ -114,6 +114,13 @@ glm_status glm_qweight_device_copy(const glm_qweight* q, uint8_t* host_out);
  * made with the environment variable GLM_QMM_TRACE set. */
 glm_status glm_debug_qmm_trace(long long* host_out);
 
+/* Diagnostics: the kernel glm_qlinear runs for M rows of q. out[0]: 0 fp16 single-token GEMV,
+ * 1 integer-MMA single-token GEMV, 2 integer-MMA multi-token GEMV, 3 fp16 multi-token GEMV,
+ * 4 fp16 TMA GEMV, 5 tcgen05 GEMM (prefill); out[1]: k-splits (the integer-MMA multi-token GEMV
+ * quantizes activations per (token, k-split) on 64-element chunk boundaries
+ * chunk = nch * s / ksplit); out[2]: nch, the 64-element chunks along K. Host only, no launch. */
+glm_status glm_debug_gemv_plan(const glm_qweight* q, int64_t M, int32_t* out);
+
 /* Diagnostics: device timeline. While a trace runs, thread 0 of every CTA of the decode
  * kernels appends (globaltimer ns, tag << 32 | block << 8 | smid) pairs; stop copies up to
  * `capacity` pairs (2 * capacity uint64) to host_out and returns the count. */

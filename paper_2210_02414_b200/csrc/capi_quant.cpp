@@ -361,6 +361,24 @@ glm_status glm_debug_qmm_trace(long long* host_out) {
   });
 }
 
+glm_status glm_debug_gemv_plan(const glm_qweight* q, int64_t M, int32_t* out) {
+  return guarded([&] {
+    if (!q || !out) fail(GLM_CONTRACT, "qlinear", "null argument");
+    if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
+    const QLayout& L = q->w.L;
+    if (M >= qmm_min_rows()) {
+      const GemvPlan p = plan_qmm(L, static_cast<int>(M));
+      out[0] = 5;
+      out[1] = p.ksplit;
+    } else {
+      const GemvPlan p = plan_gemv(L, static_cast<int>(M));
+      out[0] = gemv_kind(L.nch, static_cast<int>(M), L.bits);
+      out[1] = p.ksplit;
+    }
+    out[2] = static_cast<int32_t>(L.nch);
+  });
+}
+
 static unsigned long long* g_trace_dev = nullptr;
 
 glm_status glm_debug_trace_start(int64_t capacity) {

@@ -1267,12 +1267,11 @@ bool gemv_imma() {
   return on;
 }
 // warps per CTA of the single-token kernel family (GLM_M1_WARPS overrides): the integer-MMA
-// kernel runs 8 (tools/r2_m1_sweep2.sh: 8 x 2 x 8 KB beat 4..16 warps and 4..16 KB stages 2..4
-// deep at one token; tools/r2_b2_ab.sh: 8 warps 147-148 vs 16 warps 145-146 tok/s at two), the
-// fp16 kernels 16
+// kernel runs 8 at one token (tools/r2_m1_sweep2.sh: 8 x 2 x 8 KB beat 4..16 warps and 4..16 KB
+// stages 2..4 deep), 16 at two (tools/r2_b2_ab2.sh), the fp16 kernels 16
 int m1_warps(int M) {
   static const int env = [] { const char* e = getenv("GLM_M1_WARPS"); return e ? atoi(e) : 0; }();
-  const int v = env ? env : (gemv_imma() && M <= 2 ? 8 : kM1DefaultWarps);
+  const int v = env ? env : (gemv_imma() && M == 1 ? 8 : kM1DefaultWarps);
   return v < 4 ? 4 : (v > kM1MaxWarps ? kM1MaxWarps : v);
 }
 
@@ -1340,11 +1339,18 @@ M1Shape m1_shape(int64_t nch, int M, int nx, int plan_warps) {
 
 // The single-token kernel family takes INT4 at up to GLM_M1_TOKENS (default 2) tokens when
 // the activation vectors fit next to 12 or more warps' rings (else the multi-token kernel).
+// With the integer MMA, two tokens default to the multi-token kernel k_gemv_mk_i4
+// (tools/r2_b2_ab2.sh, batch-2 decode: 151.1 tok/s against 150.7 / 146.0 / 144.8 for
+// k_gemv_i4<., ., 2> on 16 / 12 / 8 warps); GLM_M1_TOKENS=2 selects the single-token family.
 bool use_m1(int64_t nch, int M, int bits, int nx) {
-  static const int maxm = [] { const char* e = getenv("GLM_M1_TOKENS"); const int v = e ? atoi(e) : kM1MaxTokens; return v < 1 ? 1 : (v > kM1MaxTokens ? kM1MaxTokens : v); }();
+  static const int maxm = [] {
+    const char* e = getenv("GLM_M1_TOKENS");
+    const int v = e ? atoi(e) : (gemv_imma() ? 1 : kM1MaxTokens);
+    return v < 1 ? 1 : (v > kM1MaxTokens ? kM1MaxTokens : v);
+  }();
   if (bits != 4 || M > maxm) return false;
   const M1Shape m = m1_shape(nch, M, nx, m1_warps(M));
-  return m.ok && (M == 1 || m.warps >= 12);
+  return m.ok && (M == 1 || m.warps >= std::min(12, m1_warps(M)));
 }
 }  // namespace
 
@@ -1416,6 +1422,13 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
 }
 
 GemvPlan plan_gemv(const QLayout& L, int M) { return plan_gemv(L.nrt, L.nch, M, L.bits, 1); }
+
+int gemv_kind(int64_t nch, int M, int bits, int nx) {  // mirrors gemv_launch's dispatch
+  if (M >= 2 && !use_m1(nch, M, bits, nx))
+    return (bits == 4 && gemv_imma() && M * nx <= 32) ? kGemvI4Multi : kGemvF16Multi;
+  if (use_m1(nch, M, bits, nx)) return gemv_imma() ? kGemvI4Single : kGemvF16Single;
+  return kGemvF16Tma;
+}
 
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st) {
   if (M < 1 || M > 16) fail(GLM_DIMENSION, "qlinear", "GEMV path takes 1..16 rows, got " + std::to_string(M));

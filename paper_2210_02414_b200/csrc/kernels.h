@@ -86,6 +86,9 @@ struct GemvOp {
 };
 
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
+// Which decode-GEMV kernel gemv_launch runs for M tokens (diagnostics / parity contracts)
+enum GemvKind { kGemvF16Single = 0, kGemvI4Single = 1, kGemvI4Multi = 2, kGemvF16Multi = 3, kGemvF16Tma = 4 };
+int gemv_kind(int64_t nch, int M, int bits, int nx = 1);
 // partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over k-split s of x . W
 void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,
                  cudaStream_t st);

@@ -86,6 +86,7 @@ SIGNATURES = {
     "glm_qweight_device_bytes": (I64, [P]),
     "glm_qweight_device_copy": (I32, [P, P]),
     "glm_debug_qmm_trace": (I32, [P]),
+    "glm_debug_gemv_plan": (I32, [P, I64, P]),
     "glm_qlinear": (I32, [P, P, I64, P, P]),
     "glm_qlinear_host": (I32, [P, P, I64, P]),
     "glm_qlinear_bench": (I32, [P, I64, I32, I32, C.POINTER(D)]),
@@ -316,6 +317,14 @@ class QLinear:
         y = np.empty((x.shape[0], self.cols), np.float32)
         _check(lib().glm_qlinear_host(self.h, _p(x), x.shape[0], _p(y)))
         return y
+
+    GEMV_KINDS = ("f16_single", "i4_single", "i4_multi", "f16_multi", "f16_tma", "tcgen05")
+
+    def plan(self, M):
+        """(kernel, ksplit, nch) glm_qlinear uses for M rows (glm_debug_gemv_plan)."""
+        out = np.zeros(3, np.int32)
+        _check(lib().glm_debug_gemv_plan(self.h, M, _p(out)))
+        return self.GEMV_KINDS[out[0]], int(out[1]), int(out[2])
 
     def bench(self, M, iters=20, flush=True):
         us = C.c_double()

@@ -3,10 +3,12 @@ y = x . dequantize(q) (quant.cpp:188-221 + tensor.cpp:135-155).
 
 Two bars: (1) exact-arithmetic check against a float64 evaluation of the kernel's own
 contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only fp32
-accumulation error remains: <= 2e-6 of max|y|. The single-token INT4 GEMV (1..2 tokens,
-gemv.cu k_gemv_i4) runs on the integer MMA: its contract re-quantizes each fp16 activation
-vector to 16-bit fixed point, x_int = rint(x * (32512 / max|x|)), and the products and sums
-are exact integers, so only the final fp32 scaling rounds: <= 2e-6 of max|y|;
+accumulation error remains: <= 2e-6 of max|y|. The INT4 decode GEMVs run on the integer MMA
+(gemv.cu k_gemv_i4 at one token, k_gemv_mk_i4 at 2..16): their contract re-quantizes each fp16
+activation vector to 16-bit fixed point, x_int = rint(x * (32512 / max|x|)), per token
+(k_gemv_i4) or per (token, k-split) on the plan's 64-element chunk boundaries (k_gemv_mk_i4,
+QLinear.plan), and the products and sums are exact integers, so only the fp32 scaling and the
+k-split reduction round: <= 2e-6 (one split) / 4e-6 (several) of max|y|;
 (2) the reference check against the oracle's float64 x . dequantize(q),
 max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
 import numpy as np
@@ -18,23 +20,20 @@ from paper_2210_02414_b200 import glm
 pytestmark = pytest.mark.gpu
 
 
-def contract_tol(M, bits):
-    # INT4 at 3..16 tokens (k_gemv_mk_i4) re-quantizes the fp16 activations to 16-bit fixed point
-    # per (token, k-slice) with the slice's own max, a split the contract below does not model
-    # (it uses fp16 activations there): the difference is <= 2^-16 of max|x| per element
-    return 1e-4 if (bits == 4 and 3 <= M <= 16) else 2e-6
+def contract_tol(ksplit):
+    return 2e-6 if ksplit == 1 else 4e-6
 
 
 DIGIT_Q = np.float32(32512.0)  # gemv.cu kDigitQ
 
 
 def imma_activations(xh):
-    """The integer-MMA GEMV's view of fp16 activations (gemv.cu k_gemv_i4): per row,
+    """The integer-MMA GEMV's view of fp16 activations (gemv.cu digits_group): per row,
     x_int = rint(fp32(x) * fp32(32512 / max|x|)) and the scale s_x = max|x| / 32512."""
     xh32 = xh.astype(np.float32)
     out = np.zeros(xh.shape, np.float64)
     for m in range(xh.shape[0]):
-        mx = np.float32(np.abs(xh32[m]).max())
+        mx = np.float32(np.abs(xh32[m]).max()) if xh.shape[1] else np.float32(0)
         if mx == 0:
             continue
         inv = np.float32(DIGIT_Q / mx)
@@ -44,24 +43,37 @@ def imma_activations(xh):
     return out
 
 
-def kernel_contract(x, q, M=None):
-    """float64 evaluation of what the kernel computes."""
+def kernel_view(xh, kind, ksplit, nch):
+    """The activations the MMA multiplies: fp16 values (HMMA kernels), fixed point per token
+    (k_gemv_i4) or fixed point per (token, k-split) with splits at chunks nch * s / ksplit."""
+    if kind == "i4_single":
+        return imma_activations(xh)
+    if kind == "i4_multi":
+        out = np.zeros(xh.shape, np.float64)
+        for s in range(ksplit):
+            k0, k1 = 64 * (nch * s // ksplit), min(xh.shape[1], 64 * (nch * (s + 1) // ksplit))
+            if k1 > k0:
+                out[:, k0:k1] = imma_activations(xh[:, k0:k1])
+        return out
+    return xh.astype(np.float64)
+
+
+def kernel_contract(x, q, lin):
+    """float64 evaluation of what the kernel glm_qlinear picks for these M rows computes
+    (DESIGN.md "Quantized linear"); returns (contract, ksplit)."""
     K, N = q["rows"], q["cols"]
-    M = x.shape[0] if M is None else M
+    kind, ksplit, nch = lin.plan(x.shape[0])
     codes = O.codes_of(q).reshape(K, N).astype(np.float64)
     s = q["scales"]
     x32 = x.astype(np.float32)
-    imma = q["bits"] == 4 and M <= 2  # k_gemv_i4 (integer MMA)
     if q["axis"] == "row":
         S = s.max()
         fold = (s / S).astype(np.float32) if S > 0 else np.zeros(K, np.float32)
-        xh = (x32 * fold[None, :]).astype(np.float16)
-        xv = imma_activations(xh) if imma else xh.astype(np.float64)
-        return (xv @ codes) * np.float64(np.float32(S))
-    xh = x32.astype(np.float16)
-    xv = imma_activations(xh) if imma else xh.astype(np.float64)
+        xv = kernel_view((x32 * fold[None, :]).astype(np.float16), kind, ksplit, nch)
+        return (xv @ codes) * np.float64(np.float32(S)), ksplit
+    xv = kernel_view(x32.astype(np.float16), kind, ksplit, nch)
     cs = (s if q["axis"] == "column" else np.full(N, s[0])).astype(np.float32).astype(np.float64)
-    return (xv @ codes) * cs[None, :]
+    return (xv @ codes) * cs[None, :], ksplit
 
 
 SHAPES = [(64, 16), (512, 1536), (1368, 512), (512, 1368), (200, 90), (4096, 1024)]
@@ -78,8 +90,8 @@ def test_qlinear_matches_contract_and_oracle(bits, axis, K, N):
     for M in (1, 2, 3, 8, 9, 16, 37):
         x = rng.normal(0, 1, size=(M, K))
         y = lin(x).astype(np.float64)
-        c = kernel_contract(x, q)
-        assert np.abs(y - c).max() <= contract_tol(M, bits) * np.abs(c).max() + 1e-30, (M, np.abs(y - c).max())
+        c, ks = kernel_contract(x, q, lin)
+        assert np.abs(y - c).max() <= contract_tol(ks) * np.abs(c).max() + 1e-30, (M, np.abs(y - c).max())
         ref = x @ O.dequantize(q)
         assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
 
@@ -92,11 +104,28 @@ def test_qlinear_glm130b_k_dimension_with_split_k():
     for bits, axis in ((4, "column"), (8, "row")):
         q = glm.quantize_absmax(w, bits, axis)
         lin = glm.QLinear.from_payload(q)
-        for M in (1, 2):
+        for M in (1, 2, 5, 16):
             x = rng.normal(0, 1, size=(M, K))
             y = lin(x).astype(np.float64)
-            c = kernel_contract(x, q)
-            assert np.abs(y - c).max() <= contract_tol(M, bits) * np.abs(c).max()
+            c, ks = kernel_contract(x, q, lin)
+            if bits == 4 and M > 1:
+                assert ks > 1, "the per-split activation contract is not exercised"
+            assert np.abs(y - c).max() <= contract_tol(ks) * np.abs(c).max()
+
+
+def test_qlinear_kernel_selection():
+    """Decode GEMV dispatch (gemv.cu gemv_launch): INT4 one token on the integer-MMA
+    single-token kernel, 2..16 on the integer-MMA multi-token kernel; INT8 on the fp16 kernels;
+    more than 16 rows on the tcgen05 GEMM."""
+    lin4 = glm.QLinear.synthetic(1, 0, 12288, 4096, 0.02, 4, "column")
+    lin8 = glm.QLinear.synthetic(1, 1, 12288, 4096, 0.02, 8, "row")
+    assert lin4.plan(1)[0] == "i4_single"
+    for M in (2, 3, 8, 16):
+        assert lin4.plan(M)[0] == "i4_multi"
+        assert lin8.plan(M)[0] in ("f16_multi", "f16_tma")
+    assert lin8.plan(1)[0] in ("f16_tma", "f16_multi")
+    assert lin4.plan(17)[0] == lin8.plan(300)[0] == "tcgen05"
+    assert lin4.plan(1)[2] == 12288 // 64
 
 
 def test_qlinear_quantize_handle_equals_payload_handle():
