@@ -892,6 +892,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
   if (lane == 0)
     for (int s = early; s < NST; ++s) issue();
   mbar_wait(xbar, 0);
+  trace_point(14);
   // (1) max |x| per activation vector (v, m): 16-byte units, [vm][chunk][8 units]
   const int nvm = nx * MT;
   const int upv = nch * 8;
@@ -936,6 +937,7 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
     }
     __syncthreads();
   }
+  trace_point(15);
   // (2) in-place conversion to digits, 32-byte groups [vm][chunk][t]; chunk digit sums
   {
     const int ngroups = nvm * nch * 4;

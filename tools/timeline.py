@@ -51,12 +51,15 @@ endkind = {10: 3, 20: 2, 30: 2, 40: 2, 50: 2}
 w = np.where(kind == 1)[0]
 w = w[np.argsort(t[w])]
 inst = []
+blk = ((rec[:, 1] >> 8) & 0xFFFFFF).astype(np.int64)
 for i in w:
-    if inst and inst[-1]["fam"] == fam[i] and t[i] - inst[-1]["wait_last"] < 20000:
+    if (inst and inst[-1]["fam"] == fam[i] and t[i] - inst[-1]["wait_last"] < 20000
+            and blk[i] not in inst[-1]["blocks"]):
         inst[-1]["wait_last"] = t[i]
         inst[-1]["n"] += 1
+        inst[-1]["blocks"].add(blk[i])
     else:
-        inst.append({"fam": int(fam[i]), "wait": int(t[i]), "wait_last": int(t[i]), "n": 1})
+        inst.append({"fam": int(fam[i]), "wait": int(t[i]), "wait_last": int(t[i]), "n": 1, "blocks": {blk[i]}})
 for k, c in enumerate(inst):
     nxt = inst[k + 1]["wait"] if k + 1 < len(inst) else t.max() + 1
     sel = (fam == c["fam"]) & (t >= c["wait"]) & (t <= nxt)
@@ -65,6 +68,15 @@ for k, c in enumerate(inst):
     c["end_min"] = int(ends.min()) if ends.size else c["wait"]
     rdy = t[sel & (kind == 2)] if c["fam"] == 10 else np.array([])
     c["ready"] = int(rdy.max()) if rdy.size else None
+    xa = t[sel & (kind == 4)] if c["fam"] == 10 else np.array([])
+    c["xarr"] = int(xa.max()) if xa.size else None
+    mxd = t[sel & (kind == 5)] if c["fam"] == 10 else np.array([])
+    c["maxd"] = int(mxd.max()) if mxd.size else None
+    st7 = t[sel & (kind == 7)] if c["fam"] == 10 else np.array([])
+    c["lnstat"] = int(st7.max()) if st7.size else None
+    # entry (kind 0) of this instance: the earliest entry stamp after the previous instance's release
+    ent = t[(fam == c["fam"]) & (kind == 0) & (t <= c["wait"]) & (t >= (inst[k - 1]["wait"] if k > 0 else 0))]
+    c["entry"] = int(ent.min()) if ent.size else None
 print(f"{len(rec)} records, {len(inst)} kernel instances, step span {t.max() / 1e3:.1f} us")
 total = collections.Counter()
 gaps = collections.Counter()
@@ -77,8 +89,13 @@ for i, c in enumerate(inst):
     if 40 <= i < 56:
         rdy = (c["ready"] - c["wait"]) / 1e3 if c["ready"] else float("nan")
         tail = (c["end"] - c["end_min"]) / 1e3
-        print(f"{i:4d} {names[c['fam']]:5s} CTAs {c['n']:4d} released {c['wait'] / 1e3:9.1f} us (+{gap:5.2f} after prev end)"
-              f"  x-ready +{rdy:5.2f}  work {dur:6.2f}  end spread {tail:5.2f}")
+        xa = (c["xarr"] - c["wait"]) / 1e3 if c.get("xarr") else float("nan")
+        md = (c["maxd"] - c["wait"]) / 1e3 if c.get("maxd") else float("nan")
+        lst = (c["lnstat"] - c["wait"]) / 1e3 if c.get("lnstat") else float("nan")
+        ent = (c["wait"] - c["entry"]) / 1e3 if c.get("entry") else float("nan")
+        print(f"{i:4d} {names[c['fam']]:5s} CTAs {c['n']:4d} released {c['wait'] / 1e3:9.1f} us (+{gap:5.2f} after prev end,"
+              f" first entry {ent:5.2f} before)  x-arrived +{xa:5.2f} ln-stats +{lst:5.2f} max +{md:5.2f} x-ready +{rdy:5.2f}"
+              f"  work {dur:6.2f}  end spread {tail:5.2f}")
     prev_end = c["end"]
 print("post-wait -> last end, summed per family (us):", {k: round(v, 1) for k, v in total.items()})
 # LayerNorm phases: post-wait -> loads done (23) -> cluster reduction done (24) -> end
