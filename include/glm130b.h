@@ -196,6 +196,17 @@ glm_status glm_model_set_quantized(glm_model* m, int layer, int which, const int
  * validated before device work (GLM_FORMAT on malformed input); absmax checkpoints only. */
 glm_status glm_model_load_quantized(const char* dir, int max_batch, int max_ctx, int head_bf16,
                                     int tp_rank, int tp_size, glm_model** out);
+/* QuantPolicy::scheme (quant.hpp:53-58) of every linear: GLM_ABSMAX (default) or
+ * GLM_ZEROPOINT (quantize_zeropoint, quant.cpp:145-186). Call before any weight is set;
+ * glm_model_set_tensor then quantizes with the scheme, glm_model_set_quantized_zp takes the
+ * canonical zeropoint matrix (payload, FP64 scales with 0 marking a constant group, FP64 zero
+ * points; dequantization quant.cpp:188-221). */
+glm_status glm_model_set_scheme(glm_model* m, glm_scheme scheme);
+glm_status glm_model_set_quantized_zp(glm_model* m, int layer, int which, const int8_t* payload,
+                                      int64_t payload_bytes, const double* scales,
+                                      const double* zero_points, int64_t ngroups);
+/* FP64 zero points of one quantized linear of this rank's shard (zeropoint models). */
+glm_status glm_model_export_zero_points(const glm_model* m, int layer, int which, double* zero_points);
 /* Synthetic random-init weights of the configured shape, generated and quantized on the
  * GPU with the counter-based generator of DESIGN.md (same stds as model.cpp:69-104). */
 glm_status glm_model_init_synthetic(glm_model* m, uint64_t seed);

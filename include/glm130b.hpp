@@ -229,13 +229,15 @@ struct GLMConfig {
 class QuantizedModel {
  public:
   QuantizedModel(const GLMConfig& cfg, int bits, GroupAxis axis, int max_batch, int max_ctx,
-                 bool head_bf16 = false, int tp_rank = 0, int tp_size = 1)
+                 bool head_bf16 = false, int tp_rank = 0, int tp_size = 1,
+                 QuantScheme scheme = QuantScheme::kAbsmax)
       : cfg_(cfg) {
     const glm_config c = cfg.c();
     glm_model* m = nullptr;
     check(glm_model_create(&c, bits, static_cast<glm_axis>(axis), max_batch, max_ctx, head_bf16 ? 1 : 0,
                            tp_rank, tp_size, &m));
     m_.reset(m);
+    if (scheme != QuantScheme::kAbsmax) check(glm_model_set_scheme(m, static_cast<glm_scheme>(scheme)));
   }
   // load_quantized_model (quant.cpp:450-491): a checkpoint directory written by the reference
   static QuantizedModel load_quantized(const std::string& dir, int max_batch = 1, int max_ctx = 2048,
@@ -246,6 +248,12 @@ class QuantizedModel {
   }
   // a canonical QuantizedMatrix of linear `which` (0 qkv .. 4 ffn_w2) of `layer`
   void set_quantized(int layer, int which, const QuantizedMatrix& q) {
+    if (q.scheme == QuantScheme::kZeropoint) {
+      if (q.zero_points.size() != q.scales.size()) throw FormatError("[quantlab] zero point count differs from the scale count");
+      check(glm_model_set_quantized_zp(m_.get(), layer, which, q.payload.data(), static_cast<Index>(q.payload.size()),
+                                       q.scales.data(), q.zero_points.data(), static_cast<Index>(q.scales.size())));
+      return;
+    }
     check(glm_model_set_quantized(m_.get(), layer, which, q.payload.data(), static_cast<Index>(q.payload.size()),
                                   q.scales.data(), static_cast<Index>(q.scales.size())));
   }

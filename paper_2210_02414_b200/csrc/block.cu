@@ -31,7 +31,8 @@ __device__ __forceinline__ float reduce_partial(const SubIn& in, int m, int64_t 
   float acc = 0.f;
 #pragma unroll 4
   for (int s = 0; s < in.ksplit; ++s) acc += in.p[static_cast<int64_t>(s) * in.split_stride + m * in.ld + n];
-  return in.scale ? acc * in.scale[n] : acc;
+  acc = in.scale ? acc * in.scale[n] : acc;
+  return in.zt ? acc + in.zt[m] * in.zv[n] : acc;
 }
 
 
@@ -303,6 +304,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kLnThreads) k_deepn
     y[i].x *= sc[i].x;
     y[i].y *= sc[i].y;
   }
+  if (a.in.zt && !a.zero_sublayer) {  // zeropoint weights: rank-1 term of this rank's rows
+    const float ztm = a.in.zt[m];
+#pragma unroll
+    for (int i = 0; i < kLnPairs; ++i) {
+      const int64_t p = p0 + threadIdx.x + static_cast<int64_t>(i) * kLnThreads;
+      if (p < p1) {
+        const float2 zv = *reinterpret_cast<const float2*>(a.in.zv + 2 * p);
+        y[i].x += ztm * zv.x;
+        y[i].y += ztm * zv.y;
+      }
+    }
+  }
   if (a.peer.size > 1 && !peer_allreduce(a.peer, m, rank, p0, p1, y)) return;  // push-only launch
   if (a.half_store)
 #pragma unroll
@@ -498,6 +511,10 @@ __device__ __forceinline__ float2 reduce_partial2(const SubIn& in, int m, int64_
     acc.x *= in.scale[n];
     acc.y *= in.scale[n + 1];
   }
+  if (in.zt) {
+    acc.x += in.zt[m] * in.zv[n];
+    acc.y += in.zt[m] * in.zv[n + 1];
+  }
   return acc;
 }
 
@@ -544,6 +561,9 @@ __device__ __forceinline__ void load8(const SubIn& in, int m, int64_t n, float (
   if (in.scale)
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[e] *= in.scale[n + e];
+  if (in.zt)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] += in.zt[m] * in.zv[n + e];
 }
 
 __global__ void k_geglu_act_tiles(ActArgs a) {
@@ -688,16 +708,20 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnThreads == 128 ? 12 : 1)
       const int j = threadIdx.x;
       const int jj = jt;
       const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jj;
+      // zeropoint weights: y += zt[b] * zv (after the column scale)
+      auto zp2 = [&](int64_t f) {
+        return a.qkv.zt ? make_float2(a.qkv.zt[b] * a.qkv.zv[f], a.qkv.zt[b] * a.qkv.zv[f + 1]) : make_float2(0.f, 0.f);
+      };
       if (j < DH / 2) {
-        const float2 qv = raw2(fq);
-        const float qa = qv.x * sq.x, qb = qv.y * sq.y;
+        const float2 qv = raw2(fq), qz = zp2(fq);
+        const float qa = qv.x * sq.x + qz.x, qb = qv.y * sq.y + qz.y;
         q[2 * jj] = (cs.x * qa - cs.y * qb) * inv_sqrt;
         q[2 * jj + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
       } else if (has_new) {
         const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
-        const float2 kv2 = raw2(fk), vv2 = raw2(fv);
-        const float ka = kv2.x * sk.x, kb = kv2.y * sk.y;
-        const float va = vv2.x * sv.x, vb = vv2.y * sv.y;
+        const float2 kv2 = raw2(fk), vv2 = raw2(fv), kz = zp2(fk), vz = zp2(fv);
+        const float ka = kv2.x * sk.x + kz.x, kb = kv2.y * sk.y + kz.y;
+        const float va = vv2.x * sv.x + vz.x, vb = vv2.y * sv.y + vz.y;
         const __half2 kh = __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
         const __half2 vh = __floats2half2_rn(va, vb);
         *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jj) = kh;
@@ -1477,6 +1501,7 @@ void launch_deepnorm_ln(const LnArgs& a, int M, cudaStream_t st) {
   // so occupancy sets the bandwidth (ncu, 8192 x 12288: 1 CTA/SM 487/403 us, 2: 328, 3: 341/263,
   // 4 spills: 440/361)
   if (a.peer.size > 1 && M > 16) fail(GLM_CONTRACT, "glmmodel", "fused tensor-parallel LayerNorm is a decode (<= 16 rows) kernel");
+  if (a.in.zt && M > 16) fail(GLM_CONTRACT, "glmmodel", "the zero-point term enters the LayerNorm only in decode (<= 16 rows)");
   if (M > 16 && v8 && rows8) launch_k(k_deepnorm_ln_rows8<3>, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else if (M > 16) launch_k(k_deepnorm_ln_rows, dim3(M), dim3(kLnRowThreads), 0, st, a);
   else if (cl4) launch_k(k_deepnorm_ln<4>, dim3(M * 4), dim3(kLnThreads), 0, st, a);

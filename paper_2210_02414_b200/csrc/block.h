@@ -16,6 +16,10 @@ struct SubIn {
   int ksplit = 1;
   int64_t split_stride = 0, ld = 0;
   const float* scale = nullptr;
+  // zeropoint weights (quant.cpp:145-186): y[m][n] += zt[m] * zv[n] after the column scale
+  // (gemv.cu QWeightDev::zvec / zp_sums_frag); null for absmax
+  const float* zt = nullptr;
+  const float* zv = nullptr;
 };
 
 // Destination activation buffer (fp16) of the next quantized linear, with its kRow

@@ -339,8 +339,9 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
     cfg.deepnorm_alpha = jc.at("deepnorm_alpha").as_num();
     const Json& jp = man.at("policy");
     const int bits = jp.at("bits").as_int();
-    if (jp.at("scheme").as_str() != "absmax")
-      fail(GLM_CONTRACT, "quantlab", "the B200 path runs absmax checkpoints (zeropoint is on the round-2 list)");
+    const std::string scheme_s = jp.at("scheme").as_str();  // to_string(QuantScheme), quant.cpp
+    if (scheme_s != "absmax" && scheme_s != "zeropoint") fail(GLM_FORMAT, "quantlab", "unknown quantization scheme \"" + scheme_s + "\"");
+    const bool zp = scheme_s == "zeropoint";
     const int axis = axis_from(jp.at("axis").as_str());
     std::map<std::string, const Json*> by_name;
     for (const Json& e : man.at("matrices").arr) by_name[e.at("name").as_str()] = &e;
@@ -362,7 +363,7 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
         auto it = by_name.find(nm);
         if (it == by_name.end()) fail(GLM_FORMAT, "quantlab", "manifest has no matrix " + nm);
         const Json& e = *it->second;
-        if (e.at("bits").as_int() != bits || e.at("scheme").as_str() != "absmax" ||
+        if (e.at("bits").as_int() != bits || e.at("scheme").as_str() != scheme_s ||
             axis_from(e.at("axis").as_str()) != axis)
           fail(GLM_FORMAT, "quantlab", nm + " does not follow the manifest policy");
         if (e.at("rows").as_int() != shapes[w][0] || e.at("cols").as_int() != shapes[w][1])
@@ -376,6 +377,11 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
           fail(GLM_FORMAT, "quantlab", nm + ".codes.glmt payload length does not match");
         if (sc.dtype != 0 || static_cast<int64_t>(sc.count()) != ng)
           fail(GLM_FORMAT, "quantlab", nm + ".scales.glmt group count does not match");
+        if (zp) {  // write_quantized_matrix adds .zeros.glmt for zeropoint matrices (quant.cpp:380-386)
+          const GlmtHeader z = read_glmt_header(p + names[w] + ".zeros.glmt");
+          if (z.dtype != 0 || static_cast<int64_t>(z.count()) != ng)
+            fail(GLM_FORMAT, "quantlab", nm + ".zeros.glmt group count does not match");
+        }
       }
       for (int v = 0; v < 4; ++v) {
         const GlmtHeader h = read_glmt_header(p + vecs[v] + ".glmt");
@@ -395,6 +401,7 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
     auto check = [&](glm_status st) {
       if (st != GLM_OK) fail(st, "glmmodel", glm_last_error());
     };
+    if (zp) check(glm_model_set_scheme(m, GLM_ZEROPOINT));
     {
       std::vector<double> rows;
       const uint64_t chunk = std::max<uint64_t>(1, (uint64_t{256} << 20) / (8 * static_cast<uint64_t>(d)));
@@ -410,8 +417,14 @@ extern "C" glm_status glm_model_load_quantized(const char* dir, int max_batch, i
         const Glmt c = read_glmt(p + names[w] + ".codes.glmt");
         const Glmt sc = read_glmt(p + names[w] + ".scales.glmt");
         validate_absmax_payload(c.i8.data(), static_cast<int64_t>(c.i8.size()), shapes[w][0] * shapes[w][1], bits);
-        check(glm_model_set_quantized(m, static_cast<int>(l), w, c.i8.data(), static_cast<int64_t>(c.i8.size()),
-                                      sc.f64.data(), static_cast<int64_t>(sc.f64.size())));
+        if (zp) {
+          const Glmt z = read_glmt(p + names[w] + ".zeros.glmt");
+          check(glm_model_set_quantized_zp(m, static_cast<int>(l), w, c.i8.data(), static_cast<int64_t>(c.i8.size()),
+                                           sc.f64.data(), z.f64.data(), static_cast<int64_t>(sc.f64.size())));
+        } else {
+          check(glm_model_set_quantized(m, static_cast<int>(l), w, c.i8.data(), static_cast<int64_t>(c.i8.size()),
+                                        sc.f64.data(), static_cast<int64_t>(sc.f64.size())));
+        }
       }
       for (int v = 0; v < 4; ++v) {
         const Glmt t = read_glmt(p + vecs[v] + ".glmt");

@@ -1601,6 +1601,33 @@ void zp_token_sums(const float* x, int64_t ldx, int M, const QWeightDev& w, floa
   LAUNCH_CHECK("k_zp_token_sums");
 }
 
+// zt[m] = sum_k x'[m][k] * zeta[k] over the fp16 activations exactly as the MMA reads them,
+// from the decode x_frag layout (tile == 0) or the tcgen05 token tiles (tile == 1)
+__global__ void k_zp_sums_act(const __half* __restrict__ xf, int64_t nch, int64_t Kp, int tile,
+                              const float* __restrict__ zeta, float* __restrict__ zt) {
+  const int m = blockIdx.x;
+  float acc = 0.f;
+  for (int64_t k = threadIdx.x; k < Kp; k += blockDim.x) {
+    const float z = zeta[k];
+    if (z != 0.f) acc += __half2float(xf[tile ? xtile_index(Kp, m, k) : xfrag_index(nch, m, k)]) * z;
+  }
+  __shared__ float red[8];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];
+    zt[m] = t;
+  }
+}
+
+void zp_sums_act(const __half* xf, int M, const QWeightDev& w, int tile, float* zt, cudaStream_t st) {
+  if (!w.zeta) fail(GLM_CONTRACT, "qlinear", "zero-point sums need zeropoint weights");
+  k_zp_sums_act<<<M, 256, 0, st>>>(xf, w.L.nch, w.L.Kp, tile, w.zeta, zt);
+  LAUNCH_CHECK("k_zp_sums_act");
+}
+
 void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, float* y, int64_t ldy,
                  cudaStream_t st, const float* zt) {
   const int64_t total = static_cast<int64_t>(M) * w.L.N;

@@ -61,6 +61,9 @@ struct QWeightDev {
 };
 // zt[m] = sum_k half(x[m][k] * row_scale[k]) * zeta[k]   (the zero-point term of zeropoint weights)
 void zp_token_sums(const float* x, int64_t ldx, int M, const QWeightDev& w, float* zt, cudaStream_t st);
+// the same sums from the fp16 activations already in the consumer layout (tile 0: decode x_frag,
+// 1: tcgen05 token tiles); M rows
+void zp_sums_act(const __half* xf, int M, const QWeightDev& w, int tile, float* zt, cudaStream_t st);
 
 struct GemvPlan {
   int ksplit = 1;

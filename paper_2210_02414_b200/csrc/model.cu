@@ -38,6 +38,10 @@ struct Linear {
   int64_t Kfull = 0, Nfull = 0;
   ShardSpec shard{};
   bool loaded = false;
+  // zeropoint scheme (quant.cpp:145-186): writable zvec / zeta of w, the local FP64 zero points
+  float *zvec = nullptr, *zeta = nullptr;
+  double* zps64 = nullptr;
+  int role = 0;  // QKV .. W2: index of its zero-point row sums in glm_model::zt_buf
 };
 
 struct Layer {
@@ -103,6 +107,7 @@ struct glm_model {
   double alpha = 0, eps = 1e-5, init_std = 0.0052;
   int bits = 8, axis = 0, max_batch = 1, max_ctx = 1;
   bool head_bf16 = false;
+  int scheme = GLM_ABSMAX;  // QuantPolicy::scheme (quant.hpp:53-58) of every linear
   int tp_rank = 0, tp_size = 1;
   int Hl = 0, dl = 0, fl = 0;
   int64_t vocab_offset = 0, vocab_local = 0;
@@ -130,6 +135,7 @@ struct glm_model {
   DeviceBuffer h, h_bf16, xf_qkv, xf_out, xf_w1, xf_v, xf_w2, logits, taps_attn, taps_ffn;
   DeviceBuffer y_qkv, q_rot, attn_out, y_out, y_a, y_b, y_ffn, ar_buf;
   DeviceBuffer partial;
+  DeviceBuffer zt_buf;  // zeropoint: [5 roles][rows_cap] zero-point row sums (zp_sums_act)
   int64_t partial_cap = 0;
   int64_t taps_rows = 0;
 
@@ -219,6 +225,7 @@ struct glm_model {
         lin.w.scales64 = alloc<double>(lin.w.nscales);
         for (int M = 1; M <= 16; ++M) lin.plans[M] = plan_gemv(lin.w.L, M);
       };
+      for (int i = 0; i < 5; ++i) ly.lin[i].role = i;
       mk(ly.lin[QKV], d, 3 * d, d, 3 * dl, ShardSpec{d, dl, static_cast<int64_t>(r) * dl, 0});
       mk(ly.lin[OUT], d, d, dl, d, ShardSpec{d, d, 0, static_cast<int64_t>(r) * dl});
       mk(ly.lin[W1], d, f, d, fl, ShardSpec{f, fl, static_cast<int64_t>(r) * fl, 0});
@@ -335,6 +342,7 @@ struct glm_model {
     zero(xf_w2, nt * ly.lin[W2].w.L.Kp * 2);
     zero(logits, rows * V * 4);
     zero(h_bf16, rows * d * 2);
+    zero(zt_buf, 5 * rows * 4);
     pool.emplace_back(rows * 8);
     d_argmax_rows = pool.back().as<unsigned long long>();
     CUDA_CHECK(cudaMemsetAsync(d_argmax_rows, 0, rows * 8, st));
@@ -401,11 +409,106 @@ struct glm_model {
     lin.loaded = true;
   }
 
+  // ---- zeropoint scheme --------------------------------------------------------------------
+  void set_scheme(int s) {
+    if (s != GLM_ABSMAX && s != GLM_ZEROPOINT) fail(GLM_CONTRACT, "quantlab", "unknown quantization scheme");
+    for (const Layer& ly : layers)
+      for (const Linear& lin : ly.lin)
+        if (lin.loaded) fail(GLM_CONTRACT, "glmmodel", "set the quantization scheme before loading weights");
+    if (s == GLM_ZEROPOINT && scheme != GLM_ZEROPOINT)
+      for (Layer& ly : layers)
+        for (Linear& lin : ly.lin) {
+          lin.zvec = alloc<float>(lin.w.L.Np);
+          lin.zeta = alloc<float>(lin.w.L.Kp);
+          lin.zps64 = alloc<double>(lin.w.nscales);
+        }
+    scheme = s;
+    for (Layer& ly : layers)
+      for (Linear& lin : ly.lin) {
+        lin.w.zvec = s == GLM_ZEROPOINT ? lin.zvec : nullptr;
+        lin.w.zeta = s == GLM_ZEROPOINT ? lin.zeta : nullptr;
+      }
+    drop_graphs();
+  }
+  float* zt_of(const Linear& lin) { return scheme == GLM_ZEROPOINT ? zt_buf.as<float>() + lin.role * rows_cap : nullptr; }
+  // zero-point row sums of M rows of fp16 activations xf in the consumer layout (tile: tcgen05
+  // token tiles, else x_frag); null for absmax
+  const float* zp_rows(const Linear& lin, const __half* xf, int64_t M, int tile) {
+    if (scheme != GLM_ZEROPOINT) return nullptr;
+    float* zt = zt_of(lin);
+    zp_sums_act(xf, static_cast<int>(M), lin.w, tile, zt, st);
+    return zt;
+  }
+  // Zeropoint weights of this rank's shard from the FULL canonical scales / zero points (host):
+  // runtime scales use s_eff = s (1 for constant groups, whose codes are 0 and value is z;
+  // quant.cpp:209-216), zvec / zeta carry the zero-point rank-1 term (QWeightDev).
+  void finish_linear_zp(Linear& lin, const double* scales, const double* zps) {
+    const ShardSpec& sh = lin.shard;
+    const int64_t ng = axis == GLM_AXIS_ROW ? lin.Kfull : axis == GLM_AXIS_COLUMN ? lin.Nfull : 1;
+    std::vector<double> seff(ng);
+    for (int64_t g = 0; g < ng; ++g) {
+      if (!std::isfinite(scales[g]) || scales[g] < 0.0 || !std::isfinite(zps[g]))
+        fail(GLM_FORMAT, "quantlab", "zeropoint scales must be finite and >= 0, zero points finite");
+      seff[g] = scales[g] == 0.0 ? 1.0 : scales[g];
+    }
+    DeviceBuffer ds(ng * 8), dz(ng * 8), de(ng * 8), le(lin.w.nscales * 8);
+    CUDA_CHECK(cudaMemcpyAsync(ds.ptr, scales, ng * 8, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(dz.ptr, zps, ng * 8, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(de.ptr, seff.data(), ng * 8, cudaMemcpyHostToDevice, st));
+    gather_scales_device(ds.as<double>(), sh, axis, lin.w.nscales, lin.w.scales64, st);
+    gather_scales_device(dz.as<double>(), sh, axis, lin.w.nscales, lin.zps64, st);
+    gather_scales_device(de.as<double>(), sh, axis, lin.w.nscales, le.as<double>(), st);
+    runtime_scales_device(le.as<double>(), lin.w.nscales, lin.w.L, axis, lin.w.col_scale, lin.w.row_scale, st);
+    auto fcol = [&](int64_t j) { return (j / sh.col_per_rank_block) * sh.col_block + sh.col_offset + (j % sh.col_per_rank_block); };
+    double smax = 0.0;  // the local kRow fold's S (runtime_scales_device: max over this shard)
+    if (axis == GLM_AXIS_ROW)
+      for (int64_t i = 0; i < lin.w.L.K; ++i) smax = std::max(smax, seff[sh.row_offset + i]);
+    std::vector<float> zv(lin.w.L.Np, 0.f), ze(lin.w.L.Kp, 0.f);
+    for (int64_t j = 0; j < lin.w.L.N; ++j)
+      zv[j] = static_cast<float>(axis == GLM_AXIS_ROW ? smax
+                                 : axis == GLM_AXIS_COLUMN ? seff[fcol(j)] * zps[fcol(j)]
+                                                           : seff[0] * zps[0]);
+    for (int64_t i = 0; i < lin.w.L.K; ++i) ze[i] = axis == GLM_AXIS_ROW ? static_cast<float>(zps[sh.row_offset + i]) : 1.f;
+    CUDA_CHECK(cudaMemcpyAsync(lin.zvec, zv.data(), zv.size() * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(lin.zeta, ze.data(), ze.size() * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    lin.loaded = true;
+  }
+
+  void set_linear_quantized_zp(int l, int which, const int8_t* payload, int64_t payload_bytes, const double* scales,
+                               const double* zps, int64_t nscales) {
+    if (scheme != GLM_ZEROPOINT) fail(GLM_CONTRACT, "glmmodel", "zero points given to an absmax model");
+    Linear& lin = layers[l].lin[which];
+    const int64_t K = lin.Kfull, N = lin.Nfull, n = K * N;
+    const int64_t pb = bits == 4 ? (n + 1) / 2 : n;
+    const int64_t ng = axis == GLM_AXIS_ROW ? K : axis == GLM_AXIS_COLUMN ? N : 1;
+    if (payload_bytes != pb) fail(GLM_FORMAT, "quantlab", "payload length does not match the linear's shape and bits");
+    if (nscales != ng) fail(GLM_FORMAT, "quantlab", "scale count does not match the model's group axis");
+    validate_absmax_payload(payload, pb, n, bits);  // zeropoint codes share the [-cap, cap] range (quant.cpp:27-31)
+    DeviceBuffer dp(pb);
+    CUDA_CHECK(cudaMemcpyAsync(dp.ptr, payload, pb, cudaMemcpyHostToDevice, st));
+    repack_shard_device(dp.as<int8_t>(), N, lin.shard, lin.w.L, lin.w.codes, st);
+    finish_linear_zp(lin, scales, zps);
+  }
+
   void set_linear_from_host(int l, int which, const double* w) {
     Linear& lin = layers[l].lin[which];
     const int64_t K = lin.Kfull, N = lin.Nfull, n = K * N;
     DeviceBuffer dw(n * 8), dp(bits == 4 ? (n + 1) / 2 : n), ds((axis == GLM_AXIS_ROW ? K : axis == GLM_AXIS_COLUMN ? N : 1) * 8);
     CUDA_CHECK(cudaMemcpyAsync(dw.ptr, w, n * 8, cudaMemcpyHostToDevice, st));
+    if (scheme == GLM_ZEROPOINT) {  // quantize_zeropoint (quant.cpp:145-186) on the GPU
+      const int64_t ng = ds.bytes / 8;
+      DeviceBuffer dz(ng * 8), dc(ng);
+      quantize_device(dw.ptr, GLM_F64, K, N, bits, GLM_ZEROPOINT, axis, dp.as<int8_t>(), ds.as<double>(), dz.as<double>(),
+                      dc.as<uint8_t>(), st);
+      repack_shard_device(dp.as<int8_t>(), N, lin.shard, lin.w.L, lin.w.codes, st);
+      std::vector<double> hs(ng), hz(ng);
+      CUDA_CHECK(cudaMemcpyAsync(hs.data(), ds.ptr, ng * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaMemcpyAsync(hz.data(), dz.ptr, ng * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      finish_linear_zp(lin, hs.data(), hz.data());
+      return;
+    }
     quantize_device(dw.ptr, GLM_F64, K, N, bits, GLM_ABSMAX, axis, dp.as<int8_t>(), ds.as<double>(), nullptr, nullptr, st);
     repack_shard_device(dp.as<int8_t>(), N, lin.shard, lin.w.L, lin.w.codes, st);
     finish_linear(lin, ds.as<double>());
@@ -416,6 +519,7 @@ struct glm_model {
   // payload + FP64 scales go to this rank's device layout without re-quantizing.
   void set_linear_quantized(int l, int which, const int8_t* payload, int64_t payload_bytes, const double* scales,
                             int64_t nscales) {
+    if (scheme == GLM_ZEROPOINT) fail(GLM_CONTRACT, "glmmodel", "a zeropoint model needs the zero points (glm_model_set_quantized_zp)");
     Linear& lin = layers[l].lin[which];
     const int64_t K = lin.Kfull, N = lin.Nfull, n = K * N;
     const int64_t pb = bits == 4 ? (n + 1) / 2 : n;
@@ -460,6 +564,7 @@ struct glm_model {
   }
 
   void init_synthetic(uint64_t seed) {
+    if (scheme != GLM_ABSMAX) fail(GLM_CONTRACT, "glmmodel", "synthetic init generates absmax weights");
     // stds of init_parameters (model.cpp:69-104); values from the counter-based generator
     const double factor = 1.0 / std::sqrt(2.0 * L);
     auto xavier = [](double a, double b) { return std::sqrt(2.0 / (a + b)); };
@@ -502,20 +607,21 @@ struct glm_model {
 
   // ---- row-parallel output sum across ranks (identity at t = 1) -------------------------
   // Decode: partials are reduced into ar_buf [M][d], allreduced, then consumed with scale 1.
-  SubIn row_parallel_out(const Linear& lin, const GemvPlan& p, int M) {
-    SubIn in{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale};
+  SubIn row_parallel_out(const Linear& lin, const GemvPlan& p, int M, const float* zt) {
+    SubIn in{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale, zt, lin.w.zvec};
     if (tp_size == 1) return in;
     if (ar_buf.bytes < static_cast<int64_t>(M) * d * 4) fail(GLM_CONTRACT, "glmmodel", "decode batch above max_batch");
-    gemv_reduce(partial.as<float>(), p.ksplit, M, lin.w, ar_buf.as<float>(), d, st);
+    gemv_reduce(partial.as<float>(), p.ksplit, M, lin.w, ar_buf.as<float>(), d, st, zt);
     comm->allreduce_sum(ar_buf.as<float>(), static_cast<int64_t>(M) * d, st);
     return SubIn{ar_buf.as<float>(), 1, 0, d, nullptr};
   }
 
   // DeepNorm LayerNorm after a row-parallel linear (out_proj, ffn_w2) in decode: at t > 1 the
   // rank partials are summed inside the LayerNorm kernel (PeerArgs); returns our launches.
-  int ln_after_row_parallel(LnArgs ln, const Linear& lin, const GemvPlan& p, int M) {
+  int ln_after_row_parallel(LnArgs ln, const Linear& lin, const GemvPlan& p, int M, const float* zt) {
     if (tp_size > 1 && fused_ar()) {
-      ln.in = SubIn{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale};
+      ln.in = SubIn{partial.as<float>(), p.ksplit, static_cast<int64_t>(M) * lin.w.L.Np, lin.w.L.Np, lin.w.col_scale, zt,
+                    lin.w.zvec};
       ln.peer = comm->peer_args();
       if (comm->emulated()) {  // push phase, group barrier, sum phase
         ln.peer.mode = 1;
@@ -529,7 +635,7 @@ struct glm_model {
       launch_deepnorm_ln(ln, M, st);
       return 1;
     }
-    ln.in = row_parallel_out(lin, p, M);
+    ln.in = row_parallel_out(lin, p, M, zt);
     launch_deepnorm_ln(ln, M, st);
     return tp_size > 1 ? 2 : 1;
   }
@@ -559,9 +665,12 @@ struct glm_model {
     int launches = 0;
     Layer& ly = layers[l];
     Linear &qkv = ly.lin[QKV], &out = ly.lin[OUT], &w1 = ly.lin[W1], &v = ly.lin[VV], &w2 = ly.lin[W2];
+    const int zl = scheme == GLM_ZEROPOINT ? 5 : 0;  // zero-point row-sum launches
+    const float* ztq = zp_rows(qkv, xf_qkv.as<__half>(), B, 0);
     gemv_launch(qkv.w, xf_qkv.as<__half>(), B, partial.as<float>(), qkv.plan(B), st);
     AttnDecodeArgs aa;
-    aa.qkv = SubIn{partial.as<float>(), qkv.plan(B).ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale};
+    aa.qkv = SubIn{partial.as<float>(), qkv.plan(B).ksplit, static_cast<int64_t>(B) * qkv.w.L.Np, qkv.w.L.Np, qkv.w.col_scale,
+                   ztq, qkv.w.zvec};
     aa.d_local = dl;
     aa.heads = Hl;
     aa.dh = dh;
@@ -578,6 +687,7 @@ struct glm_model {
     aa.out = nullptr;
     aa.prescale = half_store ? prescale : 0.f;
     launch_attn_decode(aa, B, st);
+    const float* zto = zp_rows(out, xf_out.as<__half>(), B, 0);
     gemv_launch(out.w, xf_out.as<__half>(), B, partial.as<float>(), out.plan(B), st);
     LnArgs ln;
     ln.h = h.as<float>();
@@ -591,18 +701,23 @@ struct glm_model {
     ln.tap = taps ? taps_attn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
     ln.zero_sublayer = zero_sub;
     ln.half_store = half_store ? 1 : 0;
-    launches += ln_after_row_parallel(ln, out, out.plan(B), B);
+    launches += ln_after_row_parallel(ln, out, out.plan(B), B, zto);
+    const float* zt1 = zp_rows(w1, xf_w1.as<__half>(), B, 0);
+    const float* ztv = zp_rows(v, (axis == GLM_AXIS_ROW ? xf_v : xf_w1).as<__half>(), B, 0);
     GemvOp op{w1.w.codes, bits, w1.w.L.nrt + v.w.L.nrt, w1.w.L.nch, xf_w1.as<__half>(),
               axis == GLM_AXIS_ROW ? xf_v.as<__half>() : xf_w1.as<__half>(), w1.w.L.nrt};
     gemv_launch(op, B, partial.as<float>(), fused_plan(B), st);
     ActArgs act;
     const int64_t np_tot = w1.w.L.Np + v.w.L.Np;
-    act.w1 = SubIn{partial.as<float>(), fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale};
-    act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale};
+    act.w1 = SubIn{partial.as<float>(), fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, w1.w.col_scale, zt1,
+                   w1.w.zvec};
+    act.v = SubIn{partial.as<float>() + w1.w.L.Np, fused_plan(B).ksplit, static_cast<int64_t>(B) * np_tot, np_tot, v.w.col_scale,
+                  ztv, v.w.zvec};
     act.M = B;
     act.f = fl;
     act.xo = xout(xf_w2.as<__half>(), w2);
     launch_geglu_act(act, st);
+    const float* zt2 = zp_rows(w2, xf_w2.as<__half>(), B, 0);
     gemv_launch(w2.w, xf_w2.as<__half>(), B, partial.as<float>(), w2.plan(B), st);
     LnArgs ln2 = ln;
     ln2.gain = ly.ln2g;
@@ -610,8 +725,8 @@ struct glm_model {
     ln2.x0 = next_x ? xout(xf_qkv.as<__half>(), layers[l + 1].lin[QKV]) : XOut{};
     ln2.x1 = XOut{};
     ln2.tap = taps ? taps_ffn.as<float>() + static_cast<int64_t>(l) * B * d : nullptr;
-    launches += ln_after_row_parallel(ln2, w2, w2.plan(B), B);
-    return launches + 6;  // + 4 GEMVs, attention, GeGLU activation
+    launches += ln_after_row_parallel(ln2, w2, w2.plan(B), B, zt2);
+    return launches + 6 + zl;  // + 4 GEMVs, attention, GeGLU activation (+ zero-point sums)
   }
 
   int enqueue_head(int M, float* logit_out, bool gather = true) {
@@ -698,18 +813,19 @@ struct glm_model {
   // tiles) + split-K reduce with the group scale.
   void linear_rows(const Linear& lin, const __half* xf, int64_t M, float* y) {
     GemvPlan p;
+    const float* zt = zp_rows(lin, xf, M, M > 16 ? 1 : 0);
     if (M <= 16) {
       p = lin.plan(static_cast<int>(M));
       gemv_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     } else {
       p = plan_qmm(lin.w.L, static_cast<int>(M));
       if (p.ksplit == 1) {  // tcgen05 epilogue writes the scaled result: no reduce pass
-        qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st, y, lin.w.L.N);
+        qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st, y, lin.w.L.N, zt);
         return;
       }
       qmm_launch(lin.w, xf, static_cast<int>(M), partial.as<float>(), p, st);
     }
-    gemv_reduce(partial.as<float>(), p.ksplit, static_cast<int>(M), lin.w, y, lin.w.L.N, st);
+    gemv_reduce(partial.as<float>(), p.ksplit, static_cast<int>(M), lin.w, y, lin.w.L.N, st, zt);
   }
 
   // One prefill block (model.cpp:198-224) over the n packed rows: input h (fp32) + its fp16
@@ -728,7 +844,8 @@ struct glm_model {
     if (nt && dh == 128) {
       const GemvPlan pq = plan_qmm(qkv.w.L, n);
       if (pq.ksplit == 1) {
-        qmm_launch(qkv.w, xf_qkv.as<__half>(), n, partial.as<float>(), pq, st, y_qkv.as<float>(), qkv.w.L.N, nullptr, true);
+        qmm_launch(qkv.w, xf_qkv.as<__half>(), n, partial.as<float>(), pq, st, y_qkv.as<float>(), qkv.w.L.N,
+                   zp_rows(qkv, xf_qkv.as<__half>(), n, 1), true);
         qkv_half = true;
       }
     }
@@ -1019,6 +1136,31 @@ glm_status glm_model_set_quantized(glm_model* m, int layer, int which, const int
   });
 }
 
+glm_status glm_model_set_scheme(glm_model* m, glm_scheme scheme) {
+  return guarded([&] { checked(m)->set_scheme(scheme); });
+}
+
+glm_status glm_model_set_quantized_zp(glm_model* m, int layer, int which, const int8_t* payload, int64_t payload_bytes,
+                                      const double* scales, const double* zero_points, int64_t ngroups) {
+  return guarded([&] {
+    checked(m);
+    if (layer < 0 || layer >= m->L || which < 0 || which > 4) fail(GLM_CONTRACT, "glmmodel", "bad linear index");
+    if (!payload || !scales || !zero_points) fail(GLM_CONTRACT, "glmmodel", "null payload, scales or zero points");
+    m->set_linear_quantized_zp(layer, which, payload, payload_bytes, scales, zero_points, ngroups);
+  });
+}
+
+glm_status glm_model_export_zero_points(const glm_model* m, int layer, int which, double* zero_points) {
+  return guarded([&] {
+    checked(m);
+    if (layer < 0 || layer >= m->L || which < 0 || which > 4) fail(GLM_CONTRACT, "glmmodel", "bad linear index");
+    if (m->scheme != GLM_ZEROPOINT) fail(GLM_CONTRACT, "glmmodel", "an absmax model has no zero points");
+    const Linear& lin = m->layers[layer].lin[which];
+    CUDA_CHECK(cudaMemcpyAsync(zero_points, lin.zps64, lin.w.nscales * 8, cudaMemcpyDeviceToHost, m->st));
+    CUDA_CHECK(cudaStreamSynchronize(m->st));
+  });
+}
+
 glm_status glm_model_init_synthetic(glm_model* m, uint64_t seed) {
   return guarded([&] { checked(m)->init_synthetic(seed); });
 }
@@ -1047,7 +1189,7 @@ glm_status glm_model_memory(const glm_model* m, glm_memory* out) {
         r.element_count += lin.Kfull * lin.Nfull;
         r.quant_payload_bytes += pbytes(lin.Kfull, lin.Nfull, m->bits);
         const int64_t groups = m->axis == GLM_AXIS_ROW ? lin.Kfull : m->axis == GLM_AXIS_COLUMN ? lin.Nfull : 1;
-        r.scale_bytes += groups * 8;
+        r.scale_bytes += groups * 8 * (m->scheme == GLM_ZEROPOINT ? 2 : 1);  // + zero points (quant.cpp:352-353)
         r.device_weight_bytes += lin.w.L.bytes();
       }
     r.half_baseline_bytes = 2 * r.element_count;

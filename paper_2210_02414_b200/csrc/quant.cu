@@ -464,6 +464,7 @@ __global__ void k_gather_scales(const double* __restrict__ full, ShardSpec sh, i
   if (i >= n) return;
   int64_t f;
   if (axis == GLM_AXIS_ROW) f = sh.row_offset + i;
+  else if (axis == GLM_AXIS_WHOLE) f = 0;  // one group, on every rank
   else f = (i / sh.col_per_rank_block) * sh.col_block + sh.col_offset + (i % sh.col_per_rank_block);
   local[i] = full[f];
 }

@@ -95,6 +95,9 @@ SIGNATURES = {
     "glm_debug_trace_start": (I32, [I64]),
     "glm_debug_trace_stop": (I32, [P, I64, P]),
     "glm_model_set_quantized": (I32, [P, I32, I32, P, I64, P, I64]),
+    "glm_model_set_scheme": (I32, [P, I32]),
+    "glm_model_set_quantized_zp": (I32, [P, I32, I32, P, I64, P, P, I64]),
+    "glm_model_export_zero_points": (I32, [P, I32, I32, P]),
     "glm_model_get_config": (I32, [P, P]),
     "glm_model_load_quantized": (I32, [C.c_char_p, I32, I32, I32, I32, I32, P]),
     "glm_qweight_create_ex": (I32, [P, P, P, I64, I64, I32, I32, I32, P]),
@@ -410,14 +413,16 @@ class Model:
     QKV, OUT, W1, V, W2, LN1G, LN1B, LN2G, LN2B = range(9)
 
     def __init__(self, cfg: GLMConfig, bits=8, axis="row", max_batch=1, max_ctx=256, head_bf16=False,
-                 tp_rank=0, tp_size=1):
+                 tp_rank=0, tp_size=1, scheme="absmax"):
         self.cfg = cfg
-        self.bits, self.axis = bits, axis
+        self.bits, self.axis, self.scheme = bits, axis, scheme
         self._c = cfg.c()
         h = C.c_void_p()
         _check(lib().glm_model_create(C.byref(self._c), bits, AXIS[axis], max_batch, max_ctx, int(head_bf16),
                                       tp_rank, tp_size, C.byref(h)))
         self.h = h
+        if scheme != "absmax":  # QuantPolicy::scheme (quant.hpp:53-58)
+            _check(lib().glm_model_set_scheme(self.h, SCHEME[scheme]))
 
     def __del__(self):
         if getattr(self, "h", None) and _LIB is not None:
@@ -439,15 +444,23 @@ class Model:
         jc, jp = man["config"], man["policy"]
         self.cfg = GLMConfig(num_layers=jc["num_layers"], hidden=jc["hidden"], num_heads=jc["num_heads"],
                              ffn_hidden=jc["ffn_hidden"], vocab=jc["vocab"])
-        self.bits, self.axis = jp["bits"], jp["axis"]
+        self.bits, self.axis, self.scheme = jp["bits"], jp["axis"], jp.get("scheme", "absmax")
         self._c = self.cfg.c()
         del cfg
         return self
 
-    def set_quantized(self, layer, which, payload, scales):
-        """A canonical QuantizedMatrix (payload int8 bytes, FP64 scales) of linear `which`."""
+    def set_quantized(self, layer, which, payload, scales, zero_points=None):
+        """A canonical QuantizedMatrix (payload int8 bytes, FP64 scales [, FP64 zero points of a
+        zeropoint model]) of linear `which`."""
         payload = np.ascontiguousarray(payload, np.int8)
         scales = np.ascontiguousarray(scales, np.float64)
+        if zero_points is not None:
+            zps = np.ascontiguousarray(zero_points, np.float64)
+            if zps.size != scales.size:
+                raise FormatError("[quantlab] zero point count differs from the scale count")
+            _check(lib().glm_model_set_quantized_zp(self.h, layer, which, _p(payload), payload.size, _p(scales), _p(zps),
+                                                    scales.size))
+            return
         _check(lib().glm_model_set_quantized(self.h, layer, which, _p(payload), payload.size, _p(scales), scales.size))
 
     def init_comm_emulated(self, group: "EmulatedGroup"):
@@ -490,6 +503,11 @@ class Model:
         scales = np.zeros(group_count(rows, cols, self.axis), np.float64)
         _check(lib().glm_model_export_linear(self.h, layer, which, _p(payload), _p(scales)))
         return payload, scales
+
+    def export_zero_points(self, layer, which, rows, cols):
+        zps = np.zeros(group_count(rows, cols, self.axis), np.float64)
+        _check(lib().glm_model_export_zero_points(self.h, layer, which, _p(zps)))
+        return zps
 
     def memory(self):
         m = _Memory()

@@ -29,25 +29,29 @@ def write_glmt(path, array, dtype):
         f.write(a.astype({"f64": "<f8", "f32": "<f4", "i8": "i1"}[dtype]).tobytes())
 
 
-def write_checkpoint(dirpath, p, bits, axis):
-    """save_quantized_model (quant.cpp:409-448) of the oracle's params under (bits, absmax, axis)."""
+def write_checkpoint(dirpath, p, bits, axis, scheme="absmax"):
+    """save_quantized_model (quant.cpp:409-448) of the oracle's params under (bits, scheme, axis);
+    zeropoint matrices add .zeros.glmt and "constant_groups" (write_quantized_matrix, :367-387)."""
     os.makedirs(dirpath, exist_ok=True)
     d, f = p.hidden, p.ffn
     man = {"config": {"num_layers": p.num_layers, "hidden": d, "num_heads": p.num_heads, "ffn_hidden": f,
                       "vocab": p.vocab, "dropout": 0.0, "init_method_std": 0.0052, "layernorm_eps": 1e-5,
                       "deepnorm_alpha": (2.0 * p.num_layers) ** 0.5},
-           "policy": {"bits": bits, "scheme": "absmax", "axis": axis}, "matrices": []}
+           "policy": {"bits": bits, "scheme": scheme, "axis": axis}, "matrices": []}
     write_glmt(os.path.join(dirpath, "embedding.glmt"), p.tensor(0, O.EMBED), "f64")
     payloads = {}
     for layer in range(p.num_layers):
         for w, nm in enumerate(NAMES):
-            q = O.quantize(p.tensor(layer, w), bits, axis)
+            q = O.quantize(p.tensor(layer, w), bits, axis, scheme=scheme)
             payloads[(layer, w)] = q
             name = f"layer{layer}.{nm}"
-            man["matrices"].append({"name": name, "bits": bits, "scheme": "absmax", "axis": axis,
-                                    "rows": q["rows"], "cols": q["cols"]})
+            entry = {"name": name, "bits": bits, "scheme": scheme, "axis": axis, "rows": q["rows"], "cols": q["cols"]}
             write_glmt(os.path.join(dirpath, name + ".codes.glmt"), np.asarray(q["payload"], np.int8), "i8")
             write_glmt(os.path.join(dirpath, name + ".scales.glmt"), q["scales"], "f64")
+            if scheme == "zeropoint":
+                write_glmt(os.path.join(dirpath, name + ".zeros.glmt"), q["zero_points"], "f64")
+                entry["constant_groups"] = [int(c) for c in q["constant_group"]]
+            man["matrices"].append(entry)
         for v, slot in (("ln1_gain", 5), ("ln2_gain", 6)):
             write_glmt(os.path.join(dirpath, f"layer{layer}.{v}.glmt"), p.tensor(layer, slot).reshape(-1), "f64")
         for v in ("ln1_bias", "ln2_bias"):
@@ -97,10 +101,50 @@ def test_policy_and_shape_mismatches_are_format_errors(tmp_path):
     with pytest.raises(glm.FormatError):
         glm.Model.load_quantized(str(tmp_path))
     man["matrices"][1]["cols"] = 128
-    man["policy"]["scheme"] = "zeropoint"
+    man["policy"]["scheme"] = "zeropoint"  # the matrices are absmax: not the manifest policy
     json.dump(man, open(man_path, "w"))
-    with pytest.raises(glm.ContractError):
+    with pytest.raises(glm.FormatError):
         glm.Model.load_quantized(str(tmp_path))
+    man["policy"]["scheme"] = "nf4"
+    json.dump(man, open(man_path, "w"))
+    with pytest.raises(glm.FormatError):
+        glm.Model.load_quantized(str(tmp_path))
+
+
+def test_zeropoint_checkpoint_without_zero_points_fails_before_device_work(tmp_path):
+    p = O.Params(1, 128, 2, vocab=64, seed=3)
+    write_checkpoint(str(tmp_path), p, 4, "column", scheme="zeropoint")
+    os.remove(os.path.join(str(tmp_path), "layer0.ffn_v.zeros.glmt"))
+    with pytest.raises(glm.FormatError):
+        glm.Model.load_quantized(str(tmp_path))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,axis", [(4, "row"), (8, "column")])
+def test_zeropoint_checkpoint_matches_the_reference_quantized_model(tmp_path, bits, axis):
+    """load_quantized_model of a zeropoint checkpoint (quant.cpp:450-491 reads .zeros.glmt):
+    codes, scales and zero points byte-exact on the device, taps and logits vs the oracle's
+    forward of the same quantized model."""
+    p = O.Params(2, 256, 4, vocab=300, seed=23)
+    payloads = write_checkpoint(str(tmp_path), p, bits, axis, scheme="zeropoint")
+    m = glm.Model.load_quantized(str(tmp_path), max_ctx=64)
+    assert m.scheme == "zeropoint"
+    for (layer, w), q in payloads.items():
+        pl, sc = m.export_linear(layer, w, q["rows"], q["cols"])
+        zp = m.export_zero_points(layer, w, q["rows"], q["cols"])
+        assert np.array_equal(pl, np.asarray(q["payload"], np.int8)) and np.array_equal(sc, q["scales"]), (layer, w)
+        assert np.array_equal(zp, q["zero_points"]), (layer, w)
+    p.quantize(bits, axis, scheme="zeropoint")
+    sample = O.gmask_sample([6 + (7 * i) % 250 for i in range(20)], [40, 41])
+    ref, at, ft = p.forward(sample, taps=True)
+    zero = p.forward(sample, zero_sublayers=True)
+    m.enable_taps(True)
+    lg = m.prefill(sample["tokens"], sample["positions"], sample["context_length"]).astype(np.float64)
+    ga, gf = m.taps(sample["n"])
+    for layer in range(2):
+        assert np.abs(ga[layer] - at[layer]).max() <= 1e-2 * np.abs(at[layer]).max()
+        assert np.abs(gf[layer] - ft[layer]).max() <= 1e-2 * np.abs(ft[layer]).max()
+    assert np.abs(lg - ref).max() <= 1e-2 * np.abs(ref - zero).max()
 
 
 @pytest.mark.gpu

@@ -29,22 +29,27 @@ def check_taps(gpu_taps, ref_taps):
         assert err <= 1e-2 * np.abs(ref_taps[layer]).max(), (layer, err)
 
 
-def rank_models(p, t, bits, axis, cfg, max_batch=1, max_ctx=256):
+def rank_models(p, t, bits, axis, cfg, max_batch=1, max_ctx=256, scheme="absmax"):
     group = glm.EmulatedGroup(t)
-    ms = [glm.Model(cfg, bits=bits, axis=axis, max_batch=max_batch, max_ctx=max_ctx, tp_rank=r, tp_size=t)
-          for r in range(t)]
+    ms = [glm.Model(cfg, bits=bits, axis=axis, max_batch=max_batch, max_ctx=max_ctx, tp_rank=r, tp_size=t,
+                    scheme=scheme) for r in range(t)]
     glm.run_ranks([lambda m=m: m.init_comm_emulated(group) for m in ms])
     for m in ms:
         m.load_reference_params(lambda layer, slot: p.tensor(0, O.EMBED) if slot == "embed" else p.tensor(layer, slot))
     return group, ms
 
 
-@pytest.mark.parametrize("t,bits,axis", [(2, 8, "row"), (4, 4, "column"), (8, 4, "row"), (8, 8, "column")])
-def test_tp_prefill_and_decode_match_oracle(t, bits, axis):
+@pytest.mark.parametrize("t,bits,axis,scheme", [(2, 8, "row", "absmax"), (4, 4, "column", "absmax"),
+                                                (8, 4, "row", "absmax"), (8, 8, "column", "absmax"),
+                                                (2, 4, "row", "zeropoint"), (4, 8, "column", "zeropoint"),
+                                                (2, 4, "whole", "zeropoint")])
+def test_tp_prefill_and_decode_match_oracle(t, bits, axis, scheme):
+    """(zeropoint: the zero-point rank-1 term of a row-parallel linear is a per-rank partial
+    summed by the allreduce; a column-parallel one carries this rank's zvec columns)"""
     cfg = glm.GLMConfig(num_layers=4, hidden=512, num_heads=8, vocab=262)
     p = O.Params(4, 512, 8, vocab=262, seed=1234)
-    group, ms = rank_models(p, t, bits, axis, cfg)
-    p.quantize(bits, axis)
+    group, ms = rank_models(p, t, bits, axis, cfg, scheme=scheme)
+    p.quantize(bits, axis, scheme=scheme)
     gen = [40, 100, 200, 57, 9]
     sample = O.gmask_sample(PREFIX[:70], gen)
     ref, at, ft = p.forward(sample, taps=True)
