@@ -771,17 +771,18 @@ constexpr float kDigitQ = 32512.f;  // 127 * 256: keeps the balanced hi digit in
 
 // One 16-k group of fragment-ordered fp16 activations (32 B, halves [j][2t, 2t+1, 2t+8, 2t+9])
 // -> 16 hi digits | 16 lo digits in weight-word byte order ([j][2t, 2t+8, 2t+1, 2t+9]); returns
-// the sum of the group's x_int. x_int = rint(fp32(x) * inv_s) via the 1.5 * 2^23 magic add
-// (|x_int| <= 32512 < 2^22, so the add rounds to the nearest even integer exactly as rint);
-// u = x_int + 128 then holds lo + 128 in its low byte and hi in the next (two's complement), so
-// two PRMT levels gather the 4 lo / 4 hi bytes of a word and one LOP flips lo's sign bit.
+// the sum of the group's x_int. x_int = rint(x * inv_s) of the exact product (one FFMA onto the
+// 1.5 * 2^23 + 128 magic: |x_int| <= 32512 < 2^22, so the sum rounds to the nearest even integer
+// and its float bits are 0x4B400000 + x_int + 128); the low 16 bits u = x_int + 128 hold lo + 128
+// in the low byte and hi in the next (two's complement), so two PRMT levels gather the 4 lo / 4
+// hi bytes of a word and one LOP flips lo's sign bit; the x_int sum is 256 * sum(hi) + sum(lo)
+// from two dp4a per word.
 __device__ __forceinline__ int digits_group(uint4* p, float inv_s) {
   const uint4 h0 = p[0], h1 = p[1];
   const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-  constexpr float kMagic = 12582912.f;              // 1.5 * 2^23
-  constexpr int kBias = 0x4B400000 - 128;           // magic bits, less the +128 offset
+  constexpr float kMagic = 12583040.f;  // 1.5 * 2^23 + 128
   uint32_t hi[4], lo[4];
-  int sum = 0;
+  int shi = 0, slo = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j]));
@@ -789,17 +790,16 @@ __device__ __forceinline__ int digits_group(uint4* p, float inv_s) {
     const float fq[4] = {f01.x, f23.x, f01.y, f23.y};  // byte order 2t, 2t+8, 2t+1, 2t+9
     uint32_t u[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      u[q] = static_cast<uint32_t>(__float_as_int(__fadd_rn(__fmul_rn(fq[q], inv_s), kMagic)) - kBias);
-      sum += static_cast<int>(u[q]);
-    }
+    for (int q = 0; q < 4; ++q) u[q] = __float_as_uint(__fmaf_rn(fq[q], inv_s, kMagic));
     const uint32_t t01 = __byte_perm(u[0], u[1], 0x5410), t23 = __byte_perm(u[2], u[3], 0x5410);
     lo[j] = __byte_perm(t01, t23, 0x6420) ^ 0x80808080u;
     hi[j] = __byte_perm(t01, t23, 0x7531);
+    shi = __dp4a(static_cast<int>(hi[j]), 0x01010101, shi);
+    slo = __dp4a(static_cast<int>(lo[j]), 0x01010101, slo);
   }
   p[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   p[1] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  return sum - 16 * 128;
+  return 256 * shi + slo;
 }
 
 // Row results of one item from the integer accumulators: rows g carry (code + 8), rows g + 8
@@ -889,30 +889,30 @@ __global__ void __launch_bounds__(kM1MaxWarps * 32, 1) k_gemv_i4(GemvArgs a, int
       }
     }
   }
+  mbar_wait(xbar, 0);  // the activation copy first: ring stages not fetched before the wait follow it
   if (lane == 0)
     for (int s = early; s < NST; ++s) issue();
-  mbar_wait(xbar, 0);
   trace_point(14);
   // (1) max |x| per activation vector (v, m): 16-byte units, [vm][chunk][8 units]
   const int nvm = nx * MT;
   const int upv = nch * 8;
   {
+    // packed fp16 maxima of |x| (exact), NaN-propagating, one vector at a time (no division)
     float mx[2 * MT];
 #pragma unroll
-    for (int i = 0; i < 2 * MT; ++i) mx[i] = 0.f;
-    for (int i = threadIdx.x; i < nvm * upv; i += blockDim.x) {
-      const uint4 v = reinterpret_cast<const uint4*>(xs)[i];
-      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-      __half2 m2 = __habs2(*reinterpret_cast<const __half2*>(&wd[0]));
+    for (int q = 0; q < 2 * MT; ++q) {
+      mx[q] = 0.f;
+      if (q >= nvm) continue;
+      const uint4* xv = reinterpret_cast<const uint4*>(xs) + q * upv;
+      __half2 m2 = __float2half2_rn(0.f);
+      for (int i = threadIdx.x; i < upv; i += blockDim.x) {
+        const uint4 v = xv[i];
+        const uint32_t wd[4] = {v.x & 0x7FFF7FFFu, v.y & 0x7FFF7FFFu, v.z & 0x7FFF7FFFu, v.w & 0x7FFF7FFFu};
 #pragma unroll
-      for (int e = 1; e < 4; ++e) m2 = __hmax2_nan(m2, __habs2(*reinterpret_cast<const __half2*>(&wd[e])));
+        for (int e = 0; e < 4; ++e) m2 = __hmax2_nan(m2, *reinterpret_cast<const __half2*>(&wd[e]));
+      }
       const float2 f = __half22float2(m2);
-      float m = fmaxf(f.x, f.y);
-      if (f.x != f.x || f.y != f.y) m = __int_as_float(0x7fc00000);
-      const int vm = i / upv;
-#pragma unroll
-      for (int q = 0; q < 2 * MT; ++q)
-        if (q == vm) mx[q] = (m != m || mx[q] != mx[q]) ? __int_as_float(0x7fc00000) : fmaxf(mx[q], m);
+      mx[q] = (f.x != f.x || f.y != f.y) ? __int_as_float(0x7fc00000) : fmaxf(f.x, f.y);
     }
 #pragma unroll
     for (int q = 0; q < 2 * MT; ++q) {

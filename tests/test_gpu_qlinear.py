@@ -29,7 +29,7 @@ DIGIT_Q = np.float32(32512.0)  # gemv.cu kDigitQ
 
 def imma_activations(xh):
     """The integer-MMA GEMV's view of fp16 activations (gemv.cu digits_group): per row,
-    x_int = rint(fp32(x) * fp32(32512 / max|x|)) and the scale s_x = max|x| / 32512."""
+    x_int = rint(x * fp32(32512 / max|x|)) of the exact product and s_x = max|x| / 32512."""
     xh32 = xh.astype(np.float32)
     out = np.zeros(xh.shape, np.float64)
     for m in range(xh.shape[0]):
@@ -37,7 +37,7 @@ def imma_activations(xh):
         if mx == 0:
             continue
         inv = np.float32(DIGIT_Q / mx)
-        xi = np.rint(xh32[m] * inv).astype(np.int64)
+        xi = np.rint(xh32[m].astype(np.float64) * np.float64(inv)).astype(np.int64)  # FFMA: one rounding
         assert np.abs(xi).max() <= 32512
         out[m] = xi.astype(np.float64) * np.float64(np.float32(mx / DIGIT_Q))
     return out

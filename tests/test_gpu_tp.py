@@ -42,7 +42,7 @@ def rank_models(p, t, bits, axis, cfg, max_batch=1, max_ctx=256, scheme="absmax"
 @pytest.mark.parametrize("t,bits,axis,scheme", [(2, 8, "row", "absmax"), (4, 4, "column", "absmax"),
                                                 (8, 4, "row", "absmax"), (8, 8, "column", "absmax"),
                                                 (2, 4, "row", "zeropoint"), (4, 8, "column", "zeropoint"),
-                                                (2, 4, "whole", "zeropoint")])
+                                                (2, 4, "whole", "zeropoint"), (4, 8, "whole", "absmax")])
 def test_tp_prefill_and_decode_match_oracle(t, bits, axis, scheme):
     """(zeropoint: the zero-point rank-1 term of a row-parallel linear is a per-rank partial
     summed by the allreduce; a column-parallel one carries this rank's zvec columns)"""
