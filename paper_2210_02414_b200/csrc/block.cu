@@ -1532,6 +1532,288 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
 // staged by one bulk copy issued before the dependency wait, for 3..8 sequences and for longer
 // caches (batch sweep, same box: B = 4 251 -> 280, B = 8 429 -> 454 tok/s; B = 16 662 -> 643, so
 // not there). GLM_ATTN_SPLIT64=0 keeps the 256-key unstaged CTAs at 3..8 sequences.
+// ---- long-context decode attention: one CTA streams a long key range -----------------
+// grid (heads, batch, splits) with split_keys = a multiple of 64 chosen so about two CTAs per SM
+// cover the caches (attn_decode_ring_split_keys): the split's cached keys pass through a ring
+// of kRingStages 64-key shared-memory blocks (one bulk copy each, the first ones issued before
+// the dependency wait): all K blocks for the scores (kept in shared memory, up to
+// kRingMaxKeys), then the V blocks for P.V, so K and V are read once at HBM speed instead of
+// 64-key CTAs waiting in waves. q / the new key / value, RoPE, the split partial format and the
+// in-order merge are those of k_attn_decode.
+constexpr int kRingBlock = 64;
+constexpr int kRingStages = 4;
+constexpr int kRingMaxKeys = 2048;
+constexpr int kRingThreads = 256;
+
+template <int DH>
+__global__ void __launch_bounds__(kRingThreads, 2) k_attn_decode_ring(AttnDecodeArgs a) {
+  trace_point(30);
+  constexpr int NW = kRingThreads / 32;
+  constexpr int FPL = DH / 32;
+  constexpr int LPK = DH / 8, KPW = 32 / LPK;
+  constexpr int BLK_BYTES = kRingBlock * DH * 2;
+  __shared__ float q[DH];
+  __shared__ float p[kRingMaxKeys + 1];
+  __shared__ float red[NW];
+  __shared__ float opart[NW][DH];
+  __shared__ int last;
+  __shared__ __align__(8) uint64_t bars[kRingStages];
+  __shared__ __align__(16) __half knew[DH];
+  __shared__ __align__(16) __half vnew[DH];
+  extern __shared__ __align__(128) __half ring[];  // [kRingStages][kRingBlock][DH]
+  const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int len = a.cache_len[b];
+  const int total = len + 1;
+  const int k0 = split * a.split_keys, k1 = min(total, k0 + a.split_keys);
+  const int kold = min(k1, len);
+  const int n_old = max(0, kold - k0);
+  const int nb = (n_old + kRingBlock - 1) / kRingBlock;  // 64-key blocks of cached keys
+  const int pos = a.positions[b];
+  const float inv_sqrt = rsqrtf(static_cast<float>(DH));
+  __half* kc = a.kcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
+  __half* vc = a.vcache + ((static_cast<int64_t>(b) * a.heads + head) * a.max_ctx) * DH;
+  float* part = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits + split) * (DH + 2);
+  // load j < nb: K block j; nb <= j < 2 nb: V block j - nb
+  auto issue = [&](int j) {
+    if (j >= 2 * nb) return;
+    const int blk = j < nb ? j : j - nb;
+    const int kk = k0 + blk * kRingBlock;
+    const uint32_t bytes = static_cast<uint32_t>(min(kRingBlock, kold - kk)) * DH * 2;
+    uint64_t* bar = bars + (j % kRingStages);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(reinterpret_cast<uint8_t*>(ring) + (j % kRingStages) * BLK_BYTES)),
+                 "l"((j < nb ? kc : vc) + static_cast<int64_t>(kk) * DH), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+  };
+  auto wait = [&](int j) {
+    const uint32_t par = static_cast<uint32_t>((j / kRingStages) & 1);
+    asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W_%=;\n}\n" ::"r"(
+                     smem_addr(bars + (j % kRingStages))),
+                 "r"(par)
+                 : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRingStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // cached keys do not depend on the running qkv GEMV
+    if (k0 < total)
+      for (int j = 0; j < kRingStages; ++j) issue(j);
+  }
+  __syncthreads();
+  const int jt = threadIdx.x < DH / 2 ? threadIdx.x : threadIdx.x - DH / 2;
+  float2 cs = make_float2(1.f, 0.f), sq = make_float2(1.f, 1.f), sk = sq, sv = sq;
+  if (threadIdx.x < DH) {
+    cs = a.rope[static_cast<int64_t>(pos) * (DH / 2) + jt];
+    const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jt;
+    if (a.qkv.scale) {
+      sq = *reinterpret_cast<const float2*>(a.qkv.scale + fq);
+      sk = *reinterpret_cast<const float2*>(a.qkv.scale + a.d_local + fq);
+      sv = *reinterpret_cast<const float2*>(a.qkv.scale + 2 * a.d_local + fq);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  trace_point(31);
+  if (k0 >= total) return;  // beyond the cache: no keys, not counted by the merge
+  const bool has_new = len >= k0 && len < k1;
+  if (threadIdx.x < DH) {
+    auto raw2 = [&](int64_t f) {
+      float2 acc = make_float2(0.f, 0.f);
+      for (int s0 = 0; s0 < a.qkv.ksplit; ++s0) {
+        const float2 v = *reinterpret_cast<const float2*>(a.qkv.p + static_cast<int64_t>(s0) * a.qkv.split_stride +
+                                                          b * a.qkv.ld + f);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      return acc;
+    };
+    auto zp2 = [&](int64_t f) {
+      return a.qkv.zt ? make_float2(a.qkv.zt[b] * a.qkv.zv[f], a.qkv.zt[b] * a.qkv.zv[f + 1]) : make_float2(0.f, 0.f);
+    };
+    const int64_t fq = static_cast<int64_t>(head) * DH + 2 * jt;
+    if (threadIdx.x < DH / 2) {
+      const float2 qv = raw2(fq), qz = zp2(fq);
+      const float qa = qv.x * sq.x + qz.x, qb = qv.y * sq.y + qz.y;
+      q[2 * jt] = (cs.x * qa - cs.y * qb) * inv_sqrt;
+      q[2 * jt + 1] = (cs.y * qa + cs.x * qb) * inv_sqrt;
+    } else if (has_new) {
+      const int64_t fk = a.d_local + fq, fv = 2 * a.d_local + fq;
+      const float2 kv2 = raw2(fk), vv2 = raw2(fv), kz = zp2(fk), vz = zp2(fv);
+      const float ka = kv2.x * sk.x + kz.x, kb = kv2.y * sk.y + kz.y;
+      const float va = vv2.x * sv.x + vz.x, vb = vv2.y * sv.y + vz.y;
+      const __half2 kh = __floats2half2_rn(cs.x * ka - cs.y * kb, cs.y * ka + cs.x * kb);
+      const __half2 vh = __floats2half2_rn(va, vb);
+      *reinterpret_cast<__half2*>(kc + static_cast<int64_t>(len) * DH + 2 * jt) = kh;
+      *reinterpret_cast<__half2*>(vc + static_cast<int64_t>(len) * DH + 2 * jt) = vh;
+      *reinterpret_cast<__half2*>(knew + 2 * jt) = kh;
+      *reinterpret_cast<__half2*>(vnew + 2 * jt) = vh;
+    }
+  }
+  __syncthreads();
+  // ---- scores over the K blocks (LPK lanes per key, one 16-byte load each) ----
+  const int sub = lane % LPK, kin = lane / LPK;
+  float qr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) qr[i] = q[sub * 8 + i];
+  auto dot8 = [&](uint4 kv) {
+    const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+      acc += qr[2 * e] * f.x + qr[2 * e + 1] * f.y;
+    }
+    return acc;
+  };
+  auto score = [&](float acc) {
+    if (a.prescale > 0.f) acc = half_round(acc / a.prescale) * a.prescale;
+    return acc;
+  };
+  for (int j = 0; j < nb; ++j) {
+    wait(j);
+    const __half* blk = ring + (j % kRingStages) * (kRingBlock * DH);
+    const int nk = min(kRingBlock, n_old - j * kRingBlock);
+    for (int s = warp * KPW + kin; s < kRingBlock; s += NW * KPW) {
+      float acc = s < nk ? dot8(*reinterpret_cast<const uint4*>(blk + s * DH + sub * 8)) : 0.f;
+#pragma unroll
+      for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sub == 0 && s < nk) p[j * kRingBlock + s] = score(acc);
+    }
+    __syncthreads();  // stage j consumed by every warp
+    if (threadIdx.x == 0) issue(j + kRingStages);
+  }
+  if (has_new && warp == 0) {
+    float acc = lane < LPK ? dot8(*reinterpret_cast<const uint4*>(knew + lane * 8)) : 0.f;
+#pragma unroll
+    for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) p[n_old] = score(acc);
+  }
+  __syncthreads();
+  const int nk_all = n_old + (has_new ? 1 : 0);
+  // ---- softmax over the split (fp32) ----
+  float mx = -FLT_MAX;
+  for (int s = threadIdx.x; s < nk_all; s += kRingThreads) mx = fmaxf(mx, p[s]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int s = threadIdx.x; s < nk_all; s += kRingThreads) {
+    const float e = __expf(p[s] - mx);
+    p[s] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  sum = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) sum += red[w];
+  // ---- P.V over the V blocks: warp w takes keys w, w + NW, ...; lane owns FPL features ----
+  float o[FPL];
+#pragma unroll
+  for (int f = 0; f < FPL; ++f) o[f] = 0.f;
+  auto pv = [&](const __half* vr, float pw) {
+    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(vr));
+    o[0] += pw * f0.x;
+    o[1] += pw * f0.y;
+    if constexpr (FPL == 4) {
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(vr + 2));
+      o[2] += pw * f1.x;
+      o[3] += pw * f1.y;
+    }
+  };
+  for (int j = nb; j < 2 * nb; ++j) {
+    wait(j);
+    const __half* blk = ring + (j % kRingStages) * (kRingBlock * DH);
+    const int jb = j - nb, nk = min(kRingBlock, n_old - jb * kRingBlock);
+    for (int s = warp; s < nk; s += NW) pv(blk + s * DH + lane * FPL, p[jb * kRingBlock + s]);
+    __syncthreads();
+    if (threadIdx.x == 0) issue(j + kRingStages);
+  }
+  if (has_new && warp == 0) pv(vnew + lane * FPL, p[n_old]);
+#pragma unroll
+  for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
+  __syncthreads();
+  if (total <= a.split_keys) {  // single active split: normalise, hand the row to out_proj
+    const float inv = 1.f / sum;
+    for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kRingThreads) {
+      float o0 = 0.f, o1 = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        o0 += opart[w][2 * c2];
+        o1 += opart[w][2 * c2 + 1];
+      }
+      const int64_t k = static_cast<int64_t>(head) * DH + 2 * c2;
+      store_xfrag_pair(a.xo, b, k, o0 * inv, o1 * inv);
+      if (a.out) {
+        a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0 * inv;
+        a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
+      }
+    }
+    return;
+  }
+  for (int c = threadIdx.x; c < DH; c += kRingThreads) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) acc += opart[w][c];
+    part[c] = acc;
+  }
+  if (threadIdx.x == 0) {
+    part[DH] = mx;
+    part[DH + 1] = sum;
+  }
+  // ---- the last of the active splits of this (head, b) merges them in order ----
+  const int nsp = (total + a.split_keys - 1) / a.split_keys;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* ctr = a.counters + b * a.heads + head;
+    last = (atomicAdd(ctr, 1) == nsp - 1);
+    if (last) *ctr = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (DH + 2);
+  float* wsp = p;
+  if (warp == 0) {
+    float gm = -FLT_MAX;
+    for (int s = lane; s < nsp; s += 32) gm = fmaxf(gm, __ldcg(base + s * (DH + 2) + DH));
+    gm = warp_max(gm);
+    float gl = 0.f;
+    for (int s = lane; s < nsp; s += 32) {
+      const float w = __expf(__ldcg(base + s * (DH + 2) + DH) - gm);
+      wsp[s] = w;
+      gl += __ldcg(base + s * (DH + 2) + DH + 1) * w;
+    }
+    gl = warp_sum(gl);
+    const float inv = 1.f / gl;
+    for (int s = lane; s < nsp; s += 32) wsp[s] *= inv;
+  }
+  __syncthreads();
+  for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kRingThreads) {
+    float o0 = 0.f, o1 = 0.f;
+    for (int s = 0; s < nsp; ++s) {
+      const float w = wsp[s];
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(base + s * (DH + 2) + 2 * c2));
+      o0 += w * v.x;
+      o1 += w * v.y;
+    }
+    const int64_t k = static_cast<int64_t>(head) * DH + 2 * c2;
+    store_xfrag_pair(a.xo, b, k, o0, o1);
+    if (a.out) {
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k] = o0;
+      a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1;
+    }
+  }
+}
+
 int attn_decode_split_keys(int max_ctx, int B) {
   static const bool many64 = [] { const char* e = getenv("GLM_ATTN_SPLIT64"); return !e || e[0] != '0'; }();
   if (max_ctx > kSplitKeys) return kSplitKeysLong;
@@ -1548,6 +1830,29 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   // two sequences, 64-key CTAs (32 KB of staging, several per SM) otherwise.
   a.split_keys = attn_decode_split_keys(a.max_ctx, B);
   if (a.max_splits != attn_decode_splits(a.max_ctx)) fail(GLM_CONTRACT, "glmmodel", "decode attention split count");
+  static const bool ring = [] { const char* e = getenv("GLM_ATTN_RING"); return !e || e[0] != '0'; }();
+  if (ring && a.max_ctx > kSplitKeys && (a.dh == 128 || a.dh == 64)) {
+    // long caches: about two streaming CTAs per SM (k_attn_decode_ring), splits of 64-key blocks
+    static const int cps = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 2; }();
+    const int64_t ctas = static_cast<int64_t>(a.heads) * B;
+    const int64_t nsplit = std::max<int64_t>(1, cps * 148 / ctas);
+    int64_t sk = (a.max_ctx + nsplit - 1) / nsplit;
+    sk = std::min<int64_t>(kRingMaxKeys, (sk + kRingBlock - 1) / kRingBlock * kRingBlock);
+    a.split_keys = static_cast<int>(sk);
+    a.stage_keys = 0;
+    const dim3 grid(a.heads, B, (a.max_ctx + a.split_keys - 1) / a.split_keys);
+    const size_t smem = static_cast<size_t>(kRingStages) * kRingBlock * a.dh * 2;
+    static bool attr_r = false;
+    if (!attr_r) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingStages * kRingBlock * 128 * 2));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingStages * kRingBlock * 64 * 2));
+      attr_r = true;
+    }
+    if (a.dh == 128) launch_k(k_attn_decode_ring<128>, grid, dim3(kRingThreads), smem, st, a);
+    else launch_k(k_attn_decode_ring<64>, grid, dim3(kRingThreads), smem, st, a);
+    LAUNCH_CHECK("k_attn_decode_ring");
+    return;
+  }
   if (a.max_splits > kSplitKeys)  // the merge keeps one weight per split in the score buffer
     fail(GLM_DIMENSION, "glmmodel", "decode attention supports caches up to 16384 tokens");
   const dim3 grid(a.heads, B, (a.max_ctx + a.split_keys - 1) / a.split_keys);

@@ -242,6 +242,32 @@ def test_prefill_attention_head_dim_128_long_context(prefix_len, gen):
     check_logits(lg.astype(np.float64), ref, zero)
 
 
+@pytest.mark.parametrize("batch,prefix_len,max_ctx", [(1, 1990, 2112), (2, 700, 2112), (1, 1200, 4200)])
+def test_decode_attention_streaming_long_context(batch, prefix_len, max_ctx):
+    """Long caches (max_ctx > 256) run k_attn_decode_ring: about two CTAs per SM, each streaming
+    its split's K then V through a 4-stage ring of 64-key blocks (splits of up to 2048 keys,
+    merged in order by the last CTA of a head). Teacher-forced decode rows vs the oracle."""
+    p, m, _ = build(4, "column", layers=2, hidden=256, heads=2, vocab=300, seed=17, max_batch=batch, max_ctx=max_ctx)
+    rng = np.random.default_rng(prefix_len)
+    prefix = [int(v) for v in rng.integers(6, 290, size=prefix_len)]
+    gen = [int(v) for v in rng.integers(6, 290, size=2)]
+    sample = O.gmask_sample(prefix, gen)
+    ref, at, ft, zero = oracle_rows(p, sample)
+    C = sample["context_length"]
+    for b in range(batch):
+        m.prefill(sample["tokens"][:C], sample["positions"][:C], C, seq=b, logits=False)
+    m.enable_taps(True)
+    rows, ta = [], []
+    for j in range(2):
+        _, lg = m.decode_step([sample["tokens"][C + j]] * batch, [sample["positions"][C + j]] * batch)
+        a, _f = m.taps(batch)
+        for b in range(batch):
+            check_taps(a[:, b:b + 1], at[:, C + j:C + j + 1])
+        rows.append(lg[batch - 1])
+    m.enable_taps(False)
+    check_logits(np.array(rows, np.float64), ref[C:C + 2], zero[C:C + 2])
+
+
 @pytest.mark.parametrize("batch", [1, 3])
 def test_decode_attention_long_cache_splits(batch):
     """Caches longer than 256 tokens run the decode attention in 64-key splits (block.cu
