@@ -1830,8 +1830,11 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   // two sequences, 64-key CTAs (32 KB of staging, several per SM) otherwise.
   a.split_keys = attn_decode_split_keys(a.max_ctx, B);
   if (a.max_splits != attn_decode_splits(a.max_ctx)) fail(GLM_CONTRACT, "glmmodel", "decode attention split count");
-  static const bool ring = [] { const char* e = getenv("GLM_ATTN_RING"); return !e || e[0] != '0'; }();
-  if (ring && a.max_ctx > kSplitKeys && (a.dh == 128 || a.dh == 64)) {
+  // GLM_ATTN_RING: 0 off, 1 long caches only, 2 (default) long caches and 3+ sequences, 3 always
+  // (same-box: 3+ sequences at ~135 cached tokens B = 4 / 8 / 16 +2.3 / +3.9 / +1.9 %; one or two
+  // sequences keep the 256-key staged CTAs: always-ring 80.1 vs 80.6 tok/s at batch 1)
+  static const int ring = [] { const char* e = getenv("GLM_ATTN_RING"); return e ? atoi(e) : 2; }();
+  if (ring && (a.max_ctx > kSplitKeys || (ring == 2 && B > 2) || ring == 3) && (a.dh == 128 || a.dh == 64)) {
     // long caches: about two streaming CTAs per SM (k_attn_decode_ring), splits of 64-key blocks
     static const int cps = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 2; }();
     const int64_t ctas = static_cast<int64_t>(a.heads) * B;
