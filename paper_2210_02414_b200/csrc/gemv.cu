@@ -24,6 +24,7 @@
 // thread ~68 cycles and the extra cross-warp hand-offs add ~350 cycles per stage); it is
 // used where it wins, for prefill (qmm_tc.cu).
 #include <cstdlib>
+#include <type_traits>
 #include <string>
 
 #include "common.cuh"
@@ -1173,44 +1174,50 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_gemv_mk_i4(GemvArgs a, int 
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc[r][q][h][i] = 0;
-      for (int c = 0; c < nck; c += U) {
-        const int n = min(U, nck - c);
-        mbar_wait(bars + cslot, cpar);
-        const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
-        auto chunk = [&](int u) {
-          uint4 xv[NQ];
+      // the k loop, instantiated for one or two row tiles so the unrolled chunk has no
+      // per-tile branch (a divergent-looking branch makes the compiler fence every MMA group)
+      auto kloop = [&](auto two_c) {
+        constexpr int NR = decltype(two_c)::value ? RT : 1;
+        for (int c = 0; c < nck; c += U) {
+          const int n = min(U, nck - c);
+          mbar_wait(bars + cslot, cpar);
+          const uint8_t* st = ring + cslot * kStageBytes + lane * 16;
+          auto chunk = [&](int u) {
+            uint4 xv[NQ];
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) xv[q] = *reinterpret_cast<const uint4*>(xrow[q] + (c + u) * 128);
+            for (int q = 0; q < NQ; ++q) xv[q] = *reinterpret_cast<const uint4*>(xrow[q] + (c + u) * 128);
 #pragma unroll
-          for (int r = 0; r < RT; ++r) {
-            if (r == 1 && !two) break;
-            const uint4 wv = *reinterpret_cast<const uint4*>(st + (r * n + u) * CHUNK);
-            const uint32_t a0 = wv.x & 0x0F0F0F0Fu, a1 = wv.x & 0xF0F0F0F0u, a2 = wv.y & 0x0F0F0F0Fu,
-                           a3 = wv.y & 0xF0F0F0F0u;
-            const uint32_t a4 = wv.z & 0x0F0F0F0Fu, a5 = wv.z & 0xF0F0F0F0u, a6 = wv.w & 0x0F0F0F0Fu,
-                           a7 = wv.w & 0xF0F0F0F0u;
+            for (int r = 0; r < NR; ++r) {
+              const uint4 wv = *reinterpret_cast<const uint4*>(st + (r * n + u) * CHUNK);
+              const uint32_t a0 = wv.x & 0x0F0F0F0Fu, a1 = wv.x & 0xF0F0F0F0u, a2 = wv.y & 0x0F0F0F0Fu,
+                             a3 = wv.y & 0xF0F0F0F0u;
+              const uint32_t a4 = wv.z & 0x0F0F0F0Fu, a5 = wv.z & 0xF0F0F0F0u, a6 = wv.w & 0x0F0F0F0Fu,
+                             a7 = wv.w & 0xF0F0F0F0u;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              imma16832(acc[r][q][0], a0, a1, a2, a3, xv[q].x, xv[q].y);
-              imma16832(acc[r][q][1], a4, a5, a6, a7, xv[q].z, xv[q].w);
+              for (int q = 0; q < NQ; ++q) {
+                imma16832(acc[r][q][0], a0, a1, a2, a3, xv[q].x, xv[q].y);
+                imma16832(acc[r][q][1], a4, a5, a6, a7, xv[q].z, xv[q].w);
+              }
             }
-          }
-        };
-        if (n == U) {
+          };
+          if (n == U) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) chunk(u);
-        } else {
-          for (int u = 0; u < n; ++u) chunk(u);
+            for (int u = 0; u < U; ++u) chunk(u);
+          } else {
+            for (int u = 0; u < n; ++u) chunk(u);
+          }
+          __syncwarp();
+          if (cslot + 1 == kMkStages) {
+            cslot = 0;
+            cpar ^= 1u;
+          } else {
+            ++cslot;
+          }
+          if (lane == 0) issue();
         }
-        __syncwarp();
-        if (cslot + 1 == kMkStages) {
-          cslot = 0;
-          cpar ^= 1u;
-        } else {
-          ++cslot;
-        }
-        if (lane == 0) issue();
-      }
+      };
+      if (two) kloop(std::true_type{});
+      else kloop(std::false_type{});
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
         if (r == 1 && !two) break;
