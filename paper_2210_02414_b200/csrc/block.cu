@@ -1541,26 +1541,28 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
 // 64-key CTAs waiting in waves. q / the new key / value, RoPE, the split partial format and the
 // in-order merge are those of k_attn_decode.
 constexpr int kRingBlock = 64;
-constexpr int kRingStages = 4;
 constexpr int kRingMaxKeys = 2048;
 constexpr int kRingThreads = 256;
 
-template <int DH>
-__global__ void __launch_bounds__(kRingThreads, 2) k_attn_decode_ring(AttnDecodeArgs a) {
+// NS ring stages: 4 for long caches (two CTAs per SM), 2 for short ones (five per SM: many
+// (head, sequence) pairs with a few blocks each)
+template <int DH, int NS>
+__global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_ring(AttnDecodeArgs a) {
   trace_point(30);
+  constexpr int kRingStages = NS;
   constexpr int NW = kRingThreads / 32;
   constexpr int FPL = DH / 32;
   constexpr int LPK = DH / 8, KPW = 32 / LPK;
   constexpr int BLK_BYTES = kRingBlock * DH * 2;
   __shared__ float q[DH];
-  __shared__ float p[kRingMaxKeys + 1];
   __shared__ float red[NW];
   __shared__ float opart[NW][DH];
   __shared__ int last;
   __shared__ __align__(8) uint64_t bars[kRingStages];
   __shared__ __align__(16) __half knew[DH];
   __shared__ __align__(16) __half vnew[DH];
-  extern __shared__ __align__(128) __half ring[];  // [kRingStages][kRingBlock][DH]
+  extern __shared__ __align__(128) __half ring[];  // [kRingStages][kRingBlock][DH], then p
+  float* p = reinterpret_cast<float*>(ring + kRingStages * kRingBlock * DH);  // [split_keys + 1] scores
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int len = a.cache_len[b];
@@ -1836,7 +1838,12 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   static const int ring = [] { const char* e = getenv("GLM_ATTN_RING"); return e ? atoi(e) : 2; }();
   if (ring && (a.max_ctx > kSplitKeys || (ring == 2 && B > 2) || ring == 3) && (a.dh == 128 || a.dh == 64)) {
     // long caches: about two streaming CTAs per SM (k_attn_decode_ring), splits of 64-key blocks
-    static const int cps = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 2; }();
+    // long caches: 4-stage rings, GLM_ATTN_RING_CPS (2) CTAs per SM; short caches of many
+    // sequences: 2-stage rings, five CTAs per SM
+    static const int cps_env = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 0; }();
+    const bool long_ctx = a.max_ctx > kSplitKeys;
+    const int ns = long_ctx ? 4 : 2;
+    const int cps = cps_env > 0 ? cps_env : (long_ctx ? 2 : 5);
     const int64_t ctas = static_cast<int64_t>(a.heads) * B;
     const int64_t nsplit = std::max<int64_t>(1, cps * 148 / ctas);
     int64_t sk = (a.max_ctx + nsplit - 1) / nsplit;
@@ -1844,15 +1851,25 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
     a.split_keys = static_cast<int>(sk);
     a.stage_keys = 0;
     const dim3 grid(a.heads, B, (a.max_ctx + a.split_keys - 1) / a.split_keys);
-    const size_t smem = static_cast<size_t>(kRingStages) * kRingBlock * a.dh * 2;
+    // p: the split's scores (sk + 1), later the merge weights of up to ceil(max_ctx / sk) splits
+    const int64_t pn = std::max<int64_t>(sk + 1, (a.max_ctx + sk - 1) / sk) + 3;
+    const size_t smem = static_cast<size_t>(ns) * kRingBlock * a.dh * 2 + pn * 4;
     static bool attr_r = false;
     if (!attr_r) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingStages * kRingBlock * 128 * 2));
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingStages * kRingBlock * 64 * 2));
+      const int mx4 = 4 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4, mx2 = 2 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4;
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
       attr_r = true;
     }
-    if (a.dh == 128) launch_k(k_attn_decode_ring<128>, grid, dim3(kRingThreads), smem, st, a);
-    else launch_k(k_attn_decode_ring<64>, grid, dim3(kRingThreads), smem, st, a);
+    if (ns == 4) {
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 4>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 4>, grid, dim3(kRingThreads), smem, st, a);
+    } else {
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 2>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 2>, grid, dim3(kRingThreads), smem, st, a);
+    }
     LAUNCH_CHECK("k_attn_decode_ring");
     return;
   }

@@ -53,8 +53,9 @@ w = w[np.argsort(t[w])]
 inst = []
 blk = ((rec[:, 1] >> 8) & 0xFFFFFF).astype(np.int64)
 for i in w:
+    # a GEMV CTA id seen twice starts the next launch (grids of other kernels are 3-D: no dedupe)
     if (inst and inst[-1]["fam"] == fam[i] and t[i] - inst[-1]["wait_last"] < 20000
-            and blk[i] not in inst[-1]["blocks"]):
+            and (fam[i] != 10 or blk[i] not in inst[-1]["blocks"])):
         inst[-1]["wait_last"] = t[i]
         inst[-1]["n"] += 1
         inst[-1]["blocks"].add(blk[i])
