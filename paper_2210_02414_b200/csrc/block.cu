@@ -1654,6 +1654,7 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
     }
   }
   __syncthreads();
+  trace_point(33);
   // ---- scores over the K blocks (LPK lanes per key, one 16-byte load each) ----
   const int sub = lane % LPK, kin = lane / LPK;
   float qr[8];
@@ -1693,6 +1694,7 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
     if (lane == 0) p[n_old] = score(acc);
   }
   __syncthreads();
+  trace_point(34);
   const int nk_all = n_old + (has_new ? 1 : 0);
   // ---- softmax over the split (fp32) ----
   float mx = -FLT_MAX;
@@ -1742,6 +1744,7 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
 #pragma unroll
   for (int f = 0; f < FPL; ++f) opart[warp][lane * FPL + f] = o[f];
   __syncthreads();
+  trace_point(35);
   if (total <= a.split_keys) {  // single active split: normalise, hand the row to out_proj
     const float inv = 1.f / sum;
     for (int c2 = threadIdx.x; c2 < DH / 2; c2 += kRingThreads) {
@@ -1758,6 +1761,7 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
         a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1 * inv;
       }
     }
+    trace_point(32);
     return;
   }
   for (int c = threadIdx.x; c < DH; c += kRingThreads) {
@@ -1780,7 +1784,10 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
     if (last) *ctr = 0;
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) {
+    trace_point(32);
+    return;
+  }
   __threadfence();
   const float* base = a.part + ((static_cast<int64_t>(b) * a.heads + head) * a.max_splits) * (DH + 2);
   float* wsp = p;
@@ -1814,6 +1821,7 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
       a.out[static_cast<int64_t>(b) * a.heads * DH + k + 1] = o1;
     }
   }
+  trace_point(32);
 }
 
 int attn_decode_split_keys(int max_ctx, int B) {
