@@ -135,8 +135,8 @@ __device__ __forceinline__ uint4 ld_nc(const uint4* p) {
 // Timeline tracer (diagnostics, tools/timeline.py): when a trace buffer is bound, thread 0
 // of every CTA appends (globaltimer ns, tag << 32 | block << 8 | smid) records. Each
 // translation unit has its own symbol, bound by trace_bind_all() (capi_quant.cpp).
-static __device__ unsigned long long* g_trace_buf = nullptr;
-static __device__ unsigned long long g_trace_cap = 0;
+static __constant__ unsigned long long* g_trace_buf = nullptr;  // constant bank: no global load at kernel entry
+static __constant__ unsigned long long g_trace_cap = 0;
 __device__ __forceinline__ void trace_point(unsigned tag) {
   unsigned long long* buf = g_trace_buf;
   if (buf == nullptr || threadIdx.x != 0) return;
