@@ -155,6 +155,42 @@ __device__ __forceinline__ RowStat block_stat(RowStat a, RowStat* red) {
 // Cluster-wide statistics: each CTA pushes its partial into slot[rank] of every CTA of the
 // cluster (distributed shared memory stores), one cluster barrier (release/acquire), then
 // every CTA merges its local slots in rank order: identical on every CTA and every run.
+// One-sided variant (k_deepnorm_ln): the partial goes to every CTA with st.async, which
+// completes on the destination's mbarrier; a CTA waits only for the CL arrivals on its own
+// barrier (initialised and published by a cluster barrier before the dependency wait), so
+// there is no cluster barrier (and no release of every earlier memory operation) on the path.
+template <int CL>
+__device__ __forceinline__ RowStat cluster_stat_async(RowStat v, RowStat* red, float4* slots, uint64_t* bar) {
+  v = warp_stat(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RowStat t = red[0];
+    for (int i = 1; i < kLnThreads / 32; ++i) t = stat_merge(t, red[i]);
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t lbar = smem_addr(bar), lslot = smem_addr(slots + rank);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lbar), "r"(CL * 16) : "memory");
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      uint32_t rslot, rbar;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rslot) : "r"(lslot), "r"(r));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lbar), "r"(r));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                       rslot),
+                   "r"(__float_as_uint(t.n)), "r"(__float_as_uint(t.mean)), "r"(__float_as_uint(t.m2)), "r"(0u), "r"(rbar)
+                   : "memory");
+    }
+  }
+  asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W_%=;\n}\n" ::"r"(
+                   smem_addr(bar))
+               : "memory");
+  RowStat r = RowStat{slots[0].x, slots[0].y, slots[0].z};
+  for (int i = 1; i < CL; ++i) r = stat_merge(r, RowStat{slots[i].x, slots[i].y, slots[i].z});
+  return r;
+}
+
 template <int CL>
 __device__ __forceinline__ RowStat cluster_stat(RowStat v, RowStat* red, RowStat* slots) {
   namespace cg = cooperative_groups;
@@ -249,9 +285,15 @@ template <int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kLnThreads) k_deepnorm_ln(LnArgs a) {
   trace_point(20);
   __shared__ RowStat red[kLnThreads / 32];
-  __shared__ RowStat slots[CL];
+  __shared__ float4 slots[CL];
+  __shared__ __align__(8) uint64_t sbar;
   namespace cg = cooperative_groups;
   const int rank = static_cast<int>(cg::this_cluster().block_rank());
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cg::this_cluster().sync();  // every CTA's statistics barrier exists before any st.async (pre-wait)
   const int m = blockIdx.x / CL;
   const int64_t npairs = a.d / 2;
   const int64_t per = (npairs + CL - 1) / CL;
@@ -335,7 +377,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kLnThreads) k_deepn
   }
   // one cluster reduction of (count, mean, M2); biased variance (tensor.cpp:267)
   trace_point(23);
-  const RowStat tot = cluster_stat<CL>(st.stat(), red, slots);
+  const RowStat tot = cluster_stat_async<CL>(st.stat(), red, slots, &sbar);
   trace_point(24);
   const float mean = tot.mean;
   const float var = tot.m2 / static_cast<float>(a.d);
