@@ -4,8 +4,10 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "collective.h"
@@ -254,7 +256,7 @@ void Collective::setup_peer(int max_b, int64_t d, cudaStream_t st) {
     cudaIpcMemHandle_t h;
     CUDA_CHECK(cudaIpcGetMemHandle(&h, peer_base_));
     void* dh = nullptr;
-    CUDA_CHECK(cudaMalloc(&dh, 64 * (size_ + 1)));
+    CUDA_CHECK(cudaMalloc(&dh, 64 * (size_ + 1) + 4 * (size_ + 1)));
     CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(dh) + 64 * size_, &h, 64, cudaMemcpyHostToDevice, st));
     if (!api().AllGather) fail(GLM_NCCL, "collective", "ncclAllGather not found in libnccl.so.2");
     check(api().AllGather(static_cast<uint8_t*>(dh) + 64 * size_, dh, 64, ncclUint8, static_cast<ncclComm_t>(comm_), st),
@@ -262,14 +264,43 @@ void Collective::setup_peer(int max_b, int64_t d, cudaStream_t st) {
     std::vector<cudaIpcMemHandle_t> hs(size_);
     CUDA_CHECK(cudaMemcpyAsync(hs.data(), dh, 64 * size_, cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
-    CUDA_CHECK(cudaFree(dh));
-    for (int r = 0; r < size_; ++r) {
+    // every rank maps every peer, then all agree (min over ranks) before any kernel relies on
+    // it: a rank that cannot map a peer turns the fused path off on every rank (NCCL decode)
+    int ok = 1;
+    std::string why;
+    for (int r = 0; r < size_ && ok; ++r) {
       if (r == rank_) {
         bases[r] = peer_base_;
         continue;
       }
-      CUDA_CHECK(cudaIpcOpenMemHandle(&peer_open_[r], hs[r], cudaIpcMemLazyEnablePeerAccess));
-      bases[r] = peer_open_[r];
+      const cudaError_t e = cudaIpcOpenMemHandle(&peer_open_[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        peer_open_[r] = nullptr;
+        ok = 0;
+        why = cudaGetErrorString(e);
+      } else {
+        bases[r] = peer_open_[r];
+      }
+    }
+    int* flag = reinterpret_cast<int*>(static_cast<uint8_t*>(dh) + 64 * (size_ + 1));
+    CUDA_CHECK(cudaMemcpyAsync(flag, &ok, 4, cudaMemcpyHostToDevice, st));
+    check(api().AllReduce(flag, flag, 1, ncclInt32, ncclMin, static_cast<ncclComm_t>(comm_), st), "ncclAllReduce(peer ok)");
+    CUDA_CHECK(cudaMemcpyAsync(&ok, flag, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    CUDA_CHECK(cudaFree(dh));
+    if (!ok) {
+      for (int r = 0; r < size_; ++r)
+        if (peer_open_[r]) {
+          cudaIpcCloseMemHandle(peer_open_[r]);
+          peer_open_[r] = nullptr;
+        }
+      cudaFree(peer_base_);
+      peer_base_ = nullptr;
+      peer_ = PeerArgs{};
+      fprintf(stderr, "[collective] rank %d: fused decode allreduce unavailable (%s); decode sums use NCCL\n", rank_,
+              why.empty() ? "a peer could not map the inboxes" : why.c_str());
+      return;
     }
   }
   PeerArgs p;
