@@ -11,7 +11,9 @@ the headline numbers are quoted on (BASELINE configs 2-5), against the CPU oracl
   (c) the quantized linear at the four G (K, N) shapes for M in {1, 16, 256, 2048, 8192} against
       x . dequantize(q) on 256 sampled output columns (quant.cpp:188-221 + tensor.cpp:135-155);
   (d) the bf16 tied head over the full 150528-token vocabulary (model.cpp:225) against the
-      oracle's h . E^T, batch 1 (fp32 h) and batch 2 (bf16 h on the tensor cores), argmax included.
+      oracle's h . E^T, batch 1 (fp32 h) and batch 2 (bf16 h on the tensor cores), argmax included;
+  (e) batched decode of 8 sequences through one G block (multi-token integer-MMA GEMV, streaming
+      attention of 3+ sequences) against the oracle block of each sequence.
 """
 import numpy as np
 import pytest
@@ -61,9 +63,9 @@ def test_synthetic_init_codes_bit_exact_70_layers(axis):
     del m
 
 
-def g_block(bits, axis, seed, max_ctx, head_bf16=False):
+def g_block(bits, axis, seed, max_ctx, head_bf16=False, max_batch=2):
     m = glm.Model(glm.GLMConfig(num_layers=1, hidden=D, num_heads=H, ffn_hidden=F, vocab=V), bits=bits, axis=axis,
-                  max_ctx=max_ctx, max_batch=2, head_bf16=head_bf16)
+                  max_ctx=max_ctx, max_batch=max_batch, head_bf16=head_bf16)
     m.init_synthetic(seed)
     return m
 
@@ -101,6 +103,41 @@ def test_g_block_prefill_and_decode_match_oracle(bits, axis, n):
         for got, ref, name in ((tag, attn[sl], "attention"), (tfg, ff[sl], "geglu"), (yg, out[sl], "block output")):
             err = np.abs(got.astype(np.float64) - ref).max()
             assert err <= 1e-2 * np.abs(ref).max(), (name, sl, err, np.abs(ref).max())
+
+
+def test_g_block_batched_decode_8_sequences_match_oracle():
+    """Batched decode at the G shape (the rows behind the batch sweep): one G block, 8 sequences
+    with their own prefixes (21..84 tokens) prefilled into their caches, then two decode steps of
+    8 rows each — the multi-token integer-MMA GEMV (k_gemv_mk_i4, M = 8) and the streaming
+    attention of 3+ sequences (k_attn_decode_ring) — against the oracle block per sequence."""
+    seed, bits, axis, B = 91, 4, "column", 8
+    m = g_block(bits, axis, seed, max_ctx=96, max_batch=B)
+    W = {w: O.dequantize(oracle_linear(seed, 1, 0, w, bits, axis)) for w in range(5)}
+    ones, zeros = np.ones(D), np.zeros(D)
+    rng = np.random.default_rng(B)
+    lens = [21 + 9 * b for b in range(B)]
+    xs, ref_out, ref_attn = [], [], []
+    for b, n in enumerate(lens):
+        N = n + 2
+        x = rng.normal(0.0, 1.0, size=(N, D))
+        pos = list(range(n - 1)) + [n - 1, n - 1, n]  # prefix, [gMASK] at n-1, two generated rows
+        mask = np.arange(N)[None, :] < np.maximum(n, np.arange(N)[:, None] + 1)
+        out, attn, _ff = O.block_forward(x, W, (ones, zeros, ones, zeros), pos, mask, H, alpha=np.sqrt(2.0))
+        xs.append((x, pos))
+        ref_out.append(out[n:])
+        ref_attn.append(attn[n:])
+        m.block_forward(0, x[:n].astype(np.float32), pos[:n], "prefill", seq=b, context_length=n)
+    del W
+    m.enable_taps(True)
+    for j in range(2):
+        rows = np.stack([xs[b][0][lens[b] + j] for b in range(B)]).astype(np.float32)
+        pos = [xs[b][1][lens[b] + j] for b in range(B)]
+        y = m.block_forward(0, rows, pos, "decode")
+        ta, _tf = m.taps(B)
+        for b in range(B):
+            for got, ref, name in ((ta[0][b], ref_attn[b][j], "attention"), (y[b], ref_out[b][j], "block output")):
+                err = np.abs(got.astype(np.float64) - ref).max()
+                assert err <= 1e-2 * np.abs(ref).max(), (name, b, j, err, np.abs(ref).max())
 
 
 G_SHAPES = [(D, 3 * D), (D, D), (D, F), (F, D)]
