@@ -1586,10 +1586,10 @@ constexpr int kRingBlock = 64;
 constexpr int kRingMaxKeys = 2048;
 constexpr int kRingThreads = 256;
 
-// NS ring stages: 4 for long caches (two CTAs per SM), 2 for short ones (five per SM: many
+// NS ring stages: 4 for long caches (two CTAs per SM), 2 for short ones (5-6 per SM: many
 // (head, sequence) pairs with a few blocks each)
-template <int DH, int NS>
-__global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_ring(AttnDecodeArgs a) {
+template <int DH, int NS, int MINB>
+__global__ void __launch_bounds__(kRingThreads, MINB) k_attn_decode_ring(AttnDecodeArgs a) {
   trace_point(30);
   constexpr int kRingStages = NS;
   constexpr int NW = kRingThreads / 32;
@@ -1598,13 +1598,15 @@ __global__ void __launch_bounds__(kRingThreads, NS == 2 ? 5 : 2) k_attn_decode_r
   constexpr int BLK_BYTES = kRingBlock * DH * 2;
   __shared__ float q[DH];
   __shared__ float red[NW];
-  __shared__ float opart[NW][DH];
   __shared__ int last;
   __shared__ __align__(8) uint64_t bars[kRingStages];
   __shared__ __align__(16) __half knew[DH];
   __shared__ __align__(16) __half vnew[DH];
   extern __shared__ __align__(128) __half ring[];  // [kRingStages][kRingBlock][DH], then p
   float* p = reinterpret_cast<float*>(ring + kRingStages * kRingBlock * DH);  // [split_keys + 1] scores
+  // per-warp P.V partials reuse the ring once every block is consumed (NW * DH floats <= one stage)
+  static_assert(NW * DH * 4 <= kRingBlock * DH * 2 * NS, "P.V partials fit the ring");
+  float (*opart)[DH] = reinterpret_cast<float (*)[DH]>(ring);
   const int head = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int len = a.cache_len[b];
@@ -1889,7 +1891,7 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   if (ring && (a.max_ctx > kSplitKeys || (ring == 2 && B > 2) || ring == 3) && (a.dh == 128 || a.dh == 64)) {
     // long caches: about two streaming CTAs per SM (k_attn_decode_ring), splits of 64-key blocks
     // long caches: 4-stage rings, GLM_ATTN_RING_CPS (2) CTAs per SM; short caches of many
-    // sequences: 2-stage rings, five CTAs per SM
+    // sequences: 2-stage rings, five or six CTAs per SM
     static const int cps_env = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 0; }();
     const bool long_ctx = a.max_ctx > kSplitKeys;
     const int ns = long_ctx ? 4 : 2;
@@ -1907,18 +1909,25 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
     static bool attr_r = false;
     if (!attr_r) {
       const int mx4 = 4 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4, mx2 = 2 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4;
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
+      for (auto k : {k_attn_decode_ring<128, 2, 5>, k_attn_decode_ring<64, 2, 5>, k_attn_decode_ring<128, 2, 6>,
+                     k_attn_decode_ring<64, 2, 6>})
+        CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
       attr_r = true;
     }
+    // short caches: six resident CTAs per SM (40 registers) once the grid exceeds one wave at
+    // five (B = 8: +1.5 %); smaller grids keep the five-CTA build (B = 3 / 4: -0.8 / -0.5 % at six)
+    const bool six = static_cast<int64_t>(grid.x) * grid.y * grid.z > 5 * 148;
     if (ns == 4) {
-      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 4>, grid, dim3(kRingThreads), smem, st, a);
-      else launch_k(k_attn_decode_ring<64, 4>, grid, dim3(kRingThreads), smem, st, a);
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 4, 2>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 4, 2>, grid, dim3(kRingThreads), smem, st, a);
+    } else if (six) {
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 2, 6>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 2, 6>, grid, dim3(kRingThreads), smem, st, a);
     } else {
-      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 2>, grid, dim3(kRingThreads), smem, st, a);
-      else launch_k(k_attn_decode_ring<64, 2>, grid, dim3(kRingThreads), smem, st, a);
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 2, 5>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 2, 5>, grid, dim3(kRingThreads), smem, st, a);
     }
     LAUNCH_CHECK("k_attn_decode_ring");
     return;
