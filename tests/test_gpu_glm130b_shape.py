@@ -13,7 +13,8 @@ the headline numbers are quoted on (BASELINE configs 2-5), against the CPU oracl
   (d) the bf16 tied head over the full 150528-token vocabulary (model.cpp:225) against the
       oracle's h . E^T, batch 1 (fp32 h) and batch 2 (bf16 h on the tensor cores), argmax included;
   (e) batched decode of 8 sequences through one G block (multi-token integer-MMA GEMV, streaming
-      attention of 3+ sequences) against the oracle block of each sequence.
+      attention of 3+ sequences) against the oracle block of each sequence;
+  (f) one G block under Megatron tensor parallelism at t = 4 and 8 (emulated group on one GPU).
 """
 import numpy as np
 import pytest
@@ -138,6 +139,49 @@ def test_g_block_batched_decode_8_sequences_match_oracle():
             for got, ref, name in ((ta[0][b], ref_attn[b][j], "attention"), (y[b], ref_out[b][j], "block output")):
                 err = np.abs(got.astype(np.float64) - ref).max()
                 assert err <= 1e-2 * np.abs(ref).max(), (name, b, j, err, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("t", [4, 8])
+def test_g_block_tensor_parallel_matches_oracle(t):
+    """Megatron tensor parallelism at the G shape: t rank-models of one GLM-130B block (heads
+    96 / t, ffn 32768 / t per rank, INT4 kColumn synthetic weights quantized on the full
+    matrices) on one GPU through the emulated group, prefill (allreduce after out_proj / ffn_w2)
+    and decode (the fused push / sum inside the LayerNorm) via glm_block_forward, against the
+    oracle block; every rank holds the same output."""
+    seed, bits, axis, n = 92, 4, "column", 64
+    group = glm.EmulatedGroup(t)
+    ms = [glm.Model(glm.GLMConfig(num_layers=1, hidden=D, num_heads=H, ffn_hidden=F, vocab=1024), bits=bits,
+                    axis=axis, max_ctx=n + 4, tp_rank=r, tp_size=t) for r in range(t)]
+    glm.run_ranks([lambda m=m: m.init_comm_emulated(group) for m in ms])
+    for m in ms:
+        m.init_synthetic(seed)
+    W = {w: O.dequantize(oracle_linear(seed, 1, 0, w, bits, axis)) for w in range(5)}
+    ones, zeros = np.ones(D), np.zeros(D)
+    N = n + 2
+    rng = np.random.default_rng(t)
+    x = rng.normal(0.0, 1.0, size=(N, D))
+    pos = list(range(n - 1)) + [n - 1, n - 1, n]
+    mask = np.arange(N)[None, :] < np.maximum(n, np.arange(N)[:, None] + 1)
+    out, attn, ff = O.block_forward(x, W, (ones, zeros, ones, zeros), pos, mask, H, alpha=np.sqrt(2.0))
+    del W
+    for m in ms:
+        m.enable_taps(True)
+    res = glm.run_ranks([lambda m=m: (m.block_forward(0, x[:n].astype(np.float32), pos[:n], "prefill", seq=0,
+                                                      context_length=n), m.taps(n)) for m in ms])
+    rows = [(res[0][0], res[0][1][0][0], res[0][1][1][0], slice(0, n))]
+    for r in range(1, t):
+        assert np.array_equal(res[r][0], res[0][0])
+    for j in range(2):
+        rr = glm.run_ranks([lambda m=m: (m.block_forward(0, x[n + j:n + j + 1].astype(np.float32), pos[n + j:n + j + 1],
+                                                         "decode"), m.taps(1)) for m in ms])
+        for r in range(1, t):
+            assert np.array_equal(rr[r][0], rr[0][0])
+        rows.append((rr[0][0], rr[0][1][0][0], rr[0][1][1][0], slice(n + j, n + j + 1)))
+    for yg, tag, tfg, sl in rows:
+        for got, ref, name in ((tag, attn[sl], "attention"), (tfg, ff[sl], "geglu"), (yg, out[sl], "block output")):
+            err = np.abs(got.astype(np.float64) - ref).max()
+            assert err <= 1e-2 * np.abs(ref).max(), (t, name, sl, err, np.abs(ref).max())
+    del ms, group
 
 
 G_SHAPES = [(D, 3 * D), (D, D), (D, F), (F, D)]
