@@ -225,6 +225,18 @@ def cpu_baseline_port(steps, warmup):
     }
 
 
+DTYPE = "int4 x s16 (u8 x s8 IMMA digits, int32 accumulate)"
+
+
+def workload_config(B, world, warmup):
+    """The workload both arms report (BASELINE configs[3] at batch B on `world` GPUs)."""
+    return {"workload": "GLM-130B-shaped 70-layer INT4 decode (BASELINE configs[3]): hidden 12288, 96 heads, "
+                        "ffn 32768 (GeGLU), vocab 150528, random-init counter-based weights (model.cpp:69-104 stds), "
+                        "absmax INT4 per output channel (kColumn)",
+            "global_batch": B, "seq_len": PROMPT + 2, "context_at_timing": PROMPT + 2 + 3 + warmup + SETTLE,
+            "parallelism": f"tp{world}", "l2": "inputs larger than L2 (63.4 GB of weights over the ranks)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -233,10 +245,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_token"] * 1000.0,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode, batch 1 (the reference's CPU path; one layer "
-                                   "per step, extrapolated x70 + head)",
-                       "model": "GLM-130B-shaped (70L, d 12288, 96 heads, ffn 32768, vocab 150528)",
-                       "global_batch": 1, "seq_len": PROMPT + 2, "parallelism": "cpu"},
+            "config": workload_config(1, args.gpus, args.warmup),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -344,15 +353,10 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "w4a16 (int4 weights; fp16 activations as 16-bit fixed-point digits on the integer MMA, exact int32 "
-                 "accumulation; fp32 residual / LayerNorm)", "data": "synthetic",
-        "config": {"workload": "GLM-130B-shaped 70-layer INT4 decode (BASELINE configs[3])",
-                   "model": "GLM-130B shape: 70 layers, hidden 12288, 96 heads, ffn 32768 (GeGLU), vocab 150528, "
-                            "random-init (counter-based, model.cpp:69-104 stds)",
-                   "quantization": "absmax INT4 per output channel (kColumn), bit-exact codes",
-                   "global_batch": B, "seq_len": PROMPT + 2, "context_at_timing": PROMPT + 2 + 3 + args.warmup + SETTLE,
-                   "parallelism": f"tp{world}", "l2": "inputs larger than L2 (63.4 GB weights / rank count)",
-                   "frac_of_weight_roofline": roofline_step_ms / ms},
+        "dtype": DTYPE, "data": "synthetic",
+        "precision": "W4A16: int4 weight codes x fp16 activations re-expressed as exact 16-bit fixed-point digits on "
+                     "the integer MMA (int32 accumulation); fp32 residual / LayerNorm; bf16 tied head",
+        "config": dict(workload_config(B, world, args.warmup), frac_of_weight_roofline=roofline_step_ms / ms),
         "e2e": {"value": e2e_tps, "unit": "tokens/s", "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": 4 * B,
                 "steps": args.e2e_steps},
         "gpu_launches": launches * args.steps,
