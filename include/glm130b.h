@@ -120,6 +120,9 @@ glm_status glm_debug_qmm_trace(long long* host_out);
  * quantizes activations per (token, k-split) on 64-element chunk boundaries
  * chunk = nch * s / ksplit); out[2]: nch, the 64-element chunks along K. Host only, no launch. */
 glm_status glm_debug_gemv_plan(const glm_qweight* q, int64_t M, int32_t* out);
+/* The same plan for a [rows, cols] weight of `bits` without a handle (host only, no device
+ * needed): out[0..2] as above, out[3] the launch's CTA count. */
+glm_status glm_debug_plan_shape(int64_t rows, int64_t cols, int bits, int64_t M, int32_t* out);
 
 /* Diagnostics: device timeline. While a trace runs, thread 0 of every CTA of the decode
  * kernels appends (globaltimer ns, tag << 32 | block << 8 | smid) pairs; stop copies up to

@@ -361,21 +361,37 @@ glm_status glm_debug_qmm_trace(long long* host_out) {
   });
 }
 
+static void plan_summary(const QLayout& L, int64_t M, int32_t* out) {
+  if (M >= qmm_min_rows()) {
+    const GemvPlan p = plan_qmm(L, static_cast<int>(M));
+    out[0] = 5;
+    out[1] = p.ksplit;
+    out[3] = p.grid;
+  } else {
+    const GemvPlan p = plan_gemv(L, static_cast<int>(M));
+    out[0] = gemv_kind(L.nch, static_cast<int>(M), L.bits);
+    out[1] = p.ksplit;
+    out[3] = p.grid;
+  }
+  out[2] = static_cast<int32_t>(L.nch);
+}
+
 glm_status glm_debug_gemv_plan(const glm_qweight* q, int64_t M, int32_t* out) {
   return guarded([&] {
     if (!q || !out) fail(GLM_CONTRACT, "qlinear", "null argument");
     if (M < 1) fail(GLM_DIMENSION, "qlinear", "M must be >= 1");
-    const QLayout& L = q->w.L;
-    if (M >= qmm_min_rows()) {
-      const GemvPlan p = plan_qmm(L, static_cast<int>(M));
-      out[0] = 5;
-      out[1] = p.ksplit;
-    } else {
-      const GemvPlan p = plan_gemv(L, static_cast<int>(M));
-      out[0] = gemv_kind(L.nch, static_cast<int>(M), L.bits);
-      out[1] = p.ksplit;
-    }
-    out[2] = static_cast<int32_t>(L.nch);
+    int32_t o[4];
+    plan_summary(q->w.L, M, o);
+    for (int i = 0; i < 3; ++i) out[i] = o[i];
+  });
+}
+
+glm_status glm_debug_plan_shape(int64_t rows, int64_t cols, int bits, int64_t M, int32_t* out) {
+  return guarded([&] {
+    if (!out) fail(GLM_CONTRACT, "qlinear", "null argument");
+    if (M < 1 || rows < 1 || cols < 1) fail(GLM_DIMENSION, "qlinear", "M, rows and cols must be >= 1");
+    if (bits != 4 && bits != 8) fail(GLM_CONTRACT, "quantlab", "bit width must be 4 or 8");
+    plan_summary(make_layout(rows, cols, bits), M, out);
   });
 }
 

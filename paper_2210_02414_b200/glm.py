@@ -87,6 +87,7 @@ SIGNATURES = {
     "glm_qweight_device_copy": (I32, [P, P]),
     "glm_debug_qmm_trace": (I32, [P]),
     "glm_debug_gemv_plan": (I32, [P, I64, P]),
+    "glm_debug_plan_shape": (I32, [I64, I64, I32, I64, P]),
     "glm_qlinear": (I32, [P, P, I64, P, P]),
     "glm_qlinear_host": (I32, [P, P, I64, P]),
     "glm_qlinear_bench": (I32, [P, I64, I32, I32, C.POINTER(D)]),
@@ -328,6 +329,13 @@ class QLinear:
         out = np.zeros(3, np.int32)
         _check(lib().glm_debug_gemv_plan(self.h, M, _p(out)))
         return self.GEMV_KINDS[out[0]], int(out[1]), int(out[2])
+
+    @classmethod
+    def plan_for(cls, rows, cols, bits, M):
+        """(kernel, ksplit, nch, grid) of a [rows, cols] weight for M rows (host only)."""
+        out = np.zeros(4, np.int32)
+        _check(lib().glm_debug_plan_shape(rows, cols, bits, M, _p(out)))
+        return cls.GEMV_KINDS[out[0]], int(out[1]), int(out[2]), int(out[3])
 
     def bench(self, M, iters=20, flush=True):
         us = C.c_double()
