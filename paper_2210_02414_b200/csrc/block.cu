@@ -1575,8 +1575,8 @@ void launch_geglu_act(const ActArgs& a, cudaStream_t st) {
 // caches (batch sweep, same box: B = 4 251 -> 280, B = 8 429 -> 454 tok/s; B = 16 662 -> 643, so
 // not there). GLM_ATTN_SPLIT64=0 keeps the 256-key unstaged CTAs at 3..8 sequences.
 // ---- long-context decode attention: one CTA streams a long key range -----------------
-// grid (heads, batch, splits) with split_keys = a multiple of 64 chosen so about two CTAs per SM
-// cover the caches (attn_decode_ring_split_keys): the split's cached keys pass through a ring
+// grid (heads, batch, splits) with split_keys = a multiple of 64 chosen so a target number of
+// CTAs per SM cover the caches (launch_attn_decode): the split's cached keys pass through a ring
 // of kRingStages 64-key shared-memory blocks (one bulk copy each, the first ones issued before
 // the dependency wait): all K blocks for the scores (kept in shared memory, up to
 // kRingMaxKeys), then the V blocks for P.V, so K and V are read once at HBM speed instead of
