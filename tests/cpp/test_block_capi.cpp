@@ -3,7 +3,8 @@
 //   * deepnorm_residual / attention / geglu op by op (model.hpp:70-80, model.cpp:125-152)
 //   * the layer-by-layer block API (glm_block_forward, model.cpp:198-224) chained over every
 //     layer of the tiny config from the embedding rows: each layer's sublayer taps equal the
-//     oracle forward's (or_forward taps), prefill rows and teacher-forced decode rows
+//     oracle forward's (or_forward taps), prefill rows and teacher-forced decode rows, for an
+//     absmax and a zeropoint model (QuantizedModel(..., QuantScheme::kZeropoint))
 // Built and run by tests/test_gpu_cpp.py.
 #include <cmath>
 #include <cstdio>
@@ -126,7 +127,8 @@ static void geglu_op() {
 }
 
 // The block API chained over the layers == the reference forward's per-layer sublayers.
-static void block_chain() {
+// (scheme: QuantPolicy::scheme of the model and of the oracle's quantize_model)
+static void block_chain(QuantScheme scheme) {
   const int L = 4, d = 512, H = 8, V = 262, P = 60, G = 3;
   or_config oc{L, d, H, 0, V, 0.0, 0.0, 0.0};
   or_params* p = or_params_init_reference(&oc, 1234);
@@ -135,7 +137,7 @@ static void block_chain() {
   cfg.hidden = d;
   cfg.num_heads = H;
   cfg.vocab = V;
-  QuantizedModel m(cfg, 4, GroupAxis::kColumn, 1, 128);
+  QuantizedModel m(cfg, 4, GroupAxis::kColumn, 1, 128, false, 0, 1, scheme);
   int64_t rows = 0, cols = 0;
   or_params_shape(p, OR_EMBED, &rows, &cols);
   const double* E = or_params_tensor(p, 0, OR_EMBED);
@@ -151,7 +153,7 @@ static void block_chain() {
     m.set_tensor(l, 7, std::vector<double>(d, 1.0));
     m.set_tensor(l, 8, std::vector<double>(d, 0.0));
   }
-  CHECK(or_params_quantize(p, 4, OR_ABSMAX, OR_AXIS_COLUMN) == 0);
+  CHECK(or_params_quantize(p, 4, scheme == QuantScheme::kZeropoint ? OR_ZEROPOINT : OR_ABSMAX, OR_AXIS_COLUMN) == 0);
   // gMASK sample (corruption.cpp:249-293): prefix, [gMASK], [sop] + generated tokens
   std::vector<int> toks, pos, span_id, span_off, seg;
   for (int i = 0; i < P; ++i) toks.push_back(6 + (37 * i + 11) % 256), pos.push_back(i), span_id.push_back(-1), span_off.push_back(-1);
@@ -179,7 +181,8 @@ static void block_chain() {
     std::vector<double> ra(at.begin() + static_cast<size_t>(l) * n * d, at.begin() + static_cast<size_t>(l) * n * d + static_cast<size_t>(C) * d);
     std::vector<double> rf(ft.begin() + static_cast<size_t>(l) * n * d, ft.begin() + static_cast<size_t>(l) * n * d + static_cast<size_t>(C) * d);
     const double ea = max_diff(ta, ra, ra.size(), static_cast<size_t>(l) * C * d), ef = max_diff(tf, rf, rf.size(), static_cast<size_t>(l) * C * d);
-    std::printf("prefill layer %d: attn tap err %.2e (max %.2e), ffn tap err %.2e (max %.2e)\n", l, ea, max_abs(ra), ef, max_abs(rf));
+    std::printf("%s prefill layer %d: attn tap err %.2e (max %.2e), ffn tap err %.2e (max %.2e)\n",
+                scheme == QuantScheme::kZeropoint ? "zeropoint" : "absmax", l, ea, max_abs(ra), ef, max_abs(rf));
     CHECK(ea <= 1e-2 * max_abs(ra));
     CHECK(ef <= 1e-2 * max_abs(rf));
   }
@@ -203,7 +206,8 @@ int main() {
   deepnorm_op();
   attention_op();
   geglu_op();
-  block_chain();
+  block_chain(QuantScheme::kAbsmax);
+  block_chain(QuantScheme::kZeropoint);
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
