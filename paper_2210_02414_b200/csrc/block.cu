@@ -1889,12 +1889,12 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
   // sequences keep the 256-key staged CTAs: always-ring 80.1 vs 80.6 tok/s at batch 1)
   static const int ring = [] { const char* e = getenv("GLM_ATTN_RING"); return e ? atoi(e) : 2; }();
   if (ring && (a.max_ctx > kSplitKeys || (ring == 2 && B > 2) || ring == 3) && (a.dh == 128 || a.dh == 64)) {
-    // long caches: about two streaming CTAs per SM (k_attn_decode_ring), splits of 64-key blocks
-    // long caches: 4-stage rings, GLM_ATTN_RING_CPS (2) CTAs per SM; short caches of many
+    // long caches: 6-stage rings of 64-key blocks, GLM_ATTN_RING_CPS (2) streaming CTAs per SM
+    // (4 / 6 / 8 stages: 0.2054 / 0.2036 / 0.2173 ms at config 2); short caches of many
     // sequences: 2-stage rings, five or six CTAs per SM
     static const int cps_env = [] { const char* e = getenv("GLM_ATTN_RING_CPS"); return e ? atoi(e) : 0; }();
     const bool long_ctx = a.max_ctx > kSplitKeys;
-    const int ns = long_ctx ? 4 : 2;
+    const int ns = long_ctx ? 6 : 2;
     const int cps = cps_env > 0 ? cps_env : (long_ctx ? 2 : 5);
     const int64_t ctas = static_cast<int64_t>(a.heads) * B;
     const int64_t nsplit = std::max<int64_t>(1, cps * 148 / ctas);
@@ -1908,9 +1908,9 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(ns) * kRingBlock * a.dh * 2 + pn * 4;
     static bool attr_r = false;
     if (!attr_r) {
-      const int mx4 = 4 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4, mx2 = 2 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4;
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
-      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx4));
+      const int mxl = 6 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4, mx2 = 2 * kRingBlock * 128 * 2 + (kRingMaxKeys + 260) * 4;
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<128, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxl));
+      CUDA_CHECK(cudaFuncSetAttribute(k_attn_decode_ring<64, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mxl));
       for (auto k : {k_attn_decode_ring<128, 2, 5>, k_attn_decode_ring<64, 2, 5>, k_attn_decode_ring<128, 2, 6>,
                      k_attn_decode_ring<64, 2, 6>})
         CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx2));
@@ -1919,9 +1919,9 @@ void launch_attn_decode(const AttnDecodeArgs& in, int B, cudaStream_t st) {
     // short caches: six resident CTAs per SM (40 registers) once the grid exceeds one wave at
     // five (B = 8: +1.5 %); smaller grids keep the five-CTA build (B = 3 / 4: -0.8 / -0.5 % at six)
     const bool six = static_cast<int64_t>(grid.x) * grid.y * grid.z > 5 * 148;
-    if (ns == 4) {
-      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 4, 2>, grid, dim3(kRingThreads), smem, st, a);
-      else launch_k(k_attn_decode_ring<64, 4, 2>, grid, dim3(kRingThreads), smem, st, a);
+    if (long_ctx) {
+      if (a.dh == 128) launch_k(k_attn_decode_ring<128, 6, 2>, grid, dim3(kRingThreads), smem, st, a);
+      else launch_k(k_attn_decode_ring<64, 6, 2>, grid, dim3(kRingThreads), smem, st, a);
     } else if (six) {
       if (a.dh == 128) launch_k(k_attn_decode_ring<128, 2, 6>, grid, dim3(kRingThreads), smem, st, a);
       else launch_k(k_attn_decode_ring<64, 2, 6>, grid, dim3(kRingThreads), smem, st, a);
