@@ -369,7 +369,7 @@ static void plan_summary(const QLayout& L, int64_t M, int32_t* out) {
     out[3] = p.grid;
   } else {
     const GemvPlan p = plan_gemv(L, static_cast<int>(M));
-    out[0] = gemv_kind(L.nch, static_cast<int>(M), L.bits);
+    out[0] = gemv_kind(p, L.nch, static_cast<int>(M), L.bits);
     out[1] = p.ksplit;
     out[3] = p.grid;
   }
@@ -406,6 +406,7 @@ glm_status glm_debug_trace_start(int64_t capacity) {
     trace_bind_gemv(g_trace_dev, capacity);
     trace_bind_block(g_trace_dev, capacity);
     trace_bind_model(g_trace_dev, capacity);
+    trace_bind_gemv_tc(g_trace_dev, capacity);
   });
 }
 
@@ -422,6 +423,7 @@ glm_status glm_debug_trace_stop(uint64_t* host_out, int64_t capacity, int64_t* c
     trace_bind_gemv(nullptr, 0);
     trace_bind_block(nullptr, 0);
     trace_bind_model(nullptr, 0);
+    trace_bind_gemv_tc(nullptr, 0);
     cudaFree(g_trace_dev);
     g_trace_dev = nullptr;
   });

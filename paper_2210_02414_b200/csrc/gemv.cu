@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "digits.cuh"
 
 namespace glm {
 
@@ -768,41 +769,6 @@ __device__ __forceinline__ void compute_chunk_i4(const uint4& wv, const uint4& x
   imma16832(acc1, wv.z & 0x0F0F0F0Fu, wv.z & 0xF0F0F0F0u, wv.w & 0x0F0F0F0Fu, wv.w & 0xF0F0F0F0u, xv.z, xv.w);
 }
 
-constexpr float kDigitQ = 32512.f;  // 127 * 256: keeps the balanced hi digit in [-127, 127]
-
-// One 16-k group of fragment-ordered fp16 activations (32 B, halves [j][2t, 2t+1, 2t+8, 2t+9])
-// -> 16 hi digits | 16 lo digits in weight-word byte order ([j][2t, 2t+8, 2t+1, 2t+9]); returns
-// the sum of the group's x_int. x_int = rint(x * inv_s) of the exact product (one FFMA onto the
-// 1.5 * 2^23 + 128 magic: |x_int| <= 32512 < 2^22, so the sum rounds to the nearest even integer
-// and its float bits are 0x4B400000 + x_int + 128); the low 16 bits u = x_int + 128 hold lo + 128
-// in the low byte and hi in the next (two's complement), so two PRMT levels gather the 4 lo / 4
-// hi bytes of a word and one LOP flips lo's sign bit; the x_int sum is 256 * sum(hi) + sum(lo)
-// from two dp4a per word.
-__device__ __forceinline__ int digits_group(uint4* p, float inv_s) {
-  const uint4 h0 = p[0], h1 = p[1];
-  const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-  constexpr float kMagic = 12583040.f;  // 1.5 * 2^23 + 128
-  uint32_t hi[4], lo[4];
-  int shi = 0, slo = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j]));
-    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * j + 1]));
-    const float fq[4] = {f01.x, f23.x, f01.y, f23.y};  // byte order 2t, 2t+8, 2t+1, 2t+9
-    uint32_t u[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) u[q] = __float_as_uint(__fmaf_rn(fq[q], inv_s, kMagic));
-    const uint32_t t01 = __byte_perm(u[0], u[1], 0x5410), t23 = __byte_perm(u[2], u[3], 0x5410);
-    lo[j] = __byte_perm(t01, t23, 0x6420) ^ 0x80808080u;
-    hi[j] = __byte_perm(t01, t23, 0x7531);
-    shi = __dp4a(static_cast<int>(hi[j]), 0x01010101, shi);
-    slo = __dp4a(static_cast<int>(lo[j]), 0x01010101, slo);
-  }
-  p[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-  p[1] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  return 256 * shi + slo;
-}
-
 // Row results of one item from the integer accumulators: rows g carry (code + 8), rows g + 8
 // carry 16 (code + 8), both against digits x_int = 256 hi + lo; S = sum of x_int over the item's
 // k-range removes the code offset exactly (int64: 256 * acc can exceed int32)
@@ -1363,8 +1329,41 @@ bool use_m1(int64_t nch, int M, int bits, int nx) {
 }
 }  // namespace
 
+// INT4 decode GEMVs of GLM_GEMV_TC = T .. 16 tokens run the tcgen05 kernel (gemv_tc.cu); off by
+// default (0): bit-identical to k_gemv_mk_i4 but slower on every GLM-130B shape (3.5-3.9 vs
+// 4.1-5.9 TB/s); it needs 128-feature tiles (always: Np % 128 == 0).
+int tc_min_tokens() {
+  static const int v = [] { const char* e = getenv("GLM_GEMV_TC"); return e ? atoi(e) : 0; }();
+  return v;
+}
+bool use_tc(int64_t nrt, int M, int bits) {
+  return bits == 4 && gemv_imma() && tc_min_tokens() > 0 && M >= tc_min_tokens() && M >= 2 && M <= 16 && nrt % 8 == 0;
+}
+
 GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
   GemvPlan p;
+  if (use_tc(nrt, M, bits)) {
+    // tcgen05 kernel: items of 128 features x one k-slice (<= kTcSliceChunks chunks), slice-major
+    // contiguous ranges of `per` items per CTA; the same k-split penalty as the IMMA kernel
+    p.tc = true;
+    p.warps = 14;
+    const int64_t ntiles = nrt / 8;
+    const int64_t ks_min = (nch + kTcSliceChunks - 1) / kTcSliceChunks;
+    double best = -1.0;
+    for (int64_t ks = ks_min; ks <= std::min<int64_t>(nch, ks_min + 24); ++ks) {
+      const int64_t items = ntiles * ks;
+      const int64_t per = (items + kNumSMs - 1) / kNumSMs;
+      const double eff = static_cast<double>(items) / static_cast<double>(per * kNumSMs) - 0.004 * static_cast<double>(ks);
+      if (eff > best + 1e-9) {
+        best = eff;
+        p.ksplit = static_cast<int>(ks);
+        p.per = static_cast<int>(per);
+      }
+    }
+    const int64_t items = ntiles * p.ksplit;
+    p.grid = static_cast<int>((items + p.per - 1) / p.per);
+    return p;
+  }
   if (M >= 2 && !use_m1(nch, M, bits, nx) && bits == 4 && gemv_imma() && nx * M <= 32) {
     // integer-MMA multi-token kernel: slice-major items, contiguous ranges of `per` items per
     // CTA, one resident activation slice (kMkXBytes) per CTA
@@ -1432,7 +1431,11 @@ GemvPlan plan_gemv(int64_t nrt, int64_t nch, int M, int bits, int nx) {
 
 GemvPlan plan_gemv(const QLayout& L, int M) { return plan_gemv(L.nrt, L.nch, M, L.bits, 1); }
 
-int gemv_kind(int64_t nch, int M, int bits, int nx) {  // mirrors gemv_launch's dispatch
+int gemv_kind(const GemvPlan& p, int64_t nch, int M, int bits, int nx) {
+  return p.tc ? kGemvI4Tc : gemv_kind(nch, M, bits, nx);
+}
+
+int gemv_kind(int64_t nch, int M, int bits, int nx) {  // mirrors gemv_launch's dispatch (plans without tc)
   if (M >= 2 && !use_m1(nch, M, bits, nx))
     return (bits == 4 && gemv_imma() && M * nx <= 32) ? kGemvI4Multi : kGemvF16Multi;
   if (use_m1(nch, M, bits, nx)) return gemv_imma() ? kGemvI4Single : kGemvF16Single;
@@ -1445,6 +1448,10 @@ void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cud
              reinterpret_cast<const uint4*>(op.xf2 ? op.xf2 : op.xf), op.xf2 ? op.rt_split : op.nrt, partial,
              op.nrt, op.nch, op.nrt * kTileN, M, p.ksplit};
   const int nx_op = (op.xf2 && op.xf2 != op.xf) ? 2 : 1;
+  if (p.tc) {
+    gemv_tc_launch(op, M, partial, p, st);
+    return;
+  }
   if (M >= 2 && !use_m1(op.nch, M, op.bits, nx_op)) {
     const int nx = nx_op;
     const int64_t slice_max = (op.nch + p.ksplit - 1) / p.ksplit;

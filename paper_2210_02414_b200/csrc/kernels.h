@@ -1,5 +1,6 @@
 // kernels.h — host-side launchers shared by the C ABI and the model runner.
 #pragma once
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -70,7 +71,8 @@ struct GemvPlan {
   int grid = 1;
   int warps = 16;  // warps per CTA the split-K balance was computed for
   int rt_per_warp = 1;  // multi-token kernel: row tiles per warp (1 or 2)
-  int per = 0;          // integer-MMA multi-token kernel: items per CTA (slice-major ranges)
+  int per = 0;          // integer-MMA multi-token kernels: items per CTA (slice-major ranges)
+  bool tc = false;      // INT4 2..16 tokens on the tcgen05 kernel (gemv_tc.cu)
 };
 int mk_row_tiles(int bits, int M);
 // Split-K plan for an M-row GEMV; the single-token INT4 kernel runs more warps per SM.
@@ -89,9 +91,16 @@ struct GemvOp {
 };
 
 void gemv_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
+// ---- gemv_tc.cu : INT4 2..16-token decode GEMV on tcgen05 (kind::i8), bit-identical to k_gemv_mk_i4 ----
+#ifndef GLM_TC_SLICE
+#define GLM_TC_SLICE 64
+#endif
+constexpr int kTcSliceChunks = GLM_TC_SLICE;  // longest k-slice (64-k chunks) of one item
+void gemv_tc_launch(const GemvOp& op, int M, float* partial, const GemvPlan& p, cudaStream_t st);
 // Which decode-GEMV kernel gemv_launch runs for M tokens (diagnostics / parity contracts)
-enum GemvKind { kGemvF16Single = 0, kGemvI4Single = 1, kGemvI4Multi = 2, kGemvF16Multi = 3, kGemvF16Tma = 4 };
+enum GemvKind { kGemvF16Single = 0, kGemvI4Single = 1, kGemvI4Multi = 2, kGemvF16Multi = 3, kGemvF16Tma = 4, kGemvI4Tc = 6 };
 int gemv_kind(int64_t nch, int M, int bits, int nx = 1);
+int gemv_kind(const GemvPlan& p, int64_t nch, int M, int bits, int nx = 1);
 // partial[s][m][n] (fp32, [ksplit][M][Np]) = sum over k-split s of x . W
 void gemv_launch(const QWeightDev& w, const __half* xfrag, int M, float* partial, const GemvPlan& p,
                  cudaStream_t st);
@@ -112,7 +121,14 @@ bool qmm_geglu_supported(const QWeightDev& w1, const QWeightDev& v, int M);
 void qmm_geglu_launch(const QWeightDev& w1, const QWeightDev& v, const __half* xt, int M, __half* xo, int64_t xo_Kp,
                       const float* xo_rs, cudaStream_t st);
 void xtile_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xt, cudaStream_t st);
-long long*& qmm_trace_ptr();  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
+long long*& qmm_trace_ptr();
+// Tensor maps (cuTensorMapEncodeTiled through the runtime): the device-layout codes of nrt row
+// tiles x nch chunks, box = box_rt row tiles of one chunk, 64 B swizzle (wide: INT4 as 128 B
+// rows of two g rows, 128 B swizzle) (cached per buffer);
+// and a 3-D byte tensor [groups][rows][inner] with free row / group strides (not cached).
+CUtensorMap codes_tensor_map_raw(const void* codes, int64_t nrt, int64_t nch, int bits, int box_rt, bool wide);
+CUtensorMap rows_tensor_map(const void* base, int64_t inner_bytes, int64_t rows, int64_t row_stride, int64_t groups,
+                            int64_t group_stride, int box_rows, int box_groups);  // diagnostics: device buffer of the last traced launch (GLM_QMM_TRACE)
 
 // x fp32 [M][K] (row stride ldx) -> x_frag fp16 with the kRow scale fold
 void xfrag_from_f32(const float* x, int64_t ldx, int M, const QWeightDev& w, __half* xfrag, cudaStream_t st);
@@ -125,5 +141,6 @@ void gemv_reduce(const float* partial, int ksplit, int M, const QWeightDev& w, f
 void trace_bind_gemv(unsigned long long* buf, unsigned long long cap);
 void trace_bind_block(unsigned long long* buf, unsigned long long cap);
 void trace_bind_model(unsigned long long* buf, unsigned long long cap);
+void trace_bind_gemv_tc(unsigned long long* buf, unsigned long long cap);
 
 }  // namespace glm

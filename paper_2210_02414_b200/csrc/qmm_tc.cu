@@ -537,52 +537,89 @@ long long*& qmm_trace_ptr() {
 // Tensor map of a linear's device-layout codes: [64 B row][8 rows g][(INT8: 2 halves)]
 // [nch chunks][nrt16 row tiles], box = one chunk of 8 row tiles, 64 B swizzle. The driver
 // entry point comes through the runtime (no libcuda link); maps are cached per buffer.
+namespace {
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 // box_rt: row tiles per copy (8; 4 for the GeGLU-paired launch, which stages W1 and V halves).
-CUtensorMap codes_tensor_map(const QWeightDev& w, int box_rt = 8) {
-  static std::mutex mu;
-  static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
-  static EncodeTiledFn encode = nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_pair(static_cast<const void*>(w.codes),
-                                  (w.L.nrt * 1000003 + w.L.nch * 17 + w.L.bits) * 16 + box_rt);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  if (!encode) {
+EncodeTiledFn tensor_map_encoder() {
+  static EncodeTiledFn encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn || q != cudaDriverEntryPointSuccess) fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<EncodeTiledFn>(fn);
-  }
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  return encode;
+}
+
+}  // namespace
+
+CUtensorMap codes_tensor_map_raw(const void* codes, int64_t nrt, int64_t nch, int bits, int box_rt, bool wide) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(codes, ((nrt * 1000003 + nch * 17 + bits) * 16 + box_rt) * 2 + (wide ? 1 : 0));
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  EncodeTiledFn encode = tensor_map_encoder();
   CUtensorMap m;
-  const bool i8 = w.L.bits == 8;
+  const bool i8 = bits == 8;
   const cuuint32_t rank = i8 ? 5 : 4;
   cuuint64_t dims[5], strides[4];
   cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-  const cuuint64_t cb = static_cast<cuuint64_t>(w.L.chunk_bytes());
-  if (i8) {
-    const cuuint64_t d[5] = {64, 8, 2, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
-    const cuuint64_t sd[4] = {64, 512, 1024, static_cast<cuuint64_t>(w.L.nch) * cb};
+  const cuuint64_t cb = i8 ? 1024 : 512;  // QLayout::chunk_bytes
+  if (wide) {
+    // INT4, rows of 128 B (two g rows), 128 B swizzle: half the copy rows of the 64 B form
+    if (i8) fail(GLM_CONTRACT, "qlinear", "128 B code rows are INT4 only");
+    const cuuint64_t d[4] = {128, 4, static_cast<cuuint64_t>(nch), static_cast<cuuint64_t>(nrt)};
+    const cuuint64_t sd[3] = {128, 512, static_cast<cuuint64_t>(nch) * cb};
+    const cuuint32_t bx[4] = {128, 4, 1, static_cast<cuuint32_t>(box_rt)};
+    for (int i = 0; i < 4; ++i) dims[i] = d[i], box[i] = bx[i];
+    for (int i = 0; i < 3; ++i) strides[i] = sd[i];
+  } else if (i8) {
+    const cuuint64_t d[5] = {64, 8, 2, static_cast<cuuint64_t>(nch), static_cast<cuuint64_t>(nrt)};
+    const cuuint64_t sd[4] = {64, 512, 1024, static_cast<cuuint64_t>(nch) * cb};
     const cuuint32_t bx[5] = {64, 8, 2, 1, static_cast<cuuint32_t>(box_rt)};
     for (int i = 0; i < 5; ++i) dims[i] = d[i], box[i] = bx[i];
     for (int i = 0; i < 4; ++i) strides[i] = sd[i];
   } else {
-    const cuuint64_t d[4] = {64, 8, static_cast<cuuint64_t>(w.L.nch), static_cast<cuuint64_t>(w.L.nrt)};
-    const cuuint64_t sd[3] = {64, 512, static_cast<cuuint64_t>(w.L.nch) * cb};
+    const cuuint64_t d[4] = {64, 8, static_cast<cuuint64_t>(nch), static_cast<cuuint64_t>(nrt)};
+    const cuuint64_t sd[3] = {64, 512, static_cast<cuuint64_t>(nch) * cb};
     const cuuint32_t bx[4] = {64, 8, 1, static_cast<cuuint32_t>(box_rt)};
     for (int i = 0; i < 4; ++i) dims[i] = d[i], box[i] = bx[i];
     for (int i = 0; i < 3; ++i) strides[i] = sd[i];
   }
-  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, w.codes, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(codes), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
   cache[key] = m;
   return m;
 }
+
+CUtensorMap rows_tensor_map(const void* base, int64_t inner_bytes, int64_t rows, int64_t row_stride, int64_t groups,
+                            int64_t group_stride, int box_rows, int box_groups) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner_bytes), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(groups)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride), static_cast<cuuint64_t>(group_stride)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(inner_bytes), static_cast<cuuint32_t>(box_rows),
+                             static_cast<cuuint32_t>(box_groups)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box,
+                                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(GLM_CUDA, "qlinear", "cuTensorMapEncodeTiled (activation rows) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+namespace {
+CUtensorMap codes_tensor_map(const QWeightDev& w, int box_rt = 8) {
+  return codes_tensor_map_raw(w.codes, w.L.nrt, w.L.nch, w.L.bits, box_rt, false);
+}
+}  // namespace
 
 // Token tiles per group (GLM_QMM_TOKGROUP overrides). The SMs hold ~148 items at once, so a
 // group of G token tiles spans 148 / G row tiles per wave: activations are read once while the

@@ -322,7 +322,7 @@ class QLinear:
         _check(lib().glm_qlinear_host(self.h, _p(x), x.shape[0], _p(y)))
         return y
 
-    GEMV_KINDS = ("f16_single", "i4_single", "i4_multi", "f16_multi", "f16_tma", "tcgen05")
+    GEMV_KINDS = ("f16_single", "i4_single", "i4_multi", "f16_multi", "f16_tma", "tcgen05", "i4_tc")
 
     def plan(self, M):
         """(kernel, ksplit, nch) glm_qlinear uses for M rows (glm_debug_gemv_plan)."""

@@ -39,3 +39,24 @@ def test_plan_rejects_bad_arguments():
         glm.QLinear.plan_for(12288, 12288, 4, 0)
     with pytest.raises(glm.ContractError):
         glm.QLinear.plan_for(12288, 12288, 3, 1)
+
+
+def test_opt_in_tcgen05_decode_plan():
+    """GLM_GEMV_TC=2 moves INT4 2..16-token GEMVs to the tcgen05 kernel: 128-feature items,
+    k-slices of <= 64 chunks, one CTA per SM."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, sys.argv[1]); from paper_2210_02414_b200 import glm\n"
+        "for K, N in %r:\n"
+        "    nch = K // 64\n"
+        "    assert glm.QLinear.plan_for(K, N, 4, 1)[0] == 'i4_single'\n"
+        "    for M in (2, 8, 16):\n"
+        "        kind, ks, _, grid = glm.QLinear.plan_for(K, N, 4, M)\n"
+        "        assert kind == 'i4_tc' and -(-nch // ks) <= 64 and 1 <= grid <= 148, (K, N, M, kind, ks, grid)\n"
+        "print('ok')\n" % (G,))
+    r = subprocess.run([sys.executable, "-c", code, root], env=dict(os.environ, GLM_GEMV_TC="2"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -6,8 +6,8 @@ contract (activations rounded to fp16 after the kRow fold, fp32 scale) -> only f
 accumulation error remains: <= 2e-6 of max|y|. The INT4 decode GEMVs run on the integer MMA
 (gemv.cu k_gemv_i4 at one token, k_gemv_mk_i4 at 2..16): their contract re-quantizes each fp16
 activation vector to 16-bit fixed point, x_int = rint(x * (32512 / max|x|)), per token
-(k_gemv_i4) or per (token, k-split) on the plan's 64-element chunk boundaries (k_gemv_mk_i4,
-QLinear.plan), and the products and sums are exact integers, so only the fp32 scaling and the
+(k_gemv_i4) or per (token, k-split) on the plan's 64-element chunk boundaries (k_gemv_mk_i4 and
+its tcgen05 twin k_gemv_tc_i4, QLinear.plan), and the products and sums are exact integers, so only the fp32 scaling and the
 k-split reduction round: <= 2e-6 (one split) / 4e-6 (several) of max|y|;
 (2) the reference check against the oracle's float64 x . dequantize(q),
 max|dy| <= 5e-3 max|y| (fp16 activation rounding)."""
@@ -48,7 +48,7 @@ def kernel_view(xh, kind, ksplit, nch):
     (k_gemv_i4) or fixed point per (token, k-split) with splits at chunks nch * s / ksplit."""
     if kind == "i4_single":
         return imma_activations(xh)
-    if kind == "i4_multi":
+    if kind in ("i4_multi", "i4_tc"):
         out = np.zeros(xh.shape, np.float64)
         for s in range(ksplit):
             k0, k1 = 64 * (nch * s // ksplit), min(xh.shape[1], 64 * (nch * (s + 1) // ksplit))
@@ -175,3 +175,41 @@ def test_tcgen05_gemm_token_tile_boundaries(bits, K, N):
         y = lin(x).astype(np.float64)
         ref = x @ deq
         assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max(), (M, np.abs(y - ref).max())
+
+
+TC_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2210_02414_b200 import glm
+from oracle import pyoracle as O
+from test_gpu_qlinear import kernel_contract, contract_tol
+rng = np.random.default_rng(5)
+for K, N, axis in ((12288, 1024, "column"), (4096, 1536, "row"), (1368, 512, "whole")):
+    w = rng.normal(0, 0.02, size=(K, N))
+    q = glm.quantize_absmax(w, 4, axis)
+    lin = glm.QLinear.from_payload(q)
+    for M in (2, 5, 16):
+        assert lin.plan(M)[0] == "i4_tc", lin.plan(M)
+        x = rng.normal(0, 1, size=(M, K))
+        x[0, 7] = 40.0  # one large activation: per-slice scales differ
+        y = lin(x).astype(np.float64)
+        c, ks = kernel_contract(x, q, lin)
+        assert np.abs(y - c).max() <= contract_tol(ks) * np.abs(c).max(), (K, N, M)
+        ref = x @ O.dequantize(q)
+        assert np.abs(y - ref).max() <= 5e-3 * np.abs(ref).max()
+print("ok")
+"""
+
+
+def test_qlinear_tcgen05_integer_kernel_contract():
+    """The opt-in tcgen05 kind::i8 decode GEMV (gemv_tc.cu, GLM_GEMV_TC=2) computes exactly the
+    integer-MMA multi-token contract (per (token, k-split) fixed point) at 2..16 tokens."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GLM_GEMV_TC="2")
+    r = subprocess.run([sys.executable, "-c", TC_SCRIPT, root], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
