@@ -1722,11 +1722,22 @@ __global__ void __launch_bounds__(kRingThreads, MINB) k_attn_decode_ring(AttnDec
     wait(j);
     const __half* blk = ring + (j % kRingStages) * (kRingBlock * DH);
     const int nk = min(kRingBlock, n_old - j * kRingBlock);
-    for (int s = warp * KPW + kin; s < kRingBlock; s += NW * KPW) {
-      float acc = s < nk ? dot8(*reinterpret_cast<const uint4*>(blk + s * DH + sub * 8)) : 0.f;
+    // the block's kRingBlock / (NW * KPW) key groups of this warp, loads first (independent chains)
+    constexpr int KIT = kRingBlock / (NW * KPW);
+    float acc[KIT];
 #pragma unroll
-      for (int o = LPK / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (sub == 0 && s < nk) p[j * kRingBlock + s] = score(acc);
+    for (int i = 0; i < KIT; ++i) {
+      const int s = warp * KPW + kin + i * NW * KPW;
+      acc[i] = s < nk ? dot8(*reinterpret_cast<const uint4*>(blk + s * DH + sub * 8)) : 0.f;
+    }
+#pragma unroll
+    for (int o = LPK / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < KIT; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+#pragma unroll
+    for (int i = 0; i < KIT; ++i) {
+      const int s = warp * KPW + kin + i * NW * KPW;
+      if (sub == 0 && s < nk) p[j * kRingBlock + s] = score(acc[i]);
     }
     __syncthreads();  // stage j consumed by every warp
     if (threadIdx.x == 0) issue(j + kRingStages);
@@ -1780,7 +1791,12 @@ __global__ void __launch_bounds__(kRingThreads, MINB) k_attn_decode_ring(AttnDec
     wait(j);
     const __half* blk = ring + (j % kRingStages) * (kRingBlock * DH);
     const int jb = j - nb, nk = min(kRingBlock, n_old - jb * kRingBlock);
-    for (int s = warp; s < nk; s += NW) pv(blk + s * DH + lane * FPL, p[jb * kRingBlock + s]);
+    if (nk == kRingBlock) {
+#pragma unroll
+      for (int i = 0; i < kRingBlock / NW; ++i) pv(blk + (warp + i * NW) * DH + lane * FPL, p[jb * kRingBlock + warp + i * NW]);
+    } else {
+      for (int s = warp; s < nk; s += NW) pv(blk + s * DH + lane * FPL, p[jb * kRingBlock + s]);
+    }
     __syncthreads();
     if (threadIdx.x == 0) issue(j + kRingStages);
   }

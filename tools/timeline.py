@@ -19,16 +19,19 @@ import bench
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=70)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--prompt", type=int, default=127, help="prompt tokens before [gMASK] (cache length)")
+ap.add_argument("--first", type=int, default=40, help="first kernel instance printed")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 cfg = dict(bench.G)
 cfg["num_layers"] = a.layers
-m = glm.Model(glm.GLMConfig(**cfg), bits=4, axis="column", max_ctx=256, head_bf16=True, max_batch=a.batch)
+m = glm.Model(glm.GLMConfig(**cfg), bits=4, axis="column", max_ctx=max(256, a.prompt + 64), head_bf16=True,
+              max_batch=a.batch)
 m.init_synthetic(2210)
-pos, Cl = glm.gmask_layout(127, 0)
+pos, Cl = glm.gmask_layout(a.prompt, 0)
 for b in range(a.batch):
-    m.prefill([7] * 127 + [2], pos[:Cl], Cl, seq=b, logits=False)
-tok, p = [3] * a.batch, [127] * a.batch
+    m.prefill([7] * a.prompt + [2], pos[:Cl], Cl, seq=b, logits=False)
+tok, p = [3] * a.batch, [a.prompt] * a.batch
 for _ in range(3):
     nxt, _ = m.decode_step(tok, p, logits=False)
     tok, p = [int(v) for v in nxt], [q + 1 for q in p]
@@ -87,7 +90,7 @@ for i, c in enumerate(inst):
     dur = (c["end"] - c["wait"]) / 1e3
     total[names[c["fam"]]] += dur
     gaps[names[c["fam"]]] += gap
-    if 40 <= i < 56:
+    if a.first <= i < a.first + 16:
         rdy = (c["ready"] - c["wait"]) / 1e3 if c["ready"] else float("nan")
         tail = (c["end"] - c["end_min"]) / 1e3
         xa = (c["xarr"] - c["wait"]) / 1e3 if c.get("xarr") else float("nan")
@@ -100,7 +103,7 @@ for i, c in enumerate(inst):
     prev_end = c["end"]
 print("post-wait -> last end, summed per family (us):", {k: round(v, 1) for k, v in total.items()})
 # LayerNorm phases: post-wait -> loads done (23) -> cluster reduction done (24) -> end
-for c in inst[40:56]:
+for c in inst[a.first:a.first + 16]:
     if c["fam"] != 20:
         continue
     nxt = [d["wait"] for d in inst if d["wait"] > c["wait"]]
@@ -111,7 +114,7 @@ for c in inst[40:56]:
         print(f"ln: loads done +{(l3.max() - c['wait']) / 1e3:.2f}  reduced +{(l4.max() - c['wait']) / 1e3:.2f}  end +{(c['end'] - c['wait']) / 1e3:.2f} us")
 print("previous end -> release gaps, summed per family (us):", {k: round(v, 1) for k, v in gaps.items()})
 
-for c in inst[40:56]:
+for c in inst[a.first:a.first + 16]:
     if c["fam"] != 30:
         continue
     nxt = [d["wait"] for d in inst if d["wait"] > c["wait"]]
