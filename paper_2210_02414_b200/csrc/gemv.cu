@@ -22,7 +22,8 @@
 // ~6 TB/s INT8 at M = 1. A tcgen05 variant (transcode into TMEM, async MMA) was built and
 // measured slower for decode (2.6 / 5.3 TB/s: a small-N tcgen05.mma costs its issuing
 // thread ~68 cycles and the extra cross-warp hand-offs add ~350 cycles per stage); it is
-// used where it wins, for prefill (qmm_tc.cu).
+// used where it wins, for prefill (qmm_tc.cu). Round 2's integer tcgen05 variant for 2..16 tokens
+// (kind::i8, gemv_tc.cu) is bit-identical to k_gemv_mk_i4 but also slower; opt-in (GLM_GEMV_TC).
 #include <cstdlib>
 #include <type_traits>
 #include <string>
