@@ -116,8 +116,9 @@ glm_status glm_debug_qmm_trace(long long* host_out);
 
 /* Diagnostics: the kernel glm_qlinear runs for M rows of q. out[0]: 0 fp16 single-token GEMV,
  * 1 integer-MMA single-token GEMV, 2 integer-MMA multi-token GEMV, 3 fp16 multi-token GEMV,
- * 4 fp16 TMA GEMV, 5 tcgen05 GEMM (prefill); out[1]: k-splits (the integer-MMA multi-token GEMV
- * quantizes activations per (token, k-split) on 64-element chunk boundaries
+ * 4 fp16 TMA GEMV, 5 tcgen05 GEMM (prefill), 6 tcgen05 integer multi-token GEMV (opt-in,
+ * GLM_GEMV_TC); out[1]: k-splits (the integer multi-token GEMVs 2 and 6
+ * quantize activations per (token, k-split) on 64-element chunk boundaries
  * chunk = nch * s / ksplit); out[2]: nch, the 64-element chunks along K. Host only, no launch. */
 glm_status glm_debug_gemv_plan(const glm_qweight* q, int64_t M, int32_t* out);
 /* The same plan for a [rows, cols] weight of `bits` without a handle (host only, no device
