@@ -445,3 +445,16 @@ def test_fp16_activation_overflow_raises_policy_error():
     m.reset()
     lg = m.prefill(PREFIX[:20], list(range(20)))
     assert np.isfinite(lg).all()
+
+
+def test_batched_decode_on_the_opt_in_tcgen05_integer_gemv():
+    """GLM_GEMV_TC=2 (gemv_tc.cu for every 2..16-token INT4 GEMV, incl. the fused W1|V launch
+    with distinct kRow activation folds): the batched-decode parity tests above pass unchanged."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_model.py"), "-q", "-x",
+                        "-m", "gpu", "-k", "batched_decode_equals_single or two_row_tiles_per_warp and 4-"],
+                       env=dict(os.environ, GLM_GEMV_TC="2"), capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
